@@ -1,0 +1,14 @@
+# Builds the C-ABI library in-tree (sm_100a).  `python -c "import __graft_entry__ as g; g.build()"` does the same.
+NVCC ?= nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+SRC := paper_2412_17560_b200/csrc
+LIB := paper_2412_17560_b200/lib/libgqsa.so
+CUFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3,-Wall -Xptxas -v --expt-relaxed-constexpr
+
+$(LIB): $(wildcard $(SRC)/*.cu $(SRC)/*.cpp $(SRC)/*.h) include/gqsa.h
+	@mkdir -p $(dir $(LIB))
+	$(NVCC) $(CUFLAGS) -shared -o $@ $(SRC)/gqsa_gemv.cu $(SRC)/gqsa_capi.cu $(SRC)/gqsa_pack.cpp 2> $(dir $(LIB))/ptxas.log || (cat $(dir $(LIB))/ptxas.log; false)
+
+clean:
+	rm -f $(LIB)
+.PHONY: clean

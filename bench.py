@@ -1,0 +1,452 @@
+#!/usr/bin/env python
+"""GQSA decode hot path benchmark (BASELINE.json metric).
+
+One STEP = one sparse GEMV on each LLaMA-3-8B layer shape of BASELINE.json
+configs[1] -- 4096x4096, 14336x4096, 4096x14336 at W4S50, G=16, batch 1 --
+i.e. every row of SURVEY §8(a) over one batch of synthetic input.  value =
+counted (compressed, algorithmic) bytes of all steps / device time, in GB/s.
+
+Timing: the weights rotate over R device copies of the layer set (> 2x the
+126 MB L2), so every launch streams from HBM.  K steps are replayed from CUDA
+graphs, bracketed by barrier + synchronize, timed with CUDA events on the
+launching stream (max over ranks).  Clocks / throttle reasons are sampled
+through NVML during the timed region.
+
+N > 1 (torchrun, NCCL): every rank owns rows [N*r/P, N*(r+1)/P) of each layer
+(output-row sharding), runs its GEMV, then all-gathers y over
+NVLink (torch.distributed.all_gather_into_tensor).  Total work is fixed:
+"scaling": "strong".
+
+--impl reference: the CPU fp64 oracle (oracle/), the tier's reference arm,
+timed on the host on a bounded row sample of the same workload (rank 0 only).
+"""
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GQSA W4S50 sparse GEMV µs & achieved HBM GB/s vs ~8 TB/s at LLaMA shapes"
+SHAPES = [(4096, 4096, "q_proj/o_proj"), (14336, 4096, "gate_proj/up_proj"), (4096, 14336, "down_proj")]
+NOMINAL_HBM_GBS = 8000.0
+FALLBACK_HBM_GBS = 6650.0
+L2_BYTES = 126 * 1024 * 1024
+
+
+def counted_bytes(rows, cols, nnzg, bits, batch=1, G=16):
+    """n*G/8 + 2 + 2 + 2 bytes per kept group, 4*(rows+1) row
+    offsets, 2*B*K of fp16 x, 4*B*N of fp32 y."""
+    return nnzg * (G * bits // 8 + 6) + 4 * (rows + 1) + 2 * batch * cols + 4 * batch * rows
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy r+w)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def make_layers(bits, sparsity, batch, world=1, rank=0, mask="uniform"):
+    from paper_2412_17560_b200 import synth
+    out = []
+    for rows, cols, name in SHAPES:
+        tag = f"llama3-8b/{rows}x{cols}/{bits}/{sparsity}/16/{mask}"
+        seed = synth.seed_for(tag)
+        bsr = synth.make_layer(seed, rows, cols, bits=bits, sparsity=sparsity, mask=mask)
+        x = synth.make_x(seed + 1, batch, cols)
+        lo, hi = synth.shard_rows(rows, world, rank)
+        out.append(dict(name=name, rows=rows, cols=cols, bsr=bsr, x=x, lo=lo, hi=hi, tag=tag))
+    return out
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, dev_index):
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover - NVML unavailable
+            self.nv = None
+
+    def _sample(self):
+        nv = self.nv
+        self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        names = {
+            getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8): "hw_slowdown",
+            getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40): "hw_thermal_slowdown",
+            getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20): "sw_thermal_slowdown",
+            getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4): "sw_power_cap",
+            getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80): "hw_power_brake_slowdown",
+        }
+        for bit, name in names.items():
+            if r & bit:
+                self.reasons.add(name)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self._sample()
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+            try:
+                self._sample()
+            except Exception:
+                pass
+
+    def summary(self):
+        if not self.nv or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- cpu baseline
+def cpu_oracle_baseline(layers, budget_s=12.0, max_reps=50):
+    """The fp64 oracle as it stands, single process (numpy, 1 core), on whole
+    layers of the workload, repeated until ~budget_s of CPU work."""
+    from oracle import gqsa_oracle as O
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    done_bytes, t_total, reps = 0, 0.0, 0
+    names = []
+    while t_total < budget_s and reps < max_reps:
+        for L in layers:
+            bsr = L["bsr"]
+            t0 = time.perf_counter()
+            O.gemv(bsr, L["x"])
+            t_total += time.perf_counter() - t0
+            done_bytes += counted_bytes(L["rows"], L["cols"], bsr["nnzg"], bsr["bits"], L["x"].shape[0])
+            names.append(L["name"])
+            if t_total >= budget_s:
+                break
+        reps += 1
+    return {
+        "value": done_bytes / t_total / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+        "sample": f"{len(names)} whole-layer oracle GEMVs ({', '.join(sorted(set(names)))}) of the "
+                  f"same synthetic workload, {t_total:.1f} s of single-core numpy fp64",
+        "seconds": round(t_total, 2),
+    }
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import gqsa_oracle as O
+    layers = make_layers(4, 0.5, args.batch)
+    total_steps = args.steps + args.warmup
+    budget = float(os.environ.get("GQSA_REF_BUDGET_S", "90"))
+    per_step = budget / max(total_steps, 1)
+    # a bounded row sample per layer, sized from a quick calibration
+    t0 = time.perf_counter()
+    O.gemv_rows(layers[0]["bsr"], layers[0]["x"], np.arange(64))
+    per_row = (time.perf_counter() - t0) / 64
+    rows_per_layer = int(max(1, min(4096, per_step / (per_row * 3 * 3.5))))
+    rng = np.random.default_rng(0)
+    samples = []
+    for L in layers:
+        ri = L["bsr"]["row_index"]
+        rs = np.sort(rng.choice(L["rows"], size=min(rows_per_layer, L["rows"]), replace=False))
+        nnz = int(np.sum(ri[rs + 1] - ri[rs]))
+        b = nnz * (16 * 4 // 8 + 6) + 4 * (len(rs) + 1) + 2 * L["cols"] + 4 * len(rs)
+        samples.append((L, rs, b))
+    for _ in range(args.warmup):
+        for L, rs, _b in samples:
+            O.gemv_rows(L["bsr"], L["x"], rs)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for L, rs, _b in samples:
+            O.gemv_rows(L["bsr"], L["x"], rs)
+    dt = time.perf_counter() - t0
+    step_bytes = sum(b for _, _, b in samples)
+    value = step_bytes * args.steps / dt / 1e9
+    sample = (f"{rows_per_layer} random output rows of each of 4096x4096, 14336x4096, 4096x14336 "
+              f"(W4S50, B={args.batch}) per step; bytes counted per sampled row")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded; DESIGN.md §4 recipe)",
+        "config": {"workload": "llama3-8b-layer-shapes-w4s50-b1", "global_batch": args.batch,
+                   "seq_len": 1, "parallelism": "host-cpu"},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2412_17560_b200 import gqsa
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    bits, sp, B = 4, 0.5, args.batch
+    layers = make_layers(bits, sp, B, world, rank)
+    hbm_peak, peak_src = peaks()
+
+    # pack this rank's row shard of every layer; R device copies for L2 rotation
+    packed = []
+    set_bytes = 0
+    for L in layers:
+        blob, desc = gqsa.pack(L["bsr"], L["lo"], L["hi"])
+        packed.append((blob, desc))
+        set_bytes += blob.size
+    R = max(2, math.ceil(2.2 * L2_BYTES / max(set_bytes, 1)) + 1) if not args.no_rotate else 1
+    ws = []
+    copies = []  # copies[r][i] = device blob of layer i
+    for r in range(R):
+        row = []
+        for blob, desc in packed:
+            row.append(torch.from_numpy(blob).to(dev))
+        copies.append(row)
+    for blob, desc in packed:
+        ws.append(torch.zeros(gqsa.workspace_size(desc, B), dtype=torch.uint8, device=dev))
+    xs = [torch.from_numpy(L["x"]).view(torch.float16).to(dev) for L in layers]
+    ys = [torch.empty(B, d.rows, dtype=torch.float32, device=dev) for _, d in packed]
+    yfull = [torch.empty(world * B * d.rows, dtype=torch.float32, device=dev) if world > 1 else None
+             for _, d in packed]
+
+    def launch(i, r):
+        _, desc = packed[i]
+        if B == 1:
+            gqsa.gemv(desc, copies[r][i], xs[i][0], ys[i][0], None, ws[i])
+        else:
+            gqsa.gemm_smallbatch(desc, copies[r][i], xs[i], ys[i], None, ws[i])
+        if world > 1:
+            dist.all_gather_into_tensor(yfull[i], ys[i].view(-1))
+
+    def step(r):
+        for i in range(len(layers)):
+            launch(i, r)
+
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.synchronize()
+    # eager warm-up (also the first launches: attribute set-up, module load)
+    with torch.cuda.stream(stream):
+        for r in range(R):
+            step(r)
+    torch.cuda.synchronize()
+
+    def capture(nsteps, start=0):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for k in range(nsteps):
+                step((start + k) % R)
+        return g
+
+    use_graph = world == 1  # NCCL collectives stay eager under torchrun
+    graphs = {}
+
+    def run_steps(n):
+        if use_graph:
+            if R not in graphs:
+                graphs[R] = capture(R)
+            for _ in range(n // R):
+                graphs[R].replay()
+            if n % R:
+                if n % R not in graphs:
+                    graphs[n % R] = capture(n % R)
+                graphs[n % R].replay()
+        else:
+            for k in range(n):
+                step(k % R)
+
+    with torch.cuda.stream(stream):
+        run_steps(max(args.warmup, 3))
+        if use_graph and args.steps % R:
+            graphs.setdefault(args.steps % R, capture(args.steps % R))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    torch.cuda.synchronize()
+    with sampler:
+        e0.record(stream)
+        with torch.cuda.stream(stream):
+            run_steps(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+
+    # counted bytes: every rank's shard (sum over ranks) + the all-gathered y
+    step_bytes_rank = sum(counted_bytes(d.rows, d.cols, d.nnzg, bits, B) for _, d in packed)
+    if world > 1:
+        t = torch.tensor([step_bytes_rank], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        step_bytes = float(t.item())
+    else:
+        step_bytes = float(step_bytes_rank)
+    value = step_bytes * args.steps / (ms * 1e-3) / 1e9
+
+    # ---- per-layer device time (dominant kernel per shape), outside the timed region
+    layer_rows = []
+    if world == 1:
+        for i, L in enumerate(layers):
+            _, desc = packed[i]
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for r in range(R):
+                    if B == 1:
+                        gqsa.gemv(desc, copies[r][i], xs[i][0], ys[i][0], None, ws[i])
+                    else:
+                        gqsa.gemm_smallbatch(desc, copies[r][i], xs[i], ys[i], None, ws[i])
+            for _ in range(3):
+                g.replay()
+            reps = max(10, 2000 // R)
+            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record(stream)
+            with torch.cuda.stream(stream):
+                for _ in range(reps):
+                    g.replay()
+            b_.record(stream)
+            torch.cuda.synchronize()
+            us = a.elapsed_time(b_) * 1e3 / (reps * R)
+            cb = counted_bytes(desc.rows, desc.cols, desc.nnzg, bits, B)
+            layer_rows.append({"shape": f"{desc.rows}x{desc.cols}", "role": L["name"],
+                               "nnzg": desc.nnzg, "counted_bytes": cb, "us": round(us, 3),
+                               "gbs": round(cb / us / 1e3, 1),
+                               "frac_of_8tbs": round(cb / us / 1e3 / NOMINAL_HBM_GBS, 4),
+                               "frac_of_measured": round(cb / us / 1e3 / hbm_peak, 4)})
+
+    # ---- end to end through the public C ABI with host buffers (pinned)
+    e2e = None
+    if world == 1:
+        hX = [torch.from_numpy(L["x"]).view(torch.float16).pin_memory() for L in layers]
+        hY = [torch.empty(B, d.rows, dtype=torch.float32).pin_memory() for _, d in packed]
+        stage = [torch.empty(gqsa.hostio_stage_size(d, B), dtype=torch.uint8, device=dev) for _, d in packed]
+        ne = min(args.steps, args.e2e_steps)
+        for k in range(3):
+            with torch.cuda.stream(stream):
+                for i in range(len(layers)):
+                    gqsa.gemm_hostio(packed[i][1], copies[k % R][i], hX[i], hY[i], stage[i], ws[i])
+            stream.synchronize()
+        a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        a.record(stream)
+        for k in range(ne):
+            with torch.cuda.stream(stream):
+                for i in range(len(layers)):
+                    gqsa.gemm_hostio(packed[i][1], copies[k % R][i], hX[i], hY[i], stage[i], ws[i])
+            stream.synchronize()  # the caller reads y every step
+        b_.record(stream)
+        stream.synchronize()
+        wall = time.perf_counter() - t0
+        e_ms = a.elapsed_time(b_)
+        e2e = {"value": step_bytes * ne / (e_ms * 1e-3) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": int(sum(2 * B * d.cols for _, d in packed)),
+               "d2h_bytes_per_step": int(sum(4 * B * d.rows for _, d in packed)),
+               "steps": ne, "ms_per_step": e_ms / ne, "wall_ms_per_step": wall * 1e3 / ne}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_oracle_baseline(layers, budget_s=args.cpu_budget)
+
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            tr = json.load(open(tp))
+            traffic = tr.get("step_dram_bytes")
+        except Exception:
+            traffic = None
+    achieved = step_bytes / (ms_step * 1e-3) / 1e9 / world if world > 1 else value
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_step,
+        "us_per_step": round(ms_step * 1e3, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "u4xf16->f32",
+        "data": "synthetic (seeded random W4 codes, fp16 s/z, uniform 50% group mask, N(0,1) fp16 x "
+                "with 0.5% outlier channels; DESIGN.md §4)",
+        "config": {"workload": "llama3-8b-layer-shapes-w4s50-b1 (4096x4096, 14336x4096, 4096x14336)",
+                   "global_batch": B, "seq_len": 1, "group_size": 16, "bits": bits, "sparsity": sp,
+                   "parallelism": f"rowshard{world}" if world > 1 else "single",
+                   "l2": f"weights rotate over {R} device copies of the layer set "
+                         f"({R * set_bytes / 2**20:.0f} MiB > 2x L2)",
+                   "timing": "CUDA graphs of gqsa_gemv launches (PDL), CUDA events on the launch stream"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                     "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+                     "peak_source": peak_src, "frac_of_nominal_8tbs": round(achieved / NOMINAL_HBM_GBS, 4),
+                     "kernel": "gqsa::gqsa_streamk_kernel<4,1,true>",
+                     "algorithmic_bytes_per_step": int(step_bytes)},
+        "layers": layer_rows,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": 3 * args.steps,
+        "clocks": sampler.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20000)
+    ap.add_argument("--warmup", type=int, default=200)
+    ap.add_argument("--impl", default="gqsa", choices=["gqsa", "reference"])
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=2000)
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-rotate", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,178 @@
+/*
+ * gqsa.h -- C ABI of libgqsa.so, the B200 (sm_100a) decode hot path of GQSA
+ * (arXiv 2412.17560): a group-sparse, weight-only-quantized GEMV / small-batch
+ * GEMM over the paper's Block-Sparse-Row (BSR) layout.
+ *
+ * Citations: PAPER.md:L = /root/reference/PAPER.md line (the paper's LaTeX),
+ * SPEC.md:L likewise; DESIGN.md Rn = the readings listed in DESIGN.md §3.
+ *
+ * Operation (PAPER.md:64-69 [Eq. 3], 95-101 [§3.2 BSR listing], 134 [§3.5
+ * "GEMV task of shape 1xNxK", "accessed according to the real group index"]):
+ *
+ *   y[b][r] = sum_{g in [row_index[r], row_index[r+1])} s_g *
+ *             sum_{t < G} (q_{g,t} - z_g) * x[b][group_cols[g]*G + t]  (+ bias[r])
+ *
+ * accumulated in fp32 (no tensor cores at batch 1, PAPER.md:9, 134 step 4
+ * "CudaCores (FMA)").  Results are deterministic: bit-identical reruns for a
+ * fixed blob, batch, grid and device.
+ *
+ * Ownership: the caller owns every buffer, host and device.  The library
+ * never allocates or frees device memory and keeps no pointer past a call.
+ * A packed blob is immutable and may be shared by concurrent calls on
+ * different streams, each with its OWN workspace.  A workspace
+ * must be zero-filled once when allocated; every call leaves it zeroed again.
+ *
+ * Errors: every int-returning function returns GQSA_OK (0) or a negative
+ * gqsa_status_t.  Errors raised during asynchronous device execution surface
+ * at the next stream synchronisation (CUDA convention).
+ *
+ * Byte layout of the packed blob: DESIGN.md §5 ("LAYOUT v1").
+ */
+#ifndef GQSA_H_
+#define GQSA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GQSA_MAGIC 0x41535147u   /* bytes "GQSA" little-endian */
+#define GQSA_VERSION 1
+#define GQSA_TILE_GROUPS 128     /* kept groups per tile record (LAYOUT v1) */
+#define GQSA_MAX_BATCH 8
+
+typedef enum {
+  GQSA_OK = 0,
+  GQSA_ERR_SHAPE = -1,       /* dims mismatch, cols % G != 0, B not in [1,8], bad row range */
+  GQSA_ERR_VALIDATION = -2,  /* BSR invariant violated (see gqsa_pack) or inconsistent blob */
+  GQSA_ERR_UNSUPPORTED = -3, /* bits not in {2,4}, G != 16, K/G > 32767 */
+  GQSA_ERR_BUFFER = -4,      /* null pointer, blob/workspace too small, misaligned device pointer */
+  GQSA_ERR_CUDA = -5         /* CUDA launch / copy failure */
+} gqsa_status_t;
+
+/*
+ * Plain host BSR.
+ *   rows, cols    : N (out_features) and K (in_features) of W[N][K].
+ *   group_size    : G, the sparse AND quantization group, 16 in v1.
+ *   bits          : n, code width (4 or 2 in v1).
+ *   nnzg          : number of kept groups = row_index[rows].
+ *   row_index     : int32[rows+1] row offsets into the kept-group list (rowIndex).
+ *   group_cols    : uint16[nnzg] column of each kept group IN GROUP UNITS (groups[]).
+ *   codes         : ceil(nnzg*G*n/8) bytes, the kept groups' codes (values[]),
+ *                   group-major in CSR order; element e at bits [e*n, e*n+n),
+ *                   least-significant bits first (n=4: low nibble first,
+ *                   SPEC.md:146).
+ *   scales_f16    : uint16[nnzg] IEEE binary16 bit patterns of s_g.
+ *   zeros_f16     : uint16[nnzg] binary16 bit patterns of z_g (any finite value,
+ *                   not necessarily an integer: E2E-OQP tunes z).
+ * For gqsa_unpack the caller allocates the arrays (sizes from gqsa_read_desc)
+ * and the function fills them and the scalar fields.
+ */
+typedef struct {
+  int32_t rows, cols, group_size, bits;
+  int64_t nnzg;
+  const int32_t* row_index;
+  const uint16_t* group_cols;
+  const uint8_t* codes;
+  const uint16_t* scales_f16;
+  const uint16_t* zeros_f16;
+} gqsa_bsr_t;
+
+/* Host copy of a packed blob's header (filled by gqsa_pack / gqsa_read_desc). */
+typedef struct {
+  uint32_t magic, version;
+  int32_t rows, cols, group_size, bits;
+  int64_t nnzg;
+  int32_t tile_groups, num_tiles;
+  int32_t n_nzrows, n_empty;
+  int32_t tile_bytes, flags;
+  int32_t row_begin, row_end;     /* source row range this blob was packed from */
+  uint64_t off_row_index, off_nzrow, off_empty, off_tiles, blob_bytes;
+} gqsa_desc_t;
+
+/*
+ * gqsa_pack_size: bytes needed to pack rows [row_begin, row_end) of `bsr`.
+ * gqsa_pack: validate, then lay rows [row_begin, row_end) of `bsr` out as a
+ *   device blob (offline pre-processing, "grouped by size G and
+ *   saved ... along with scaling factors and zero points").  The row range
+ *   lets each rank pack its output-row shard; row offsets are rebased.
+ *   Validation: row_index[0] == 0, non-decreasing,
+ *   row_index[rows] == nnzg; group_cols strictly increasing within a row and
+ *   < cols/G; scales finite and > 0; zeros finite -> GQSA_ERR_VALIDATION.
+ *   `blob` is host memory of at least gqsa_pack_size bytes; `desc` may be NULL.
+ */
+int gqsa_pack_size(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_end, size_t* blob_bytes);
+int gqsa_pack(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_end,
+              void* blob, size_t blob_bytes, gqsa_desc_t* desc);
+
+/* Parse and bounds-check a (host) blob header: magic, version, section
+ * offsets, sizes.  GQSA_ERR_VALIDATION on any inconsistency. */
+int gqsa_read_desc(const void* blob, size_t blob_bytes, gqsa_desc_t* desc);
+
+/* Inverse of gqsa_pack (bit-exact): rebuild the plain BSR of the packed rows
+ * from the tile stream, checking it against the stored row offsets.  `out`'s
+ * array pointers must point to caller memory of the sizes given by the desc:
+ * row_index int32[rows+1], group_cols/scales/zeros [nnzg], codes
+ * ceil(nnzg*G*n/8) bytes. */
+int gqsa_unpack(const void* blob, size_t blob_bytes, gqsa_bsr_t* out);
+
+/* Workspace bytes a gemv/gemm call needs for `batch` columns on the current
+ * device (cross-warp fix-up records).  Zero-fill once. */
+int gqsa_workspace_size(const gqsa_desc_t* desc, int32_t batch, size_t* bytes);
+
+/*
+ * gqsa_gemv: y = W_hat x (+ bias), batch 1.
+ *   d_blob : device copy of the packed blob (256-B aligned).
+ *   d_x    : device fp16 bit patterns [cols] (16-B aligned).
+ *   d_y    : device fp32 [rows] (written in full, empty rows = bias or 0).
+ *   d_bias : device fp32 [rows] or NULL.
+ *   d_ws / ws_bytes : workspace (see gqsa_workspace_size).
+ *   stream : cudaStream_t (NULL = legacy default stream).
+ * Asynchronous; graph-capturable.  Uses Programmatic Dependent Launch so that
+ * weight fetch overlaps the previous kernel on the stream; activations are
+ * read only after the previous kernel completes.
+ */
+int gqsa_gemv(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_x, float* d_y,
+              const float* d_bias, void* d_ws, size_t ws_bytes, void* stream);
+
+/*
+ * gqsa_gemm_smallbatch: Y[b] = W_hat X[b] (+ bias) for b < B, 1 <= B <= 8.
+ *   d_X : device fp16 [B][ldx] (ldx >= cols, ldx % 8 == 0), d_Y : fp32 [B][ldy]
+ *   (ldy >= rows).  B == 1 is the GEMV.
+ */
+int gqsa_gemm_smallbatch(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_X,
+                         int32_t B, int64_t ldx, float* d_Y, int64_t ldy, const float* d_bias,
+                         void* d_ws, size_t ws_bytes, void* stream);
+
+/*
+ * gqsa_gemm_hostio: the end-to-end call with HOST activations and outputs.
+ * Copies h_X (pinned or pageable host fp16 [B][cols], dense) into the
+ * device staging area d_stage, runs gqsa_gemm_smallbatch, and copies Y back
+ * into h_Y (host fp32 [B][rows], dense), all on `stream`; returns after
+ * enqueueing (synchronize the stream before reading h_Y).  d_stage needs
+ * gqsa_hostio_stage_size bytes.
+ */
+int gqsa_hostio_stage_size(const gqsa_desc_t* desc, int32_t B, size_t* bytes);
+int gqsa_gemm_hostio(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* h_X, int32_t B,
+                     float* h_Y, const float* d_bias, void* d_stage, size_t stage_bytes,
+                     void* d_ws, size_t ws_bytes, void* stream);
+
+/* Launch plan the next gemv/gemm call will use on the current device:
+ * CTAs, warps per CTA, active warps (Stream-K units), tiles.  For tooling. */
+typedef struct {
+  int32_t grid, warps_per_cta, active_warps, num_tiles, smem_bytes, x_in_smem;
+} gqsa_plan_t;
+int gqsa_launch_plan(const gqsa_desc_t* desc, int32_t B, gqsa_plan_t* plan);
+
+/* Number of GQSA kernels launched by this process so far (all entry points). */
+uint64_t gqsa_launch_count(void);
+
+const char* gqsa_status_string(int status);
+int gqsa_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GQSA_H_ */

@@ -1,0 +1,206 @@
+// gqsa_capi.cu -- extern "C" entry points that validate arguments, plan the
+// Stream-K grid and launch the sm_100a kernels (see include/gqsa.h).
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/gqsa.h"
+#include "gqsa_kernels.h"
+#include "gqsa_layout.h"
+
+using namespace gqsa;
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+
+struct DevInfo {
+  int sms = 0;
+  bool attr_set[2][kMaxBatch + 1][2] = {};
+};
+std::mutex g_mu;
+DevInfo g_dev[64];
+
+int device_sms(int dev) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (dev < 0 || dev >= 64) return 0;
+  if (!g_dev[dev].sms) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+    g_dev[dev].sms = v;
+  }
+  return g_dev[dev].sms;
+}
+
+bool desc_ok(const gqsa_desc_t* d) {
+  return d && d->magic == kMagic && d->version == (uint32_t)kVersion && d->group_size == kGroup &&
+         (d->bits == 4 || d->bits == 2) && d->tile_groups == kTileGroups && d->rows >= 0 &&
+         d->cols > 0 && d->cols % kGroup == 0 && d->num_tiles >= 0;
+}
+
+size_t smem_for(const gqsa_desc_t* d, int B, bool* xsmem) {
+  const size_t xc = (size_t)B * (d->cols / kGroup) * 4;
+  const size_t xb = (size_t)B * d->cols * 2;
+  *xsmem = xb + xc <= (size_t)kSmemBudget;
+  return *xsmem ? xb + xc : xc;
+}
+
+// Fill the launch plan; returns a status.
+int make_plan(const gqsa_desc_t* d, int B, gqsa_plan_t* pl, const void** kfn) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return GQSA_ERR_CUDA;
+  const int sms = device_sms(dev);
+  if (sms <= 0) return GQSA_ERR_CUDA;
+  bool xsmem = false;
+  const size_t smem = smem_for(d, B, &xsmem);
+  const void* fn = select_kernel(d->bits, B, xsmem);
+  if (!fn) return GQSA_ERR_UNSUPPORTED;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    bool& set = g_dev[dev].attr_set[d->bits == 4][B][xsmem];
+    if (!set) {
+      if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget) !=
+          cudaSuccess)
+        return GQSA_ERR_CUDA;
+      set = true;
+    }
+  }
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem) != cudaSuccess)
+    return GQSA_ERR_CUDA;
+  if (occ < 1) return GQSA_ERR_UNSUPPORTED;
+  if (occ > kMaxCtasPerSm) occ = kMaxCtasPerSm;
+  int warps = sms * occ * kWarps;
+  if (warps > kMaxWarpsBound) warps = kMaxWarpsBound;
+  const int active = d->num_tiles < warps ? d->num_tiles : warps;
+  int grid = (active + kWarps - 1) / kWarps;
+  if (grid == 0) {  // nnzg == 0: only empty rows to write
+    grid = (d->n_empty + kThreads - 1) / kThreads;
+    if (grid > sms) grid = sms;
+    if (grid < 1) grid = 1;
+  }
+  pl->grid = grid;
+  pl->warps_per_cta = kWarps;
+  pl->active_warps = active;
+  pl->num_tiles = d->num_tiles;
+  pl->smem_bytes = (int32_t)smem;
+  pl->x_in_smem = xsmem ? 1 : 0;
+  if (kfn) *kfn = fn;
+  return GQSA_OK;
+}
+
+inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+}  // namespace
+
+extern "C" int gqsa_workspace_size(const gqsa_desc_t* desc, int32_t batch, size_t* bytes) {
+  if (!desc || !bytes) return GQSA_ERR_BUFFER;
+  if (!desc_ok(desc)) return GQSA_ERR_VALIDATION;
+  if (batch < 1 || batch > kMaxBatch) return GQSA_ERR_SHAPE;
+  const int64_t recs = desc->num_tiles < kMaxWarpsBound ? desc->num_tiles : kMaxWarpsBound;
+  *bytes = (size_t)(recs > 0 ? recs : 1) * kWsWords * 4;
+  return GQSA_OK;
+}
+
+extern "C" int gqsa_launch_plan(const gqsa_desc_t* desc, int32_t B, gqsa_plan_t* plan) {
+  if (!desc || !plan) return GQSA_ERR_BUFFER;
+  if (!desc_ok(desc)) return GQSA_ERR_VALIDATION;
+  if (B < 1 || B > kMaxBatch) return GQSA_ERR_SHAPE;
+  return make_plan(desc, B, plan, nullptr);
+}
+
+extern "C" int gqsa_gemm_smallbatch(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_X,
+                                    int32_t B, int64_t ldx, float* d_Y, int64_t ldy,
+                                    const float* d_bias, void* d_ws, size_t ws_bytes, void* stream) {
+  if (!desc || !d_blob || !d_X || !d_Y || !d_ws) return GQSA_ERR_BUFFER;
+  if (!desc_ok(desc)) return GQSA_ERR_VALIDATION;
+  if (B < 1 || B > kMaxBatch) return GQSA_ERR_SHAPE;
+  if (ldx < desc->cols || ldx % 8 || ldy < desc->rows) return GQSA_ERR_SHAPE;
+  if (!aligned(d_blob, 256) || !aligned(d_X, 16) || !aligned(d_ws, 16) ||
+      (d_bias && !aligned(d_bias, 4)) || !aligned(d_Y, 4))
+    return GQSA_ERR_BUFFER;
+  size_t need = 0;
+  gqsa_workspace_size(desc, B, &need);
+  if (ws_bytes < need) return GQSA_ERR_BUFFER;
+
+  gqsa_plan_t pl;
+  const void* fn = nullptr;
+  int st = make_plan(desc, B, &pl, &fn);
+  if (st) return st;
+
+  const uint8_t* blob = static_cast<const uint8_t*>(d_blob);
+  KParams p;
+  p.tiles = blob + desc->off_tiles;
+  p.nzrow = reinterpret_cast<const int32_t*>(blob + desc->off_nzrow);
+  p.empty = reinterpret_cast<const int32_t*>(blob + desc->off_empty);
+  p.X = d_X;
+  p.Y = d_Y;
+  p.bias = d_bias;
+  p.ws = static_cast<uint32_t*>(d_ws);
+  p.ldx = ldx;
+  p.ldy = ldy;
+  p.rows = desc->rows;
+  p.cols = desc->cols;
+  p.num_tiles = desc->num_tiles;
+  p.n_empty = desc->n_empty;
+  p.active_warps = pl.active_warps;
+  if (desc->rows == 0) return GQSA_OK;
+
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(pl.grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = pl.smem_bytes;
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* args[] = {&p};
+  if (cudaLaunchKernelExC(&cfg, fn, args) != cudaSuccess) return GQSA_ERR_CUDA;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return GQSA_OK;
+}
+
+extern "C" int gqsa_gemv(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_x, float* d_y,
+                         const float* d_bias, void* d_ws, size_t ws_bytes, void* stream) {
+  if (!desc) return GQSA_ERR_BUFFER;
+  return gqsa_gemm_smallbatch(desc, d_blob, d_x, 1, desc->cols, d_y, desc->rows, d_bias, d_ws,
+                              ws_bytes, stream);
+}
+
+extern "C" int gqsa_hostio_stage_size(const gqsa_desc_t* desc, int32_t B, size_t* bytes) {
+  if (!desc || !bytes) return GQSA_ERR_BUFFER;
+  if (!desc_ok(desc)) return GQSA_ERR_VALIDATION;
+  if (B < 1 || B > kMaxBatch) return GQSA_ERR_SHAPE;
+  const size_t xb = ((size_t)B * desc->cols * 2 + 255) / 256 * 256;
+  *bytes = xb + (size_t)B * desc->rows * 4;
+  return GQSA_OK;
+}
+
+extern "C" int gqsa_gemm_hostio(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* h_X,
+                                int32_t B, float* h_Y, const float* d_bias, void* d_stage,
+                                size_t stage_bytes, void* d_ws, size_t ws_bytes, void* stream) {
+  if (!desc || !h_X || !h_Y || !d_stage) return GQSA_ERR_BUFFER;
+  size_t need = 0;
+  int st = gqsa_hostio_stage_size(desc, B, &need);
+  if (st) return st;
+  if (stage_bytes < need || !aligned(d_stage, 256)) return GQSA_ERR_BUFFER;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint8_t* stage = static_cast<uint8_t*>(d_stage);
+  const size_t xb = ((size_t)B * desc->cols * 2 + 255) / 256 * 256;
+  uint16_t* dX = reinterpret_cast<uint16_t*>(stage);
+  float* dY = reinterpret_cast<float*>(stage + xb);
+  if (cudaMemcpyAsync(dX, h_X, (size_t)B * desc->cols * 2, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return GQSA_ERR_CUDA;
+  st = gqsa_gemm_smallbatch(desc, d_blob, dX, B, desc->cols, dY, desc->rows, d_bias, d_ws, ws_bytes,
+                            stream);
+  if (st) return st;
+  if (cudaMemcpyAsync(h_Y, dY, (size_t)B * desc->rows * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return GQSA_ERR_CUDA;
+  return GQSA_OK;
+}
+
+extern "C" uint64_t gqsa_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }

@@ -1,0 +1,469 @@
+// gqsa_gemv.cu -- sm_100a Stream-K group-sparse W4/W2 GEMV / small-batch GEMM.
+//
+// Computes, for every batch column b < B and output row r (PAPER.md:64-69
+// [Eq. 3], 95-101 [§3.2 BSR], 134 [§3.5]):
+//
+//   y[b][r] = sum_{g in row r} s_g * ( sum_t q_{g,t} x[b][c_g*G+t] - z_g * X_{b,c_g} ),
+//   X_{b,c} = sum_t x[b][c*G+t]       (Eq. 3 applied per group, z folded once)
+//
+// Design:
+//  * Task-centric partition (PAPER.md:161 Stream-K, App. J): the
+//    tile stream (128 kept groups per tile, CSR order) is cut into contiguous,
+//    equal (+-1 tile) ranges, one per WARP, regardless of row boundaries.
+//  * Weights stream HBM -> registers with 128-bit L1::no_allocate loads,
+//    double-buffered per warp; the first tiles are requested BEFORE
+//    griddepcontrol.wait so they overlap the previous kernel (PDL).
+//  * Activations are staged in shared memory once per CTA, together with the
+//    per-column-group sums X_{b,c} (fp32).
+//  * Dequantization: LOP3 magic (0x6400 = fp16 1024) turns 4-bit (2-bit)
+//    fields into exact fp16 integers; FHFMA (fma.rn.f32.f16) multiplies the
+//    exact fp16 code by fp16 x and accumulates in fp32 (products exact).
+//    No tensor cores: batch-1 GEMV is bandwidth-bound.
+//  * Row reduction: segmented warp scan keyed by the tile's row-start mask;
+//    rows split across warps are fixed up deterministically: the warp that
+//    owns a row's first group sums the partials its successors publish
+//    (flag + release/acquire), in warp order.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gqsa_kernels.h"
+#include "gqsa_layout.h"
+
+namespace gqsa {
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint4 ldg_stream128(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint2 ldg_stream64(const void* p) {
+  uint2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v2.u32 {%0,%1}, [%2];"
+               : "=r"(v.x), "=r"(v.y)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ float ld_relaxed_f32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return __uint_as_float(v);
+}
+__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// fp32 += fp16 * fp16 with the exact product (FHFMA).  `a`/`b` are half2
+// registers; H0/H1 pick the half (folded into the SASS operand selector).
+template <int HA, int HB>
+__device__ __forceinline__ float fhfma(uint32_t a, uint32_t b, float c) {
+  const unsigned short ah = HA ? (unsigned short)(a >> 16) : (unsigned short)(a & 0xffffu);
+  const unsigned short bh = HB ? (unsigned short)(b >> 16) : (unsigned short)(b & 0xffffu);
+  float d;
+  asm("fma.rn.f32.f16 %0, %1, %2, %3;" : "=f"(d) : "h"(ah), "h"(bh), "f"(c));
+  return d;
+}
+
+__device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t mask, uint32_t magic) {
+  uint32_t d;  // (a & mask) | magic
+  asm("lop3.b32 %0, %1, %2, %3, 0xea;" : "=r"(d) : "r"(a), "r"(mask), "r"(magic));
+  return d;
+}
+__device__ __forceinline__ uint32_t hadd2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("add.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t hfma2(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+constexpr uint32_t kMagic1024 = 0x64006400u;   // half2(1024, 1024)
+constexpr uint32_t kNeg1024 = 0xE400E400u;     // half2(-1024, -1024)
+
+// Dot product of one word of eight 4-bit codes (elements j = 0..7 at bits
+// 4j..4j+3) with x[0..7] held as half2 (x0,x1) (x2,x3) (x4,x5) (x6,x7).
+// Every code becomes an exact fp16 integer; every product is exact in fp32.
+__device__ __forceinline__ float dot8_w4(uint32_t w, uint32_t x01, uint32_t x23, uint32_t x45,
+                                         uint32_t x67, float acc) {
+  const uint32_t kM1 = 0x000F000Fu, kM2 = 0x00F000F0u;
+  const uint32_t k116 = 0x2C002C00u;   // half2(1/16)
+  const uint32_t kN64 = 0xD400D400u;   // half2(-64)
+  const uint32_t w8 = w >> 8;
+  const uint32_t e04 = hadd2(lop3_and_or(w, kM1, kMagic1024), kNeg1024);          // (e0, e4)
+  const uint32_t e15 = hfma2(lop3_and_or(w, kM2, kMagic1024), k116, kN64);        // (e1, e5)
+  const uint32_t e26 = hadd2(lop3_and_or(w8, kM1, kMagic1024), kNeg1024);         // (e2, e6)
+  const uint32_t e37 = hfma2(lop3_and_or(w8, kM2, kMagic1024), k116, kN64);       // (e3, e7)
+  acc = fhfma<0, 0>(e04, x01, acc);
+  acc = fhfma<0, 1>(e15, x01, acc);
+  acc = fhfma<0, 0>(e26, x23, acc);
+  acc = fhfma<0, 1>(e37, x23, acc);
+  acc = fhfma<1, 0>(e04, x45, acc);
+  acc = fhfma<1, 1>(e15, x45, acc);
+  acc = fhfma<1, 0>(e26, x67, acc);
+  acc = fhfma<1, 1>(e37, x67, acc);
+  return acc;
+}
+
+// Dot of one word of sixteen 2-bit codes (element j at bits 2j..2j+1) with
+// x[0..15] in eight half2 registers.  Masks pick elements (j, j+8).
+__device__ __forceinline__ float dot16_w2(uint32_t w, const uint32_t (&x)[8], float acc) {
+  const uint32_t w8 = w >> 8;
+  // scale constants: 1/4, 1/16, 1/64 and offsets -256, -64, -16 (exact fp16)
+  const uint32_t k14 = 0x34003400u, kN256 = 0xDC00DC00u;
+  const uint32_t k116 = 0x2C002C00u, kN64 = 0xD400D400u;
+  const uint32_t k164 = 0x24002400u, kN16 = 0xCC00CC00u;
+  const uint32_t a0 = hadd2(lop3_and_or(w, 0x00030003u, kMagic1024), kNeg1024);     // (e0, e8)
+  const uint32_t a1 = hfma2(lop3_and_or(w, 0x000C000Cu, kMagic1024), k14, kN256);  // (e1, e9)
+  const uint32_t a2 = hfma2(lop3_and_or(w, 0x00300030u, kMagic1024), k116, kN64);  // (e2, e10)
+  const uint32_t a3 = hfma2(lop3_and_or(w, 0x00C000C0u, kMagic1024), k164, kN16);  // (e3, e11)
+  const uint32_t b0 = hadd2(lop3_and_or(w8, 0x00030003u, kMagic1024), kNeg1024);    // (e4, e12)
+  const uint32_t b1 = hfma2(lop3_and_or(w8, 0x000C000Cu, kMagic1024), k14, kN256); // (e5, e13)
+  const uint32_t b2 = hfma2(lop3_and_or(w8, 0x00300030u, kMagic1024), k116, kN64); // (e6, e14)
+  const uint32_t b3 = hfma2(lop3_and_or(w8, 0x00C000C0u, kMagic1024), k164, kN16); // (e7, e15)
+  acc = fhfma<0, 0>(a0, x[0], acc);
+  acc = fhfma<0, 1>(a1, x[0], acc);
+  acc = fhfma<0, 0>(a2, x[1], acc);
+  acc = fhfma<0, 1>(a3, x[1], acc);
+  acc = fhfma<0, 0>(b0, x[2], acc);
+  acc = fhfma<0, 1>(b1, x[2], acc);
+  acc = fhfma<0, 0>(b2, x[3], acc);
+  acc = fhfma<0, 1>(b3, x[3], acc);
+  acc = fhfma<1, 0>(a0, x[4], acc);
+  acc = fhfma<1, 1>(a1, x[4], acc);
+  acc = fhfma<1, 0>(a2, x[5], acc);
+  acc = fhfma<1, 1>(a3, x[5], acc);
+  acc = fhfma<1, 0>(b0, x[6], acc);
+  acc = fhfma<1, 1>(b1, x[6], acc);
+  acc = fhfma<1, 0>(b2, x[7], acc);
+  acc = fhfma<1, 1>(b3, x[7], acc);
+  return acc;
+}
+
+// ---------------------------------------------------------------- tile regs
+template <int BITS>
+struct TileRegs {
+  uint4 codes[BITS == 4 ? 2 : 1];  // lane's 4 groups (W4: 2 planes x 16 B)
+  uint4 sz;                        // 4 x (s, z) half pairs
+  uint2 cols;                      // 4 x u16 (2c + swap)
+  uint4 seg;                       // tile row-start masks, one word per sub-tile
+  int m0;                          // row ordinal of the tile's first group
+};
+
+template <int BITS>
+__device__ __forceinline__ void load_tile(TileRegs<BITS>& r, const uint8_t* tile, int lane) {
+  r.codes[0] = ldg_stream128(tile + kTileHeaderBytes + lane * 16);
+  if (BITS == 4) r.codes[BITS == 4 ? 1 : 0] = ldg_stream128(tile + kTileHeaderBytes + 512 + lane * 16);
+  r.sz = ldg_stream128(tile + off_sz(BITS) + lane * 16);
+  r.cols = ldg_stream64(tile + off_cols(BITS) + lane * 8);
+  r.seg = ldg_stream128(tile);                 // broadcast within the warp
+  r.m0 = *reinterpret_cast<const int*>(tile + 16);
+}
+
+// Group code word(s) of slot u from the lane's codes.
+template <int BITS>
+__device__ __forceinline__ uint2 group_words(const TileRegs<BITS>& r, int u) {
+  if (BITS == 4) {
+    const uint4& c = r.codes[u >> 1];
+    return (u & 1) ? make_uint2(c.z, c.w) : make_uint2(c.x, c.y);
+  } else {
+    const uint4& c = r.codes[0];
+    const uint32_t w = u == 0 ? c.x : u == 1 ? c.y : u == 2 ? c.z : c.w;
+    return make_uint2(w, 0u);
+  }
+}
+
+// ---------------------------------------------------------------- kernel
+struct WarpRowState {
+  float carry[kMaxBatch];  // running sum of the open row
+  int ord;                 // row ordinal (into nzrow) of the open row
+  bool have;               // an open row exists
+  bool foreign;            // the open row started in an earlier warp's range
+};
+
+template <int B>
+__device__ __forceinline__ void store_row(const KParams& p, int ord, const float (&v)[kMaxBatch]) {
+  const int row = __ldg(p.nzrow + ord);
+  const float bias = p.bias ? __ldg(p.bias + row) : 0.f;
+#pragma unroll
+  for (int b = 0; b < B; ++b) p.Y[(int64_t)b * p.ldy + row] = v[b] + bias;
+}
+
+template <int B>
+__device__ __forceinline__ void publish(const KParams& p, int gw, const float (&v)[kMaxBatch],
+                                        uint32_t flag) {
+  uint32_t* rec = p.ws + (int64_t)gw * kWsWords;
+#pragma unroll
+  for (int b = 0; b < B; ++b) st_relaxed(rec + b, __float_as_uint(v[b]));
+  st_release(rec + kWsFlag, flag);
+}
+
+// Sum the partials published by warps gw+1, gw+2, ... until a CLOSED record
+// (deterministic warp order) into v, resetting each flag for the next call.
+template <int B>
+__device__ __forceinline__ void collect(const KParams& p, int gw, float (&v)[kMaxBatch]) {
+  for (int w = gw + 1; w < p.active_warps; ++w) {
+    uint32_t* rec = p.ws + (int64_t)w * kWsWords;
+    uint32_t f;
+    int spins = 0;
+    while ((f = ld_acquire(rec + kWsFlag)) == 0u) {
+      if (++spins > 8) __nanosleep(64);
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) v[b] += ld_relaxed_f32(rec + b);
+    st_relaxed(rec + kWsFlag, 0u);
+    if (f == kFlagClosed) break;
+  }
+}
+
+template <int BITS, int B, bool XSMEM>
+__device__ __forceinline__ void process_tile(const KParams& p, const TileRegs<BITS>& tr,
+                                             const uint8_t* __restrict__ xs,
+                                             const float* __restrict__ xc, int lane, int gw,
+                                             WarpRowState& st) {
+  // -------- per-group partials: part[u][b] = s * (sum_t q x - z * X_c)
+  float part[kPerLane][kMaxBatch];
+  const uint32_t colw[2] = {tr.cols.x, tr.cols.y};
+  const uint32_t szw[4] = {tr.sz.x, tr.sz.y, tr.sz.z, tr.sz.w};
+#pragma unroll
+  for (int u = 0; u < kPerLane; ++u) {
+    const uint32_t f = (colw[u >> 1] >> ((u & 1) * 16)) & 0xffffu;  // 2c + swap
+    const uint32_t xoff0 = f * 16u;         // = c*32 + swap*16 : first x chunk
+    const uint32_t xoff1 = xoff0 ^ 16u;     // second x chunk
+    const uint32_t c = f >> 1;
+    const uint2 w = group_words<BITS>(tr, u);
+    const __half2 sz = *reinterpret_cast<const __half2*>(&szw[u]);
+    const float s = __low2float(sz), z = __high2float(sz);
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const uint8_t* xb;
+      if (XSMEM) xb = xs + (size_t)b * (size_t)p.cols * 2;
+      else xb = reinterpret_cast<const uint8_t*>(p.X + (int64_t)b * p.ldx);
+      uint4 xa, xbv;
+      if (XSMEM) {
+        xa = *reinterpret_cast<const uint4*>(xb + xoff0);
+        xbv = *reinterpret_cast<const uint4*>(xb + xoff1);
+      } else {
+        xa = __ldg(reinterpret_cast<const uint4*>(xb + xoff0));
+        xbv = __ldg(reinterpret_cast<const uint4*>(xb + xoff1));
+      }
+      const float Xc = xc[(size_t)b * (p.cols / kGroup) + c];
+      float dot;
+      if (BITS == 4) {
+        // word 0 pairs with the first x chunk, word 1 with the second
+        float d0 = dot8_w4(w.x, xa.x, xa.y, xa.z, xa.w, 0.f);
+        float d1 = dot8_w4(w.y, xbv.x, xbv.y, xbv.z, xbv.w, 0.f);
+        dot = d0 + d1;
+      } else {
+        // 16-bit half h of the word holds elements of chunk h; the masks in
+        // dot16_w2 pair element j (low half) with element j+8 (high half).
+        const uint32_t xr[8] = {xa.x, xa.y, xa.z, xa.w, xbv.x, xbv.y, xbv.z, xbv.w};
+        dot = dot16_w2(w.x, xr, 0.f);
+      }
+      part[u][b] = s * fmaf(-z, Xc, dot);
+    }
+  }
+
+  // -------- segmented reduction per sub-tile (32 consecutive stream groups)
+  const uint32_t segw[4] = {tr.seg.x, tr.seg.y, tr.seg.z, tr.seg.w};
+  int base = tr.m0 - (int)(segw[0] & 1u);  // ordinal of the row before lane 0
+  const uint32_t le = 0xffffffffu >> (31 - lane);  // lanes 0..lane
+#pragma unroll
+  for (int u = 0; u < kPerLane; ++u) {
+    const uint32_t mask = segw[u];
+    // the open row closes when this sub-tile starts with a new row
+    if ((mask & 1u) && st.have) {
+      if (lane == 0) {
+        if (st.foreign) publish<B>(p, gw, st.carry, kFlagClosed);
+        else store_row<B>(p, st.ord, st.carry);
+      }
+      st.have = false;
+    }
+    const int s0 = 31 - __clz((mask | 1u) & le);  // this lane's segment start
+    float v[kMaxBatch];
+#pragma unroll
+    for (int b = 0; b < B; ++b) v[b] = part[u][b];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        const float n = __shfl_up_sync(0xffffffffu, v[b], d);
+        if (lane - d >= s0) v[b] += n;
+      }
+    }
+    const bool joins_carry = (s0 == 0) && !(mask & 1u) && st.have;
+    if (joins_carry) {
+#pragma unroll
+      for (int b = 0; b < B; ++b) v[b] = st.carry[b] + v[b];
+    }
+    const int ord = base + __popc(mask & le);
+    const bool tail = (lane == 31) || ((mask >> (lane + 1)) & 1u);
+    if (tail && lane != 31) {  // a row that ends inside this sub-tile
+      if (joins_carry && st.foreign) publish<B>(p, gw, v, kFlagClosed);
+      else store_row<B>(p, ord, v);
+    }
+    // lane 31's segment stays open: it becomes the carry
+    const bool foreign31 = __shfl_sync(0xffffffffu, (int)(joins_carry && st.foreign), 31) != 0;
+#pragma unroll
+    for (int b = 0; b < B; ++b) st.carry[b] = __shfl_sync(0xffffffffu, v[b], 31);
+    st.ord = __shfl_sync(0xffffffffu, ord, 31);
+    st.foreign = foreign31;
+    st.have = true;
+    base = st.ord;
+  }
+}
+
+template <int BITS, int B, bool XSMEM>
+__global__ void __launch_bounds__(kThreads) gqsa_streamk_kernel(KParams p) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int gw = blockIdx.x * kWarps + warp;
+
+  // ---- task-centric partition: contiguous tile range per warp (+-1 tile)
+  int t_begin = 0, t_end = 0;
+  if (gw < p.active_warps) {
+    const int q = p.num_tiles / p.active_warps, r = p.num_tiles % p.active_warps;
+    t_begin = gw * q + min(gw, r);
+    t_end = t_begin + q + (gw < r ? 1 : 0);
+  }
+  const uint8_t* tiles = p.tiles;
+  const int tb = tile_bytes(BITS);
+
+  // ---- prefetch the first tiles: weights never depend on the previous kernel
+  TileRegs<BITS> buf[kDepth];
+#pragma unroll
+  for (int i = 0; i < kDepth; ++i)
+    if (t_begin + i < t_end) load_tile<BITS>(buf[i], tiles + (int64_t)(t_begin + i) * tb, lane);
+  uint32_t next_seg0 = 1u;  // does the group after this warp's range start a row?
+  if (t_end > t_begin && t_end < p.num_tiles)
+    next_seg0 = __ldg(reinterpret_cast<const uint32_t*>(tiles + (int64_t)t_end * tb)) & 1u;
+
+  pdl_launch_dependents();
+  pdl_wait();  // x, y, bias and the workspace may belong to the previous kernel
+
+  // ---- stage activations and per-column-group sums in shared memory
+  const int KG = p.cols / kGroup;
+  uint8_t* xs = smem;
+  float* xc = reinterpret_cast<float*>(smem + (XSMEM ? (size_t)B * p.cols * 2 : 0));
+  if (XSMEM) {
+    const int n16 = p.cols / 8;  // uint4 per batch row
+    for (int i = threadIdx.x; i < B * n16; i += kThreads) {
+      const int b = i / n16, j = i - b * n16;
+      reinterpret_cast<uint4*>(xs)[i] =
+          __ldg(reinterpret_cast<const uint4*>(p.X + (int64_t)b * p.ldx) + j);
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < B * KG; i += kThreads) {
+    const int b = i / KG, c = i - b * KG;
+    uint4 v0, v1;
+    if (XSMEM) {
+      v0 = reinterpret_cast<const uint4*>(xs + (size_t)b * p.cols * 2)[2 * c];
+      v1 = reinterpret_cast<const uint4*>(xs + (size_t)b * p.cols * 2)[2 * c + 1];
+    } else {
+      v0 = __ldg(reinterpret_cast<const uint4*>(p.X + (int64_t)b * p.ldx) + 2 * c);
+      v1 = __ldg(reinterpret_cast<const uint4*>(p.X + (int64_t)b * p.ldx) + 2 * c + 1);
+    }
+    const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {  // t = 0..15 in order
+      const __half2 h = *reinterpret_cast<const __half2*>(&w[k]);
+      acc += __low2float(h);
+      acc += __high2float(h);
+    }
+    xc[i] = acc;
+  }
+  __syncthreads();
+
+  // ---- empty rows get bias (or 0): grid-stride over the empty-row list
+  for (int i = blockIdx.x * kThreads + threadIdx.x; i < p.n_empty; i += gridDim.x * kThreads) {
+    const int row = __ldg(p.empty + i);
+    const float bias = p.bias ? __ldg(p.bias + row) : 0.f;
+#pragma unroll
+    for (int b = 0; b < B; ++b) p.Y[(int64_t)b * p.ldy + row] = bias;
+  }
+  if (t_end <= t_begin) return;
+
+  // ---- stream the warp's tile range
+  WarpRowState st;
+#pragma unroll
+  for (int b = 0; b < kMaxBatch; ++b) st.carry[b] = 0.f;
+  st.have = !(buf[0].seg.x & 1u);  // the range starts inside a row owned by an earlier warp
+  st.foreign = st.have;
+  st.ord = buf[0].m0;
+
+  for (int t0 = t_begin; t0 < t_end; t0 += kDepth) {
+#pragma unroll
+    for (int i = 0; i < kDepth; ++i) {
+      const int t = t0 + i;
+      if (t < t_end) {
+        process_tile<BITS, B, XSMEM>(p, buf[i], xs, xc, lane, gw, st);
+        if (t + kDepth < t_end) load_tile<BITS>(buf[i], tiles + (int64_t)(t + kDepth) * tb, lane);
+      }
+    }
+  }
+
+  // ---- the open row at the end of the range
+  if (next_seg0) {  // it ends exactly here
+    if (lane == 0) {
+      if (st.foreign) publish<B>(p, gw, st.carry, kFlagClosed);
+      else store_row<B>(p, st.ord, st.carry);
+    }
+  } else if (st.foreign) {  // the whole range lies inside a row owned upstream
+    if (lane == 0) publish<B>(p, gw, st.carry, kFlagOpen);
+  } else {  // owner of a row that continues downstream: collect, then store
+    if (lane == 0) {
+      collect<B>(p, gw, st.carry);
+      store_row<B>(p, st.ord, st.carry);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- launchers
+template <int BITS, int B, bool XSMEM>
+const void* kernel_ptr() {
+  return reinterpret_cast<const void*>(&gqsa_streamk_kernel<BITS, B, XSMEM>);
+}
+
+#define GQSA_KSEL(BITS, XS)                                                              \
+  switch (B) {                                                                         \
+    case 1: return kernel_ptr<BITS, 1, XS>();                                          \
+    case 2: return kernel_ptr<BITS, 2, XS>();                                          \
+    case 3: return kernel_ptr<BITS, 3, XS>();                                          \
+    case 4: return kernel_ptr<BITS, 4, XS>();                                          \
+    case 5: return kernel_ptr<BITS, 5, XS>();                                          \
+    case 6: return kernel_ptr<BITS, 6, XS>();                                          \
+    case 7: return kernel_ptr<BITS, 7, XS>();                                          \
+    case 8: return kernel_ptr<BITS, 8, XS>();                                          \
+    default: return nullptr;                                                           \
+  }
+
+const void* select_kernel(int bits, int B, bool xsmem) {
+  if (bits == 4) {
+    if (xsmem) { GQSA_KSEL(4, true) } else { GQSA_KSEL(4, false) }
+  } else if (bits == 2) {
+    if (xsmem) { GQSA_KSEL(2, true) } else { GQSA_KSEL(2, false) }
+  }
+  return nullptr;
+}
+
+}  // namespace gqsa

@@ -1,0 +1,265 @@
+"""Thin ctypes binding of libgqsa.so (include/gqsa.h) -- argument marshalling only.
+
+Every step of the hot path runs in the library's sm_100a kernels; PyTorch only
+provides device memory and streams.  If the shared library is missing the
+import of any entry point raises: there is no CPU fallback.
+
+Names follow the C ABI: :func:`pack`, :func:`unpack`, :func:`read_desc`,
+:func:`workspace_size`, :func:`gemv`, :func:`gemm_smallbatch`,
+:func:`gemm_hostio`, plus :class:`Layer`, a device-resident packed layer.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libgqsa.so")
+
+GQSA_OK = 0
+_STATUS = {0: "ok", -1: "shape", -2: "validation", -3: "unsupported", -4: "buffer", -5: "cuda"}
+
+
+class GQSAError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        super().__init__(f"{what}: {status_string(status)} ({status})")
+        self.status = status
+
+
+class BSR(ctypes.Structure):
+    _fields_ = [
+        ("rows", ctypes.c_int32), ("cols", ctypes.c_int32),
+        ("group_size", ctypes.c_int32), ("bits", ctypes.c_int32),
+        ("nnzg", ctypes.c_int64),
+        ("row_index", ctypes.c_void_p), ("group_cols", ctypes.c_void_p),
+        ("codes", ctypes.c_void_p), ("scales_f16", ctypes.c_void_p),
+        ("zeros_f16", ctypes.c_void_p),
+    ]
+
+
+class Desc(ctypes.Structure):
+    _fields_ = [
+        ("magic", ctypes.c_uint32), ("version", ctypes.c_uint32),
+        ("rows", ctypes.c_int32), ("cols", ctypes.c_int32),
+        ("group_size", ctypes.c_int32), ("bits", ctypes.c_int32),
+        ("nnzg", ctypes.c_int64),
+        ("tile_groups", ctypes.c_int32), ("num_tiles", ctypes.c_int32),
+        ("n_nzrows", ctypes.c_int32), ("n_empty", ctypes.c_int32),
+        ("tile_bytes", ctypes.c_int32), ("flags", ctypes.c_int32),
+        ("row_begin", ctypes.c_int32), ("row_end", ctypes.c_int32),
+        ("off_row_index", ctypes.c_uint64), ("off_nzrow", ctypes.c_uint64),
+        ("off_empty", ctypes.c_uint64), ("off_tiles", ctypes.c_uint64),
+        ("blob_bytes", ctypes.c_uint64),
+    ]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class Plan(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_int32) for k in
+                ("grid", "warps_per_cta", "active_warps", "num_tiles", "smem_bytes", "x_in_smem")]
+
+
+EXPORTS = (
+    "gqsa_pack_size", "gqsa_pack", "gqsa_read_desc", "gqsa_unpack", "gqsa_workspace_size",
+    "gqsa_gemv", "gqsa_gemm_smallbatch", "gqsa_hostio_stage_size", "gqsa_gemm_hostio",
+    "gqsa_launch_plan", "gqsa_launch_count", "gqsa_status_string", "gqsa_version",
+)
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libgqsa.so (raises if it has not been built -- no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: build it with `make` or __graft_entry__.build()")
+    L = ctypes.CDLL(LIB_PATH)
+    P, I32, I64, SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+    PSZ = ctypes.POINTER(ctypes.c_size_t)
+    L.gqsa_pack_size.argtypes = [ctypes.POINTER(BSR), I32, I32, PSZ]
+    L.gqsa_pack.argtypes = [ctypes.POINTER(BSR), I32, I32, P, SZ, ctypes.POINTER(Desc)]
+    L.gqsa_read_desc.argtypes = [P, SZ, ctypes.POINTER(Desc)]
+    L.gqsa_unpack.argtypes = [P, SZ, ctypes.POINTER(BSR)]
+    L.gqsa_workspace_size.argtypes = [ctypes.POINTER(Desc), I32, PSZ]
+    L.gqsa_gemv.argtypes = [ctypes.POINTER(Desc), P, P, P, P, P, SZ, P]
+    L.gqsa_gemm_smallbatch.argtypes = [ctypes.POINTER(Desc), P, P, I32, I64, P, I64, P, P, SZ, P]
+    L.gqsa_hostio_stage_size.argtypes = [ctypes.POINTER(Desc), I32, PSZ]
+    L.gqsa_gemm_hostio.argtypes = [ctypes.POINTER(Desc), P, P, I32, P, P, P, SZ, P, SZ, P]
+    L.gqsa_launch_plan.argtypes = [ctypes.POINTER(Desc), I32, ctypes.POINTER(Plan)]
+    L.gqsa_launch_count.restype = ctypes.c_uint64
+    L.gqsa_status_string.restype = ctypes.c_char_p
+    L.gqsa_status_string.argtypes = [ctypes.c_int]
+    for name in EXPORTS:
+        if name not in ("gqsa_launch_count", "gqsa_status_string"):
+            getattr(L, name).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def status_string(status: int) -> str:
+    return lib().gqsa_status_string(int(status)).decode()
+
+
+def _check(st: int, what: str) -> None:
+    if st != GQSA_OK:
+        raise GQSAError(st, what)
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data if a.size else 0
+
+
+def _bsr_struct(bsr: dict, keep: list) -> BSR:
+    arrs = {
+        "row_index": np.ascontiguousarray(bsr["row_index"], dtype=np.int32),
+        "group_cols": np.ascontiguousarray(bsr["group_cols"], dtype=np.uint16),
+        "codes": np.ascontiguousarray(bsr["codes"], dtype=np.uint8),
+        "scales_f16": np.ascontiguousarray(bsr["scales_f16"], dtype=np.uint16),
+        "zeros_f16": np.ascontiguousarray(bsr["zeros_f16"], dtype=np.uint16),
+    }
+    keep.append(arrs)
+    return BSR(int(bsr["rows"]), int(bsr["cols"]), int(bsr["group_size"]), int(bsr["bits"]),
+               int(np.asarray(bsr["group_cols"]).size),
+               _ptr(arrs["row_index"]), _ptr(arrs["group_cols"]), _ptr(arrs["codes"]),
+               _ptr(arrs["scales_f16"]), _ptr(arrs["zeros_f16"]))
+
+
+def pack(bsr: dict, row_begin: int = 0, row_end: Optional[int] = None):
+    """gqsa_pack: plain BSR (host) -> (blob uint8 ndarray, Desc)."""
+    L = lib()
+    keep: list = []
+    b = _bsr_struct(bsr, keep)
+    row_end = int(bsr["rows"]) if row_end is None else int(row_end)
+    n = ctypes.c_size_t(0)
+    _check(L.gqsa_pack_size(ctypes.byref(b), int(row_begin), row_end, ctypes.byref(n)), "gqsa_pack_size")
+    blob = np.empty(n.value, dtype=np.uint8)
+    d = Desc()
+    _check(L.gqsa_pack(ctypes.byref(b), int(row_begin), row_end, _ptr(blob), n.value, ctypes.byref(d)),
+           "gqsa_pack")
+    return blob, d
+
+
+def read_desc(blob: np.ndarray) -> Desc:
+    d = Desc()
+    blob = np.ascontiguousarray(blob, dtype=np.uint8)
+    _check(lib().gqsa_read_desc(_ptr(blob), blob.size, ctypes.byref(d)), "gqsa_read_desc")
+    return d
+
+
+def unpack(blob: np.ndarray) -> dict:
+    """gqsa_unpack: blob -> plain BSR dict (numpy arrays)."""
+    blob = np.ascontiguousarray(blob, dtype=np.uint8)
+    d = read_desc(blob)
+    G, n = d.group_size, d.bits
+    out = {
+        "rows": d.rows, "cols": d.cols, "group_size": G, "bits": n, "nnzg": d.nnzg,
+        "row_index": np.zeros(d.rows + 1, np.int32),
+        "group_cols": np.zeros(d.nnzg, np.uint16),
+        "codes": np.zeros((d.nnzg * G * n + 7) // 8, np.uint8),
+        "scales_f16": np.zeros(d.nnzg, np.uint16),
+        "zeros_f16": np.zeros(d.nnzg, np.uint16),
+    }
+    b = BSR(0, 0, 0, 0, 0, _ptr(out["row_index"]), _ptr(out["group_cols"]), _ptr(out["codes"]),
+            _ptr(out["scales_f16"]), _ptr(out["zeros_f16"]))
+    _check(lib().gqsa_unpack(_ptr(blob), blob.size, ctypes.byref(b)), "gqsa_unpack")
+    return out
+
+
+def workspace_size(desc: Desc, batch: int = 1) -> int:
+    n = ctypes.c_size_t(0)
+    _check(lib().gqsa_workspace_size(ctypes.byref(desc), int(batch), ctypes.byref(n)), "gqsa_workspace_size")
+    return n.value
+
+
+def hostio_stage_size(desc: Desc, batch: int = 1) -> int:
+    n = ctypes.c_size_t(0)
+    _check(lib().gqsa_hostio_stage_size(ctypes.byref(desc), int(batch), ctypes.byref(n)),
+           "gqsa_hostio_stage_size")
+    return n.value
+
+
+def launch_plan(desc: Desc, batch: int = 1) -> Plan:
+    p = Plan()
+    _check(lib().gqsa_launch_plan(ctypes.byref(desc), int(batch), ctypes.byref(p)), "gqsa_launch_plan")
+    return p
+
+
+def launch_count() -> int:
+    return int(lib().gqsa_launch_count())
+
+
+def _stream_ptr(stream) -> int:
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return int(s.cuda_stream)
+
+
+def gemv(desc: Desc, d_blob, x, y, bias=None, ws=None, stream=None) -> None:
+    """gqsa_gemv on torch CUDA tensors: x fp16 [K], y fp32 [N], ws uint8."""
+    _check(lib().gqsa_gemv(ctypes.byref(desc), d_blob.data_ptr(), x.data_ptr(), y.data_ptr(),
+                           bias.data_ptr() if bias is not None else None, ws.data_ptr(), ws.numel(),
+                           _stream_ptr(stream)), "gqsa_gemv")
+
+
+def gemm_smallbatch(desc: Desc, d_blob, X, Y, bias=None, ws=None, stream=None) -> None:
+    """gqsa_gemm_smallbatch on torch CUDA tensors: X fp16 [B][ldx], Y fp32 [B][ldy]."""
+    B = X.shape[0]
+    _check(lib().gqsa_gemm_smallbatch(ctypes.byref(desc), d_blob.data_ptr(), X.data_ptr(), B,
+                                      X.stride(0), Y.data_ptr(), Y.stride(0),
+                                      bias.data_ptr() if bias is not None else None,
+                                      ws.data_ptr(), ws.numel(), _stream_ptr(stream)),
+           "gqsa_gemm_smallbatch")
+
+
+def gemm_hostio(desc: Desc, d_blob, h_X, h_Y, stage, ws, bias=None, stream=None) -> None:
+    """gqsa_gemm_hostio: host (ideally pinned) X fp16 [B][K] and Y fp32 [B][N]."""
+    B = h_X.shape[0]
+    _check(lib().gqsa_gemm_hostio(ctypes.byref(desc), d_blob.data_ptr(), h_X.data_ptr(), B,
+                                  h_Y.data_ptr(), bias.data_ptr() if bias is not None else None,
+                                  stage.data_ptr(), stage.numel(), ws.data_ptr(), ws.numel(),
+                                  _stream_ptr(stream)), "gqsa_gemm_hostio")
+
+
+class Layer:
+    """A packed GQSA layer resident on a CUDA device, with its own workspace.
+
+    ``Layer(bsr)`` packs on the host (C++), copies the blob to the device once
+    (offline, not part of the hot path) and allocates a zeroed workspace.
+    """
+
+    def __init__(self, bsr: Optional[dict] = None, blob: Optional[np.ndarray] = None,
+                 row_begin: int = 0, row_end: Optional[int] = None, device=None,
+                 max_batch: int = 8):
+        import torch
+        if blob is None:
+            blob, desc = pack(bsr, row_begin, row_end)
+        else:
+            desc = read_desc(blob)
+        self.desc = desc
+        self.host_blob = blob
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.device = dev
+        self.blob = torch.from_numpy(blob).to(dev)  # caching allocator: >= 512-B aligned
+        self.ws = torch.zeros(workspace_size(desc, max_batch), dtype=torch.uint8, device=dev)
+        self.rows, self.cols = desc.rows, desc.cols
+
+    def gemv(self, x, y=None, bias=None, stream=None):
+        import torch
+        if y is None:
+            y = torch.empty(self.rows, dtype=torch.float32, device=self.device)
+        gemv(self.desc, self.blob, x, y, bias, self.ws, stream)
+        return y
+
+    def gemm(self, X, Y=None, bias=None, stream=None):
+        import torch
+        if Y is None:
+            Y = torch.empty(X.shape[0], self.rows, dtype=torch.float32, device=self.device)
+        gemm_smallbatch(self.desc, self.blob, X, Y, bias, self.ws, stream)
+        return Y

@@ -1,0 +1,187 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the fp64 oracle on
+the same seeded inputs.  Bit-exact in exact-integer and one-hot modes,
+tolerance gates G1/G2/G3 (tests/parity.py) otherwise."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import gqsa_oracle as O
+from paper_2412_17560_b200 import gqsa, synth
+from tests.parity import abs_bound, check_gates
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    torch.cuda.init()
+
+
+def run(bsr, xbits, bias=None, layer=None, **kw):
+    """Pack, upload, run gqsa_gemm_smallbatch (B = rows of x), return y [B][N] float32."""
+    L = layer or gqsa.Layer(bsr)
+    X = torch.from_numpy(np.ascontiguousarray(xbits)).view(torch.float16).cuda()
+    if X.ndim == 1:
+        X = X[None]
+    b = None if bias is None else torch.from_numpy(bias).cuda()
+    if X.shape[0] == 1 and not kw.get("force_gemm"):
+        y = L.gemv(X[0], bias=b)[None]
+    else:
+        y = L.gemm(X, bias=b)
+    torch.cuda.synchronize()
+    assert int(L.ws.count_nonzero()) == 0, "workspace must be left zeroed"
+    return y.cpu().numpy()
+
+
+# ------------------------------------------------------------------ paper fixture
+def test_paper_fixture_embedded_g16():
+    """PAPER.md:95-101 listing (tests/golden/paper_fig3.json) embedded in G=16:
+    each 4-wide group sits in the first 4 slots of a 16-wide group whose other
+    codes equal z (dequantize to exactly 0).  y must equal the paper-derived
+    values exactly."""
+    fx = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_fig3.json")))
+    codes = np.array(fx["codes"]).reshape(-1, 4)
+    z = np.array(fx["zeros"])
+    full = np.repeat(z[:, None], 16, 1).astype(np.int64)
+    full[:, :4] = codes
+    keep = np.zeros((4, 2), bool)
+    ri = fx["row_index"]
+    for r in range(4):
+        for g in range(ri[r], ri[r + 1]):
+            keep[r, fx["group_cols"][g]] = True
+    bsr = synth.bsr_from_parts(4, 32, 16, 4, keep, full, np.array(fx["scales"]), z)
+    for case in fx["cases"]:
+        x = np.zeros(32)
+        for j, v in enumerate(case["x"]):
+            x[(j // 4) * 16 + j % 4] = v
+        x[4:16] = 7.0  # multiplied by exact zeros
+        x[20:32] = -3.0
+        y = run(bsr, x.astype(np.float16).view(np.uint16))[0]
+        assert list(y) == [float(v) for v in case["y"]]
+
+
+# ------------------------------------------------------------------ exact modes
+EXACT_CASES = [
+    # rows, cols, bits, sparsity, mask, B
+    (256, 256, 4, 0.5, "uniform", 1),
+    (256, 256, 2, 0.5, "uniform", 1),
+    (1024, 4096, 4, 0.5, "uniform", 1),
+    (1024, 4096, 2, 0.5, "uniform", 3),
+    (512, 2048, 4, 0.5, "skewed", 1),
+    (300, 1024, 4, 0.3, "row_balanced", 4),
+    (77, 208, 4, 0.2, "uniform", 8),      # ragged tile tail, odd rows
+    (3, 16384, 4, 0.5, "uniform", 2),     # few long rows: rows span many warps
+    (1, 65536, 4, 0.5, "uniform", 1),     # one row across every warp (chained fix-up)
+    (4096, 16, 4, 0.5, "uniform", 1),     # K = G: many empty rows, 1-group rows
+    (5, 64, 4, 0.5, "uniform", 1),        # nnzg < one tile
+    (640, 512, 2, 0.9, "uniform", 5),     # mostly-empty rows
+    (2048, 28672, 4, 0.5, "uniform", 4),  # K too large for x in smem at B=4
+]
+
+
+@pytest.mark.parametrize("rows,cols,bits,sp,mask,B", EXACT_CASES)
+def test_exact_integer_mode_bit_exact(rows, cols, bits, sp, mask, B):
+    seed = synth.seed_for(f"exact/{rows}/{cols}/{bits}/{sp}/{mask}/{B}")
+    bsr = synth.make_layer(seed, rows, cols, bits=bits, sparsity=sp, mask=mask, mode="exact_int")
+    x = synth.make_x(seed + 1, B, cols, mode="exact_int")
+    y = run(bsr, x)
+    ref = O.gemv(bsr, x)
+    assert np.array_equal(y.astype(np.float64), ref), np.argwhere(y != ref)[:5]
+
+
+def test_empty_layer_and_bias():
+    bsr = synth.make_layer(5, 100, 64, sparsity=1.0)
+    bias = np.linspace(-1, 1, 100).astype(np.float32)
+    y = run(bsr, synth.make_x(6, 1, 64), bias=bias)[0]
+    assert np.array_equal(y, bias)
+    bsr = synth.make_layer(7, 333, 512, sparsity=0.5, mask="skewed", mode="exact_int")
+    x = synth.make_x(8, 2, 512, mode="exact_int")
+    bias = np.arange(333, dtype=np.float32) * 0.5
+    assert np.array_equal(run(bsr, x, bias=bias).astype(np.float64), O.gemv(bsr, x, bias=bias))
+
+
+@pytest.mark.parametrize("bits", [4, 2])
+def test_onehot_columns_exact(bits):
+    """x = e_j: y = W_hat[:, j] exactly (z multiple of 1/128, |z| < 16)."""
+    bsr = synth.make_layer(21 + bits, 512, 1024, bits=bits, sparsity=0.5, mode="onehot_safe")
+    W = O.decompress(bsr)
+    L = gqsa.Layer(bsr)
+    x = synth.make_x(31, 8, 1024, mode="onehot")
+    y = run(bsr, x, layer=L)
+    cols = np.argmax(x.view(np.float16) != 0, axis=1)
+    for b in range(8):
+        assert np.array_equal(y[b].astype(np.float64), W[:, cols[b]])
+
+
+# ------------------------------------------------------------------ realistic
+REAL_CASES = [
+    (4096, 4096, 4, 0.5, "uniform", 1),
+    (1024, 4096, 4, 0.5, "uniform", 2),
+    (4096, 4096, 2, 0.5, "uniform", 1),
+    (4096, 4096, 4, 0.3, "uniform", 8),
+    (2048, 5120, 4, 0.5, "row_balanced", 4),
+    (1024, 2048, 4, 0.5, "skewed", 1),
+]
+
+
+@pytest.mark.parametrize("rows,cols,bits,sp,mask,B", REAL_CASES)
+def test_realistic_tolerance_gates(rows, cols, bits, sp, mask, B):
+    seed = synth.seed_for(f"real/{rows}/{cols}/{bits}/{sp}/{mask}/{B}")
+    bsr = synth.make_layer(seed, rows, cols, bits=bits, sparsity=sp, mask=mask)
+    x = synth.make_x(seed + 1, B, cols)
+    y = run(bsr, x)
+    check_gates(y, O.gemv(bsr, x), abs_bound(bsr, x), f"{rows}x{cols} W{bits} S{sp} {mask} B{B}")
+
+
+def test_determinism_and_batch_consistency():
+    bsr = synth.make_layer(41, 4096, 4096, sparsity=0.5)
+    x = synth.make_x(42, 4, 4096)
+    L = gqsa.Layer(bsr)
+    first = run(bsr, x, layer=L)
+    for _ in range(20):
+        assert np.array_equal(run(bsr, x, layer=L), first)
+    # the batch-1 GEMV equals row 0 of the batched GEMM bit for bit (same order)
+    assert np.array_equal(run(bsr, x[:1], layer=L)[0], first[0])
+
+
+def test_hostio_end_to_end_path():
+    bsr = synth.make_layer(51, 1024, 2048, sparsity=0.5, mode="exact_int")
+    x = synth.make_x(52, 3, 2048, mode="exact_int")
+    L = gqsa.Layer(bsr)
+    hX = torch.from_numpy(x).view(torch.float16).pin_memory()
+    hY = torch.empty(3, 1024, dtype=torch.float32).pin_memory()
+    stage = torch.empty(gqsa.hostio_stage_size(L.desc, 3), dtype=torch.uint8, device="cuda")
+    n0 = gqsa.launch_count()
+    gqsa.gemm_hostio(L.desc, L.blob, hX, hY, stage, L.ws)
+    torch.cuda.synchronize()
+    assert gqsa.launch_count() == n0 + 1
+    assert np.array_equal(hY.numpy().astype(np.float64), O.gemv(bsr, x))
+
+
+def test_argument_errors():
+    bsr = synth.make_layer(61, 64, 256, sparsity=0.5)
+    L = gqsa.Layer(bsr)
+    X = torch.zeros(9, 256, dtype=torch.float16, device="cuda")
+    with pytest.raises(gqsa.GQSAError) as e:
+        L.gemm(X)  # B = 9 > 8
+    assert e.value.status == -1
+    small = torch.zeros(8, dtype=torch.uint8, device="cuda")
+    with pytest.raises(gqsa.GQSAError) as e:
+        gqsa.gemv(L.desc, L.blob, X[0], torch.empty(64, device="cuda"), None, small)
+    assert e.value.status == -4
+    with pytest.raises(gqsa.GQSAError) as e:  # misaligned x
+        gqsa.gemv(L.desc, L.blob, X.view(-1)[1:257], torch.empty(64, device="cuda"), None, L.ws)
+    assert e.value.status == -4
+
+
+def test_launch_plan_is_persistent_stream_k():
+    bsr = synth.make_layer(71, 14336, 4096, sparsity=0.5)
+    _, d = gqsa.pack(bsr)
+    p = gqsa.launch_plan(d, 1)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    assert p.active_warps == min(d.num_tiles, p.grid * p.warps_per_cta)
+    assert p.grid <= 2 * sms and p.x_in_smem == 1

@@ -1,0 +1,154 @@
+"""Host-side boundary tests (CPU): the C-ABI library loads and exports every
+symbol include/gqsa.h declares; gqsa_pack / gqsa_unpack round-trip bit-exactly;
+the C++ packer's bytes equal the independent Python LAYOUT implementation;
+validation rejects malformed BSR with the documented status."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle.layout_reference import pack_reference
+from paper_2412_17560_b200 import gqsa, synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_functions():
+    src = open(os.path.join(ROOT, "include", "gqsa.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(gqsa_\w+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol():
+    names = _header_functions()
+    assert "gqsa_gemv" in names and "gqsa_pack" in names and "gqsa_gemm_smallbatch" in names
+    L = gqsa.lib()
+    for n in names:
+        assert hasattr(L, n), n
+    out = subprocess.run(["nm", "-D", "--defined-only", gqsa.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (gqsa_\w+)", out))
+    assert set(names) <= exported
+    assert set(gqsa.EXPORTS) == set(names)
+    assert gqsa.lib().gqsa_version() == 1
+    assert gqsa.status_string(-2) == "validation error"
+
+
+def _eq_bsr(a, b):
+    for k in ("rows", "cols", "group_size", "bits"):
+        assert int(a[k]) == int(b[k]), k
+    for k in ("row_index", "group_cols", "codes", "scales_f16", "zeros_f16"):
+        assert np.array_equal(np.asarray(a[k]), np.asarray(b[k])), k
+
+
+CASES = [
+    # rows, cols, bits, sparsity, mask, seed
+    (256, 256, 4, 0.5, "uniform", 1),
+    (256, 256, 2, 0.5, "uniform", 2),
+    (64, 512, 4, 0.5, "skewed", 3),       # half the rows empty
+    (37, 208, 4, 0.3, "row_balanced", 4),  # ragged last tile, odd rows
+    (5, 16, 4, 0.0, "uniform", 5),         # K = G: one group per row
+    (300, 32, 2, 0.8, "uniform", 6),       # many empty rows, tiny rows
+    (8, 64, 4, 1.0, "uniform", 7),         # nnzg = 0
+    (1, 4096, 4, 0.5, "uniform", 8),       # all groups in one row
+]
+
+
+@pytest.mark.parametrize("rows,cols,bits,sp,mask,seed", CASES)
+def test_roundtrip_and_reference_bytes(rows, cols, bits, sp, mask, seed):
+    bsr = synth.make_layer(seed, rows, cols, bits=bits, sparsity=sp, mask=mask)
+    blob, desc = gqsa.pack(bsr)
+    assert desc.blob_bytes == blob.size and desc.nnzg == bsr["nnzg"]
+    assert bytes(blob) == pack_reference(bsr)
+    _eq_bsr(gqsa.unpack(blob), bsr)
+
+
+def test_shard_ranges_rebase_and_reassemble():
+    bsr = synth.make_layer(9, 96, 256, sparsity=0.5, mask="skewed")
+    world = 4
+    parts = []
+    for r in range(world):
+        lo, hi = synth.shard_rows(96, world, r)
+        blob, d = gqsa.pack(bsr, lo, hi)
+        assert (d.row_begin, d.row_end, d.rows) == (lo, hi, hi - lo)
+        assert bytes(blob) == pack_reference(bsr, lo, hi)
+        sh = gqsa.unpack(blob)
+        _eq_bsr(sh, synth.slice_rows(bsr, lo, hi))
+        parts.append(sh)
+    # concatenating the shards reproduces the layer
+    assert np.array_equal(np.concatenate([p["group_cols"] for p in parts]), bsr["group_cols"])
+    offs = np.concatenate([[0], np.cumsum([p["nnzg"] for p in parts])])
+    ri = np.concatenate([parts[0]["row_index"][:1]] + [p["row_index"][1:] + offs[i] for i, p in enumerate(parts)])
+    assert np.array_equal(ri, bsr["row_index"])
+
+
+def test_tile_fields_match_layout():
+    """Spot-check the documented tile fields directly."""
+    bsr = synth.make_layer(10, 64, 1024, sparsity=0.5)
+    blob, d = gqsa.pack(bsr)
+    assert d.tile_bytes == 1824 and d.num_tiles == -(-bsr["nnzg"] // 128)
+    t0 = blob[d.off_tiles:d.off_tiles + d.tile_bytes]
+    seg = t0[:16].view(np.uint32)
+    assert seg[0] & 1  # first group starts row 0
+    cols = t0[32 + 1024 + 512:].view(np.uint16)
+    # lane l, slot u -> stream position u*32+l; field = 2c + (l & 1)
+    for lane in range(32):
+        for u in range(4):
+            f = int(cols[lane * 4 + u])
+            assert f & 1 == lane & 1
+            assert f >> 1 == int(bsr["group_cols"][u * 32 + lane])
+
+
+def test_validation_errors():
+    bsr = synth.make_layer(11, 16, 128, sparsity=0.5)
+    with pytest.raises(gqsa.GQSAError) as e:
+        bad = dict(bsr, row_index=bsr["row_index"].copy())
+        bad["row_index"][5] = bad["row_index"][6] + 1  # non-monotone
+        gqsa.pack(bad)
+    assert e.value.status == -2
+    bad = dict(bsr, group_cols=bsr["group_cols"].copy())
+    bad["group_cols"][0] = 200  # >= K/G
+    with pytest.raises(gqsa.GQSAError) as e:
+        gqsa.pack(bad)
+    assert e.value.status == -2
+    bad = dict(bsr, scales_f16=bsr["scales_f16"].copy())
+    bad["scales_f16"][3] = 0x7C00  # +inf scale
+    with pytest.raises(gqsa.GQSAError) as e:
+        gqsa.pack(bad)
+    assert e.value.status == -2
+    bad = dict(bsr, zeros_f16=bsr["zeros_f16"].copy())
+    bad["zeros_f16"][3] = 0x7E00  # NaN zero
+    with pytest.raises(gqsa.GQSAError):
+        gqsa.pack(bad)
+    bad = dict(bsr, bits=3)
+    with pytest.raises(gqsa.GQSAError) as e:
+        gqsa.pack(bad)
+    assert e.value.status == -3
+    with pytest.raises(gqsa.GQSAError) as e:
+        gqsa.pack(bsr, 5, 3)
+    assert e.value.status == -1
+
+
+def test_read_desc_rejects_corruption():
+    bsr = synth.make_layer(12, 16, 128, sparsity=0.5)
+    blob, _ = gqsa.pack(bsr)
+    for off, val in ((0, 0x00), (4, 0x07), (36, 0x7F)):
+        b = blob.copy()
+        b[off] = val
+        with pytest.raises(gqsa.GQSAError):
+            gqsa.read_desc(b)
+    with pytest.raises(gqsa.GQSAError):
+        gqsa.read_desc(blob[:blob.size - 256])
+    # a flipped row-start bit is caught by unpack's consistency checks
+    d = gqsa.read_desc(blob)
+    b = blob.copy()
+    b[d.off_tiles] ^= 0x01
+    with pytest.raises(gqsa.GQSAError):
+        gqsa.unpack(b)
+
+
+def test_workspace_size_is_device_independent():
+    bsr = synth.make_layer(13, 4096, 4096, sparsity=0.5)
+    _, d = gqsa.pack(bsr)
+    assert gqsa.workspace_size(d, 1) == gqsa.workspace_size(d, 8) == 4096 * 64
