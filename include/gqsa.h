@@ -20,7 +20,8 @@
  * never allocates or frees device memory and keeps no pointer past a call.
  * A packed blob is immutable and may be shared by concurrent calls on
  * different streams, each with its OWN workspace.  A workspace
- * must be zero-filled once when allocated; every call leaves it zeroed again.
+ * must be zero-filled once when allocated; every call returns each 64-B
+ * record's flag word to zero (the partial-sum words are scratch).
  *
  * Errors: every int-returning function returns GQSA_OK (0) or a negative
  * gqsa_status_t.  Errors raised during asynchronous device execution surface

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -47,6 +48,16 @@ size_t smem_for(const gqsa_desc_t* d, int B, bool* xsmem) {
   return *xsmem ? xb + xc : xc;
 }
 
+// Upper bound on resident CTAs per SM (tuning knob: GQSA_CTAS_PER_SM).
+int ctas_per_sm_cap() {
+  static int cap = [] {
+    const char* e = std::getenv("GQSA_CTAS_PER_SM");
+    const int v = e ? std::atoi(e) : kMaxCtasPerSm;
+    return v >= 1 && v <= 8 ? v : kMaxCtasPerSm;
+  }();
+  return cap;
+}
+
 // Fill the launch plan; returns a status.
 int make_plan(const gqsa_desc_t* d, int B, gqsa_plan_t* pl, const void** kfn) {
   int dev = 0;
@@ -71,7 +82,7 @@ int make_plan(const gqsa_desc_t* d, int B, gqsa_plan_t* pl, const void** kfn) {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem) != cudaSuccess)
     return GQSA_ERR_CUDA;
   if (occ < 1) return GQSA_ERR_UNSUPPORTED;
-  if (occ > kMaxCtasPerSm) occ = kMaxCtasPerSm;
+  if (occ > ctas_per_sm_cap()) occ = ctas_per_sm_cap();
   int warps = sms * occ * kWarps;
   if (warps > kMaxWarpsBound) warps = kMaxWarpsBound;
   const int active = d->num_tiles < warps ? d->num_tiles : warps;

@@ -51,23 +51,6 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ float ld_relaxed_f32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return __uint_as_float(v);
-}
-__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
-  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
 // fp32 += fp16 * fp16 with the exact product (FHFMA).  `a`/`b` are half2
 // registers; H0/H1 pick the half (folded into the SASS operand selector).
 template <int HA, int HB>
@@ -95,6 +78,7 @@ __device__ __forceinline__ uint32_t hfma2(uint32_t a, uint32_t b, uint32_t c) {
   return d;
 }
 
+constexpr uint32_t kBulkChunk = 32768u;     // bytes per 1-D bulk copy
 constexpr uint32_t kMagic1024 = 0x64006400u;   // half2(1024, 1024)
 constexpr uint32_t kNeg1024 = 0xE400E400u;     // half2(-1024, -1024)
 
@@ -111,14 +95,16 @@ __device__ __forceinline__ float dot8_w4(uint32_t w, uint32_t x01, uint32_t x23,
   const uint32_t e15 = hfma2(lop3_and_or(w, kM2, kMagic1024), k116, kN64);        // (e1, e5)
   const uint32_t e26 = hadd2(lop3_and_or(w8, kM1, kMagic1024), kNeg1024);         // (e2, e6)
   const uint32_t e37 = hfma2(lop3_and_or(w8, kM2, kMagic1024), k116, kN64);       // (e3, e7)
-  acc = fhfma<0, 0>(e04, x01, acc);
-  acc = fhfma<0, 1>(e15, x01, acc);
-  acc = fhfma<0, 0>(e26, x23, acc);
-  acc = fhfma<0, 1>(e37, x23, acc);
-  acc = fhfma<1, 0>(e04, x45, acc);
-  acc = fhfma<1, 1>(e15, x45, acc);
-  acc = fhfma<1, 0>(e26, x67, acc);
-  acc = fhfma<1, 1>(e37, x67, acc);
+  // two independent chains (ILP); products are exact, only the adds round
+  float a0 = fhfma<0, 0>(e04, x01, acc);
+  float a1 = fhfma<1, 0>(e04, x45, 0.f);
+  a0 = fhfma<0, 1>(e15, x01, a0);
+  a1 = fhfma<1, 1>(e15, x45, a1);
+  a0 = fhfma<0, 0>(e26, x23, a0);
+  a1 = fhfma<1, 0>(e26, x67, a1);
+  a0 = fhfma<0, 1>(e37, x23, a0);
+  a1 = fhfma<1, 1>(e37, x67, a1);
+  acc = a0 + a1;
   return acc;
 }
 
@@ -164,7 +150,6 @@ struct TileRegs {
   uint4 sz;                        // 4 x (s, z) half pairs
   uint2 cols;                      // 4 x u16 (2c + swap)
   uint4 seg;                       // tile row-start masks, one word per sub-tile
-  int m0;                          // row ordinal of the tile's first group
 };
 
 template <int BITS>
@@ -173,8 +158,7 @@ __device__ __forceinline__ void load_tile(TileRegs<BITS>& r, const uint8_t* tile
   if (BITS == 4) r.codes[BITS == 4 ? 1 : 0] = ldg_stream128(tile + kTileHeaderBytes + 512 + lane * 16);
   r.sz = ldg_stream128(tile + off_sz(BITS) + lane * 16);
   r.cols = ldg_stream64(tile + off_cols(BITS) + lane * 8);
-  r.seg = ldg_stream128(tile);                 // broadcast within the warp
-  r.m0 = *reinterpret_cast<const int*>(tile + 16);
+  r.seg = ldg_stream128(tile);  // broadcast within the warp
 }
 
 // Group code word(s) of slot u from the lane's codes.
@@ -190,13 +174,24 @@ __device__ __forceinline__ uint2 group_words(const TileRegs<BITS>& r, int u) {
   }
 }
 
-// ---------------------------------------------------------------- kernel
-struct WarpRowState {
-  float carry[kMaxBatch];  // running sum of the open row
-  int ord;                 // row ordinal (into nzrow) of the open row
-  bool have;               // an open row exists
-  bool foreign;            // the open row started in an earlier warp's range
+// ---------------------------------------------------------------- row state
+// Each lane accumulates its own groups of the current (open) row in acc[];
+// a row is reduced across the warp (fixed butterfly order) only when it ends.
+struct RowState {
+  float acc[kMaxBatch];
+  int ord;       // nzrow ordinal of the current row
+  bool have;     // a current row exists
+  bool foreign;  // the current row started in an earlier warp's range
 };
+
+template <int B>
+__device__ __forceinline__ void warp_sum(float (&v)[kMaxBatch]) {
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) {
+#pragma unroll
+    for (int b = 0; b < B; ++b) v[b] += __shfl_xor_sync(0xffffffffu, v[b], d);
+  }
+}
 
 template <int B>
 __device__ __forceinline__ void store_row(const KParams& p, int ord, const float (&v)[kMaxBatch]) {
@@ -206,30 +201,94 @@ __device__ __forceinline__ void store_row(const KParams& p, int ord, const float
   for (int b = 0; b < B; ++b) p.Y[(int64_t)b * p.ldy + row] = v[b] + bias;
 }
 
+// Fix-up record of warp gw: kMaxBatch 8-byte slots {partial_b, flag}; each
+// slot is written with ONE 64-bit store, so a reader that sees the flag sees
+// the value (single-copy atomicity) -- no fence needed.
 template <int B>
 __device__ __forceinline__ void publish(const KParams& p, int gw, const float (&v)[kMaxBatch],
                                         uint32_t flag) {
-  uint32_t* rec = p.ws + (int64_t)gw * kWsWords;
+  unsigned long long* rec = reinterpret_cast<unsigned long long*>(p.ws + (int64_t)gw * kWsWords);
 #pragma unroll
-  for (int b = 0; b < B; ++b) st_relaxed(rec + b, __float_as_uint(v[b]));
-  st_release(rec + kWsFlag, flag);
+  for (int b = 0; b < B; ++b) {
+    const unsigned long long w = ((unsigned long long)flag << 32) | __float_as_uint(v[b]);
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(rec + b), "l"(w) : "memory");
+  }
 }
 
-// Sum the partials published by warps gw+1, gw+2, ... until a CLOSED record
-// (deterministic warp order) into v, resetting each flag for the next call.
+// Add the partials published by warps gw+1, gw+2, ... (warp order, so the
+// result is deterministic) until a CLOSED record; reset each slot.
 template <int B>
 __device__ __forceinline__ void collect(const KParams& p, int gw, float (&v)[kMaxBatch]) {
   for (int w = gw + 1; w < p.active_warps; ++w) {
-    uint32_t* rec = p.ws + (int64_t)w * kWsWords;
-    uint32_t f;
-    int spins = 0;
-    while ((f = ld_acquire(rec + kWsFlag)) == 0u) {
-      if (++spins > 8) __nanosleep(64);
-    }
+    unsigned long long* rec = reinterpret_cast<unsigned long long*>(p.ws + (int64_t)w * kWsWords);
+    uint32_t flag = 0;
 #pragma unroll
-    for (int b = 0; b < B; ++b) v[b] += ld_relaxed_f32(rec + b);
-    st_relaxed(rec + kWsFlag, 0u);
-    if (f == kFlagClosed) break;
+    for (int b = 0; b < B; ++b) {
+      unsigned long long s;
+      int spins = 0;
+      while (true) {
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(s) : "l"(rec + b) : "memory");
+        if ((s >> 32) != 0ull) break;
+        if (++spins > 4) __nanosleep(32);
+      }
+      flag = (uint32_t)(s >> 32);
+      v[b] += __uint_as_float((uint32_t)s);
+      asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(rec + b), "l"(0ull) : "memory");
+    }
+    if (flag == kFlagClosed) break;
+  }
+}
+
+// A row is complete (lane 0 holds its total in v): store it, or hand it to
+// the owning warp when it started upstream.
+template <int B>
+__device__ __forceinline__ void finish_row(const KParams& p, int gw, int ord, bool foreign,
+                                           const float (&v)[kMaxBatch], int lane) {
+  if (lane == 0) {
+    if (foreign) publish<B>(p, gw, v, kFlagClosed);
+    else store_row<B>(p, ord, v);
+  }
+}
+
+// part[b] = s * (sum_t q_t x_t - z * X_c) for the lane's group in slot u.
+template <int BITS, int B, bool XSMEM>
+__device__ __forceinline__ void group_partial(const KParams& p, const TileRegs<BITS>& tr, int u,
+                                              const uint8_t* __restrict__ xs,
+                                              const float* __restrict__ xc, float (&part)[kMaxBatch]) {
+  const uint32_t colw = (u < 2) ? tr.cols.x : tr.cols.y;
+  const uint32_t f = (colw >> ((u & 1) * 16)) & 0xffffu;  // 2c + swap
+  const uint32_t xoff0 = f * 16u;                         // = c*32 + swap*16: first x chunk
+  const uint32_t xoff1 = xoff0 ^ 16u;                     // second x chunk
+  const uint32_t c = f >> 1;
+  const uint2 w = group_words<BITS>(tr, u);
+  const uint32_t szw = u == 0 ? tr.sz.x : u == 1 ? tr.sz.y : u == 2 ? tr.sz.z : tr.sz.w;
+  const __half2 sz = *reinterpret_cast<const __half2*>(&szw);
+  const float s = __low2float(sz), z = __high2float(sz);
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    uint4 xa, xb;
+    if (XSMEM) {
+      const uint8_t* xrow = xs + (size_t)b * (size_t)p.cols * 2;
+      xa = *reinterpret_cast<const uint4*>(xrow + xoff0);
+      xb = *reinterpret_cast<const uint4*>(xrow + xoff1);
+    } else {
+      const uint8_t* xrow = reinterpret_cast<const uint8_t*>(p.X + (int64_t)b * p.ldx);
+      xa = __ldg(reinterpret_cast<const uint4*>(xrow + xoff0));
+      xb = __ldg(reinterpret_cast<const uint4*>(xrow + xoff1));
+    }
+    const float Xc = xc[(size_t)b * (p.cols / kGroup) + c];
+    float dot;
+    if (BITS == 4) {
+      // word 0 pairs with the first x chunk, word 1 with the second
+      const float d0 = dot8_w4(w.x, xa.x, xa.y, xa.z, xa.w, 0.f);
+      const float d1 = dot8_w4(w.y, xb.x, xb.y, xb.z, xb.w, 0.f);
+      dot = d0 + d1;
+    } else {
+      // 16-bit half h of the word holds the elements of x chunk h
+      const uint32_t xr[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+      dot = dot16_w2(w.x, xr, 0.f);
+    }
+    part[b] = s * fmaf(-z, Xc, dot);
   }
 }
 
@@ -237,96 +296,54 @@ template <int BITS, int B, bool XSMEM>
 __device__ __forceinline__ void process_tile(const KParams& p, const TileRegs<BITS>& tr,
                                              const uint8_t* __restrict__ xs,
                                              const float* __restrict__ xc, int lane, int gw,
-                                             WarpRowState& st) {
-  // -------- per-group partials: part[u][b] = s * (sum_t q x - z * X_c)
+                                             RowState& st) {
   float part[kPerLane][kMaxBatch];
-  const uint32_t colw[2] = {tr.cols.x, tr.cols.y};
-  const uint32_t szw[4] = {tr.sz.x, tr.sz.y, tr.sz.z, tr.sz.w};
 #pragma unroll
-  for (int u = 0; u < kPerLane; ++u) {
-    const uint32_t f = (colw[u >> 1] >> ((u & 1) * 16)) & 0xffffu;  // 2c + swap
-    const uint32_t xoff0 = f * 16u;         // = c*32 + swap*16 : first x chunk
-    const uint32_t xoff1 = xoff0 ^ 16u;     // second x chunk
-    const uint32_t c = f >> 1;
-    const uint2 w = group_words<BITS>(tr, u);
-    const __half2 sz = *reinterpret_cast<const __half2*>(&szw[u]);
-    const float s = __low2float(sz), z = __high2float(sz);
-#pragma unroll
-    for (int b = 0; b < B; ++b) {
-      const uint8_t* xb;
-      if (XSMEM) xb = xs + (size_t)b * (size_t)p.cols * 2;
-      else xb = reinterpret_cast<const uint8_t*>(p.X + (int64_t)b * p.ldx);
-      uint4 xa, xbv;
-      if (XSMEM) {
-        xa = *reinterpret_cast<const uint4*>(xb + xoff0);
-        xbv = *reinterpret_cast<const uint4*>(xb + xoff1);
-      } else {
-        xa = __ldg(reinterpret_cast<const uint4*>(xb + xoff0));
-        xbv = __ldg(reinterpret_cast<const uint4*>(xb + xoff1));
-      }
-      const float Xc = xc[(size_t)b * (p.cols / kGroup) + c];
-      float dot;
-      if (BITS == 4) {
-        // word 0 pairs with the first x chunk, word 1 with the second
-        float d0 = dot8_w4(w.x, xa.x, xa.y, xa.z, xa.w, 0.f);
-        float d1 = dot8_w4(w.y, xbv.x, xbv.y, xbv.z, xbv.w, 0.f);
-        dot = d0 + d1;
-      } else {
-        // 16-bit half h of the word holds elements of chunk h; the masks in
-        // dot16_w2 pair element j (low half) with element j+8 (high half).
-        const uint32_t xr[8] = {xa.x, xa.y, xa.z, xa.w, xbv.x, xbv.y, xbv.z, xbv.w};
-        dot = dot16_w2(w.x, xr, 0.f);
-      }
-      part[u][b] = s * fmaf(-z, Xc, dot);
-    }
-  }
+  for (int u = 0; u < kPerLane; ++u) group_partial<BITS, B, XSMEM>(p, tr, u, xs, xc, part[u]);
 
-  // -------- segmented reduction per sub-tile (32 consecutive stream groups)
   const uint32_t segw[4] = {tr.seg.x, tr.seg.y, tr.seg.z, tr.seg.w};
-  int base = tr.m0 - (int)(segw[0] & 1u);  // ordinal of the row before lane 0
-  const uint32_t le = 0xffffffffu >> (31 - lane);  // lanes 0..lane
 #pragma unroll
   for (int u = 0; u < kPerLane; ++u) {
-    const uint32_t mask = segw[u];
-    // the open row closes when this sub-tile starts with a new row
-    if ((mask & 1u) && st.have) {
-      if (lane == 0) {
-        if (st.foreign) publish<B>(p, gw, st.carry, kFlagClosed);
-        else store_row<B>(p, st.ord, st.carry);
-      }
-      st.have = false;
+    const uint32_t m = segw[u];
+    if (m == 0u) {  // the whole sub-tile continues the current row
+#pragma unroll
+      for (int b = 0; b < B; ++b) st.acc[b] += part[u][b];
+      continue;
     }
-    const int s0 = 31 - __clz((mask | 1u) & le);  // this lane's segment start
-    float v[kMaxBatch];
+    // lanes before the first row start still belong to the current row
+    const int f = __ffs(m) - 1;
+    if (lane < f) {
 #pragma unroll
-    for (int b = 0; b < B; ++b) v[b] = part[u][b];
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-#pragma unroll
-      for (int b = 0; b < B; ++b) {
-        const float n = __shfl_up_sync(0xffffffffu, v[b], d);
-        if (lane - d >= s0) v[b] += n;
-      }
+      for (int b = 0; b < B; ++b) st.acc[b] += part[u][b];
     }
-    const bool joins_carry = (s0 == 0) && !(mask & 1u) && st.have;
-    if (joins_carry) {
+    if (st.have) {  // the current row ends here
+      float v[kMaxBatch];
 #pragma unroll
-      for (int b = 0; b < B; ++b) v[b] = st.carry[b] + v[b];
+      for (int b = 0; b < B; ++b) v[b] = st.acc[b];
+      warp_sum<B>(v);
+      finish_row<B>(p, gw, st.ord, st.foreign, v, lane);
     }
-    const int ord = base + __popc(mask & le);
-    const bool tail = (lane == 31) || ((mask >> (lane + 1)) & 1u);
-    if (tail && lane != 31) {  // a row that ends inside this sub-tile
-      if (joins_carry && st.foreign) publish<B>(p, gw, v, kFlagClosed);
-      else store_row<B>(p, ord, v);
-    }
-    // lane 31's segment stays open: it becomes the carry
-    const bool foreign31 = __shfl_sync(0xffffffffu, (int)(joins_carry && st.foreign), 31) != 0;
+    // rows that start and end inside this sub-tile: [start_k, start_{k+1})
+    uint32_t mm = m;
+    int ord = st.ord;
+    while (__popc(mm) > 1) {
+      const int a = __ffs(mm) - 1;
+      mm &= mm - 1u;
+      const int e = __ffs(mm) - 1;
+      float v[kMaxBatch];
 #pragma unroll
-    for (int b = 0; b < B; ++b) st.carry[b] = __shfl_sync(0xffffffffu, v[b], 31);
-    st.ord = __shfl_sync(0xffffffffu, ord, 31);
-    st.foreign = foreign31;
+      for (int b = 0; b < B; ++b) v[b] = (lane >= a && lane < e) ? part[u][b] : 0.f;
+      warp_sum<B>(v);
+      ++ord;
+      finish_row<B>(p, gw, ord, false, v, lane);
+    }
+    // the last segment [last start, 31] becomes the current row
+    const int a = __ffs(mm) - 1;
+#pragma unroll
+    for (int b = 0; b < B; ++b) st.acc[b] = (lane >= a) ? part[u][b] : 0.f;
+    st.ord = ord + 1;
     st.have = true;
-    base = st.ord;
+    st.foreign = false;
   }
 }
 
@@ -353,24 +370,53 @@ __global__ void __launch_bounds__(kThreads) gqsa_streamk_kernel(KParams p) {
   for (int i = 0; i < kDepth; ++i)
     if (t_begin + i < t_end) load_tile<BITS>(buf[i], tiles + (int64_t)(t_begin + i) * tb, lane);
   uint32_t next_seg0 = 1u;  // does the group after this warp's range start a row?
-  if (t_end > t_begin && t_end < p.num_tiles)
-    next_seg0 = __ldg(reinterpret_cast<const uint32_t*>(tiles + (int64_t)t_end * tb)) & 1u;
+  int m0 = 0;
+  if (t_end > t_begin) {
+    m0 = __ldg(reinterpret_cast<const int*>(tiles + (int64_t)t_begin * tb + 16));
+    if (t_end < p.num_tiles)
+      next_seg0 = __ldg(reinterpret_cast<const uint32_t*>(tiles + (int64_t)t_end * tb)) & 1u;
+  }
 
   pdl_launch_dependents();
   pdl_wait();  // x, y, bias and the workspace may belong to the previous kernel
 
-  // ---- stage activations and per-column-group sums in shared memory
+  // ---- stage activations (1-D TMA bulk copies into shared memory) and the
+  //      per-column-group sums X_{b,c} (fp32, fixed t order)
   const int KG = p.cols / kGroup;
   uint8_t* xs = smem;
   float* xc = reinterpret_cast<float*>(smem + (XSMEM ? (size_t)B * p.cols * 2 : 0));
   if (XSMEM) {
-    const int n16 = p.cols / 8;  // uint4 per batch row
-    for (int i = threadIdx.x; i < B * n16; i += kThreads) {
-      const int b = i / n16, j = i - b * n16;
-      reinterpret_cast<uint4*>(xs)[i] =
-          __ldg(reinterpret_cast<const uint4*>(p.X + (int64_t)b * p.ldx) + j);
+    __shared__ __align__(8) uint64_t xbar;
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&xbar);
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      const uint32_t row_bytes = (uint32_t)p.cols * 2u;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                   "r"(row_bytes * B)
+                   : "memory");
+      for (int b = 0; b < B; ++b) {
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(p.X + (int64_t)b * p.ldx);
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(xs + (size_t)b * row_bytes);
+        for (uint32_t off = 0; off < row_bytes; off += kBulkChunk) {
+          const uint32_t n = min(kBulkChunk, row_bytes - off);
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  dst + off),
+              "l"(src + off), "r"(n), "r"(bar)
+              : "memory");
+        }
+      }
     }
-    __syncthreads();
+    __syncthreads();  // barrier initialised before anyone polls it
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(bar)
+          : "memory");
+    }
   }
   for (int i = threadIdx.x; i < B * KG; i += kThreads) {
     const int b = i / KG, c = i - b * KG;
@@ -404,12 +450,14 @@ __global__ void __launch_bounds__(kThreads) gqsa_streamk_kernel(KParams p) {
   if (t_end <= t_begin) return;
 
   // ---- stream the warp's tile range
-  WarpRowState st;
+  RowState st;
 #pragma unroll
-  for (int b = 0; b < kMaxBatch; ++b) st.carry[b] = 0.f;
-  st.have = !(buf[0].seg.x & 1u);  // the range starts inside a row owned by an earlier warp
+  for (int b = 0; b < kMaxBatch; ++b) st.acc[b] = 0.f;
+  // If the range starts inside a row, that row (ordinal m0) was opened by an
+  // earlier warp; otherwise the first row starts at lane 0 of sub-tile 0.
+  st.have = !(buf[0].seg.x & 1u);
   st.foreign = st.have;
-  st.ord = buf[0].m0;
+  st.ord = st.have ? m0 : m0 - 1;
 
   for (int t0 = t_begin; t0 < t_end; t0 += kDepth) {
 #pragma unroll
@@ -423,18 +471,17 @@ __global__ void __launch_bounds__(kThreads) gqsa_streamk_kernel(KParams p) {
   }
 
   // ---- the open row at the end of the range
+  float v[kMaxBatch];
+#pragma unroll
+  for (int b = 0; b < B; ++b) v[b] = st.acc[b];
+  warp_sum<B>(v);
   if (next_seg0) {  // it ends exactly here
-    if (lane == 0) {
-      if (st.foreign) publish<B>(p, gw, st.carry, kFlagClosed);
-      else store_row<B>(p, st.ord, st.carry);
-    }
+    finish_row<B>(p, gw, st.ord, st.foreign, v, lane);
   } else if (st.foreign) {  // the whole range lies inside a row owned upstream
-    if (lane == 0) publish<B>(p, gw, st.carry, kFlagOpen);
-  } else {  // owner of a row that continues downstream: collect, then store
-    if (lane == 0) {
-      collect<B>(p, gw, st.carry);
-      store_row<B>(p, st.ord, st.carry);
-    }
+    if (lane == 0) publish<B>(p, gw, v, kFlagOpen);
+  } else if (lane == 0) {  // owner of a row that continues downstream
+    collect<B>(p, gw, v);
+    store_row<B>(p, st.ord, v);
   }
 }
 

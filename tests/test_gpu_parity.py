@@ -33,7 +33,8 @@ def run(bsr, xbits, bias=None, layer=None, **kw):
     else:
         y = L.gemm(X, bias=b)
     torch.cuda.synchronize()
-    assert int(L.ws.count_nonzero()) == 0, "workspace must be left zeroed"
+    flags = L.ws.view(torch.int32).view(-1, 16)[:, 15]
+    assert int(flags.count_nonzero()) == 0, "every fix-up flag must be left zero"
     return y.cpu().numpy()
 
 
