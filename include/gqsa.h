@@ -27,7 +27,7 @@
  * gqsa_status_t.  Errors raised during asynchronous device execution surface
  * at the next stream synchronisation (CUDA convention).
  *
- * Byte layout of the packed blob: DESIGN.md §5 ("LAYOUT v1").
+ * Byte layout of the packed blob: DESIGN.md §5 ("LAYOUT v2").
  */
 #ifndef GQSA_H_
 #define GQSA_H_
@@ -40,7 +40,7 @@ extern "C" {
 #endif
 
 #define GQSA_MAGIC 0x41535147u   /* bytes "GQSA" little-endian */
-#define GQSA_VERSION 1
+#define GQSA_VERSION 2
 #define GQSA_TILE_GROUPS 128     /* kept groups per tile record (LAYOUT v1) */
 #define GQSA_MAX_BATCH 8
 

@@ -1,4 +1,4 @@
-"""Independent Python implementation of the packed-blob LAYOUT v1 -- TEST
+"""Independent Python implementation of the packed-blob LAYOUT v2 -- TEST
 INFRASTRUCTURE ONLY (same import rules as gqsa_oracle.py).
 
 Written from the prose specification in DESIGN.md §5, not from the C++
@@ -12,9 +12,10 @@ import struct
 import numpy as np
 
 MAGIC = 0x41535147
-VERSION = 1
-T = 128          # groups per tile
+VERSION = 2
+T = 128          # groups per tile (4 slots x 32 lanes)
 LANES = 32
+SLOTS = 4
 HDR = 256
 ALIGN = 256
 
@@ -28,68 +29,103 @@ def tile_bytes(bits: int) -> int:
     return 32 + T * 16 * bits // 8 + T * 4 + T * 2
 
 
+TARGET_SLOTS = 32
+
+
+def lanes_per_row(n_nz: int, max_len: int) -> int:
+    """S = the larger of (a) the smallest power of two with
+    ceil(max_len / S) <= 32 slots per lane and (b) 32 / (next power of two
+    >= n_nz) when fewer than 32 rows are non-empty; capped at 32."""
+    if n_nz <= 0:
+        return 1
+    s = 1
+    while s < LANES and -(-max_len // s) > TARGET_SLOTS:
+        s *= 2
+    p = 1
+    while p < n_nz and p < LANES:
+        p *= 2
+    return max(s, LANES // p)
+
+
+def rotation(row: int, n: int) -> int:
+    """Dealing start of a row: ((row * 2654435761) mod 2^32) >> 7, mod n."""
+    return (((row * 2654435761) & 0xFFFFFFFF) >> 7) % n
+
+
 def pack_reference(bsr: dict, row_begin: int = 0, row_end=None) -> bytes:
-    rows_all = int(bsr["rows"])
-    row_end = rows_all if row_end is None else int(row_end)
+    row_end = int(bsr["rows"]) if row_end is None else int(row_end)
     G, n, K = int(bsr["group_size"]), int(bsr["bits"]), int(bsr["cols"])
     ri_all = [int(v) for v in np.asarray(bsr["row_index"])]
-    g0, g1 = ri_all[row_begin], ri_all[row_end]
+    g0 = ri_all[row_begin]
     rows = row_end - row_begin
-    nnzg = g1 - g0
-    ri = [v - g0 for v in ri_all[row_begin:row_end + 1]]
-    counts = [ri[r + 1] - ri[r] for r in range(rows)]
-    nzrows = [r for r in range(rows) if counts[r] > 0]
+    nnzg = ri_all[row_end] - g0
+    counts = [ri_all[row_begin + r + 1] - ri_all[row_begin + r] for r in range(rows)]
+    nz = [r for r in range(rows) if counts[r] > 0]
+    nz.sort(key=lambda r: (-counts[r], r))          # count descending, then row
     empty = [r for r in range(rows) if counts[r] == 0]
-    ordinal = {r: i for i, r in enumerate(nzrows)}
-    row_of = []
-    for r in range(rows):
-        row_of += [r] * counts[r]
-    num_tiles = -(-nnzg // T)
+    S = lanes_per_row(len(nz), counts[nz[0]] if nz else 0)
+    rps = LANES // S                                # rows per slice
+    n_slices = -(-len(nz) // rps)
+    slice_tiles = []
+    for s in range(n_slices):
+        slots = -(-counts[nz[s * rps]] // S)        # the slice's longest row sets its length
+        slice_tiles.append(-(-slots // SLOTS))
+    num_tiles = sum(slice_tiles)
     tb = tile_bytes(n)
     off_ri = HDR
-    off_nz = _align(off_ri + 4 * (rows + 1))
-    off_em = _align(off_nz + 4 * len(nzrows))
+    off_perm = _align(off_ri + 4 * (rows + 1))
+    off_em = _align(off_perm + 4 * LANES * n_slices)
     off_tiles = _align(off_em + 4 * len(empty))
     total = _align(off_tiles + num_tiles * tb)
 
     out = bytearray(total)
     struct.pack_into("<IIiiiiqiiiiiiiiQQQQQ", out, 0,
-                     MAGIC, VERSION, rows, K, G, n, nnzg, T, num_tiles, len(nzrows), len(empty),
-                     tb, 1, row_begin, row_end, off_ri, off_nz, off_em, off_tiles, total)
-    struct.pack_into(f"<{rows + 1}i", out, off_ri, *ri)
-    if nzrows:
-        struct.pack_into(f"<{len(nzrows)}i", out, off_nz, *nzrows)
+                     MAGIC, VERSION, rows, K, G, n, nnzg, T, num_tiles, len(nz), len(empty),
+                     tb, 2 | (S << 8), row_begin, row_end, off_ri, off_perm, off_em, off_tiles, total)
+    struct.pack_into(f"<{rows + 1}i", out, off_ri, *[v - g0 for v in ri_all[row_begin:row_end + 1]])
     if empty:
         struct.pack_into(f"<{len(empty)}i", out, off_em, *empty)
 
-    cb = G * n // 8                       # code bytes per group
+    cb = G * n // 8
     codes = np.asarray(bsr["codes"], np.uint8)
     gcols = np.asarray(bsr["group_cols"], np.uint16)
     sc = np.asarray(bsr["scales_f16"], np.uint16)
     zr = np.asarray(bsr["zeros_f16"], np.uint16)
-    per_plane = 16 // cb                  # groups of one lane in a 16-B code vector
+    per_plane = 16 // cb
     codes_total = T * cb
-    for t in range(num_tiles):
-        base = off_tiles + t * tb
-        masks = [0, 0, 0, 0]
-        for j in range(T):                # j = u*32 + lane
-            pos = t * T + j
-            if pos >= nnzg:
-                continue
-            u, lane = divmod(j, LANES)
-            g = g0 + pos
-            if pos == 0 or row_of[pos] != row_of[pos - 1]:
-                masks[u] |= 1 << lane
-            swap = lane & 1
-            gb = bytes(codes[g * cb:(g + 1) * cb])
-            if swap:
-                gb = gb[cb // 2:] + gb[:cb // 2]
-            off_c = base + 32 + (u // per_plane) * 512 + lane * 16 + (u % per_plane) * cb
-            out[off_c:off_c + cb] = gb
-            off_sz = base + 32 + codes_total + lane * 16 + u * 4
-            struct.pack_into("<HH", out, off_sz, int(sc[g]), int(zr[g]))
-            off_col = base + 32 + codes_total + T * 4 + lane * 8 + u * 2
-            struct.pack_into("<H", out, off_col, (int(gcols[g]) << 1) | swap)
-        m0 = ordinal[row_of[t * T]]
-        struct.pack_into("<IIIIi", out, base, *masks, m0)
+    t = 0
+    for s in range(n_slices):
+        lane_row = []
+        for lane in range(LANES):
+            k = s * rps + lane // S
+            lane_row.append(nz[k] if k < len(nz) else -1)
+        struct.pack_into(f"<{LANES}i", out, off_perm + 4 * LANES * s, *lane_row)
+        nt = slice_tiles[s]
+        for tau in range(nt):
+            base = off_tiles + t * tb
+            flags = (1 if tau == 0 else 0) | (2 if tau == nt - 1 else 0)
+            struct.pack_into("<IIII", out, base, s, flags, nt - 1 - tau, 0)
+            for u in range(SLOTS):
+                for lane in range(LANES):
+                    if lane % 8 == 0:
+                        load = [0] * 8                  # bank-quad load of the quarter-warp
+                    row = lane_row[lane]
+                    k = (tau * SLOTS + u) * S + lane % S  # position in the row's dealing order
+                    if row < 0 or k >= counts[row]:
+                        load[0] += 1                    # padding reads x chunk 0
+                        continue
+                    g = ri_all[row_begin + row] + (k + rotation(row_begin + row, counts[row])) % counts[row]
+                    q0 = (2 * int(gcols[g])) % 8
+                    swap = 1 if load[q0 + 1] < load[q0] else 0
+                    load[q0 + swap] += 1
+                    gb = bytes(codes[g * cb:(g + 1) * cb])
+                    if swap:
+                        gb = gb[cb // 2:] + gb[:cb // 2]
+                    off_c = base + 32 + (u // per_plane) * 512 + lane * 16 + (u % per_plane) * cb
+                    out[off_c:off_c + cb] = gb
+                    struct.pack_into("<HH", out, base + 32 + codes_total + lane * 16 + u * 4,
+                                     int(sc[g]), int(zr[g]))
+                    struct.pack_into("<H", out, base + 32 + codes_total + T * 4 + lane * 8 + u * 2,
+                                     (int(gcols[g]) << 1) | swap)
+            t += 1
     return bytes(out)

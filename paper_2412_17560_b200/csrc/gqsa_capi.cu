@@ -35,10 +35,13 @@ int device_sms(int dev) {
   return g_dev[dev].sms;
 }
 
+bool lanes_per_row_ok(uint32_t s) { return s >= 1 && s <= 32 && (s & (s - 1)) == 0; }
+
 bool desc_ok(const gqsa_desc_t* d) {
   return d && d->magic == kMagic && d->version == (uint32_t)kVersion && d->group_size == kGroup &&
          (d->bits == 4 || d->bits == 2) && d->tile_groups == kTileGroups && d->rows >= 0 &&
-         d->cols > 0 && d->cols % kGroup == 0 && d->num_tiles >= 0;
+         d->cols > 0 && d->cols % kGroup == 0 && d->num_tiles >= 0 &&
+         lanes_per_row_ok(((uint32_t)d->flags >> kFlagLanesPerRowShift) & 0xff);
 }
 
 size_t smem_for(const gqsa_desc_t* d, int B, bool* xsmem) {
@@ -111,7 +114,7 @@ extern "C" int gqsa_workspace_size(const gqsa_desc_t* desc, int32_t batch, size_
   if (!desc_ok(desc)) return GQSA_ERR_VALIDATION;
   if (batch < 1 || batch > kMaxBatch) return GQSA_ERR_SHAPE;
   const int64_t recs = desc->num_tiles < kMaxWarpsBound ? desc->num_tiles : kMaxWarpsBound;
-  *bytes = (size_t)(recs > 0 ? recs : 1) * kWsWords * 4;
+  *bytes = (size_t)(recs > 0 ? recs : 1) * batch * kLanes * kWsSlotBytes;
   return GQSA_OK;
 }
 
@@ -144,7 +147,7 @@ extern "C" int gqsa_gemm_smallbatch(const gqsa_desc_t* desc, const void* d_blob,
   const uint8_t* blob = static_cast<const uint8_t*>(d_blob);
   KParams p;
   p.tiles = blob + desc->off_tiles;
-  p.nzrow = reinterpret_cast<const int32_t*>(blob + desc->off_nzrow);
+  p.perm = reinterpret_cast<const int32_t*>(blob + desc->off_nzrow);
   p.empty = reinterpret_cast<const int32_t*>(blob + desc->off_empty);
   p.X = d_X;
   p.Y = d_Y;
@@ -157,6 +160,7 @@ extern "C" int gqsa_gemm_smallbatch(const gqsa_desc_t* desc, const void* d_blob,
   p.num_tiles = desc->num_tiles;
   p.n_empty = desc->n_empty;
   p.active_warps = pl.active_warps;
+  p.lanes_per_row = ((uint32_t)desc->flags >> kFlagLanesPerRowShift) & 0xff;
   if (desc->rows == 0) return GQSA_OK;
 
   cudaLaunchConfig_t cfg = {};

@@ -7,9 +7,12 @@
 //   X_{b,c} = sum_t x[b][c*G+t]       (Eq. 3 applied per group, z folded once)
 //
 // Design:
+//  * Layout: rows are sorted by kept-group count and cut into
+//    32-row slices (sliced ELL); a lane owns a row and walks its groups slot
+//    by slot, so the hot loop has no cross-lane reduction at all.
 //  * Task-centric partition (PAPER.md:161 Stream-K, App. J): the
-//    tile stream (128 kept groups per tile, CSR order) is cut into contiguous,
-//    equal (+-1 tile) ranges, one per WARP, regardless of row boundaries.
+//    tile stream (128 groups per tile) is cut into contiguous, equal (+-1
+//    tile) ranges, one per WARP, regardless of row or slice boundaries.
 //  * Weights stream HBM -> registers with 128-bit L1::no_allocate loads,
 //    double-buffered per warp; the first tiles are requested BEFORE
 //    griddepcontrol.wait so they overlap the previous kernel (PDL).
@@ -19,10 +22,9 @@
 //    fields into exact fp16 integers; FHFMA (fma.rn.f32.f16) multiplies the
 //    exact fp16 code by fp16 x and accumulates in fp32 (products exact).
 //    No tensor cores: batch-1 GEMV is bandwidth-bound.
-//  * Row reduction: segmented warp scan keyed by the tile's row-start mask;
-//    rows split across warps are fixed up deterministically: the warp that
-//    owns a row's first group sums the partials its successors publish
-//    (flag + release/acquire), in warp order.
+//  * Fix-up: a slice split across warps is finished by the warp that owns its
+//    first tile, which adds the per-lane partials its successors publish
+//    (64-bit {value, flag} slots, no fences), in warp order: deterministic.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -95,16 +97,15 @@ __device__ __forceinline__ float dot8_w4(uint32_t w, uint32_t x01, uint32_t x23,
   const uint32_t e15 = hfma2(lop3_and_or(w, kM2, kMagic1024), k116, kN64);        // (e1, e5)
   const uint32_t e26 = hadd2(lop3_and_or(w8, kM1, kMagic1024), kNeg1024);         // (e2, e6)
   const uint32_t e37 = hfma2(lop3_and_or(w8, kM2, kMagic1024), k116, kN64);       // (e3, e7)
-  // two independent chains (ILP); products are exact, only the adds round
-  float a0 = fhfma<0, 0>(e04, x01, acc);
-  float a1 = fhfma<1, 0>(e04, x45, 0.f);
-  a0 = fhfma<0, 1>(e15, x01, a0);
-  a1 = fhfma<1, 1>(e15, x45, a1);
-  a0 = fhfma<0, 0>(e26, x23, a0);
-  a1 = fhfma<1, 0>(e26, x67, a1);
-  a0 = fhfma<0, 1>(e37, x23, a0);
-  a1 = fhfma<1, 1>(e37, x67, a1);
-  acc = a0 + a1;
+  // products are exact; only the fp32 adds round
+  acc = fhfma<0, 0>(e04, x01, acc);
+  acc = fhfma<0, 1>(e15, x01, acc);
+  acc = fhfma<0, 0>(e26, x23, acc);
+  acc = fhfma<0, 1>(e37, x23, acc);
+  acc = fhfma<1, 0>(e04, x45, acc);
+  acc = fhfma<1, 1>(e15, x45, acc);
+  acc = fhfma<1, 0>(e26, x67, acc);
+  acc = fhfma<1, 1>(e37, x67, acc);
   return acc;
 }
 
@@ -146,10 +147,10 @@ __device__ __forceinline__ float dot16_w2(uint32_t w, const uint32_t (&x)[8], fl
 // ---------------------------------------------------------------- tile regs
 template <int BITS>
 struct TileRegs {
-  uint4 codes[BITS == 4 ? 2 : 1];  // lane's 4 groups (W4: 2 planes x 16 B)
+  uint4 codes[BITS == 4 ? 2 : 1];  // lane's 4 slots (W4: 2 planes x 16 B)
   uint4 sz;                        // 4 x (s, z) half pairs
   uint2 cols;                      // 4 x u16 (2c + swap)
-  uint4 seg;                       // tile row-start masks, one word per sub-tile
+  uint4 hdr;                       // slice, flags, tiles to slice end, 0
 };
 
 template <int BITS>
@@ -158,7 +159,7 @@ __device__ __forceinline__ void load_tile(TileRegs<BITS>& r, const uint8_t* tile
   if (BITS == 4) r.codes[BITS == 4 ? 1 : 0] = ldg_stream128(tile + kTileHeaderBytes + 512 + lane * 16);
   r.sz = ldg_stream128(tile + off_sz(BITS) + lane * 16);
   r.cols = ldg_stream64(tile + off_cols(BITS) + lane * 8);
-  r.seg = ldg_stream128(tile);  // broadcast within the warp
+  r.hdr = ldg_stream128(tile);  // broadcast within the warp
 }
 
 // Group code word(s) of slot u from the lane's codes.
@@ -174,83 +175,8 @@ __device__ __forceinline__ uint2 group_words(const TileRegs<BITS>& r, int u) {
   }
 }
 
-// ---------------------------------------------------------------- row state
-// Each lane accumulates its own groups of the current (open) row in acc[];
-// a row is reduced across the warp (fixed butterfly order) only when it ends.
-struct RowState {
-  float acc[kMaxBatch];
-  int ord;       // nzrow ordinal of the current row
-  bool have;     // a current row exists
-  bool foreign;  // the current row started in an earlier warp's range
-};
-
-template <int B>
-__device__ __forceinline__ void warp_sum(float (&v)[kMaxBatch]) {
-#pragma unroll
-  for (int d = 16; d >= 1; d >>= 1) {
-#pragma unroll
-    for (int b = 0; b < B; ++b) v[b] += __shfl_xor_sync(0xffffffffu, v[b], d);
-  }
-}
-
-template <int B>
-__device__ __forceinline__ void store_row(const KParams& p, int ord, const float (&v)[kMaxBatch]) {
-  const int row = __ldg(p.nzrow + ord);
-  const float bias = p.bias ? __ldg(p.bias + row) : 0.f;
-#pragma unroll
-  for (int b = 0; b < B; ++b) p.Y[(int64_t)b * p.ldy + row] = v[b] + bias;
-}
-
-// Fix-up record of warp gw: kMaxBatch 8-byte slots {partial_b, flag}; each
-// slot is written with ONE 64-bit store, so a reader that sees the flag sees
-// the value (single-copy atomicity) -- no fence needed.
-template <int B>
-__device__ __forceinline__ void publish(const KParams& p, int gw, const float (&v)[kMaxBatch],
-                                        uint32_t flag) {
-  unsigned long long* rec = reinterpret_cast<unsigned long long*>(p.ws + (int64_t)gw * kWsWords);
-#pragma unroll
-  for (int b = 0; b < B; ++b) {
-    const unsigned long long w = ((unsigned long long)flag << 32) | __float_as_uint(v[b]);
-    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(rec + b), "l"(w) : "memory");
-  }
-}
-
-// Add the partials published by warps gw+1, gw+2, ... (warp order, so the
-// result is deterministic) until a CLOSED record; reset each slot.
-template <int B>
-__device__ __forceinline__ void collect(const KParams& p, int gw, float (&v)[kMaxBatch]) {
-  for (int w = gw + 1; w < p.active_warps; ++w) {
-    unsigned long long* rec = reinterpret_cast<unsigned long long*>(p.ws + (int64_t)w * kWsWords);
-    uint32_t flag = 0;
-#pragma unroll
-    for (int b = 0; b < B; ++b) {
-      unsigned long long s;
-      int spins = 0;
-      while (true) {
-        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(s) : "l"(rec + b) : "memory");
-        if ((s >> 32) != 0ull) break;
-        if (++spins > 4) __nanosleep(32);
-      }
-      flag = (uint32_t)(s >> 32);
-      v[b] += __uint_as_float((uint32_t)s);
-      asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(rec + b), "l"(0ull) : "memory");
-    }
-    if (flag == kFlagClosed) break;
-  }
-}
-
-// A row is complete (lane 0 holds its total in v): store it, or hand it to
-// the owning warp when it started upstream.
-template <int B>
-__device__ __forceinline__ void finish_row(const KParams& p, int gw, int ord, bool foreign,
-                                           const float (&v)[kMaxBatch], int lane) {
-  if (lane == 0) {
-    if (foreign) publish<B>(p, gw, v, kFlagClosed);
-    else store_row<B>(p, ord, v);
-  }
-}
-
-// part[b] = s * (sum_t q_t x_t - z * X_c) for the lane's group in slot u.
+// part[b] = s * (sum_t q_t x_t - z * X_c) for the lane's group in slot u
+// (Eq. 3 per group: sum_t (q_t - z) s x_t with z applied once).
 template <int BITS, int B, bool XSMEM>
 __device__ __forceinline__ void group_partial(const KParams& p, const TileRegs<BITS>& tr, int u,
                                               const uint8_t* __restrict__ xs,
@@ -292,61 +218,80 @@ __device__ __forceinline__ void group_partial(const KParams& p, const TileRegs<B
   }
 }
 
-template <int BITS, int B, bool XSMEM>
-__device__ __forceinline__ void process_tile(const KParams& p, const TileRegs<BITS>& tr,
-                                             const uint8_t* __restrict__ xs,
-                                             const float* __restrict__ xc, int lane, int gw,
-                                             RowState& st) {
-  float part[kPerLane][kMaxBatch];
-#pragma unroll
-  for (int u = 0; u < kPerLane; ++u) group_partial<BITS, B, XSMEM>(p, tr, u, xs, xc, part[u]);
+// ---------------------------------------------------------------- fix-up
+// Record of warp w: [B][32 lanes] 8-byte slots {partial, flag}; each slot is
+// written with ONE 64-bit store, so a reader that sees the flag sees the
+// value (single-copy atomicity): no fence needed.
+template <int B>
+__device__ __forceinline__ unsigned long long* ws_slot(const KParams& p, int w, int b, int lane) {
+  return reinterpret_cast<unsigned long long*>(p.ws) + ((int64_t)w * B + b) * kLanes + lane;
+}
 
-  const uint32_t segw[4] = {tr.seg.x, tr.seg.y, tr.seg.z, tr.seg.w};
+template <int B>
+__device__ __forceinline__ void publish(const KParams& p, int gw, const float (&v)[kMaxBatch], int lane) {
 #pragma unroll
-  for (int u = 0; u < kPerLane; ++u) {
-    const uint32_t m = segw[u];
-    if (m == 0u) {  // the whole sub-tile continues the current row
-#pragma unroll
-      for (int b = 0; b < B; ++b) st.acc[b] += part[u][b];
-      continue;
-    }
-    // lanes before the first row start still belong to the current row
-    const int f = __ffs(m) - 1;
-    if (lane < f) {
-#pragma unroll
-      for (int b = 0; b < B; ++b) st.acc[b] += part[u][b];
-    }
-    if (st.have) {  // the current row ends here
-      float v[kMaxBatch];
-#pragma unroll
-      for (int b = 0; b < B; ++b) v[b] = st.acc[b];
-      warp_sum<B>(v);
-      finish_row<B>(p, gw, st.ord, st.foreign, v, lane);
-    }
-    // rows that start and end inside this sub-tile: [start_k, start_{k+1})
-    uint32_t mm = m;
-    int ord = st.ord;
-    while (__popc(mm) > 1) {
-      const int a = __ffs(mm) - 1;
-      mm &= mm - 1u;
-      const int e = __ffs(mm) - 1;
-      float v[kMaxBatch];
-#pragma unroll
-      for (int b = 0; b < B; ++b) v[b] = (lane >= a && lane < e) ? part[u][b] : 0.f;
-      warp_sum<B>(v);
-      ++ord;
-      finish_row<B>(p, gw, ord, false, v, lane);
-    }
-    // the last segment [last start, 31] becomes the current row
-    const int a = __ffs(mm) - 1;
-#pragma unroll
-    for (int b = 0; b < B; ++b) st.acc[b] = (lane >= a) ? part[u][b] : 0.f;
-    st.ord = ord + 1;
-    st.have = true;
-    st.foreign = false;
+  for (int b = 0; b < B; ++b) {
+    const unsigned long long w = (1ull << 32) | __float_as_uint(v[b]);
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(ws_slot<B>(p, gw, b, lane)), "l"(w) : "memory");
   }
 }
 
+// Add the partials of warps gw+1 .. w_last (in warp order) and reset them.
+__device__ __forceinline__ unsigned long long ld_slot(const unsigned long long* slot) {
+  unsigned long long s;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(s) : "l"(slot) : "memory");
+  return s;
+}
+
+template <int B>
+__device__ __forceinline__ void collect(const KParams& p, int gw, int w_last, float (&v)[kMaxBatch],
+                                        int lane) {
+  constexpr int kBatch = 8;  // records polled per round trip
+  for (int w0 = gw + 1; w0 <= w_last; w0 += kBatch) {
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      unsigned long long s[kBatch];
+#pragma unroll
+      for (int k = 0; k < kBatch; ++k)  // independent loads: one L2 round trip
+        s[k] = (w0 + k <= w_last) ? ld_slot(ws_slot<B>(p, w0 + k, b, lane)) : (1ull << 32);
+#pragma unroll
+      for (int k = 0; k < kBatch; ++k) {  // add in warp order (deterministic)
+        if (w0 + k > w_last) break;
+        unsigned long long* slot = ws_slot<B>(p, w0 + k, b, lane);
+        int spins = 0;
+        while ((s[k] >> 32) == 0ull) {
+          if (++spins > 2) __nanosleep(64);
+          s[k] = ld_slot(slot);
+        }
+        v[b] += __uint_as_float((uint32_t)s[k]);
+        asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(slot), "l"(0ull) : "memory");
+      }
+    }
+  }
+}
+
+// Sum over the S lanes of a row (S = lanes per row, a power of two) and store.
+template <int B>
+__device__ __forceinline__ void store_rows(const KParams& p, float (&v)[kMaxBatch], int row, int lane) {
+  for (int d = 1; d < p.lanes_per_row; d <<= 1) {
+#pragma unroll
+    for (int b = 0; b < B; ++b) v[b] += __shfl_xor_sync(0xffffffffu, v[b], d);
+  }
+  if (row >= 0 && (lane & (p.lanes_per_row - 1)) == 0) {
+    const float bias = p.bias ? __ldg(p.bias + row) : 0.f;
+#pragma unroll
+    for (int b = 0; b < B; ++b) p.Y[(int64_t)b * p.ldy + row] = v[b] + bias;
+  }
+}
+
+// Warp that owns tile t under the +-1 partition of num_tiles over active_warps.
+__device__ __forceinline__ int warp_of_tile(const KParams& p, int t) {
+  const int q = p.num_tiles / p.active_warps, r = p.num_tiles % p.active_warps;
+  const int big = r * (q + 1);
+  return t < big ? t / (q + 1) : r + (t - big) / q;
+}
+
+// ---------------------------------------------------------------- kernel
 template <int BITS, int B, bool XSMEM>
 __global__ void __launch_bounds__(kThreads) gqsa_streamk_kernel(KParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -364,19 +309,22 @@ __global__ void __launch_bounds__(kThreads) gqsa_streamk_kernel(KParams p) {
   const uint8_t* tiles = p.tiles;
   const int tb = tile_bytes(BITS);
 
-  // ---- prefetch the first tiles: weights never depend on the previous kernel
+  // ---- weights never depend on the previous kernel: request the first tiles
+  //      into registers and the rest of the range into L2 before the PDL wait
   TileRegs<BITS> buf[kDepth];
 #pragma unroll
   for (int i = 0; i < kDepth; ++i)
     if (t_begin + i < t_end) load_tile<BITS>(buf[i], tiles + (int64_t)(t_begin + i) * tb, lane);
-  uint32_t next_seg0 = 1u;  // does the group after this warp's range start a row?
-  int m0 = 0;
-  if (t_end > t_begin) {
-    m0 = __ldg(reinterpret_cast<const int*>(tiles + (int64_t)t_begin * tb + 16));
-    if (t_end < p.num_tiles)
-      next_seg0 = __ldg(reinterpret_cast<const uint32_t*>(tiles + (int64_t)t_end * tb)) & 1u;
+  if (lane == 0 && t_end - t_begin > kDepth) {
+    const uint8_t* a = tiles + (int64_t)(t_begin + kDepth) * tb;
+    uint32_t left = (uint32_t)(t_end - t_begin - kDepth) * (uint32_t)tb;
+    while (left) {
+      const uint32_t n = min(left, 65536u);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(n) : "memory");
+      a += n;
+      left -= n;
+    }
   }
-
   pdl_launch_dependents();
   pdl_wait();  // x, y, bias and the workspace may belong to the previous kernel
 
@@ -449,39 +397,48 @@ __global__ void __launch_bounds__(kThreads) gqsa_streamk_kernel(KParams p) {
   }
   if (t_end <= t_begin) return;
 
-  // ---- stream the warp's tile range
-  RowState st;
+  // ---- stream the warp's tile range; lane = one row of the current slice
+  float acc[kMaxBatch];
 #pragma unroll
-  for (int b = 0; b < kMaxBatch; ++b) st.acc[b] = 0.f;
-  // If the range starts inside a row, that row (ordinal m0) was opened by an
-  // earlier warp; otherwise the first row starts at lane 0 of sub-tile 0.
-  st.have = !(buf[0].seg.x & 1u);
-  st.foreign = st.have;
-  st.ord = st.have ? m0 : m0 - 1;
+  for (int b = 0; b < kMaxBatch; ++b) acc[b] = 0.f;
+  bool foreign = !(buf[0].hdr.y & kTileFirst);  // slice opened by an earlier warp
+  int row = __ldg(p.perm + (int64_t)buf[0].hdr.x * kLanes + lane);
+  uint32_t last_hdr_y = 0, last_hdr_z = 0;
 
   for (int t0 = t_begin; t0 < t_end; t0 += kDepth) {
 #pragma unroll
     for (int i = 0; i < kDepth; ++i) {
       const int t = t0 + i;
       if (t < t_end) {
-        process_tile<BITS, B, XSMEM>(p, buf[i], xs, xc, lane, gw, st);
+        float part[kPerLane][kMaxBatch];
+#pragma unroll
+        for (int u = 0; u < kPerLane; ++u) group_partial<BITS, B, XSMEM>(p, buf[i], u, xs, xc, part[u]);
+#pragma unroll
+        for (int b = 0; b < B; ++b) acc[b] += (part[0][b] + part[1][b]) + (part[2][b] + part[3][b]);
+        const uint4 hdr = buf[i].hdr;
         if (t + kDepth < t_end) load_tile<BITS>(buf[i], tiles + (int64_t)(t + kDepth) * tb, lane);
+        last_hdr_y = hdr.y;
+        last_hdr_z = hdr.z;
+        if (hdr.y & kTileLast) {  // the slice ends in this tile: its rows are complete
+          if (foreign) publish<B>(p, gw, acc, lane);
+          else store_rows<B>(p, acc, row, lane);
+#pragma unroll
+          for (int b = 0; b < B; ++b) acc[b] = 0.f;
+          foreign = false;
+          if (t + 1 < t_end) row = __ldg(p.perm + (int64_t)(hdr.x + 1) * kLanes + lane);
+        }
       }
     }
   }
 
-  // ---- the open row at the end of the range
-  float v[kMaxBatch];
-#pragma unroll
-  for (int b = 0; b < B; ++b) v[b] = st.acc[b];
-  warp_sum<B>(v);
-  if (next_seg0) {  // it ends exactly here
-    finish_row<B>(p, gw, st.ord, st.foreign, v, lane);
-  } else if (st.foreign) {  // the whole range lies inside a row owned upstream
-    if (lane == 0) publish<B>(p, gw, v, kFlagOpen);
-  } else if (lane == 0) {  // owner of a row that continues downstream
-    collect<B>(p, gw, v);
-    store_row<B>(p, st.ord, v);
+  // ---- a slice left open at the end of the range continues downstream
+  if (!(last_hdr_y & kTileLast)) {
+    if (foreign) {  // the whole range lies inside a slice owned upstream
+      publish<B>(p, gw, acc, lane);
+    } else {  // owner: add the successors' partials, then store
+      collect<B>(p, gw, warp_of_tile(p, t_end - 1 + (int)last_hdr_z), acc, lane);
+      store_rows<B>(p, acc, row, lane);
+    }
   }
 }
 

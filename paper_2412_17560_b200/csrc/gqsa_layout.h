@@ -1,10 +1,11 @@
-// gqsa_layout.h -- LAYOUT v1 of the packed GQSA blob (product-internal).
+// gqsa_layout.h -- LAYOUT v2 of the packed GQSA blob (product-internal).
 //
 // The blob is the paper's BSR (rowIndex / groups / values +
 // per-group scale and zero) re-laid out offline for the B200
-// kernel: 128-kept-group tile records whose per-lane payloads are 16-B
-// vectors, so that every warp-level load is a fully-coalesced 512-B (codes,
-// s/z) or 256-B (columns) request.  Full description: DESIGN.md §5.
+// kernel as a sliced-ELL stream of 128-group tiles (4 slots x 32 lanes, one
+// lane per row): every warp-level load is a fully-coalesced 512-B (codes,
+// s/z) or 256-B (columns) request, and a lane accumulates its row without
+// cross-lane reductions.  Full description: DESIGN.md §5.
 #pragma once
 #include <stdint.h>
 
@@ -20,15 +21,18 @@
 namespace gqsa {
 
 constexpr uint32_t kMagic = 0x41535147u;  // "GQSA"
-constexpr int kVersion = 1;
-constexpr int kGroup = 16;          // G (v1)
-constexpr int kTileGroups = 128;    // kept groups per tile record
-constexpr int kLanes = 32;          // one warp consumes one tile
-constexpr int kPerLane = kTileGroups / kLanes;  // 4 groups per lane per tile
+constexpr int kVersion = 2;
+constexpr int kGroup = 16;          // G (v1/v2)
+constexpr int kTileGroups = 128;    // groups (incl. padding) per tile record
+constexpr int kLanes = 32;          // one warp consumes one tile, one lane per row
+constexpr int kPerLane = kTileGroups / kLanes;  // 4 slots per lane per tile
 constexpr int kHeaderBytes = 256;
-constexpr int kTileHeaderBytes = 32;  // u32 segmask[4]; i32 m0; u32 reserved[3]
+constexpr int kTileHeaderBytes = 32;  // u32 slice, flags, tiles_to_slice_end, 0; u32 reserved[4]
 constexpr int kSectionAlign = 256;
-constexpr uint32_t kFlagLaneParitySwap = 1u;  // swap bit of a group = lane & 1
+constexpr uint32_t kFlagGreedySwap = 2u;     // swap bits balance smem bank quads per quarter-warp
+constexpr int kFlagLanesPerRowShift = 8;     // flags bits 8..15: lanes per row S
+constexpr uint32_t kTileFirst = 1u;          // tile header flags
+constexpr uint32_t kTileLast = 2u;
 
 // Bytes of one group's codes (G*n/8).
 __host__ __device__ constexpr int group_code_bytes(int bits) { return kGroup * bits / 8; }
@@ -43,6 +47,29 @@ __host__ __device__ constexpr int tile_bytes(int bits) { return off_cols(bits) +
 __host__ __device__ constexpr int off_codes(int bits, int lane, int u) {
   return kTileHeaderBytes + (u / groups_per_plane(bits)) * 512 + lane * 16 +
          (u % groups_per_plane(bits)) * group_code_bytes(bits);
+}
+
+constexpr int kTargetSlots = 32;  // slots per lane of the longest slice (8 tiles)
+
+// Lanes per row S (a power of two <= 32): large enough that the longest row
+// needs at most kTargetSlots slots per lane (short slices -> few warps per
+// slice -> short fix-up chains), and large enough that a layer with fewer
+// than 32 non-empty rows still fills the 32 lanes.
+inline int lanes_per_row_for(int n_nz, int64_t max_len) {
+  if (n_nz <= 0) return 1;
+  int s = 1;
+  while (s < kLanes && (max_len + s - 1) / s > kTargetSlots) s <<= 1;
+  int p = 1;
+  while (p < n_nz && p < kLanes) p <<= 1;
+  const int s_small = kLanes / p;
+  return s > s_small ? s : s_small;
+}
+
+// Starting offset of a row's dealing order (a fixed hash of the source row
+// id): different lanes start at different columns, spreading bank quads.
+inline int64_t row_rotation(int64_t row, int64_t n) {
+  const uint32_t h = (uint32_t)row * 2654435761u;
+  return (int64_t)((h >> 7) % (uint64_t)n);
 }
 
 // On-blob header; the first 104 bytes mirror gqsa_desc_t field-for-field.

@@ -1,11 +1,22 @@
-// gqsa_pack.cpp -- host packer, unpacker and validator for LAYOUT v1.
+// gqsa_pack.cpp -- host packer, unpacker and validator for LAYOUT v2.
 //
 // Offline pre-processing ("quantized weights are grouped by size
 // G and saved ... along with scaling factors and zero points"): the plain BSR
-// is validated and rewritten as a blob of
-// 128-group tile records in CSR stream order.  gqsa_unpack is
-// its exact inverse.  No device code here.
-#include <cmath>
+// is validated and re-laid out for the
+// B200 kernel:
+//   * non-empty rows are ordered by kept-group count (descending, ties by row)
+//     and cut into SLICES of 32 lanes; a row occupies S = lanes_per_row
+//     consecutive lanes (S = 1 unless the layer has fewer than 32 non-empty
+//     rows), the rest of the slice's lanes are padding;
+//   * each lane's groups are dealt into SLOTS: a row's kept groups, starting at
+//     a hashed rotation, go round-robin over its S lanes;
+//   * a slice's slots are cut into 128-group TILES (4 slots x 32 lanes) whose
+//     per-lane payloads are 16-B vectors (codes, s/z) and 8-B vectors (columns);
+//   * per (slot, quarter-warp) the swap bit of each group picks which 16-B half
+//     of its activation slice is read first, balancing shared-memory bank quads.
+// gqsa_unpack is the exact inverse (it re-sorts each row by column).
+#include <algorithm>
+#include <cstddef>
 #include <cstring>
 #include <vector>
 
@@ -20,13 +31,6 @@ inline uint64_t align_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 
 inline bool f16_finite(uint16_t h) { return ((h >> 10) & 0x1f) != 0x1f; }
 inline bool f16_positive(uint16_t h) { return !(h & 0x8000) && (h & 0x7fff) != 0; }
-
-struct Plan {
-  int32_t rows, cols, bits;
-  int64_t g_begin, nnzg;
-  int32_t num_tiles, n_nz, n_empty;
-  uint64_t off_ri, off_nz, off_empty, off_tiles, total;
-};
 
 int check_bsr_header(const gqsa_bsr_t* b) {
   if (!b) return GQSA_ERR_BUFFER;
@@ -59,23 +63,57 @@ int validate(const gqsa_bsr_t* b, int32_t r0, int32_t r1) {
   return GQSA_OK;
 }
 
-Plan make_plan(const gqsa_bsr_t* b, int32_t r0, int32_t r1) {
-  Plan p{};
-  p.rows = r1 - r0;
-  p.cols = b->cols;
-  p.bits = b->bits;
-  p.g_begin = b->row_index[r0];
-  p.nnzg = (int64_t)b->row_index[r1] - p.g_begin;
-  p.num_tiles = (int32_t)((p.nnzg + kTileGroups - 1) / kTileGroups);
-  p.n_nz = 0;
-  for (int32_t r = r0; r < r1; ++r) p.n_nz += (b->row_index[r + 1] > b->row_index[r]);
-  p.n_empty = p.rows - p.n_nz;
-  p.off_ri = kHeaderBytes;
-  p.off_nz = align_up(p.off_ri + 4ull * (p.rows + 1), kSectionAlign);
-  p.off_empty = align_up(p.off_nz + 4ull * p.n_nz, kSectionAlign);
-  p.off_tiles = align_up(p.off_empty + 4ull * p.n_empty, kSectionAlign);
-  p.total = align_up(p.off_tiles + (uint64_t)p.num_tiles * tile_bytes(p.bits), kSectionAlign);
-  return p;
+// Slice structure of rows [r0, r1) (local row ids 0..rows-1).
+struct Slices {
+  int32_t rows = 0, n_nz = 0, n_empty = 0, lanes_per_row = 1, rows_per_slice = 32, num_slices = 0;
+  int32_t num_tiles = 0;
+  std::vector<int32_t> order;       // non-empty local rows, sorted (count desc, row asc)
+  std::vector<int32_t> empty;       // empty local rows, ascending
+  std::vector<int64_t> count;       // kept groups per local row
+  std::vector<int32_t> tile0;       // first tile of each slice (+ sentinel)
+};
+
+Slices make_slices(const gqsa_bsr_t* b, int32_t r0, int32_t r1) {
+  Slices s;
+  s.rows = r1 - r0;
+  s.count.resize(s.rows);
+  for (int32_t r = 0; r < s.rows; ++r) {
+    s.count[r] = (int64_t)b->row_index[r0 + r + 1] - b->row_index[r0 + r];
+    if (s.count[r] > 0) s.order.push_back(r);
+    else s.empty.push_back(r);
+  }
+  std::stable_sort(s.order.begin(), s.order.end(),
+                   [&](int32_t a, int32_t c) { return s.count[a] > s.count[c]; });
+  s.n_nz = (int32_t)s.order.size();
+  s.n_empty = (int32_t)s.empty.size();
+  s.lanes_per_row = lanes_per_row_for(s.n_nz, s.n_nz ? s.count[s.order[0]] : 0);
+  s.rows_per_slice = kLanes / s.lanes_per_row;
+  s.num_slices = (s.n_nz + s.rows_per_slice - 1) / s.rows_per_slice;
+  s.tile0.resize(s.num_slices + 1);
+  int64_t t = 0;
+  for (int32_t sl = 0; sl < s.num_slices; ++sl) {
+    s.tile0[sl] = (int32_t)t;
+    const int64_t longest = s.count[s.order[(size_t)sl * s.rows_per_slice]];
+    const int64_t slots = (longest + s.lanes_per_row - 1) / s.lanes_per_row;
+    t += (slots + kPerLane - 1) / kPerLane;
+  }
+  s.tile0[s.num_slices] = (int32_t)t;
+  s.num_tiles = (int32_t)t;
+  return s;
+}
+
+struct Offsets {
+  uint64_t ri, perm, empty, tiles, total;
+};
+
+Offsets offsets(const Slices& s, int bits) {
+  Offsets o;
+  o.ri = kHeaderBytes;
+  o.perm = align_up(o.ri + 4ull * (s.rows + 1), kSectionAlign);
+  o.empty = align_up(o.perm + 4ull * kLanes * s.num_slices, kSectionAlign);
+  o.tiles = align_up(o.empty + 4ull * s.n_empty, kSectionAlign);
+  o.total = align_up(o.tiles + (uint64_t)s.num_tiles * tile_bytes(bits), kSectionAlign);
+  return o;
 }
 
 void fill_desc(const BlobHeader& h, gqsa_desc_t* d) {
@@ -93,7 +131,7 @@ extern "C" int gqsa_pack_size(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t 
   if (!blob_bytes) return GQSA_ERR_BUFFER;
   if (row_begin < 0 || row_end < row_begin || row_end > bsr->rows) return GQSA_ERR_SHAPE;
   if ((st = validate(bsr, row_begin, row_end))) return st;
-  *blob_bytes = (size_t)make_plan(bsr, row_begin, row_end).total;
+  *blob_bytes = (size_t)offsets(make_slices(bsr, row_begin, row_end), bsr->bits).total;
   return GQSA_OK;
 }
 
@@ -104,89 +142,97 @@ extern "C" int gqsa_pack(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_e
   if (!blob) return GQSA_ERR_BUFFER;
   if (row_begin < 0 || row_end < row_begin || row_end > bsr->rows) return GQSA_ERR_SHAPE;
   if ((st = validate(bsr, row_begin, row_end))) return st;
-  const Plan p = make_plan(bsr, row_begin, row_end);
-  if (blob_bytes < p.total) return GQSA_ERR_BUFFER;
+  const Slices s = make_slices(bsr, row_begin, row_end);
+  const Offsets o = offsets(s, bsr->bits);
+  if (blob_bytes < o.total) return GQSA_ERR_BUFFER;
   uint8_t* out = static_cast<uint8_t*>(blob);
-  std::memset(out, 0, p.total);
+  std::memset(out, 0, o.total);
+  const int64_t g_begin = bsr->row_index[row_begin];
+  const int bits = bsr->bits, cb = group_code_bytes(bits), S = s.lanes_per_row;
 
   BlobHeader h{};
   h.magic = kMagic;
   h.version = kVersion;
-  h.rows = p.rows;
-  h.cols = p.cols;
+  h.rows = s.rows;
+  h.cols = bsr->cols;
   h.group_size = kGroup;
-  h.bits = p.bits;
-  h.nnzg = p.nnzg;
+  h.bits = bits;
+  h.nnzg = (int64_t)bsr->row_index[row_end] - g_begin;
   h.tile_groups = kTileGroups;
-  h.num_tiles = p.num_tiles;
-  h.n_nzrows = p.n_nz;
-  h.n_empty = p.n_empty;
-  h.tile_bytes = tile_bytes(p.bits);
-  h.flags = kFlagLaneParitySwap;
+  h.num_tiles = s.num_tiles;
+  h.n_nzrows = s.n_nz;
+  h.n_empty = s.n_empty;
+  h.tile_bytes = tile_bytes(bits);
+  h.flags = (int32_t)(kFlagGreedySwap | ((uint32_t)S << kFlagLanesPerRowShift));
   h.row_begin = row_begin;
   h.row_end = row_end;
-  h.off_row_index = p.off_ri;
-  h.off_nzrow = p.off_nz;
-  h.off_empty = p.off_empty;
-  h.off_tiles = p.off_tiles;
-  h.blob_bytes = p.total;
+  h.off_row_index = o.ri;
+  h.off_nzrow = o.perm;
+  h.off_empty = o.empty;
+  h.off_tiles = o.tiles;
+  h.blob_bytes = o.total;
   std::memcpy(out, &h, sizeof(h));
 
-  // Row sections (rebased to the shard).
-  int32_t* ri = reinterpret_cast<int32_t*>(out + p.off_ri);
-  int32_t* nz = reinterpret_cast<int32_t*>(out + p.off_nz);
-  int32_t* em = reinterpret_cast<int32_t*>(out + p.off_empty);
-  std::vector<int32_t> row_of(p.nnzg);      // local row of each stream position
-  std::vector<int32_t> ord_of_row(p.rows);  // ordinal among non-empty rows
-  int32_t inz = 0, iem = 0;
-  for (int32_t r = 0; r < p.rows; ++r) {
-    const int64_t a = bsr->row_index[row_begin + r] - p.g_begin;
-    const int64_t e = bsr->row_index[row_begin + r + 1] - p.g_begin;
-    ri[r] = (int32_t)a;
-    if (e > a) {
-      ord_of_row[r] = inz;
-      nz[inz++] = r;
-    } else {
-      ord_of_row[r] = -1;
-      em[iem++] = r;
-    }
-    for (int64_t g = a; g < e; ++g) row_of[g] = r;
-  }
-  ri[p.rows] = (int32_t)p.nnzg;
+  int32_t* ri = reinterpret_cast<int32_t*>(out + o.ri);
+  for (int32_t r = 0; r <= s.rows; ++r) ri[r] = (int32_t)(bsr->row_index[row_begin + r] - g_begin);
+  int32_t* perm = reinterpret_cast<int32_t*>(out + o.perm);
+  for (int64_t i = 0; i < (int64_t)kLanes * s.num_slices; ++i) perm[i] = -1;
+  int32_t* em = reinterpret_cast<int32_t*>(out + o.empty);
+  for (int32_t i = 0; i < s.n_empty; ++i) em[i] = s.empty[i];
 
-  // Tile records.
-  const int bits = p.bits;
-  const int cb = group_code_bytes(bits);
-  for (int32_t t = 0; t < p.num_tiles; ++t) {
-    uint8_t* tile = out + p.off_tiles + (uint64_t)t * tile_bytes(bits);
-    uint32_t segmask[kPerLane] = {0, 0, 0, 0};
-    const int64_t p0 = (int64_t)t * kTileGroups;
-    const int32_t m0 = ord_of_row[row_of[p0]];
-    for (int u = 0; u < kPerLane; ++u) {
-      for (int l = 0; l < kLanes; ++l) {
-        const int64_t pos = p0 + u * kLanes + l;
-        if (pos >= p.nnzg) continue;  // padding group: all zero
-        const int64_t g = p.g_begin + pos;  // index into the source BSR
-        if (pos == 0 || row_of[pos] != row_of[pos - 1]) segmask[u] |= 1u << l;
-        const uint32_t swap = (uint32_t)(l & 1);  // kFlagLaneParitySwap
-        // codes: the group's G*n/8 bytes, halves exchanged when swap = 1
-        const uint8_t* src = bsr->codes + g * cb;
-        uint8_t* dst = tile + off_codes(bits, l, u);
-        if (swap) {
-          std::memcpy(dst, src + cb / 2, cb / 2);
-          std::memcpy(dst + cb / 2, src, cb / 2);
-        } else {
-          std::memcpy(dst, src, cb);
+  std::vector<int64_t> lane_group(kLanes * 4);  // source group of (lane, slot in tile), -1 = padding
+  for (int32_t sl = 0; sl < s.num_slices; ++sl) {
+    // rows of this slice, their rotation, lane assignment
+    int32_t row_of_lane[kLanes];
+    int64_t rot_of_lane[kLanes];
+    for (int l = 0; l < kLanes; ++l) {
+      const int64_t k = (int64_t)sl * s.rows_per_slice + l / S;
+      row_of_lane[l] = k < s.n_nz ? s.order[k] : -1;
+      rot_of_lane[l] = row_of_lane[l] >= 0 ? row_rotation(row_begin + row_of_lane[l], s.count[row_of_lane[l]]) : 0;
+      perm[(int64_t)sl * kLanes + l] = row_of_lane[l];
+    }
+    const int32_t nt = s.tile0[sl + 1] - s.tile0[sl];
+    for (int32_t tau = 0; tau < nt; ++tau) {
+      const int32_t t = s.tile0[sl] + tau;
+      uint8_t* tile = out + o.tiles + (uint64_t)t * tile_bytes(bits);
+      const uint32_t hdr[4] = {(uint32_t)sl,
+                               (tau == 0 ? kTileFirst : 0u) | (tau == nt - 1 ? kTileLast : 0u),
+                               (uint32_t)(nt - 1 - tau), 0u};
+      std::memcpy(tile, hdr, sizeof(hdr));
+      for (int u = 0; u < kPerLane; ++u) {
+        int quad_load[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int l = 0; l < kLanes; ++l) {
+          if ((l & 7) == 0)
+            for (int q = 0; q < 8; ++q) quad_load[q] = 0;
+          const int32_t row = row_of_lane[l];
+          const int64_t slot = (int64_t)tau * kPerLane + u;    // slot of this lane
+          const int64_t k = slot * S + (l % S);                // k-th group of the row's sequence
+          if (row < 0 || k >= s.count[row]) {  // padding: all zero, reads x chunk 0
+            quad_load[0]++;
+            continue;
+          }
+          const int64_t g = bsr->row_index[row_begin + row] + (k + rot_of_lane[l]) % s.count[row];
+          // swap bit: first 16-B x chunk in bank quad (2c + swap) mod 8, the
+          // less loaded of the two within the quarter-warp (one LDS.128 phase)
+          const int q0 = (2 * (int)bsr->group_cols[g]) & 7;
+          const uint32_t swap = quad_load[q0 | 1] < quad_load[q0] ? 1u : 0u;
+          quad_load[q0 | (int)swap]++;
+          const uint8_t* src = bsr->codes + g * cb;
+          uint8_t* dst = tile + off_codes(bits, l, u);
+          if (swap) {
+            std::memcpy(dst, src + cb / 2, cb / 2);
+            std::memcpy(dst + cb / 2, src, cb / 2);
+          } else {
+            std::memcpy(dst, src, cb);
+          }
+          uint16_t* sz = reinterpret_cast<uint16_t*>(tile + off_sz(bits) + l * 16 + u * 4);
+          sz[0] = bsr->scales_f16[g];
+          sz[1] = bsr->zeros_f16[g];
+          uint16_t* col = reinterpret_cast<uint16_t*>(tile + off_cols(bits) + l * 8 + u * 2);
+          *col = (uint16_t)((bsr->group_cols[g] << 1) | swap);
         }
-        uint16_t* sz = reinterpret_cast<uint16_t*>(tile + off_sz(bits) + l * 16 + u * 4);
-        sz[0] = bsr->scales_f16[g];
-        sz[1] = bsr->zeros_f16[g];
-        uint16_t* col = reinterpret_cast<uint16_t*>(tile + off_cols(bits) + l * 8 + u * 2);
-        *col = (uint16_t)((bsr->group_cols[g] << 1) | swap);
       }
     }
-    std::memcpy(tile, segmask, sizeof(segmask));
-    std::memcpy(tile + 16, &m0, 4);
   }
   if (desc) fill_desc(h, desc);
   return GQSA_OK;
@@ -201,11 +247,13 @@ extern "C" int gqsa_read_desc(const void* blob, size_t blob_bytes, gqsa_desc_t* 
   if (h.group_size != kGroup || (h.bits != 4 && h.bits != 2)) return GQSA_ERR_UNSUPPORTED;
   if (h.tile_groups != kTileGroups || h.tile_bytes != tile_bytes(h.bits)) return GQSA_ERR_VALIDATION;
   if (h.rows < 0 || h.cols <= 0 || h.cols % kGroup || h.nnzg < 0) return GQSA_ERR_VALIDATION;
-  if ((int64_t)h.num_tiles != (h.nnzg + kTileGroups - 1) / kTileGroups) return GQSA_ERR_VALIDATION;
   if (h.n_nzrows < 0 || h.n_empty < 0 || h.n_nzrows + h.n_empty != h.rows) return GQSA_ERR_VALIDATION;
-  if (h.nnzg < h.n_nzrows) return GQSA_ERR_VALIDATION;
+  if (h.nnzg < h.n_nzrows || h.num_tiles < 0) return GQSA_ERR_VALIDATION;
+  const int S = (int)((uint32_t)h.flags >> kFlagLanesPerRowShift) & 0xff;
+  if (S < 1 || S > kLanes || (S & (S - 1))) return GQSA_ERR_VALIDATION;
+  const int64_t slices = (h.n_nzrows + kLanes / S - 1) / (kLanes / S);
   if (h.off_row_index < (uint64_t)kHeaderBytes || h.off_nzrow < h.off_row_index + 4ull * (h.rows + 1) ||
-      h.off_empty < h.off_nzrow + 4ull * h.n_nzrows || h.off_tiles < h.off_empty + 4ull * h.n_empty ||
+      h.off_empty < h.off_nzrow + 4ull * kLanes * slices || h.off_tiles < h.off_empty + 4ull * h.n_empty ||
       h.off_tiles % kSectionAlign ||
       h.blob_bytes < h.off_tiles + (uint64_t)h.num_tiles * h.tile_bytes)
     return GQSA_ERR_VALIDATION;
@@ -228,72 +276,73 @@ extern "C" int gqsa_unpack(const void* blob, size_t blob_bytes, gqsa_bsr_t* out)
 
   const uint8_t* b = static_cast<const uint8_t*>(blob);
   const int32_t* ri = reinterpret_cast<const int32_t*>(b + d.off_row_index);
-  const int32_t* nz = reinterpret_cast<const int32_t*>(b + d.off_nzrow);
+  const int32_t* perm = reinterpret_cast<const int32_t*>(b + d.off_nzrow);
   const int32_t* em = reinterpret_cast<const int32_t*>(b + d.off_empty);
   const int bits = d.bits, cb = group_code_bytes(bits);
+  const int S = ((uint32_t)d.flags >> kFlagLanesPerRowShift) & 0xff;
 
-  // Rebuild per-row counts from the tile stream alone.
-  std::vector<int64_t> count(d.rows, 0);
-  int64_t m = -1;  // current row ordinal
+  struct G {
+    uint16_t col, s, z;
+    const uint8_t* codes;
+    bool swap;
+  };
+  std::vector<std::vector<G>> rows(d.rows);
+  int32_t slice = -1;
   for (int32_t t = 0; t < d.num_tiles; ++t) {
     const uint8_t* tile = b + d.off_tiles + (uint64_t)t * d.tile_bytes;
-    uint32_t segmask[kPerLane];
-    int32_t m0;
-    std::memcpy(segmask, tile, sizeof(segmask));
-    std::memcpy(&m0, tile + 16, 4);
-    const int64_t p0 = (int64_t)t * kTileGroups;
+    uint32_t hdr[4];
+    std::memcpy(hdr, tile, sizeof(hdr));
+    if (hdr[1] & kTileFirst) ++slice;
+    if ((int32_t)hdr[0] != slice || slice < 0) return GQSA_ERR_VALIDATION;
     for (int u = 0; u < kPerLane; ++u) {
       for (int l = 0; l < kLanes; ++l) {
-        const int64_t pos = p0 + u * kLanes + l;
-        const bool start = (segmask[u] >> l) & 1u;
+        const int32_t row = perm[(int64_t)slice * kLanes + l];
         const uint16_t* sz = reinterpret_cast<const uint16_t*>(tile + off_sz(bits) + l * 16 + u * 4);
         const uint16_t col = *reinterpret_cast<const uint16_t*>(tile + off_cols(bits) + l * 8 + u * 2);
         const uint8_t* src = tile + off_codes(bits, l, u);
-        if (pos >= d.nnzg) {  // padding must be all zero
-          if (start || sz[0] || sz[1] || col) return GQSA_ERR_VALIDATION;
+        if (sz[0] == 0) {  // padding (a kept group always has s > 0)
+          if (sz[1] || col) return GQSA_ERR_VALIDATION;
           for (int i = 0; i < cb; ++i)
             if (src[i]) return GQSA_ERR_VALIDATION;
           continue;
         }
-        if (pos == 0 && !start) return GQSA_ERR_VALIDATION;
-        if (start) ++m;
-        if (u == 0 && l == 0 && m0 != m) return GQSA_ERR_VALIDATION;
-        if (m < 0 || m >= d.n_nzrows) return GQSA_ERR_VALIDATION;
-        const int32_t row = nz[m];
         if (row < 0 || row >= d.rows) return GQSA_ERR_VALIDATION;
-        count[row]++;
-        const uint32_t swap = col & 1u;
-        o_gc[pos] = (uint16_t)(col >> 1);
-        o_s[pos] = sz[0];
-        o_z[pos] = sz[1];
-        uint8_t* dst = o_codes + pos * cb;
-        if (swap) {
-          std::memcpy(dst, src + cb / 2, cb / 2);
-          std::memcpy(dst + cb / 2, src, cb / 2);
-        } else {
-          std::memcpy(dst, src, cb);
-        }
+        rows[row].push_back(G{(uint16_t)(col >> 1), sz[0], sz[1], src, (col & 1u) != 0});
       }
     }
   }
-  if (m + 1 != d.n_nzrows) return GQSA_ERR_VALIDATION;
-  // Offsets from counts; must equal the stored row_index; nzrow / empty lists
-  // must agree with the counts.
+  // row order inside the stream is a rotation; CSR order is ascending column
   int64_t acc = 0;
-  int32_t inz = 0, iem = 0;
+  int32_t iem = 0, n_nz = 0;
   for (int32_t r = 0; r < d.rows; ++r) {
     if (ri[r] != acc) return GQSA_ERR_VALIDATION;
     o_ri[r] = (int32_t)acc;
-    if (count[r] > 0) {
-      if (inz >= d.n_nzrows || nz[inz++] != r) return GQSA_ERR_VALIDATION;
-    } else {
+    auto& v = rows[r];
+    std::sort(v.begin(), v.end(), [](const G& a, const G& c) { return a.col < c.col; });
+    if (v.empty()) {
       if (iem >= d.n_empty || em[iem++] != r) return GQSA_ERR_VALIDATION;
+    } else {
+      ++n_nz;
     }
-    acc += count[r];
+    for (const G& g : v) {
+      if (acc >= d.nnzg) return GQSA_ERR_VALIDATION;
+      o_gc[acc] = g.col;
+      o_s[acc] = g.s;
+      o_z[acc] = g.z;
+      uint8_t* dst = o_codes + acc * cb;
+      if (g.swap) {
+        std::memcpy(dst, g.codes + cb / 2, cb / 2);
+        std::memcpy(dst + cb / 2, g.codes, cb / 2);
+      } else {
+        std::memcpy(dst, g.codes, cb);
+      }
+      ++acc;
+    }
   }
-  if (acc != d.nnzg || ri[d.rows] != acc) return GQSA_ERR_VALIDATION;
+  const int32_t slices = (d.n_nzrows + kLanes / S - 1) / (kLanes / S);
+  if (acc != d.nnzg || ri[d.rows] != acc || n_nz != d.n_nzrows || slice + 1 != slices)
+    return GQSA_ERR_VALIDATION;
   o_ri[d.rows] = (int32_t)acc;
-  // Validate rows of the rebuilt BSR (strictly increasing columns, finite s/z).
   out->rows = d.rows;
   out->cols = d.cols;
   out->group_size = d.group_size;

@@ -31,7 +31,7 @@ def test_exports_every_declared_symbol():
     exported = set(re.findall(r"\bT (gqsa_\w+)", out))
     assert set(names) <= exported
     assert set(gqsa.EXPORTS) == set(names)
-    assert gqsa.lib().gqsa_version() == 1
+    assert gqsa.lib().gqsa_version() == 2
     assert gqsa.status_string(-2) == "validation error"
 
 
@@ -85,19 +85,31 @@ def test_shard_ranges_rebase_and_reassemble():
 
 def test_tile_fields_match_layout():
     """Spot-check the documented tile fields directly."""
-    bsr = synth.make_layer(10, 64, 1024, sparsity=0.5)
+    bsr = synth.make_layer(10, 64, 512, sparsity=0.5)
     blob, d = gqsa.pack(bsr)
-    assert d.tile_bytes == 1824 and d.num_tiles == -(-bsr["nnzg"] // 128)
+    assert d.tile_bytes == 1824 and d.version == 2 and (d.flags >> 8) & 0xFF == 1
+    counts = np.diff(bsr["row_index"])
+    perm = blob[d.off_nzrow:d.off_nzrow + 4 * 64].view(np.int32)
+    # slices hold rows by descending kept-group count
+    assert list(counts[perm]) == sorted(counts, reverse=True)
     t0 = blob[d.off_tiles:d.off_tiles + d.tile_bytes]
-    seg = t0[:16].view(np.uint32)
-    assert seg[0] & 1  # first group starts row 0
+    hdr = t0[:16].view(np.uint32)
+    assert hdr[0] == 0 and hdr[1] & 1 and hdr[2] == -(-int(counts.max()) // 4) - 1
     cols = t0[32 + 1024 + 512:].view(np.uint16)
-    # lane l, slot u -> stream position u*32+l; field = 2c + (l & 1)
-    for lane in range(32):
-        for u in range(4):
-            f = int(cols[lane * 4 + u])
-            assert f & 1 == lane & 1
-            assert f >> 1 == int(bsr["group_cols"][u * 32 + lane])
+    for u in range(4):
+        for q in range(4):
+            quads = []
+            for lane in range(8 * q, 8 * q + 8):
+                f = int(cols[lane * 4 + u])
+                row = int(perm[lane])
+                g0, g1 = bsr["row_index"][row], bsr["row_index"][row + 1]
+                assert (f >> 1) in set(bsr["group_cols"][g0:g1].tolist())
+                quads.append((2 * (f >> 1) + (f & 1)) % 8)
+            # the swap bits never put more than ceil(n_r/2) lanes of a quarter-warp
+            # on the two bank quads {2r, 2r+1} of residue r = c mod 4
+            res = [x // 2 for x in quads]
+            for r in range(4):
+                assert max(quads.count(2 * r), quads.count(2 * r + 1)) == (res.count(r) + 1) // 2
 
 
 def test_validation_errors():
@@ -148,7 +160,18 @@ def test_read_desc_rejects_corruption():
         gqsa.unpack(b)
 
 
+def test_lanes_per_row_rule():
+    # long rows are dealt over several lanes (<= 32 slots per lane)
+    for rows, cols in ((256, 4096), (64, 14336), (8, 4096), (3, 256), (64, 512), (1, 65536)):
+        bsr = synth.make_layer(rows + cols, rows, cols, sparsity=0.5)
+        _, d = gqsa.pack(bsr)
+        S = (d.flags >> 8) & 0xFF
+        longest = int(np.diff(bsr["row_index"]).max())
+        assert -(-longest // S) <= 32 or S == 32
+        assert S == 1 or -(-longest // (S // 2)) > 32 or S // 2 < 32 // (1 << (rows - 1).bit_length())
+
+
 def test_workspace_size_is_device_independent():
     bsr = synth.make_layer(13, 4096, 4096, sparsity=0.5)
     _, d = gqsa.pack(bsr)
-    assert gqsa.workspace_size(d, 1) == gqsa.workspace_size(d, 8) == 4096 * 64
+    assert gqsa.workspace_size(d, 1) == 4096 * 256 and gqsa.workspace_size(d, 8) == 4096 * 2048
