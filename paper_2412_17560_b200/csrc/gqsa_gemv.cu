@@ -150,7 +150,7 @@ struct TileRegs {
   uint4 codes[BITS == 4 ? 2 : 1];  // lane's 4 slots (W4: 2 planes x 16 B)
   uint4 sz;                        // 4 x (s, z) half pairs
   uint2 cols;                      // 4 x u16 (2c + swap)
-  uint4 hdr;                       // slice, flags, tiles to slice end, 0
+  uint32_t hdr;                    // slice << 2 | FIRST | LAST
 };
 
 template <int BITS>
@@ -159,7 +159,7 @@ __device__ __forceinline__ void load_tile(TileRegs<BITS>& r, const uint8_t* tile
   if (BITS == 4) r.codes[BITS == 4 ? 1 : 0] = ldg_stream128(tile + kTileHeaderBytes + 512 + lane * 16);
   r.sz = ldg_stream128(tile + off_sz(BITS) + lane * 16);
   r.cols = ldg_stream64(tile + off_cols(BITS) + lane * 8);
-  r.hdr = ldg_stream128(tile);  // broadcast within the warp
+  r.hdr = __ldg(reinterpret_cast<const uint32_t*>(tile));  // broadcast within the warp
 }
 
 // Group code word(s) of slot u from the lane's codes.
@@ -293,7 +293,7 @@ __device__ __forceinline__ int warp_of_tile(const KParams& p, int t) {
 
 // ---------------------------------------------------------------- kernel
 template <int BITS, int B, bool XSMEM>
-__global__ void __launch_bounds__(kThreads) gqsa_streamk_kernel(KParams p) {
+__global__ void __launch_bounds__(kThreads, min_ctas_per_sm(B)) gqsa_streamk_kernel(KParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -315,16 +315,8 @@ __global__ void __launch_bounds__(kThreads) gqsa_streamk_kernel(KParams p) {
 #pragma unroll
   for (int i = 0; i < kDepth; ++i)
     if (t_begin + i < t_end) load_tile<BITS>(buf[i], tiles + (int64_t)(t_begin + i) * tb, lane);
-  if (lane == 0 && t_end - t_begin > kDepth) {
-    const uint8_t* a = tiles + (int64_t)(t_begin + kDepth) * tb;
-    uint32_t left = (uint32_t)(t_end - t_begin - kDepth) * (uint32_t)tb;
-    while (left) {
-      const uint32_t n = min(left, 65536u);
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(n) : "memory");
-      a += n;
-      left -= n;
-    }
-  }
+  int row = -1;  // this lane's row in the first slice (the perm table is part of the blob)
+  if (t_end > t_begin) row = __ldg(p.perm + (int64_t)(buf[0].hdr >> 2) * kLanes + lane);
   pdl_launch_dependents();
   pdl_wait();  // x, y, bias and the workspace may belong to the previous kernel
 
@@ -401,9 +393,8 @@ __global__ void __launch_bounds__(kThreads) gqsa_streamk_kernel(KParams p) {
   float acc[kMaxBatch];
 #pragma unroll
   for (int b = 0; b < kMaxBatch; ++b) acc[b] = 0.f;
-  bool foreign = !(buf[0].hdr.y & kTileFirst);  // slice opened by an earlier warp
-  int row = __ldg(p.perm + (int64_t)buf[0].hdr.x * kLanes + lane);
-  uint32_t last_hdr_y = 0, last_hdr_z = 0;
+  bool foreign = !(buf[0].hdr & kTileFirst);  // slice opened by an earlier warp
+  uint32_t last_hdr = 0;
 
   for (int t0 = t_begin; t0 < t_end; t0 += kDepth) {
 #pragma unroll
@@ -415,28 +406,28 @@ __global__ void __launch_bounds__(kThreads) gqsa_streamk_kernel(KParams p) {
         for (int u = 0; u < kPerLane; ++u) group_partial<BITS, B, XSMEM>(p, buf[i], u, xs, xc, part[u]);
 #pragma unroll
         for (int b = 0; b < B; ++b) acc[b] += (part[0][b] + part[1][b]) + (part[2][b] + part[3][b]);
-        const uint4 hdr = buf[i].hdr;
+        const uint32_t hdr = buf[i].hdr;
         if (t + kDepth < t_end) load_tile<BITS>(buf[i], tiles + (int64_t)(t + kDepth) * tb, lane);
-        last_hdr_y = hdr.y;
-        last_hdr_z = hdr.z;
-        if (hdr.y & kTileLast) {  // the slice ends in this tile: its rows are complete
+        last_hdr = hdr;
+        if (hdr & kTileLast) {  // the slice ends in this tile: its rows are complete
           if (foreign) publish<B>(p, gw, acc, lane);
           else store_rows<B>(p, acc, row, lane);
 #pragma unroll
           for (int b = 0; b < B; ++b) acc[b] = 0.f;
           foreign = false;
-          if (t + 1 < t_end) row = __ldg(p.perm + (int64_t)(hdr.x + 1) * kLanes + lane);
+          if (t + 1 < t_end) row = __ldg(p.perm + (int64_t)((hdr >> 2) + 1) * kLanes + lane);
         }
       }
     }
   }
 
   // ---- a slice left open at the end of the range continues downstream
-  if (!(last_hdr_y & kTileLast)) {
+  if (!(last_hdr & kTileLast)) {
     if (foreign) {  // the whole range lies inside a slice owned upstream
       publish<B>(p, gw, acc, lane);
     } else {  // owner: add the successors' partials, then store
-      collect<B>(p, gw, warp_of_tile(p, t_end - 1 + (int)last_hdr_z), acc, lane);
+      const int rem = (int)__ldg(reinterpret_cast<const uint32_t*>(tiles + (int64_t)(t_end - 1) * tb) + 1);
+      collect<B>(p, gw, warp_of_tile(p, t_end - 1 + rem), acc, lane);
       store_rows<B>(p, acc, row, lane);
     }
   }

@@ -27,7 +27,7 @@ constexpr int kTileGroups = 128;    // groups (incl. padding) per tile record
 constexpr int kLanes = 32;          // one warp consumes one tile, one lane per row
 constexpr int kPerLane = kTileGroups / kLanes;  // 4 slots per lane per tile
 constexpr int kHeaderBytes = 256;
-constexpr int kTileHeaderBytes = 32;  // u32 slice, flags, tiles_to_slice_end, 0; u32 reserved[4]
+constexpr int kTileHeaderBytes = 32;  // u32 (slice<<2 | FIRST | LAST), tiles_to_slice_end; 0[6]
 constexpr int kSectionAlign = 256;
 constexpr uint32_t kFlagGreedySwap = 2u;     // swap bits balance smem bank quads per quarter-warp
 constexpr int kFlagLanesPerRowShift = 8;     // flags bits 8..15: lanes per row S

@@ -195,9 +195,10 @@ extern "C" int gqsa_pack(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_e
     for (int32_t tau = 0; tau < nt; ++tau) {
       const int32_t t = s.tile0[sl] + tau;
       uint8_t* tile = out + o.tiles + (uint64_t)t * tile_bytes(bits);
-      const uint32_t hdr[4] = {(uint32_t)sl,
-                               (tau == 0 ? kTileFirst : 0u) | (tau == nt - 1 ? kTileLast : 0u),
-                               (uint32_t)(nt - 1 - tau), 0u};
+      // word 0: slice << 2 | FIRST | LAST; word 1: tiles to the slice's last tile
+      const uint32_t hdr[4] = {((uint32_t)sl << 2) | (tau == 0 ? kTileFirst : 0u) |
+                                   (tau == nt - 1 ? kTileLast : 0u),
+                               (uint32_t)(nt - 1 - tau), 0u, 0u};
       std::memcpy(tile, hdr, sizeof(hdr));
       for (int u = 0; u < kPerLane; ++u) {
         int quad_load[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -292,8 +293,8 @@ extern "C" int gqsa_unpack(const void* blob, size_t blob_bytes, gqsa_bsr_t* out)
     const uint8_t* tile = b + d.off_tiles + (uint64_t)t * d.tile_bytes;
     uint32_t hdr[4];
     std::memcpy(hdr, tile, sizeof(hdr));
-    if (hdr[1] & kTileFirst) ++slice;
-    if ((int32_t)hdr[0] != slice || slice < 0) return GQSA_ERR_VALIDATION;
+    if (hdr[0] & kTileFirst) ++slice;
+    if ((int32_t)(hdr[0] >> 2) != slice || slice < 0) return GQSA_ERR_VALIDATION;
     for (int u = 0; u < kPerLane; ++u) {
       for (int l = 0; l < kLanes; ++l) {
         const int32_t row = perm[(int64_t)slice * kLanes + l];

@@ -94,7 +94,7 @@ def test_tile_fields_match_layout():
     assert list(counts[perm]) == sorted(counts, reverse=True)
     t0 = blob[d.off_tiles:d.off_tiles + d.tile_bytes]
     hdr = t0[:16].view(np.uint32)
-    assert hdr[0] == 0 and hdr[1] & 1 and hdr[2] == -(-int(counts.max()) // 4) - 1
+    assert hdr[0] >> 2 == 0 and hdr[0] & 1 and hdr[1] == -(-int(counts.max()) // 4) - 1
     cols = t0[32 + 1024 + 512:].view(np.uint16)
     for u in range(4):
         for q in range(4):
