@@ -29,12 +29,12 @@ def tile_bytes(bits: int) -> int:
     return 32 + T * 16 * bits // 8 + T * 4 + T * 2
 
 
-TARGET_SLOTS = 32
+TARGET_SLOTS = 64
 
 
 def lanes_per_row(n_nz: int, max_len: int) -> int:
     """S = the larger of (a) the smallest power of two with
-    ceil(max_len / S) <= 32 slots per lane and (b) 32 / (next power of two
+    ceil(max_len / S) <= 64 slots per lane and (b) 32 / (next power of two
     >= n_nz) when fewer than 32 rows are non-empty; capped at 32."""
     if n_nz <= 0:
         return 1

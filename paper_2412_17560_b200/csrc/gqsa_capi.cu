@@ -161,6 +161,8 @@ extern "C" int gqsa_gemm_smallbatch(const gqsa_desc_t* desc, const void* d_blob,
   p.n_empty = desc->n_empty;
   p.active_warps = pl.active_warps;
   p.lanes_per_row = ((uint32_t)desc->flags >> kFlagLanesPerRowShift) & 0xff;
+  p.part_q = pl.active_warps ? desc->num_tiles / pl.active_warps : 0;
+  p.part_r = pl.active_warps ? desc->num_tiles % pl.active_warps : 0;
   if (desc->rows == 0) return GQSA_OK;
 
   cudaLaunchConfig_t cfg = {};

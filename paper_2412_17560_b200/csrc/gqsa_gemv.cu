@@ -286,9 +286,8 @@ __device__ __forceinline__ void store_rows(const KParams& p, float (&v)[kMaxBatc
 
 // Warp that owns tile t under the +-1 partition of num_tiles over active_warps.
 __device__ __forceinline__ int warp_of_tile(const KParams& p, int t) {
-  const int q = p.num_tiles / p.active_warps, r = p.num_tiles % p.active_warps;
-  const int big = r * (q + 1);
-  return t < big ? t / (q + 1) : r + (t - big) / q;
+  const int big = p.part_r * (p.part_q + 1);
+  return t < big ? t / (p.part_q + 1) : p.part_r + (t - big) / p.part_q;
 }
 
 // ---------------------------------------------------------------- kernel
@@ -301,16 +300,15 @@ __global__ void __launch_bounds__(kThreads, min_ctas_per_sm(B)) gqsa_streamk_ker
 
   // ---- task-centric partition: contiguous tile range per warp (+-1 tile)
   int t_begin = 0, t_end = 0;
-  if (gw < p.active_warps) {
-    const int q = p.num_tiles / p.active_warps, r = p.num_tiles % p.active_warps;
-    t_begin = gw * q + min(gw, r);
-    t_end = t_begin + q + (gw < r ? 1 : 0);
+  if (gw < p.active_warps) {  // q = num_tiles / warps, r = num_tiles % warps (host)
+    t_begin = gw * p.part_q + min(gw, p.part_r);
+    t_end = t_begin + p.part_q + (gw < p.part_r ? 1 : 0);
   }
   const uint8_t* tiles = p.tiles;
   const int tb = tile_bytes(BITS);
 
   // ---- weights never depend on the previous kernel: request the first tiles
-  //      into registers and the rest of the range into L2 before the PDL wait
+  //      into registers before the PDL wait
   TileRegs<BITS> buf[kDepth];
 #pragma unroll
   for (int i = 0; i < kDepth; ++i)
@@ -369,12 +367,12 @@ __global__ void __launch_bounds__(kThreads, min_ctas_per_sm(B)) gqsa_streamk_ker
       v1 = __ldg(reinterpret_cast<const uint4*>(p.X + (int64_t)b * p.ldx) + 2 * c + 1);
     }
     const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+    const uint32_t one = 0x3C003C00u;  // half2(1, 1): x * 1 is exact, one FHFMA per element
     float acc = 0.f;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {  // t = 0..15 in order
-      const __half2 h = *reinterpret_cast<const __half2*>(&w[k]);
-      acc += __low2float(h);
-      acc += __high2float(h);
+      acc = fhfma<0, 0>(w[k], one, acc);
+      acc = fhfma<1, 0>(w[k], one, acc);
     }
     xc[i] = acc;
   }

@@ -6,13 +6,13 @@ namespace gqsa {
 
 constexpr int kThreads = 256;            // 8 warps per CTA
 constexpr int kWarps = kThreads / 32;
-constexpr int kDepth = 2;                // tiles in flight per warp (register ring)
+constexpr int kDepth = 3;                // tiles in flight per warp (register ring)
 constexpr int kMaxBatch = 8;
 constexpr int kMaxCtasPerSm = 4;
 // Register budget: 4 resident CTAs (64 regs/thread) at batch 1 -- the HBM
 // stream wants many warps with loads in flight; bigger batches need more
 // accumulators and are ALU / smem-bound anyway.
-constexpr int min_ctas_per_sm(int B) { return B == 1 ? 4 : (B <= 4 ? 2 : 1); }
+constexpr int min_ctas_per_sm(int B) { return B <= 4 ? 2 : 1; }
 constexpr int kMaxWarpsBound = 4096;     // workspace records (>= any grid we launch)
 constexpr int kWsSlotBytes = 8;          // fix-up slot {partial, flag} per (warp, batch, lane)
 constexpr int kSmemBudget = 200 * 1024;  // above this, x is gathered from L1/L2
@@ -27,6 +27,7 @@ struct KParams {
   uint32_t* ws;           // [active_warps][B][32] 8-B slots, zero between calls
   int64_t ldx, ldy;
   int32_t rows, cols, num_tiles, n_empty, active_warps, lanes_per_row;
+  int32_t part_q, part_r;  // num_tiles = part_q * active_warps + part_r
 };
 
 const void* select_kernel(int bits, int B, bool xsmem);

@@ -49,7 +49,7 @@ __host__ __device__ constexpr int off_codes(int bits, int lane, int u) {
          (u % groups_per_plane(bits)) * group_code_bytes(bits);
 }
 
-constexpr int kTargetSlots = 32;  // slots per lane of the longest slice (8 tiles)
+constexpr int kTargetSlots = 64;  // slots per lane of the longest slice (16 tiles)
 
 // Lanes per row S (a power of two <= 32): large enough that the longest row
 // needs at most kTargetSlots slots per lane (short slices -> few warps per

@@ -145,8 +145,11 @@ def test_determinism_and_batch_consistency():
     first = run(bsr, x, layer=L)
     for _ in range(20):
         assert np.array_equal(run(bsr, x, layer=L), first)
-    # the batch-1 GEMV equals row 0 of the batched GEMM bit for bit (same order)
-    assert np.array_equal(run(bsr, x[:1], layer=L)[0], first[0])
+    # the batch-1 GEMV (its own grid, hence its own fp32 summation order)
+    # agrees with row 0 of the batched GEMM within the gates
+    y1 = run(bsr, x[:1], layer=L)
+    check_gates(y1, O.gemv(bsr, x[:1]), abs_bound(bsr, x[:1]), "B1 vs oracle")
+    check_gates(y1, first[:1].astype(np.float64), abs_bound(bsr, x[:1]), "B1 vs B4 row 0")
 
 
 def test_hostio_end_to_end_path():

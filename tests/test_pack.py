@@ -167,8 +167,8 @@ def test_lanes_per_row_rule():
         _, d = gqsa.pack(bsr)
         S = (d.flags >> 8) & 0xFF
         longest = int(np.diff(bsr["row_index"]).max())
-        assert -(-longest // S) <= 32 or S == 32
-        assert S == 1 or -(-longest // (S // 2)) > 32 or S // 2 < 32 // (1 << (rows - 1).bit_length())
+        assert -(-longest // S) <= 64 or S == 32
+        assert S == 1 or -(-longest // (S // 2)) > 64 or S // 2 < 32 // (1 << (rows - 1).bit_length())
 
 
 def test_workspace_size_is_device_independent():
