@@ -164,6 +164,7 @@ int gqsa_gemm_hostio(const gqsa_desc_t* desc, const void* d_blob, const uint16_t
  * CTAs, warps per CTA, active warps (Stream-K units), tiles.  For tooling. */
 typedef struct {
   int32_t grid, warps_per_cta, active_warps, num_tiles, smem_bytes, x_in_smem;
+  int32_t stages, ctas_per_sm, ring_bytes;  /* TMA ring depth per warp, residency, ring size */
 } gqsa_plan_t;
 int gqsa_launch_plan(const gqsa_desc_t* desc, int32_t B, gqsa_plan_t* plan);
 

@@ -44,21 +44,50 @@ bool desc_ok(const gqsa_desc_t* d) {
          lanes_per_row_ok(((uint32_t)d->flags >> kFlagLanesPerRowShift) & 0xff);
 }
 
-size_t smem_for(const gqsa_desc_t* d, int B, bool* xsmem) {
-  const size_t xc = (size_t)B * (d->cols / kGroup) * 4;
-  const size_t xb = (size_t)B * d->cols * 2;
-  *xsmem = xb + xc <= (size_t)kSmemBudget;
-  return *xsmem ? xb + xc : xc;
+// Tuning knobs (environment, read once): resident CTAs per SM and ring depth.
+int env_int(const char* name, int dflt, int lo, int hi) {
+  const char* e = std::getenv(name);
+  const int v = e ? std::atoi(e) : dflt;
+  return v >= lo && v <= hi ? v : dflt;
+}
+int ctas_per_sm_cap() {
+  static int cap = env_int("GQSA_CTAS_PER_SM", kMaxCtasPerSm, 1, 8);
+  return cap;
+}
+int stages_cap() {
+  static int cap = env_int("GQSA_STAGES", kMaxStages, kMinStages, kMaxStages);
+  return cap;
 }
 
-// Upper bound on resident CTAs per SM (tuning knob: GQSA_CTAS_PER_SM).
-int ctas_per_sm_cap() {
-  static int cap = [] {
-    const char* e = std::getenv("GQSA_CTAS_PER_SM");
-    const int v = e ? std::atoi(e) : kMaxCtasPerSm;
-    return v >= 1 && v <= 8 ? v : kMaxCtasPerSm;
-  }();
-  return cap;
+// Shared-memory plan: [TMA ring: kWarps x NS tiles][x: B*K fp16 (if it fits)][X_c: B*K/G fp32].
+// Picks the most CTAs per SM (<= cap) that still leave a ring of >= kMinStages.
+struct SmemPlan {
+  bool xsmem;
+  int ctas, stages;
+  size_t ring, total;
+};
+SmemPlan smem_plan(const gqsa_desc_t* d, int B) {
+  SmemPlan sp{};
+  const size_t tb = (size_t)tile_bytes(d->bits);
+  const size_t xc = (size_t)B * (d->cols / kGroup) * 4;
+  const size_t xb = (size_t)B * d->cols * 2;
+  for (int c = ctas_per_sm_cap(); c >= 1; --c) {
+    const size_t budget = (size_t)kSmemPerSm / c - 1024 - 1024;  // reserved + static smem
+    const size_t min_ring = (size_t)kWarps * kMinStages * tb;
+    bool xs = xb + xc + min_ring <= budget;
+    const size_t xbytes = xs ? xb + xc : xc;
+    if (xbytes + min_ring > budget && c > 1) continue;
+    int ns = (int)((budget - xbytes) / ((size_t)kWarps * tb));
+    if (ns > stages_cap()) ns = stages_cap();
+    if (ns < kMinStages) ns = kMinStages;
+    sp.xsmem = xs;
+    sp.ctas = c;
+    sp.stages = ns;
+    sp.ring = (size_t)kWarps * ns * tb;
+    sp.total = sp.ring + xbytes;
+    return sp;
+  }
+  return sp;
 }
 
 // Fill the launch plan; returns a status.
@@ -67,16 +96,17 @@ int make_plan(const gqsa_desc_t* d, int B, gqsa_plan_t* pl, const void** kfn) {
   if (cudaGetDevice(&dev) != cudaSuccess) return GQSA_ERR_CUDA;
   const int sms = device_sms(dev);
   if (sms <= 0) return GQSA_ERR_CUDA;
-  bool xsmem = false;
-  const size_t smem = smem_for(d, B, &xsmem);
+  const SmemPlan sp = smem_plan(d, B);
+  const bool xsmem = sp.xsmem;
+  const size_t smem = sp.total;
   const void* fn = select_kernel(d->bits, B, xsmem);
   if (!fn) return GQSA_ERR_UNSUPPORTED;
   {
     std::lock_guard<std::mutex> lk(g_mu);
     bool& set = g_dev[dev].attr_set[d->bits == 4][B][xsmem];
     if (!set) {
-      if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget) !=
-          cudaSuccess)
+      if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               kSmemPerSm - 1024 - 1024) != cudaSuccess)
         return GQSA_ERR_CUDA;
       set = true;
     }
@@ -85,7 +115,7 @@ int make_plan(const gqsa_desc_t* d, int B, gqsa_plan_t* pl, const void** kfn) {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem) != cudaSuccess)
     return GQSA_ERR_CUDA;
   if (occ < 1) return GQSA_ERR_UNSUPPORTED;
-  if (occ > ctas_per_sm_cap()) occ = ctas_per_sm_cap();
+  if (occ > sp.ctas) occ = sp.ctas;
   int warps = sms * occ * kWarps;
   if (warps > kMaxWarpsBound) warps = kMaxWarpsBound;
   const int active = d->num_tiles < warps ? d->num_tiles : warps;
@@ -101,6 +131,9 @@ int make_plan(const gqsa_desc_t* d, int B, gqsa_plan_t* pl, const void** kfn) {
   pl->num_tiles = d->num_tiles;
   pl->smem_bytes = (int32_t)smem;
   pl->x_in_smem = xsmem ? 1 : 0;
+  pl->stages = sp.stages;
+  pl->ctas_per_sm = occ;
+  pl->ring_bytes = (int32_t)sp.ring;
   if (kfn) *kfn = fn;
   return GQSA_OK;
 }
@@ -163,6 +196,8 @@ extern "C" int gqsa_gemm_smallbatch(const gqsa_desc_t* desc, const void* d_blob,
   p.lanes_per_row = ((uint32_t)desc->flags >> kFlagLanesPerRowShift) & 0xff;
   p.part_q = pl.active_warps ? desc->num_tiles / pl.active_warps : 0;
   p.part_r = pl.active_warps ? desc->num_tiles % pl.active_warps : 0;
+  p.stages = pl.stages;
+  p.ring_bytes = pl.ring_bytes;
   if (desc->rows == 0) return GQSA_OK;
 
   cudaLaunchConfig_t cfg = {};

@@ -291,9 +291,44 @@ __device__ __forceinline__ int warp_of_tile(const KParams& p, int t) {
 }
 
 // ---------------------------------------------------------------- kernel
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+
+// One lane's view of a tile that has landed in shared memory.
+template <int BITS>
+__device__ __forceinline__ void read_tile(TileRegs<BITS>& r, const uint8_t* tile, int lane) {
+  r.codes[0] = *reinterpret_cast<const uint4*>(tile + kTileHeaderBytes + lane * 16);
+  if (BITS == 4) r.codes[BITS == 4 ? 1 : 0] = *reinterpret_cast<const uint4*>(tile + kTileHeaderBytes + 512 + lane * 16);
+  r.sz = *reinterpret_cast<const uint4*>(tile + off_sz(BITS) + lane * 16);
+  r.cols = *reinterpret_cast<const uint2*>(tile + off_cols(BITS) + lane * 8);
+  r.hdr = *reinterpret_cast<const uint32_t*>(tile);  // broadcast
+}
+
 template <int BITS, int B, bool XSMEM>
 __global__ void __launch_bounds__(kThreads, min_ctas_per_sm(B)) gqsa_streamk_kernel(KParams p) {
-  extern __shared__ __align__(16) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t ring_bar[kWarps][kMaxStages];
+  __shared__ __align__(8) uint64_t xbar;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int gw = blockIdx.x * kWarps + warp;
@@ -306,55 +341,53 @@ __global__ void __launch_bounds__(kThreads, min_ctas_per_sm(B)) gqsa_streamk_ker
   }
   const uint8_t* tiles = p.tiles;
   const int tb = tile_bytes(BITS);
+  const int NS = p.stages;
 
-  // ---- weights never depend on the previous kernel: request the first tiles
-  //      into registers before the PDL wait
-  TileRegs<BITS> buf[kDepth];
-#pragma unroll
-  for (int i = 0; i < kDepth; ++i)
-    if (t_begin + i < t_end) load_tile<BITS>(buf[i], tiles + (int64_t)(t_begin + i) * tb, lane);
+  // ---- weights never depend on the previous kernel: each warp's first NS
+  //      tiles are requested (1-D TMA bulk copies into its shared-memory
+  //      ring) BEFORE the PDL wait, so they overlap the previous kernel
+  uint8_t* ring = smem + (size_t)warp * NS * tb;
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+  const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&ring_bar[warp][0]);
+  if (lane == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(bar0 + 8 * s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < NS && t_begin + s < t_end; ++s) {
+      mbar_expect_tx(bar0 + 8 * s, tb);
+      bulk_g2s(ring_s + s * tb, tiles + (int64_t)(t_begin + s) * tb, tb, bar0 + 8 * s);
+    }
+  }
+  __syncwarp();
   int row = -1;  // this lane's row in the first slice (the perm table is part of the blob)
-  if (t_end > t_begin) row = __ldg(p.perm + (int64_t)(buf[0].hdr >> 2) * kLanes + lane);
+  uint32_t hdr0 = 0;
+  if (t_end > t_begin) {
+    hdr0 = __ldg(reinterpret_cast<const uint32_t*>(tiles + (int64_t)t_begin * tb));
+    row = __ldg(p.perm + (int64_t)(hdr0 >> 2) * kLanes + lane);
+  }
   pdl_launch_dependents();
   pdl_wait();  // x, y, bias and the workspace may belong to the previous kernel
 
   // ---- stage activations (1-D TMA bulk copies into shared memory) and the
   //      per-column-group sums X_{b,c} (fp32, fixed t order)
   const int KG = p.cols / kGroup;
-  uint8_t* xs = smem;
-  float* xc = reinterpret_cast<float*>(smem + (XSMEM ? (size_t)B * p.cols * 2 : 0));
+  uint8_t* xs = smem + p.ring_bytes;
+  float* xc = reinterpret_cast<float*>(xs + (XSMEM ? (size_t)B * p.cols * 2 : 0));
+  const uint32_t xb = (uint32_t)__cvta_generic_to_shared(&xbar);
   if (XSMEM) {
-    __shared__ __align__(8) uint64_t xbar;
-    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&xbar);
     if (threadIdx.x == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+      mbar_init(xb, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       const uint32_t row_bytes = (uint32_t)p.cols * 2u;
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                   "r"(row_bytes * B)
-                   : "memory");
+      mbar_expect_tx(xb, row_bytes * B);
       for (int b = 0; b < B; ++b) {
         const uint8_t* src = reinterpret_cast<const uint8_t*>(p.X + (int64_t)b * p.ldx);
         const uint32_t dst = (uint32_t)__cvta_generic_to_shared(xs + (size_t)b * row_bytes);
-        for (uint32_t off = 0; off < row_bytes; off += kBulkChunk) {
-          const uint32_t n = min(kBulkChunk, row_bytes - off);
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  dst + off),
-              "l"(src + off), "r"(n), "r"(bar)
-              : "memory");
-        }
+        for (uint32_t off = 0; off < row_bytes; off += kBulkChunk)
+          bulk_g2s(dst + off, src + off, min(kBulkChunk, row_bytes - off), xb);
       }
     }
     __syncthreads();  // barrier initialised before anyone polls it
-    uint32_t done = 0;
-    while (!done) {
-      asm volatile(
-          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
-          : "=r"(done)
-          : "r"(bar)
-          : "memory");
-    }
+    mbar_wait(xb, 0);
   }
   for (int i = threadIdx.x; i < B * KG; i += kThreads) {
     const int b = i / KG, c = i - b * KG;
@@ -380,10 +413,10 @@ __global__ void __launch_bounds__(kThreads, min_ctas_per_sm(B)) gqsa_streamk_ker
 
   // ---- empty rows get bias (or 0): grid-stride over the empty-row list
   for (int i = blockIdx.x * kThreads + threadIdx.x; i < p.n_empty; i += gridDim.x * kThreads) {
-    const int row = __ldg(p.empty + i);
-    const float bias = p.bias ? __ldg(p.bias + row) : 0.f;
+    const int erow = __ldg(p.empty + i);
+    const float bias = p.bias ? __ldg(p.bias + erow) : 0.f;
 #pragma unroll
-    for (int b = 0; b < B; ++b) p.Y[(int64_t)b * p.ldy + row] = bias;
+    for (int b = 0; b < B; ++b) p.Y[(int64_t)b * p.ldy + erow] = bias;
   }
   if (t_end <= t_begin) return;
 
@@ -391,31 +424,37 @@ __global__ void __launch_bounds__(kThreads, min_ctas_per_sm(B)) gqsa_streamk_ker
   float acc[kMaxBatch];
 #pragma unroll
   for (int b = 0; b < kMaxBatch; ++b) acc[b] = 0.f;
-  bool foreign = !(buf[0].hdr & kTileFirst);  // slice opened by an earlier warp
+  bool foreign = !(hdr0 & kTileFirst);  // slice opened by an earlier warp
   uint32_t last_hdr = 0;
-
-  for (int t0 = t_begin; t0 < t_end; t0 += kDepth) {
+  int s = 0;
+  uint32_t phase = 0;
+  for (int t = t_begin; t < t_end; ++t) {
+    mbar_wait(bar0 + 8 * s, phase);
+    TileRegs<BITS> tr;
+    read_tile<BITS>(tr, ring + (size_t)s * tb, lane);
+    __syncwarp();  // every lane has read stage s: refill it with tile t + NS
+    if (lane == 0 && t + NS < t_end) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(bar0 + 8 * s, tb);
+      bulk_g2s(ring_s + s * tb, tiles + (int64_t)(t + NS) * tb, tb, bar0 + 8 * s);
+    }
+    if (++s == NS) {
+      s = 0;
+      phase ^= 1u;
+    }
+    float part[kPerLane][kMaxBatch];
 #pragma unroll
-    for (int i = 0; i < kDepth; ++i) {
-      const int t = t0 + i;
-      if (t < t_end) {
-        float part[kPerLane][kMaxBatch];
+    for (int u = 0; u < kPerLane; ++u) group_partial<BITS, B, XSMEM>(p, tr, u, xs, xc, part[u]);
 #pragma unroll
-        for (int u = 0; u < kPerLane; ++u) group_partial<BITS, B, XSMEM>(p, buf[i], u, xs, xc, part[u]);
+    for (int b = 0; b < B; ++b) acc[b] += (part[0][b] + part[1][b]) + (part[2][b] + part[3][b]);
+    last_hdr = tr.hdr;
+    if (tr.hdr & kTileLast) {  // the slice ends in this tile: its rows are complete
+      if (foreign) publish<B>(p, gw, acc, lane);
+      else store_rows<B>(p, acc, row, lane);
 #pragma unroll
-        for (int b = 0; b < B; ++b) acc[b] += (part[0][b] + part[1][b]) + (part[2][b] + part[3][b]);
-        const uint32_t hdr = buf[i].hdr;
-        if (t + kDepth < t_end) load_tile<BITS>(buf[i], tiles + (int64_t)(t + kDepth) * tb, lane);
-        last_hdr = hdr;
-        if (hdr & kTileLast) {  // the slice ends in this tile: its rows are complete
-          if (foreign) publish<B>(p, gw, acc, lane);
-          else store_rows<B>(p, acc, row, lane);
-#pragma unroll
-          for (int b = 0; b < B; ++b) acc[b] = 0.f;
-          foreign = false;
-          if (t + 1 < t_end) row = __ldg(p.perm + (int64_t)((hdr >> 2) + 1) * kLanes + lane);
-        }
-      }
+      for (int b = 0; b < B; ++b) acc[b] = 0.f;
+      foreign = false;
+      if (t + 1 < t_end) row = __ldg(p.perm + (int64_t)((tr.hdr >> 2) + 1) * kLanes + lane);
     }
   }
 

@@ -6,7 +6,9 @@ namespace gqsa {
 
 constexpr int kThreads = 256;            // 8 warps per CTA
 constexpr int kWarps = kThreads / 32;
-constexpr int kDepth = 3;                // tiles in flight per warp (register ring)
+constexpr int kMaxStages = 8;            // tiles in flight per warp (shared-memory TMA ring)
+constexpr int kMinStages = 2;
+constexpr int kSmemPerSm = 228 * 1024;   // shared memory per SM (incl. 1 KB reserved per CTA)
 constexpr int kMaxBatch = 8;
 constexpr int kMaxCtasPerSm = 4;
 // Register budget: 4 resident CTAs (64 regs/thread) at batch 1 -- the HBM
@@ -28,6 +30,8 @@ struct KParams {
   int64_t ldx, ldy;
   int32_t rows, cols, num_tiles, n_empty, active_warps, lanes_per_row;
   int32_t part_q, part_r;  // num_tiles = part_q * active_warps + part_r
+  int32_t stages;          // ring depth NS (tiles) per warp
+  int32_t ring_bytes;      // kWarps * NS * tile_bytes: the x / X_c area starts here
 };
 
 const void* select_kernel(int bits, int B, bool xsmem);

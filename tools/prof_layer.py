@@ -40,7 +40,7 @@ def main():
     Y = torch.empty(a.batch, a.rows, dtype=torch.float32, device="cuda")
     plan = gqsa.launch_plan(desc, a.batch)
     print(f"plan grid={plan.grid} active_warps={plan.active_warps} tiles={plan.num_tiles} "
-          f"smem={plan.smem_bytes} R={R}", flush=True)
+          f"smem={plan.smem_bytes} stages={plan.stages} ctas/SM={plan.ctas_per_sm} R={R}", flush=True)
     for i in range(a.launches):
         gqsa.gemm_smallbatch(desc, blobs[i % R], X, Y, None, ws)
     torch.cuda.synchronize()
