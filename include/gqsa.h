@@ -171,6 +171,13 @@ int gqsa_launch_plan(const gqsa_desc_t* desc, int32_t B, gqsa_plan_t* plan);
 /* Number of GQSA kernels launched by this process so far (all entry points). */
 uint64_t gqsa_launch_count(void);
 
+/* Profiling hook: while set, every launch writes, per active warp w, eight
+ * uint64 %globaltimer stamps at d_buf[8w .. 8w+7] (0 start, 1 after the PDL
+ * wait, 2 activations staged, 3 first tile landed, 4 tile loop done, 5 exit)
+ * when bytes >= 64 * active_warps.  d_buf = NULL turns it off (default).
+ * The buffer is caller-owned device memory; not for production use. */
+int gqsa_debug_trace(void* d_buf, size_t bytes);
+
 const char* gqsa_status_string(int status);
 int gqsa_version(void);
 

@@ -16,6 +16,8 @@ using namespace gqsa;
 namespace {
 
 std::atomic<uint64_t> g_launches{0};
+uint64_t* g_trace = nullptr;  // gqsa_debug_trace buffer (device), or null
+size_t g_trace_bytes = 0;
 
 struct DevInfo {
   int sms = 0;
@@ -198,6 +200,7 @@ extern "C" int gqsa_gemm_smallbatch(const gqsa_desc_t* desc, const void* d_blob,
   p.part_r = pl.active_warps ? desc->num_tiles % pl.active_warps : 0;
   p.stages = pl.stages;
   p.ring_bytes = pl.ring_bytes;
+  p.trace = (g_trace && g_trace_bytes >= (size_t)pl.active_warps * 64) ? g_trace : nullptr;
   if (desc->rows == 0) return GQSA_OK;
 
   cudaLaunchConfig_t cfg = {};
@@ -256,3 +259,9 @@ extern "C" int gqsa_gemm_hostio(const gqsa_desc_t* desc, const void* d_blob, con
 }
 
 extern "C" uint64_t gqsa_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+extern "C" int gqsa_debug_trace(void* d_buf, size_t bytes) {
+  g_trace = static_cast<uint64_t*>(d_buf);
+  g_trace_bytes = d_buf ? bytes : 0;
+  return GQSA_OK;
+}

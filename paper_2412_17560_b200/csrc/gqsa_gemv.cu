@@ -314,6 +314,16 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   }
 }
 
+// Optional timeline instrumentation (gqsa_debug_trace): lane 0 of each warp
+// stamps %globaltimer at fixed points; off (one predicated branch) by default.
+__device__ __forceinline__ void trace_point(const KParams& p, int gw, int lane, int k) {
+  if (p.trace && lane == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[(int64_t)gw * 8 + k] = t;
+  }
+}
+
 // One lane's view of a tile that has landed in shared memory.
 template <int BITS>
 __device__ __forceinline__ void read_tile(TileRegs<BITS>& r, const uint8_t* tile, int lane) {
@@ -364,8 +374,10 @@ __global__ void __launch_bounds__(kThreads, min_ctas_per_sm(B)) gqsa_streamk_ker
     hdr0 = __ldg(reinterpret_cast<const uint32_t*>(tiles + (int64_t)t_begin * tb));
     row = __ldg(p.perm + (int64_t)(hdr0 >> 2) * kLanes + lane);
   }
+  trace_point(p, gw, lane, 0);
   pdl_launch_dependents();
   pdl_wait();  // x, y, bias and the workspace may belong to the previous kernel
+  trace_point(p, gw, lane, 1);
 
   // ---- stage activations (1-D TMA bulk copies into shared memory) and the
   //      per-column-group sums X_{b,c} (fp32, fixed t order)
@@ -418,6 +430,7 @@ __global__ void __launch_bounds__(kThreads, min_ctas_per_sm(B)) gqsa_streamk_ker
 #pragma unroll
     for (int b = 0; b < B; ++b) p.Y[(int64_t)b * p.ldy + erow] = bias;
   }
+  trace_point(p, gw, lane, 2);
   if (t_end <= t_begin) return;
 
   // ---- stream the warp's tile range; lane = one row of the current slice
@@ -430,6 +443,7 @@ __global__ void __launch_bounds__(kThreads, min_ctas_per_sm(B)) gqsa_streamk_ker
   uint32_t phase = 0;
   for (int t = t_begin; t < t_end; ++t) {
     mbar_wait(bar0 + 8 * s, phase);
+    if (t == t_begin) trace_point(p, gw, lane, 3);
     TileRegs<BITS> tr;
     read_tile<BITS>(tr, ring + (size_t)s * tb, lane);
     __syncwarp();  // every lane has read stage s: refill it with tile t + NS
@@ -458,6 +472,7 @@ __global__ void __launch_bounds__(kThreads, min_ctas_per_sm(B)) gqsa_streamk_ker
     }
   }
 
+  trace_point(p, gw, lane, 4);
   // ---- a slice left open at the end of the range continues downstream
   if (!(last_hdr & kTileLast)) {
     if (foreign) {  // the whole range lies inside a slice owned upstream
@@ -468,6 +483,7 @@ __global__ void __launch_bounds__(kThreads, min_ctas_per_sm(B)) gqsa_streamk_ker
       store_rows<B>(p, acc, row, lane);
     }
   }
+  trace_point(p, gw, lane, 5);
 }
 
 // ---------------------------------------------------------------- launchers

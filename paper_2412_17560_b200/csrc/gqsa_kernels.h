@@ -32,6 +32,7 @@ struct KParams {
   int32_t part_q, part_r;  // num_tiles = part_q * active_warps + part_r
   int32_t stages;          // ring depth NS (tiles) per warp
   int32_t ring_bytes;      // kWarps * NS * tile_bytes: the x / X_c area starts here
+  uint64_t* trace;         // optional [active_warps][8] %globaltimer stamps (debug)
 };
 
 const void* select_kernel(int bits, int B, bool xsmem);

@@ -69,6 +69,7 @@ EXPORTS = (
     "gqsa_pack_size", "gqsa_pack", "gqsa_read_desc", "gqsa_unpack", "gqsa_workspace_size",
     "gqsa_gemv", "gqsa_gemm_smallbatch", "gqsa_hostio_stage_size", "gqsa_gemm_hostio",
     "gqsa_launch_plan", "gqsa_launch_count", "gqsa_status_string", "gqsa_version",
+    "gqsa_debug_trace",
 )
 
 _lib = None
@@ -95,6 +96,7 @@ def lib() -> ctypes.CDLL:
     L.gqsa_gemm_hostio.argtypes = [ctypes.POINTER(Desc), P, P, I32, P, P, P, SZ, P, SZ, P]
     L.gqsa_launch_plan.argtypes = [ctypes.POINTER(Desc), I32, ctypes.POINTER(Plan)]
     L.gqsa_launch_count.restype = ctypes.c_uint64
+    L.gqsa_debug_trace.argtypes = [P, SZ]
     L.gqsa_status_string.restype = ctypes.c_char_p
     L.gqsa_status_string.argtypes = [ctypes.c_int]
     for name in EXPORTS:
@@ -194,6 +196,14 @@ def launch_plan(desc: Desc, batch: int = 1) -> Plan:
 
 def launch_count() -> int:
     return int(lib().gqsa_launch_count())
+
+
+def debug_trace(buf=None) -> None:
+    """Enable (torch uint64/int64 CUDA tensor) or disable (None) timeline stamps."""
+    if buf is None:
+        lib().gqsa_debug_trace(None, 0)
+    else:
+        lib().gqsa_debug_trace(buf.data_ptr(), buf.numel() * buf.element_size())
 
 
 def _stream_ptr(stream) -> int:

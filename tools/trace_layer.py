@@ -1,0 +1,77 @@
+#!/usr/bin/env python
+"""Timeline of GQSA launches from the kernel's %globaltimer stamps (gqsa_debug_trace).
+
+    python tools/trace_layer.py --rows 14336 --cols 4096 [--launches 6]
+For a CUDA graph of back-to-back launches (rotating weight copies, PDL on),
+prints per launch: start spread, PDL-wait release, activation staging, first
+tile arrival, tile-loop end and exit (µs relative to the first launch's
+earliest start; percentiles over warps).
+"""
+import argparse
+import math
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2412_17560_b200 import gqsa, synth  # noqa: E402
+
+NAMES = ["start", "pdl_wait", "x_staged", "tile0", "loop_end", "exit"]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--rows", type=int, default=14336)
+    ap.add_argument("--cols", type=int, default=4096)
+    ap.add_argument("--bits", type=int, default=4)
+    ap.add_argument("--sparsity", type=float, default=0.5)
+    ap.add_argument("--launches", type=int, default=6)
+    a = ap.parse_args()
+    seed = synth.seed_for(f"trace/{a.rows}x{a.cols}")
+    bsr = synth.make_layer(seed, a.rows, a.cols, bits=a.bits, sparsity=a.sparsity)
+    x = synth.make_x(seed + 1, 1, a.cols)
+    blob, desc = gqsa.pack(bsr)
+    R = max(a.launches, math.ceil(300e6 / blob.size))
+    blobs = [torch.from_numpy(blob).cuda() for _ in range(R)]
+    ws = torch.zeros(gqsa.workspace_size(desc, 1), dtype=torch.uint8, device="cuda")
+    X = torch.from_numpy(x).view(torch.float16).cuda()
+    Y = torch.empty(1, a.rows, dtype=torch.float32, device="cuda")
+    plan = gqsa.launch_plan(desc, 1)
+    W = plan.active_warps
+    bufs = [torch.zeros(W * 8, dtype=torch.int64, device="cuda") for _ in range(R)]
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for i in range(R):
+            gqsa.debug_trace(bufs[i])
+            gqsa.gemm_smallbatch(desc, blobs[i], X, Y, None, ws)
+    gqsa.debug_trace(None)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    T = np.stack([b.cpu().numpy().reshape(W, 8)[:, :6] for b in bufs])  # [R][W][6]
+    t0 = T[0, :, 0].min()
+    T = (T - t0) / 1e3
+    print(f"{a.rows}x{a.cols} W{a.bits}: grid={plan.grid} warps={W} stages={plan.stages} "
+          f"ctas/SM={plan.ctas_per_sm} tiles={plan.num_tiles}")
+    print("launch  " + "  ".join(f"{n:>17s}" for n in NAMES) + "   (min/median/max µs)")
+    for i in range(min(R, a.launches)):
+        cols = []
+        for k in range(6):
+            v = T[i, :, k]
+            cols.append(f"{v.min():5.2f}/{np.median(v):5.2f}/{v.max():5.2f}")
+        print(f"{i:6d}  " + "  ".join(f"{c:>17s}" for c in cols))
+    per = [(T[i + 1, :, 5].max() - T[i, :, 5].max()) for i in range(min(R, a.launches) - 1)]
+    print("exit-to-exit per launch (µs):", " ".join(f"{p:.2f}" for p in per))
+    d = T[1:, :, :]
+    print("median phase durations (µs): wait=%.2f stage=%.2f tile0=%.2f loop=%.2f fixup=%.2f" % (
+        np.median(d[..., 1] - d[..., 0]), np.median(d[..., 2] - d[..., 1]), np.median(d[..., 3] - d[..., 2]),
+        np.median(d[..., 4] - d[..., 3]), np.median(d[..., 5] - d[..., 4])))
+
+
+if __name__ == "__main__":
+    main()
