@@ -61,11 +61,18 @@ int stages_cap() {
   return cap;
 }
 
-// Shared-memory plan: [TMA ring: kWarps x NS tiles][x: B*K fp16 (if it fits)][X_c: B*K/G fp32].
-// Picks the most CTAs per SM (<= cap) that still leave a ring of >= kMinStages.
+int warps_per_cta(int B) {
+  static int w1 = env_int("GQSA_WARPS", kMaxWarps, 1, kMaxWarps);
+  return B <= 2 ? w1 : 8;
+}
+
+// Shared-memory plan per CTA of W warps: [TMA ring: W x NS tiles][x: B*K fp16
+// (if it fits)][X_c: B*K/G fp32].  By default one CTA per SM that uses at most
+// half of the SM's shared memory, so the next GEMV on the stream (PDL) can be
+// resident at the same time and stream its weights during this one's tail.
 struct SmemPlan {
   bool xsmem;
-  int ctas, stages;
+  int ctas, stages, warps;
   size_t ring, total;
 };
 SmemPlan smem_plan(const gqsa_desc_t* d, int B) {
@@ -73,22 +80,22 @@ SmemPlan smem_plan(const gqsa_desc_t* d, int B) {
   const size_t tb = (size_t)tile_bytes(d->bits);
   const size_t xc = (size_t)B * (d->cols / kGroup) * 4;
   const size_t xb = (size_t)B * d->cols * 2;
-  for (int c = ctas_per_sm_cap(); c >= 1; --c) {
-    const size_t budget = (size_t)kSmemPerSm / c - 1024 - 1024;  // reserved + static smem
-    const size_t min_ring = (size_t)kWarps * kMinStages * tb;
-    bool xs = xb + xc + min_ring <= budget;
-    const size_t xbytes = xs ? xb + xc : xc;
-    if (xbytes + min_ring > budget && c > 1) continue;
-    int ns = (int)((budget - xbytes) / ((size_t)kWarps * tb));
-    if (ns > stages_cap()) ns = stages_cap();
-    if (ns < kMinStages) ns = kMinStages;
-    sp.xsmem = xs;
-    sp.ctas = c;
-    sp.stages = ns;
-    sp.ring = (size_t)kWarps * ns * tb;
-    sp.total = sp.ring + xbytes;
-    return sp;
-  }
+  const int W = warps_per_cta(B);
+  const int c = ctas_per_sm_cap();
+  const size_t share = (size_t)kSmemPerSm / (c * kCoResidentKernels);
+  const size_t budget = share > 2048 ? share - 2048 : 0;  // reserved + static smem
+  const size_t min_ring = (size_t)W * kMinStages * tb;
+  const bool xs = xb + xc + min_ring <= budget || xb + xc <= (size_t)kSmemPerSm / 2;
+  const size_t xbytes = xs ? xb + xc : xc;
+  int ns = budget > xbytes ? (int)((budget - xbytes) / ((size_t)W * tb)) : 0;
+  if (ns > stages_cap()) ns = stages_cap();
+  if (ns < kMinStages) ns = kMinStages;
+  sp.xsmem = xs;
+  sp.ctas = c;
+  sp.warps = W;
+  sp.stages = ns;
+  sp.ring = (size_t)W * ns * tb;
+  sp.total = sp.ring + xbytes;
   return sp;
 }
 
@@ -113,22 +120,23 @@ int make_plan(const gqsa_desc_t* d, int B, gqsa_plan_t* pl, const void** kfn) {
       set = true;
     }
   }
+  const int W = sp.warps, threads = 32 * sp.warps;
   int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem) != cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem) != cudaSuccess)
     return GQSA_ERR_CUDA;
   if (occ < 1) return GQSA_ERR_UNSUPPORTED;
   if (occ > sp.ctas) occ = sp.ctas;
-  int warps = sms * occ * kWarps;
+  int warps = sms * occ * W;
   if (warps > kMaxWarpsBound) warps = kMaxWarpsBound;
   const int active = d->num_tiles < warps ? d->num_tiles : warps;
-  int grid = (active + kWarps - 1) / kWarps;
+  int grid = (active + W - 1) / W;
   if (grid == 0) {  // nnzg == 0: only empty rows to write
-    grid = (d->n_empty + kThreads - 1) / kThreads;
+    grid = (d->n_empty + threads - 1) / threads;
     if (grid > sms) grid = sms;
     if (grid < 1) grid = 1;
   }
   pl->grid = grid;
-  pl->warps_per_cta = kWarps;
+  pl->warps_per_cta = W;
   pl->active_warps = active;
   pl->num_tiles = d->num_tiles;
   pl->smem_bytes = (int32_t)smem;
@@ -205,7 +213,7 @@ extern "C" int gqsa_gemm_smallbatch(const gqsa_desc_t* desc, const void* d_blob,
 
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(pl.grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(32 * pl.warps_per_cta);
   cfg.dynamicSmemBytes = pl.smem_bytes;
   cfg.stream = static_cast<cudaStream_t>(stream);
   cudaLaunchAttribute attr[1];

@@ -335,13 +335,13 @@ __device__ __forceinline__ void read_tile(TileRegs<BITS>& r, const uint8_t* tile
 }
 
 template <int BITS, int B, bool XSMEM>
-__global__ void __launch_bounds__(kThreads, min_ctas_per_sm(B)) gqsa_streamk_kernel(KParams p) {
+__global__ void __launch_bounds__(kMaxThreads, min_ctas_per_sm(B)) gqsa_streamk_kernel(KParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t ring_bar[kWarps][kMaxStages];
-  __shared__ __align__(8) uint64_t xbar;
+  __shared__ __align__(8) uint64_t ring_bar[kMaxWarps][kMaxStages];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int gw = blockIdx.x * kWarps + warp;
+  const int nthreads = blockDim.x;
+  const int gw = blockIdx.x * (nthreads >> 5) + warp;
 
   // ---- task-centric partition: contiguous tile range per warp (+-1 tile)
   int t_begin = 0, t_end = 0;
@@ -379,29 +379,32 @@ __global__ void __launch_bounds__(kThreads, min_ctas_per_sm(B)) gqsa_streamk_ker
   pdl_wait();  // x, y, bias and the workspace may belong to the previous kernel
   trace_point(p, gw, lane, 1);
 
-  // ---- stage activations (1-D TMA bulk copies into shared memory) and the
-  //      per-column-group sums X_{b,c} (fp32, fixed t order)
+  // ---- stage activations in shared memory with plain 128-bit loads (not
+  //      through the TMA unit, whose queue already holds the weight ring
+  //      fills), then the per-column-group sums X_{b,c} (fp32, fixed t order)
   const int KG = p.cols / kGroup;
   uint8_t* xs = smem + p.ring_bytes;
   float* xc = reinterpret_cast<float*>(xs + (XSMEM ? (size_t)B * p.cols * 2 : 0));
-  const uint32_t xb = (uint32_t)__cvta_generic_to_shared(&xbar);
   if (XSMEM) {
-    if (threadIdx.x == 0) {
-      mbar_init(xb, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      const uint32_t row_bytes = (uint32_t)p.cols * 2u;
-      mbar_expect_tx(xb, row_bytes * B);
-      for (int b = 0; b < B; ++b) {
-        const uint8_t* src = reinterpret_cast<const uint8_t*>(p.X + (int64_t)b * p.ldx);
-        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(xs + (size_t)b * row_bytes);
-        for (uint32_t off = 0; off < row_bytes; off += kBulkChunk)
-          bulk_g2s(dst + off, src + off, min(kBulkChunk, row_bytes - off), xb);
+    const int n16 = p.cols / 8;  // uint4 per batch row
+    constexpr int U = 4;
+    for (int i0 = threadIdx.x; i0 < B * n16; i0 += U * nthreads) {
+      uint4 v[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {  // U independent loads in flight
+        const int i = i0 + k * nthreads;
+        if (i < B * n16) {
+          const int b = i / n16, j = i - b * n16;
+          v[k] = __ldg(reinterpret_cast<const uint4*>(p.X + (int64_t)b * p.ldx) + j);
+        }
       }
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        if (i0 + k * nthreads < B * n16) reinterpret_cast<uint4*>(xs)[i0 + k * nthreads] = v[k];
     }
-    __syncthreads();  // barrier initialised before anyone polls it
-    mbar_wait(xb, 0);
+    __syncthreads();
   }
-  for (int i = threadIdx.x; i < B * KG; i += kThreads) {
+  for (int i = threadIdx.x; i < B * KG; i += nthreads) {
     const int b = i / KG, c = i - b * KG;
     uint4 v0, v1;
     if (XSMEM) {
@@ -424,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, min_ctas_per_sm(B)) gqsa_streamk_ker
   __syncthreads();
 
   // ---- empty rows get bias (or 0): grid-stride over the empty-row list
-  for (int i = blockIdx.x * kThreads + threadIdx.x; i < p.n_empty; i += gridDim.x * kThreads) {
+  for (int i = blockIdx.x * nthreads + threadIdx.x; i < p.n_empty; i += gridDim.x * nthreads) {
     const int erow = __ldg(p.empty + i);
     const float bias = p.bias ? __ldg(p.bias + erow) : 0.f;
 #pragma unroll

@@ -4,17 +4,19 @@
 
 namespace gqsa {
 
-constexpr int kThreads = 256;            // 8 warps per CTA
-constexpr int kWarps = kThreads / 32;
+constexpr int kMaxWarps = 16;           // warps per CTA: a launch-time choice <= 16
+constexpr int kMaxThreads = 32 * kMaxWarps;
 constexpr int kMaxStages = 8;            // tiles in flight per warp (shared-memory TMA ring)
 constexpr int kMinStages = 2;
 constexpr int kSmemPerSm = 228 * 1024;   // shared memory per SM (incl. 1 KB reserved per CTA)
 constexpr int kMaxBatch = 8;
-constexpr int kMaxCtasPerSm = 4;
+constexpr int kMaxCtasPerSm = 1;         // default residency: one CTA of up to 16 warps per SM
+constexpr int kCoResidentKernels = 2;    // leave room for the next PDL-launched GEMV
 // Register budget: 4 resident CTAs (64 regs/thread) at batch 1 -- the HBM
 // stream wants many warps with loads in flight; bigger batches need more
 // accumulators and are ALU / smem-bound anyway.
-constexpr int min_ctas_per_sm(int B) { return B <= 4 ? 2 : 1; }
+// (for kMaxThreads-thread CTAs: 2 -> <= 64 registers per thread)
+constexpr int min_ctas_per_sm(int B) { return B <= 2 ? 2 : 1; }
 constexpr int kMaxWarpsBound = 4096;     // workspace records (>= any grid we launch)
 constexpr int kWsSlotBytes = 8;          // fix-up slot {partial, flag} per (warp, batch, lane)
 constexpr int kSmemBudget = 200 * 1024;  // above this, x is gathered from L1/L2
@@ -31,7 +33,7 @@ struct KParams {
   int32_t rows, cols, num_tiles, n_empty, active_warps, lanes_per_row;
   int32_t part_q, part_r;  // num_tiles = part_q * active_warps + part_r
   int32_t stages;          // ring depth NS (tiles) per warp
-  int32_t ring_bytes;      // kWarps * NS * tile_bytes: the x / X_c area starts here
+  int32_t ring_bytes;      // warps * NS * tile_bytes: the x / X_c area starts here
   uint64_t* trace;         // optional [active_warps][8] %globaltimer stamps (debug)
 };
 

@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--bits", type=int, default=4)
     ap.add_argument("--sparsity", type=float, default=0.5)
     ap.add_argument("--launches", type=int, default=6)
+    ap.add_argument("--eager", action="store_true", help="stream launches instead of a CUDA graph")
     a = ap.parse_args()
     seed = synth.seed_for(f"trace/{a.rows}x{a.cols}")
     bsr = synth.make_layer(seed, a.rows, a.cols, bits=a.bits, sparsity=a.sparsity)
@@ -44,14 +45,22 @@ def main():
     W = plan.active_warps
     bufs = [torch.zeros(W * 8, dtype=torch.int64, device="cuda") for _ in range(R)]
     s = torch.cuda.Stream()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g, stream=s):
-        for i in range(R):
-            gqsa.debug_trace(bufs[i])
-            gqsa.gemm_smallbatch(desc, blobs[i], X, Y, None, ws)
+    if a.eager:  # plain stream launches (PDL attribute on each)
+        for _ in range(2):
+            with torch.cuda.stream(s):
+                for i in range(R):
+                    gqsa.debug_trace(bufs[i])
+                    gqsa.gemm_smallbatch(desc, blobs[i], X, Y, None, ws)
+            torch.cuda.synchronize()
+    else:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for i in range(R):
+                gqsa.debug_trace(bufs[i])
+                gqsa.gemm_smallbatch(desc, blobs[i], X, Y, None, ws)
+        for _ in range(3):
+            g.replay()
     gqsa.debug_trace(None)
-    for _ in range(3):
-        g.replay()
     torch.cuda.synchronize()
     T = np.stack([b.cpu().numpy().reshape(W, 8)[:, :6] for b in bufs])  # [R][W][6]
     t0 = T[0, :, 0].min()
