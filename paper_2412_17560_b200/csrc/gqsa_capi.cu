@@ -78,7 +78,7 @@ struct SmemPlan {
 SmemPlan smem_plan(const gqsa_desc_t* d, int B) {
   SmemPlan sp{};
   const size_t tb = (size_t)tile_bytes(d->bits);
-  const size_t xc = (size_t)B * (d->cols / kGroup) * 4;
+  const size_t xc = (size_t)B * (d->cols / kGroup) * 8;  // float2 (even, odd) column sums
   const size_t xb = (size_t)B * d->cols * 2;
   const int W = warps_per_cta(B);
   const int c = ctas_per_sm_cap();

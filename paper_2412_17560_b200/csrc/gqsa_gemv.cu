@@ -109,6 +109,26 @@ __device__ __forceinline__ float dot8_w4(uint32_t w, uint32_t x01, uint32_t x23,
   return acc;
 }
 
+// Raw (offset-carrying) dot of one word of eight 4-bit codes with x[0..7]:
+// de += sum_{j even} (1024 + e_j) x_j,  dd += sum_{j odd} (1024 + 16 e_j) x_j.
+// Each LOP3 makes two exact fp16 values; each product is exact in fp32.
+__device__ __forceinline__ void dot8_w4_raw(uint32_t w, uint32_t x01, uint32_t x23, uint32_t x45,
+                                            uint32_t x67, float& de, float& dd) {
+  const uint32_t w8 = w >> 8;
+  const uint32_t e04 = lop3_and_or(w, 0x000F000Fu, kMagic1024);   // (1024+e0, 1024+e4)
+  const uint32_t e15 = lop3_and_or(w, 0x00F000F0u, kMagic1024);   // (1024+16e1, 1024+16e5)
+  const uint32_t e26 = lop3_and_or(w8, 0x000F000Fu, kMagic1024);  // (1024+e2, 1024+e6)
+  const uint32_t e37 = lop3_and_or(w8, 0x00F000F0u, kMagic1024);  // (1024+16e3, 1024+16e7)
+  de = fhfma<0, 0>(e04, x01, de);
+  dd = fhfma<0, 1>(e15, x01, dd);
+  de = fhfma<0, 0>(e26, x23, de);
+  dd = fhfma<0, 1>(e37, x23, dd);
+  de = fhfma<1, 0>(e04, x45, de);
+  dd = fhfma<1, 1>(e15, x45, dd);
+  de = fhfma<1, 0>(e26, x67, de);
+  dd = fhfma<1, 1>(e37, x67, dd);
+}
+
 // Dot of one word of sixteen 2-bit codes (element j at bits 2j..2j+1) with
 // x[0..15] in eight half2 registers.  Masks pick elements (j, j+8).
 __device__ __forceinline__ float dot16_w2(uint32_t w, const uint32_t (&x)[8], float acc) {
@@ -151,6 +171,7 @@ struct TileRegs {
   uint4 sz;                        // 4 x (s, z) half pairs
   uint2 cols;                      // 4 x u16 (2c + swap)
   uint32_t hdr;                    // slice << 2 | FIRST | LAST
+  uint32_t rem;                    // tiles from this one to its slice's last tile
 };
 
 template <int BITS>
@@ -180,7 +201,7 @@ __device__ __forceinline__ uint2 group_words(const TileRegs<BITS>& r, int u) {
 template <int BITS, int B, bool XSMEM>
 __device__ __forceinline__ void group_partial(const KParams& p, const TileRegs<BITS>& tr, int u,
                                               const uint8_t* __restrict__ xs,
-                                              const float* __restrict__ xc, float (&part)[kMaxBatch]) {
+                                              const float2* __restrict__ xc, float (&part)[kMaxBatch]) {
   const uint32_t colw = (u < 2) ? tr.cols.x : tr.cols.y;
   const uint32_t f = (colw >> ((u & 1) * 16)) & 0xffffu;  // 2c + swap
   const uint32_t xoff0 = f * 16u;                         // = c*32 + swap*16: first x chunk
@@ -202,19 +223,26 @@ __device__ __forceinline__ void group_partial(const KParams& p, const TileRegs<B
       xa = __ldg(reinterpret_cast<const uint4*>(xrow + xoff0));
       xb = __ldg(reinterpret_cast<const uint4*>(xrow + xoff1));
     }
-    const float Xc = xc[(size_t)b * (p.cols / kGroup) + c];
-    float dot;
+    const float2 X = xc[(size_t)b * (p.cols / kGroup) + c];  // (sum over even t, odd t)
     if (BITS == 4) {
-      // word 0 pairs with the first x chunk, word 1 with the second
-      const float d0 = dot8_w4(w.x, xa.x, xa.y, xa.z, xa.w, 0.f);
-      const float d1 = dot8_w4(w.y, xb.x, xb.y, xb.z, xb.w, 0.f);
-      dot = d0 + d1;
+      // Offset-folded dequantization: the LOP3 magic leaves
+      // 1024 + q (even elements) and 1024 + 16 q (odd elements) as exact fp16;
+      // their products with x are exact in fp32, and the offsets are removed
+      // once per group with the parity sums: sum_t (q_t - z) x_t =
+      //   D_even + D_odd/16 - (1024 + z) X_even - (64 + z) X_odd.
+      float de = 0.f, dd = 0.f;
+      dot8_w4_raw(w.x, xa.x, xa.y, xa.z, xa.w, de, dd);  // word 0 <-> first x chunk
+      dot8_w4_raw(w.y, xb.x, xb.y, xb.z, xb.w, de, dd);  // word 1 <-> second x chunk
+      float t = fmaf(dd, 0.0625f, de);
+      t = fmaf(-(1024.f + z), X.x, t);
+      t = fmaf(-(64.f + z), X.y, t);
+      part[b] = s * t;
     } else {
       // 16-bit half h of the word holds the elements of x chunk h
       const uint32_t xr[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-      dot = dot16_w2(w.x, xr, 0.f);
+      const float dot = dot16_w2(w.x, xr, 0.f);
+      part[b] = s * fmaf(-z, X.y, fmaf(-z, X.x, dot));
     }
-    part[b] = s * fmaf(-z, Xc, dot);
   }
 }
 
@@ -243,11 +271,31 @@ __device__ __forceinline__ unsigned long long ld_slot(const unsigned long long* 
   return s;
 }
 
+constexpr int kPre = 2;  // successor records an owner requests before its last tile
+
 template <int B>
 __device__ __forceinline__ void collect(const KParams& p, int gw, int w_last, float (&v)[kMaxBatch],
-                                        int lane) {
-  constexpr int kBatch = 8;  // records polled per round trip
-  for (int w0 = gw + 1; w0 <= w_last; w0 += kBatch) {
+                                        int lane, unsigned long long (&pre)[kPre][kMaxBatch]) {
+  // records requested early (during the owner's last tile): usually ready
+#pragma unroll
+  for (int k = 0; k < kPre; ++k) {
+    const int w = gw + 1 + k;
+    if (w > w_last) break;
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      unsigned long long* slot = ws_slot<B>(p, w, b, lane);
+      unsigned long long s = pre[k][b];
+      int spins = 0;
+      while ((s >> 32) == 0ull) {
+        if (++spins > 2) __nanosleep(64);
+        s = ld_slot(slot);
+      }
+      v[b] += __uint_as_float((uint32_t)s);
+      asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(slot), "l"(0ull) : "memory");
+    }
+  }
+  constexpr int kBatch = 8;  // further records polled per round trip
+  for (int w0 = gw + 1 + kPre; w0 <= w_last; w0 += kBatch) {
 #pragma unroll
     for (int b = 0; b < B; ++b) {
       unsigned long long s[kBatch];
@@ -331,7 +379,9 @@ __device__ __forceinline__ void read_tile(TileRegs<BITS>& r, const uint8_t* tile
   if (BITS == 4) r.codes[BITS == 4 ? 1 : 0] = *reinterpret_cast<const uint4*>(tile + kTileHeaderBytes + 512 + lane * 16);
   r.sz = *reinterpret_cast<const uint4*>(tile + off_sz(BITS) + lane * 16);
   r.cols = *reinterpret_cast<const uint2*>(tile + off_cols(BITS) + lane * 8);
-  r.hdr = *reinterpret_cast<const uint32_t*>(tile);  // broadcast
+  const uint2 h = *reinterpret_cast<const uint2*>(tile);  // broadcast
+  r.hdr = h.x;
+  r.rem = h.y;
 }
 
 template <int BITS, int B, bool XSMEM>
@@ -380,50 +430,51 @@ __global__ void __launch_bounds__(kMaxThreads, min_ctas_per_sm(B)) gqsa_streamk_
   trace_point(p, gw, lane, 1);
 
   // ---- stage activations in shared memory with plain 128-bit loads (not
-  //      through the TMA unit, whose queue already holds the weight ring
-  //      fills), then the per-column-group sums X_{b,c} (fp32, fixed t order)
+  //      through the TMA unit, whose queue holds the weight ring fills) and
+  //      compute the per-column-group sums X_{b,c} (fp32, fixed t order) from
+  //      the same registers: one pass, one barrier.
   const int KG = p.cols / kGroup;
   uint8_t* xs = smem + p.ring_bytes;
-  float* xc = reinterpret_cast<float*>(xs + (XSMEM ? (size_t)B * p.cols * 2 : 0));
-  if (XSMEM) {
-    const int n16 = p.cols / 8;  // uint4 per batch row
-    constexpr int U = 4;
-    for (int i0 = threadIdx.x; i0 < B * n16; i0 += U * nthreads) {
-      uint4 v[U];
+  float2* xc = reinterpret_cast<float2*>(xs + (XSMEM ? (size_t)B * p.cols * 2 : 0));
+  {
+    constexpr int U = 2;  // column groups per thread per round (2 x 32 B in flight)
+    for (int i0 = threadIdx.x; i0 < B * KG; i0 += U * nthreads) {
+      uint4 v[U][2];
 #pragma unroll
-      for (int k = 0; k < U; ++k) {  // U independent loads in flight
+      for (int k = 0; k < U; ++k) {
         const int i = i0 + k * nthreads;
-        if (i < B * n16) {
-          const int b = i / n16, j = i - b * n16;
-          v[k] = __ldg(reinterpret_cast<const uint4*>(p.X + (int64_t)b * p.ldx) + j);
+        if (i < B * KG) {
+          const int b = i / KG, c = i - b * KG;
+          const uint4* src = reinterpret_cast<const uint4*>(p.X + (int64_t)b * p.ldx) + 2 * c;
+          v[k][0] = __ldg(src);
+          v[k][1] = __ldg(src + 1);
         }
       }
 #pragma unroll
-      for (int k = 0; k < U; ++k)
-        if (i0 + k * nthreads < B * n16) reinterpret_cast<uint4*>(xs)[i0 + k * nthreads] = v[k];
-    }
-    __syncthreads();
-  }
-  for (int i = threadIdx.x; i < B * KG; i += nthreads) {
-    const int b = i / KG, c = i - b * KG;
-    uint4 v0, v1;
-    if (XSMEM) {
-      v0 = reinterpret_cast<const uint4*>(xs + (size_t)b * p.cols * 2)[2 * c];
-      v1 = reinterpret_cast<const uint4*>(xs + (size_t)b * p.cols * 2)[2 * c + 1];
-    } else {
-      v0 = __ldg(reinterpret_cast<const uint4*>(p.X + (int64_t)b * p.ldx) + 2 * c);
-      v1 = __ldg(reinterpret_cast<const uint4*>(p.X + (int64_t)b * p.ldx) + 2 * c + 1);
-    }
-    const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-    const uint32_t one = 0x3C003C00u;  // half2(1, 1): x * 1 is exact, one FHFMA per element
-    float acc = 0.f;
+      for (int k = 0; k < U; ++k) {
+        const int i = i0 + k * nthreads;
+        if (i < B * KG) {
+          const int b = i / KG, c = i - b * KG;
+          if (XSMEM) {
+            uint4* dst = reinterpret_cast<uint4*>(xs + (size_t)b * p.cols * 2) + 2 * c;
+            dst[0] = v[k][0];
+            dst[1] = v[k][1];
+          }
+          const uint32_t w[8] = {v[k][0].x, v[k][0].y, v[k][0].z, v[k][0].w,
+                                 v[k][1].x, v[k][1].y, v[k][1].z, v[k][1].w};
+          const uint32_t one = 0x3C003C00u;  // half2(1, 1): x * 1 is exact, one FHFMA per element
+          float ae = 0.f, ao = 0.f;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {  // t = 0..15 in order
-      acc = fhfma<0, 0>(w[k], one, acc);
-      acc = fhfma<1, 0>(w[k], one, acc);
+          for (int e = 0; e < 8; ++e) {  // even t = 0, 2, .., 14 and odd t = 1, .., 15, in order
+            ae = fhfma<0, 0>(w[e], one, ae);
+            ao = fhfma<1, 0>(w[e], one, ao);
+          }
+          xc[i] = make_float2(ae, ao);
+        }
+      }
     }
-    xc[i] = acc;
   }
+  trace_point(p, gw, lane, 6);
   __syncthreads();
 
   // ---- empty rows get bias (or 0): grid-stride over the empty-row list
@@ -442,6 +493,8 @@ __global__ void __launch_bounds__(kMaxThreads, min_ctas_per_sm(B)) gqsa_streamk_
   for (int b = 0; b < kMaxBatch; ++b) acc[b] = 0.f;
   bool foreign = !(hdr0 & kTileFirst);  // slice opened by an earlier warp
   uint32_t last_hdr = 0;
+  int w_last = gw;
+  unsigned long long pre[kPre][kMaxBatch];
   int s = 0;
   uint32_t phase = 0;
   for (int t = t_begin; t < t_end; ++t) {
@@ -458,6 +511,16 @@ __global__ void __launch_bounds__(kMaxThreads, min_ctas_per_sm(B)) gqsa_streamk_
     if (++s == NS) {
       s = 0;
       phase ^= 1u;
+    }
+    if (t == t_end - 1 && !(tr.hdr & kTileLast) && !foreign) {
+      // this warp will own a slice that continues downstream: request the
+      // successors' fix-up records now, so they arrive during this tile's math
+      w_last = warp_of_tile(p, t_end - 1 + (int)tr.rem);
+#pragma unroll
+      for (int k = 0; k < kPre; ++k)
+#pragma unroll
+        for (int b = 0; b < B; ++b)
+          pre[k][b] = (gw + 1 + k <= w_last) ? ld_slot(ws_slot<B>(p, gw + 1 + k, b, lane)) : 0ull;
     }
     float part[kPerLane][kMaxBatch];
 #pragma unroll
@@ -480,11 +543,14 @@ __global__ void __launch_bounds__(kMaxThreads, min_ctas_per_sm(B)) gqsa_streamk_
   if (!(last_hdr & kTileLast)) {
     if (foreign) {  // the whole range lies inside a slice owned upstream
       publish<B>(p, gw, acc, lane);
+      if (p.trace && lane == 0) p.trace[(int64_t)gw * 8 + 7] = 1;
     } else {  // owner: add the successors' partials, then store
-      const int rem = (int)__ldg(reinterpret_cast<const uint32_t*>(tiles + (int64_t)(t_end - 1) * tb) + 1);
-      collect<B>(p, gw, warp_of_tile(p, t_end - 1 + rem), acc, lane);
+      collect<B>(p, gw, w_last, acc, lane, pre);
       store_rows<B>(p, acc, row, lane);
+      if (p.trace && lane == 0) p.trace[(int64_t)gw * 8 + 7] = 100 + w_last - gw;
     }
+  } else if (p.trace && lane == 0) {
+    p.trace[(int64_t)gw * 8 + 7] = 0;
   }
   trace_point(p, gw, lane, 5);
 }

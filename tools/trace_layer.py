@@ -80,6 +80,25 @@ def main():
     print("median phase durations (µs): wait=%.2f stage=%.2f tile0=%.2f loop=%.2f fixup=%.2f" % (
         np.median(d[..., 1] - d[..., 0]), np.median(d[..., 2] - d[..., 1]), np.median(d[..., 3] - d[..., 2]),
         np.median(d[..., 4] - d[..., 3]), np.median(d[..., 5] - d[..., 4])))
+    raw = np.stack([b.cpu().numpy().reshape(W, 8) for b in bufs])
+    role = raw[1:, :, 7]
+    T8 = (raw - t0) / 1e3
+    e = T8[1:]
+    print("staging split (µs): x_loads+xc=%.2f barrier+rest=%.2f" % (
+        np.median(e[..., 6] - e[..., 1]), np.median(e[..., 2] - e[..., 6])))
+    fx = e[..., 5] - e[..., 4]
+    for name, m in (("closed", role == 0), ("publisher", role == 1), ("owner", role >= 100)):
+        if m.any():
+            v = fx[m]
+            print("fixup %-9s %4.0f%% of warps: p50/p90/max %.2f/%.2f/%.2f us" % (
+                name, 100 * m.mean(), np.median(v), np.percentile(v, 90), v.max()))
+    if (role >= 100).any():
+        ch = role[role >= 100] - 100
+        print("owner chain length (successor warps) p50/p90/max: %d/%d/%d" % (
+            np.median(ch), np.percentile(ch, 90), ch.max()))
+    prev_exit = T[:-1, :, 5].max(axis=1)
+    rel = T[1:, :, 1].min(axis=1) - prev_exit
+    print("PDL release after previous launch's last exit (µs):", " ".join(f"{r:.2f}" for r in rel[:5]))
 
 
 if __name__ == "__main__":
