@@ -48,7 +48,7 @@ typedef enum {
   GQSA_OK = 0,
   GQSA_ERR_SHAPE = -1,       /* dims mismatch, cols % G != 0, B not in [1,8], bad row range */
   GQSA_ERR_VALIDATION = -2,  /* BSR invariant violated (see gqsa_pack) or inconsistent blob */
-  GQSA_ERR_UNSUPPORTED = -3, /* bits not in {2,4}, G != 16, K/G > 32767 */
+  GQSA_ERR_UNSUPPORTED = -3, /* bits not in {2,4}, G != 16, cols > 32768 */
   GQSA_ERR_BUFFER = -4,      /* null pointer, blob/workspace too small, misaligned device pointer */
   GQSA_ERR_CUDA = -5         /* CUDA launch / copy failure */
 } gqsa_status_t;

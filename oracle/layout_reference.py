@@ -126,6 +126,6 @@ def pack_reference(bsr: dict, row_begin: int = 0, row_end=None) -> bytes:
                     struct.pack_into("<HH", out, base + 32 + codes_total + lane * 16 + u * 4,
                                      int(sc[g]), int(zr[g]))
                     struct.pack_into("<H", out, base + 32 + codes_total + T * 4 + lane * 8 + u * 2,
-                                     (int(gcols[g]) << 1) | swap)
+                                     ((int(gcols[g]) << 1) | swap) << 4)
             t += 1
     return bytes(out)

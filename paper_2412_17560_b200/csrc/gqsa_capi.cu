@@ -78,7 +78,7 @@ struct SmemPlan {
 SmemPlan smem_plan(const gqsa_desc_t* d, int B) {
   SmemPlan sp{};
   const size_t tb = (size_t)tile_bytes(d->bits);
-  const size_t xc = (size_t)B * (d->cols / kGroup) * 8;  // float2 (even, odd) column sums
+  const size_t xc = (size_t)B * d->cols;  // float2 (P, Q) per 16-B chunk: K/8 x 8 B per batch row
   const size_t xb = (size_t)B * d->cols * 2;
   const int W = warps_per_cta(B);
   const int c = ctas_per_sm_cap();
@@ -95,7 +95,7 @@ SmemPlan smem_plan(const gqsa_desc_t* d, int B) {
   sp.warps = W;
   sp.stages = ns;
   sp.ring = (size_t)W * ns * tb;
-  sp.total = sp.ring + xbytes;
+  sp.total = xbytes + sp.ring + (size_t)W * kMaxStages * 8;  // + the ring's mbarriers
   return sp;
 }
 
@@ -207,7 +207,7 @@ extern "C" int gqsa_gemm_smallbatch(const gqsa_desc_t* desc, const void* d_blob,
   p.part_q = pl.active_warps ? desc->num_tiles / pl.active_warps : 0;
   p.part_r = pl.active_warps ? desc->num_tiles % pl.active_warps : 0;
   p.stages = pl.stages;
-  p.ring_bytes = pl.ring_bytes;
+  p.ring_offset = pl.smem_bytes - pl.ring_bytes - pl.warps_per_cta * kMaxStages * 8;
   p.trace = (g_trace && g_trace_bytes >= (size_t)pl.active_warps * 64) ? g_trace : nullptr;
   if (desc->rows == 0) return GQSA_OK;
 

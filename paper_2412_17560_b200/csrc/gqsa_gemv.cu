@@ -196,17 +196,35 @@ __device__ __forceinline__ uint2 group_words(const TileRegs<BITS>& r, int u) {
   }
 }
 
-// part[b] = s * (sum_t q_t x_t - z * X_c) for the lane's group in slot u
-// (Eq. 3 per group: sum_t (q_t - z) s x_t with z applied once).
+// acc[b] += s * sum_t (q_t - z) x_t for the lane's group in slot u (Eq. 3
+// per group, z applied once through the column-group sums).
+//   xs : activations [B][K] fp16 in shared memory (or global when !XSMEM)
+//   pq : per 16-B chunk index f = 2c + swap, float2 (P, Q) with
+//        P = 1024 X_even + 64 X_odd and Q = X_even + X_odd of column group c
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float2 lds64f(uint32_t a) {
+  float2 v;
+  asm("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
+
+extern __shared__ __align__(128) uint8_t smem[];
+
 template <int BITS, int B, bool XSMEM>
-__device__ __forceinline__ void group_partial(const KParams& p, const TileRegs<BITS>& tr, int u,
-                                              const uint8_t* __restrict__ xs,
-                                              const float2* __restrict__ xc, float (&part)[kMaxBatch]) {
+__device__ __forceinline__ void group_accumulate(const KParams& p, const TileRegs<BITS>& tr, int u,
+                                                 float (&acc)[kMaxBatch]) {
+  // shared-window offsets recomputed here so that they stay in uniform
+  // registers ([R + UR] addressing on every LDS)
+  const uint32_t xs = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t pq = xs + (XSMEM ? (uint32_t)B * 2u * (uint32_t)p.cols : 0u);
   const uint32_t colw = (u < 2) ? tr.cols.x : tr.cols.y;
-  const uint32_t f = (colw >> ((u & 1) * 16)) & 0xffffu;  // 2c + swap
-  const uint32_t xoff0 = f * 16u;                         // = c*32 + swap*16: first x chunk
-  const uint32_t xoff1 = xoff0 ^ 16u;                     // second x chunk
-  const uint32_t c = f >> 1;
+  const uint32_t xoff0 = (u & 1) ? (colw >> 16) : (colw & 0xffffu);  // byte offset of the first x chunk
+  const uint32_t xoff1 = xoff0 ^ 16u;                                  // the other chunk
+  const uint32_t pqoff = xoff0 >> 1;                                   // f * 8
   const uint2 w = group_words<BITS>(tr, u);
   const uint32_t szw = u == 0 ? tr.sz.x : u == 1 ? tr.sz.y : u == 2 ? tr.sz.z : tr.sz.w;
   const __half2 sz = *reinterpret_cast<const __half2*>(&szw);
@@ -214,34 +232,31 @@ __device__ __forceinline__ void group_partial(const KParams& p, const TileRegs<B
 #pragma unroll
   for (int b = 0; b < B; ++b) {
     uint4 xa, xb;
-    if (XSMEM) {
-      const uint8_t* xrow = xs + (size_t)b * (size_t)p.cols * 2;
-      xa = *reinterpret_cast<const uint4*>(xrow + xoff0);
-      xb = *reinterpret_cast<const uint4*>(xrow + xoff1);
+    if (XSMEM) {  // x of batch row b at shared offset b * 2K (x is at the start of smem)
+      xa = lds128(xs + b * 2u * (uint32_t)p.cols + xoff0);
+      xb = lds128(xs + b * 2u * (uint32_t)p.cols + xoff1);
     } else {
       const uint8_t* xrow = reinterpret_cast<const uint8_t*>(p.X + (int64_t)b * p.ldx);
       xa = __ldg(reinterpret_cast<const uint4*>(xrow + xoff0));
       xb = __ldg(reinterpret_cast<const uint4*>(xrow + xoff1));
     }
-    const float2 X = xc[(size_t)b * (p.cols / kGroup) + c];  // (sum over even t, odd t)
+    const float2 X = lds64f(pq + b * (uint32_t)p.cols + pqoff);
     if (BITS == 4) {
       // Offset-folded dequantization: the LOP3 magic leaves
       // 1024 + q (even elements) and 1024 + 16 q (odd elements) as exact fp16;
       // their products with x are exact in fp32, and the offsets are removed
-      // once per group with the parity sums: sum_t (q_t - z) x_t =
-      //   D_even + D_odd/16 - (1024 + z) X_even - (64 + z) X_odd.
+      // once per group with the column sums: sum_t (q_t - z) x_t =
+      //   D_even + D_odd/16 - (1024 X_even + 64 X_odd) - z (X_even + X_odd).
       float de = 0.f, dd = 0.f;
       dot8_w4_raw(w.x, xa.x, xa.y, xa.z, xa.w, de, dd);  // word 0 <-> first x chunk
       dot8_w4_raw(w.y, xb.x, xb.y, xb.z, xb.w, de, dd);  // word 1 <-> second x chunk
-      float t = fmaf(dd, 0.0625f, de);
-      t = fmaf(-(1024.f + z), X.x, t);
-      t = fmaf(-(64.f + z), X.y, t);
-      part[b] = s * t;
+      const float t = fmaf(-z, X.y, fmaf(dd, 0.0625f, de) - X.x);
+      acc[b] = fmaf(s, t, acc[b]);
     } else {
       // 16-bit half h of the word holds the elements of x chunk h
       const uint32_t xr[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
       const float dot = dot16_w2(w.x, xr, 0.f);
-      part[b] = s * fmaf(-z, X.y, fmaf(-z, X.x, dot));
+      acc[b] = fmaf(s, fmaf(-z, X.y, dot), acc[b]);
     }
   }
 }
@@ -386,8 +401,6 @@ __device__ __forceinline__ void read_tile(TileRegs<BITS>& r, const uint8_t* tile
 
 template <int BITS, int B, bool XSMEM>
 __global__ void __launch_bounds__(kMaxThreads, min_ctas_per_sm(B)) gqsa_streamk_kernel(KParams p) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t ring_bar[kMaxWarps][kMaxStages];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int nthreads = blockDim.x;
@@ -406,9 +419,12 @@ __global__ void __launch_bounds__(kMaxThreads, min_ctas_per_sm(B)) gqsa_streamk_
   // ---- weights never depend on the previous kernel: each warp's first NS
   //      tiles are requested (1-D TMA bulk copies into its shared-memory
   //      ring) BEFORE the PDL wait, so they overlap the previous kernel
-  uint8_t* ring = smem + (size_t)warp * NS * tb;
+  // shared memory: [x: B*K fp16 (XSMEM)][(P,Q): B*K/8 float2][TMA ring: W x NS tiles]
+  uint8_t* ring = smem + p.ring_offset + (size_t)warp * NS * tb;
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
-  const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&ring_bar[warp][0]);
+  // the ring's mbarriers follow the ring: [W][kMaxStages] u64
+  const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(
+      smem + p.ring_offset + (size_t)(nthreads >> 5) * NS * tb + (size_t)warp * kMaxStages * 8);
   if (lane == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(bar0 + 8 * s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -434,8 +450,8 @@ __global__ void __launch_bounds__(kMaxThreads, min_ctas_per_sm(B)) gqsa_streamk_
   //      compute the per-column-group sums X_{b,c} (fp32, fixed t order) from
   //      the same registers: one pass, one barrier.
   const int KG = p.cols / kGroup;
-  uint8_t* xs = smem + p.ring_bytes;
-  float2* xc = reinterpret_cast<float2*>(xs + (XSMEM ? (size_t)B * p.cols * 2 : 0));
+  uint8_t* xs = smem;
+  uint8_t* pq = xs + (XSMEM ? (size_t)B * p.cols * 2 : 0);  // [B][K/8] float2 (P, Q) per chunk index
   {
     constexpr int U = 2;  // column groups per thread per round (2 x 32 B in flight)
     for (int i0 = threadIdx.x; i0 < B * KG; i0 += U * nthreads) {
@@ -469,7 +485,12 @@ __global__ void __launch_bounds__(kMaxThreads, min_ctas_per_sm(B)) gqsa_streamk_
             ae = fhfma<0, 0>(w[e], one, ae);
             ao = fhfma<1, 0>(w[e], one, ao);
           }
-          xc[i] = make_float2(ae, ao);
+          // P = 1024 X_even + 64 X_odd, Q = X_even + X_odd; stored for both
+          // chunk orders (swap = 0, 1) of column group c
+          const float2 v2 = make_float2(fmaf(1024.f, ae, 64.f * ao), ae + ao);
+          float2* dst = reinterpret_cast<float2*>(pq + (size_t)b * p.cols) + 2 * c;
+          dst[0] = v2;
+          dst[1] = v2;
         }
       }
     }
@@ -497,24 +518,13 @@ __global__ void __launch_bounds__(kMaxThreads, min_ctas_per_sm(B)) gqsa_streamk_
   unsigned long long pre[kPre][kMaxBatch];
   int s = 0;
   uint32_t phase = 0;
-  for (int t = t_begin; t < t_end; ++t) {
-    mbar_wait(bar0 + 8 * s, phase);
-    if (t == t_begin) trace_point(p, gw, lane, 3);
-    TileRegs<BITS> tr;
-    read_tile<BITS>(tr, ring + (size_t)s * tb, lane);
-    __syncwarp();  // every lane has read stage s: refill it with tile t + NS
-    if (lane == 0 && t + NS < t_end) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect_tx(bar0 + 8 * s, tb);
-      bulk_g2s(ring_s + s * tb, tiles + (int64_t)(t + NS) * tb, tb, bar0 + 8 * s);
-    }
-    if (++s == NS) {
-      s = 0;
-      phase ^= 1u;
-    }
+  trace_point(p, gw, lane, 3);
+
+  // Per-tile work once its registers are loaded: accumulate the lane's four
+  // groups, close the slice at its LAST tile, and (at the warp's final tile,
+  // when it owns a slice continuing downstream) request the fix-up records.
+  auto consume = [&](const TileRegs<BITS>& tr, int t) {
     if (t == t_end - 1 && !(tr.hdr & kTileLast) && !foreign) {
-      // this warp will own a slice that continues downstream: request the
-      // successors' fix-up records now, so they arrive during this tile's math
       w_last = warp_of_tile(p, t_end - 1 + (int)tr.rem);
 #pragma unroll
       for (int k = 0; k < kPre; ++k)
@@ -522,11 +532,8 @@ __global__ void __launch_bounds__(kMaxThreads, min_ctas_per_sm(B)) gqsa_streamk_
         for (int b = 0; b < B; ++b)
           pre[k][b] = (gw + 1 + k <= w_last) ? ld_slot(ws_slot<B>(p, gw + 1 + k, b, lane)) : 0ull;
     }
-    float part[kPerLane][kMaxBatch];
 #pragma unroll
-    for (int u = 0; u < kPerLane; ++u) group_partial<BITS, B, XSMEM>(p, tr, u, xs, xc, part[u]);
-#pragma unroll
-    for (int b = 0; b < B; ++b) acc[b] += (part[0][b] + part[1][b]) + (part[2][b] + part[3][b]);
+    for (int u = 0; u < kPerLane; ++u) group_accumulate<BITS, B, XSMEM>(p, tr, u, acc);
     last_hdr = tr.hdr;
     if (tr.hdr & kTileLast) {  // the slice ends in this tile: its rows are complete
       if (foreign) publish<B>(p, gw, acc, lane);
@@ -536,6 +543,43 @@ __global__ void __launch_bounds__(kMaxThreads, min_ctas_per_sm(B)) gqsa_streamk_
       foreign = false;
       if (t + 1 < t_end) row = __ldg(p.perm + (int64_t)((tr.hdr >> 2) + 1) * kLanes + lane);
     }
+  };
+  auto refill = [&](int stage, int t_next) {  // lane 0, after __syncwarp
+    if (t_next < t_end) {
+      mbar_expect_tx(bar0 + 8 * stage, tb);
+      bulk_g2s(ring_s + stage * tb, tiles + (int64_t)t_next * tb, tb, bar0 + 8 * stage);
+    }
+  };
+
+  // two tiles per iteration: one ring handshake per pair, and the x gathers
+  // of both tiles can be in flight together
+  int t = t_begin;
+  for (; t + 1 < t_end; t += 2) {
+    const int s0 = s;
+    const uint32_t ph0 = phase;
+    if (++s == NS) { s = 0; phase ^= 1u; }
+    const int s1 = s;
+    const uint32_t ph1 = phase;
+    if (++s == NS) { s = 0; phase ^= 1u; }
+    mbar_wait(bar0 + 8 * s0, ph0);
+    mbar_wait(bar0 + 8 * s1, ph1);
+    TileRegs<BITS> tr0, tr1;
+    read_tile<BITS>(tr0, ring + (size_t)s0 * tb, lane);
+    read_tile<BITS>(tr1, ring + (size_t)s1 * tb, lane);
+    __syncwarp();  // every lane has read both stages: refill them
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      refill(s0, t + NS);
+      refill(s1, t + 1 + NS);
+    }
+    consume(tr0, t);
+    consume(tr1, t + 1);
+  }
+  if (t < t_end) {
+    mbar_wait(bar0 + 8 * s, phase);
+    TileRegs<BITS> tr;
+    read_tile<BITS>(tr, ring + (size_t)s * tb, lane);
+    consume(tr, t);
   }
 
   trace_point(p, gw, lane, 4);

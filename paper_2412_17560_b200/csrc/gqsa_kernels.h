@@ -33,7 +33,7 @@ struct KParams {
   int32_t rows, cols, num_tiles, n_empty, active_warps, lanes_per_row;
   int32_t part_q, part_r;  // num_tiles = part_q * active_warps + part_r
   int32_t stages;          // ring depth NS (tiles) per warp
-  int32_t ring_bytes;      // warps * NS * tile_bytes: the x / X_c area starts here
+  int32_t ring_offset;     // shared-memory offset of the TMA ring (after x and the column sums)
   uint64_t* trace;         // optional [active_warps][8] %globaltimer stamps (debug)
 };
 

@@ -31,6 +31,7 @@ constexpr int kTileHeaderBytes = 32;  // u32 (slice<<2 | FIRST | LAST), tiles_to
 constexpr int kSectionAlign = 256;
 constexpr uint32_t kFlagGreedySwap = 2u;     // swap bits balance smem bank quads per quarter-warp
 constexpr int kFlagLanesPerRowShift = 8;     // flags bits 8..15: lanes per row S
+constexpr int kMaxCols = 32768;              // column field = byte offset (2c+swap)*16 < 65536
 constexpr uint32_t kTileFirst = 1u;          // tile header flags
 constexpr uint32_t kTileLast = 2u;
 

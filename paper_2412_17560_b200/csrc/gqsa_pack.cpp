@@ -37,7 +37,7 @@ int check_bsr_header(const gqsa_bsr_t* b) {
   if (b->rows < 0 || b->cols <= 0 || b->group_size <= 0 || b->nnzg < 0) return GQSA_ERR_SHAPE;
   if (b->group_size != kGroup || (b->bits != 4 && b->bits != 2)) return GQSA_ERR_UNSUPPORTED;
   if (b->cols % b->group_size) return GQSA_ERR_SHAPE;
-  if (b->cols / kGroup > 32767) return GQSA_ERR_UNSUPPORTED;  // col field = 2c+swap in u16
+  if (b->cols > kMaxCols) return GQSA_ERR_UNSUPPORTED;  // col field = byte offset in u16
   if (!b->row_index) return GQSA_ERR_BUFFER;
   if (b->nnzg > 0 && (!b->group_cols || !b->codes || !b->scales_f16 || !b->zeros_f16))
     return GQSA_ERR_BUFFER;
@@ -230,7 +230,7 @@ extern "C" int gqsa_pack(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_e
           sz[0] = bsr->scales_f16[g];
           sz[1] = bsr->zeros_f16[g];
           uint16_t* col = reinterpret_cast<uint16_t*>(tile + off_cols(bits) + l * 8 + u * 2);
-          *col = (uint16_t)((bsr->group_cols[g] << 1) | swap);
+          *col = (uint16_t)(((bsr->group_cols[g] << 1) | swap) << 4);  // byte offset of the first x chunk
         }
       }
     }
@@ -247,7 +247,8 @@ extern "C" int gqsa_read_desc(const void* blob, size_t blob_bytes, gqsa_desc_t* 
   if (h.magic != kMagic || h.version != (uint32_t)kVersion) return GQSA_ERR_VALIDATION;
   if (h.group_size != kGroup || (h.bits != 4 && h.bits != 2)) return GQSA_ERR_UNSUPPORTED;
   if (h.tile_groups != kTileGroups || h.tile_bytes != tile_bytes(h.bits)) return GQSA_ERR_VALIDATION;
-  if (h.rows < 0 || h.cols <= 0 || h.cols % kGroup || h.nnzg < 0) return GQSA_ERR_VALIDATION;
+  if (h.rows < 0 || h.cols <= 0 || h.cols % kGroup || h.cols > kMaxCols || h.nnzg < 0)
+    return GQSA_ERR_VALIDATION;
   if (h.n_nzrows < 0 || h.n_empty < 0 || h.n_nzrows + h.n_empty != h.rows) return GQSA_ERR_VALIDATION;
   if (h.nnzg < h.n_nzrows || h.num_tiles < 0) return GQSA_ERR_VALIDATION;
   const int S = (int)((uint32_t)h.flags >> kFlagLanesPerRowShift) & 0xff;
@@ -308,7 +309,8 @@ extern "C" int gqsa_unpack(const void* blob, size_t blob_bytes, gqsa_bsr_t* out)
           continue;
         }
         if (row < 0 || row >= d.rows) return GQSA_ERR_VALIDATION;
-        rows[row].push_back(G{(uint16_t)(col >> 1), sz[0], sz[1], src, (col & 1u) != 0});
+        if (col & 15u) return GQSA_ERR_VALIDATION;
+        rows[row].push_back(G{(uint16_t)(col >> 5), sz[0], sz[1], src, ((col >> 4) & 1u) != 0});
       }
     }
   }

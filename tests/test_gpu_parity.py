@@ -76,7 +76,7 @@ EXACT_CASES = [
     (300, 1024, 4, 0.3, "row_balanced", 4),
     (77, 208, 4, 0.2, "uniform", 8),      # ragged tile tail, odd rows
     (3, 16384, 4, 0.5, "uniform", 2),     # few long rows: rows span many warps
-    (1, 65536, 4, 0.5, "uniform", 1),     # one row across every warp (chained fix-up)
+    (1, 32768, 4, 0.5, "uniform", 1),     # one row over 32 lanes (S = 32), max K
     (4096, 16, 4, 0.5, "uniform", 1),     # K = G: many empty rows, 1-group rows
     (5, 64, 4, 0.5, "uniform", 1),        # nnzg < one tile
     (640, 512, 2, 0.9, "uniform", 5),     # mostly-empty rows
