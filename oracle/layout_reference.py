@@ -47,9 +47,32 @@ def lanes_per_row(n_nz: int, max_len: int) -> int:
     return max(s, LANES // p)
 
 
-def rotation(row: int, n: int) -> int:
-    """Dealing start of a row: ((row * 2654435761) mod 2^32) >> 7, mod n."""
-    return (((row * 2654435761) & 0xFFFFFFFF) >> 7) % n
+def deal_row(cols_of_row, lanes, slots):
+    """Bank-aware dealing of one row's kept groups (CSR positions 0..n-1 with
+    group columns cols_of_row) over its lanes: slot by slot, lane l takes the
+    first remaining group whose column c has c mod 8 == (l mod 16) // 2, else
+    c mod 8 == that ^ 4, else the first remaining group of the fullest bucket
+    (lowest bucket index on ties).  Returns {(lane, slot): position}."""
+    buckets = [[] for _ in range(8)]
+    for k, c in enumerate(cols_of_row):
+        buckets[int(c) % 8].append(k)
+    heads = [0] * 8
+    left = len(cols_of_row)
+    out = {}
+    for j in range(slots):
+        for lane in lanes:
+            if left == 0:
+                return out
+            want = (lane % 16) // 2
+            b = want
+            if heads[b] == len(buckets[b]):
+                b = want ^ 4
+            if heads[b] == len(buckets[b]):
+                b = max(range(8), key=lambda i: (len(buckets[i]) - heads[i], -i))
+            out[(lane, j)] = buckets[b][heads[b]]
+            heads[b] += 1
+            left -= 1
+    return out
 
 
 def pack_reference(bsr: dict, row_begin: int = 0, row_end=None) -> bytes:
@@ -81,7 +104,7 @@ def pack_reference(bsr: dict, row_begin: int = 0, row_end=None) -> bytes:
     out = bytearray(total)
     struct.pack_into("<IIiiiiqiiiiiiiiQQQQQ", out, 0,
                      MAGIC, VERSION, rows, K, G, n, nnzg, T, num_tiles, len(nz), len(empty),
-                     tb, 2 | (S << 8), row_begin, row_end, off_ri, off_perm, off_em, off_tiles, total)
+                     tb, 4 | (S << 8), row_begin, row_end, off_ri, off_perm, off_em, off_tiles, total)
     struct.pack_into(f"<{rows + 1}i", out, off_ri, *[v - g0 for v in ri_all[row_begin:row_end + 1]])
     if empty:
         struct.pack_into(f"<{len(empty)}i", out, off_em, *empty)
@@ -101,23 +124,25 @@ def pack_reference(bsr: dict, row_begin: int = 0, row_end=None) -> bytes:
             lane_row.append(nz[k] if k < len(nz) else -1)
         struct.pack_into(f"<{LANES}i", out, off_perm + 4 * LANES * s, *lane_row)
         nt = slice_tiles[s]
+        deal = {}
+        for l0 in range(0, LANES, S):
+            row = lane_row[l0]
+            if row >= 0:
+                gr = ri_all[row_begin + row]
+                for key, pos in deal_row(gcols[gr:gr + counts[row]], range(l0, l0 + S), nt * SLOTS).items():
+                    deal[key] = gr + pos
         for tau in range(nt):
             base = off_tiles + t * tb
             flags = (1 if tau == 0 else 0) | (2 if tau == nt - 1 else 0)
             struct.pack_into("<IIII", out, base, (s << 2) | flags, nt - 1 - tau, 0, 0)
             for u in range(SLOTS):
                 for lane in range(LANES):
-                    if lane % 8 == 0:
-                        load = [0] * 8                  # bank-quad load of the quarter-warp
-                    row = lane_row[lane]
-                    k = (tau * SLOTS + u) * S + lane % S  # position in the row's dealing order
-                    if row < 0 or k >= counts[row]:
-                        load[0] += 1                    # padding reads x chunk 0
+                    g = deal.get((lane, tau * SLOTS + u))
+                    off_col = base + 32 + codes_total + T * 4 + lane * 8 + u * 2
+                    if g is None:  # padding: reads the lane's target chunk
+                        struct.pack_into("<H", out, off_col, ((lane % 16) % (K // 8)) << 4)
                         continue
-                    g = ri_all[row_begin + row] + (k + rotation(row_begin + row, counts[row])) % counts[row]
-                    q0 = (2 * int(gcols[g])) % 8
-                    swap = 1 if load[q0 + 1] < load[q0] else 0
-                    load[q0 + swap] += 1
+                    swap = lane % 2
                     gb = bytes(codes[g * cb:(g + 1) * cb])
                     if swap:
                         gb = gb[cb // 2:] + gb[:cb // 2]
@@ -125,7 +150,6 @@ def pack_reference(bsr: dict, row_begin: int = 0, row_end=None) -> bytes:
                     out[off_c:off_c + cb] = gb
                     struct.pack_into("<HH", out, base + 32 + codes_total + lane * 16 + u * 4,
                                      int(sc[g]), int(zr[g]))
-                    struct.pack_into("<H", out, base + 32 + codes_total + T * 4 + lane * 8 + u * 2,
-                                     ((int(gcols[g]) << 1) | swap) << 4)
+                    struct.pack_into("<H", out, off_col, ((int(gcols[g]) << 1) | swap) << 4)
             t += 1
     return bytes(out)

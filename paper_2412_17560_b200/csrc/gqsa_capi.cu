@@ -62,7 +62,7 @@ int stages_cap() {
 }
 
 int warps_per_cta(int B) {
-  static int w1 = env_int("GQSA_WARPS", kMaxWarps, 1, kMaxWarps);
+  static int w1 = env_int("GQSA_WARPS", 16, 1, kMaxWarps);
   return B <= 2 ? w1 : 8;
 }
 
@@ -209,6 +209,8 @@ extern "C" int gqsa_gemm_smallbatch(const gqsa_desc_t* desc, const void* d_blob,
   p.stages = pl.stages;
   p.ring_offset = pl.smem_bytes - pl.ring_bytes - pl.warps_per_cta * kMaxStages * 8;
   p.trace = (g_trace && g_trace_bytes >= (size_t)pl.active_warps * 64) ? g_trace : nullptr;
+  static const int skip_math = env_int("GQSA_DEBUG_SKIP_MATH", 0, 0, 1);
+  p.debug_skip_math = skip_math;
   if (desc->rows == 0) return GQSA_OK;
 
   cudaLaunchConfig_t cfg = {};

@@ -4,7 +4,7 @@
 
 namespace gqsa {
 
-constexpr int kMaxWarps = 16;           // warps per CTA: a launch-time choice <= 16
+constexpr int kMaxWarps = 32;           // warps per CTA: a launch-time choice <= 32
 constexpr int kMaxThreads = 32 * kMaxWarps;
 constexpr int kMaxStages = 8;            // tiles in flight per warp (shared-memory TMA ring)
 constexpr int kMinStages = 2;
@@ -15,9 +15,10 @@ constexpr int kCoResidentKernels = 2;    // leave room for the next PDL-launched
 // Register budget: 4 resident CTAs (64 regs/thread) at batch 1 -- the HBM
 // stream wants many warps with loads in flight; bigger batches need more
 // accumulators and are ALU / smem-bound anyway.
-// (for kMaxThreads-thread CTAs: 2 -> <= 64 registers per thread)
-constexpr int min_ctas_per_sm(int B) { return B <= 2 ? 2 : 1; }
-constexpr int kMaxWarpsBound = 4096;     // workspace records (>= any grid we launch)
+// Launch bounds: batch <= 2 launches up to 32 warps per CTA at <= 64
+// registers; larger batches (more accumulators) use 8 warps.
+constexpr int max_threads_for(int B) { return B <= 2 ? kMaxThreads : 256; }
+constexpr int kMaxWarpsBound = 8192;     // workspace records (>= any grid we launch)
 constexpr int kWsSlotBytes = 8;          // fix-up slot {partial, flag} per (warp, batch, lane)
 constexpr int kSmemBudget = 200 * 1024;  // above this, x is gathered from L1/L2
 
@@ -35,6 +36,7 @@ struct KParams {
   int32_t stages;          // ring depth NS (tiles) per warp
   int32_t ring_offset;     // shared-memory offset of the TMA ring (after x and the column sums)
   uint64_t* trace;         // optional [active_warps][8] %globaltimer stamps (debug)
+  int32_t debug_skip_math; // experiment only (GQSA_DEBUG_SKIP_MATH): stream tiles, no math
 };
 
 const void* select_kernel(int bits, int B, bool xsmem);

@@ -29,7 +29,8 @@ constexpr int kPerLane = kTileGroups / kLanes;  // 4 slots per lane per tile
 constexpr int kHeaderBytes = 256;
 constexpr int kTileHeaderBytes = 32;  // u32 (slice<<2 | FIRST | LAST), tiles_to_slice_end; 0[6]
 constexpr int kSectionAlign = 256;
-constexpr uint32_t kFlagGreedySwap = 2u;     // swap bits balance smem bank quads per quarter-warp
+constexpr uint32_t kFlagTargetDeal = 4u;     // bank-aware dealing: lane l reads chunk f = 2c+swap,
+                                             // f mod 16 == l mod 16 whenever the row allows
 constexpr int kFlagLanesPerRowShift = 8;     // flags bits 8..15: lanes per row S
 constexpr int kMaxCols = 32768;              // column field = byte offset (2c+swap)*16 < 65536
 constexpr uint32_t kTileFirst = 1u;          // tile header flags
@@ -66,11 +67,9 @@ inline int lanes_per_row_for(int n_nz, int64_t max_len) {
   return s > s_small ? s : s_small;
 }
 
-// Starting offset of a row's dealing order (a fixed hash of the source row
-// id): different lanes start at different columns, spreading bank quads.
-inline int64_t row_rotation(int64_t row, int64_t n) {
-  const uint32_t h = (uint32_t)row * 2654435761u;
-  return (int64_t)((h >> 7) % (uint64_t)n);
+// Offset (within a tile) of the column field of lane l, slot u.
+__host__ __device__ constexpr int off_cols(int bits, int lane, int u) {
+  return off_cols(bits) + lane * 8 + u * 2;
 }
 
 // On-blob header; the first 104 bytes mirror gqsa_desc_t field-for-field.

@@ -163,7 +163,7 @@ extern "C" int gqsa_pack(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_e
   h.n_nzrows = s.n_nz;
   h.n_empty = s.n_empty;
   h.tile_bytes = tile_bytes(bits);
-  h.flags = (int32_t)(kFlagGreedySwap | ((uint32_t)S << kFlagLanesPerRowShift));
+  h.flags = (int32_t)(kFlagTargetDeal | ((uint32_t)S << kFlagLanesPerRowShift));
   h.row_begin = row_begin;
   h.row_end = row_end;
   h.off_row_index = o.ri;
@@ -180,18 +180,46 @@ extern "C" int gqsa_pack(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_e
   int32_t* em = reinterpret_cast<int32_t*>(out + o.empty);
   for (int32_t i = 0; i < s.n_empty; ++i) em[i] = s.empty[i];
 
-  std::vector<int64_t> lane_group(kLanes * 4);  // source group of (lane, slot in tile), -1 = padding
+  const int nchunks = bsr->cols / 8;  // 16-B activation chunks per batch row
+  std::vector<int64_t> deal;          // [lane][slot] source group, -1 = padding
   for (int32_t sl = 0; sl < s.num_slices; ++sl) {
-    // rows of this slice, their rotation, lane assignment
     int32_t row_of_lane[kLanes];
-    int64_t rot_of_lane[kLanes];
     for (int l = 0; l < kLanes; ++l) {
       const int64_t k = (int64_t)sl * s.rows_per_slice + l / S;
       row_of_lane[l] = k < s.n_nz ? s.order[k] : -1;
-      rot_of_lane[l] = row_of_lane[l] >= 0 ? row_rotation(row_begin + row_of_lane[l], s.count[row_of_lane[l]]) : 0;
       perm[(int64_t)sl * kLanes + l] = row_of_lane[l];
     }
     const int32_t nt = s.tile0[sl + 1] - s.tile0[sl];
+    const int64_t L = (int64_t)nt * kPerLane;  // slots per lane
+    deal.assign((size_t)kLanes * L, -1);
+    // Bank-aware dealing (kFlagTargetDeal): lane l wants groups whose column
+    // c has c mod 8 == (l mod 16) / 2, read with swap = l mod 2, so the 16-B
+    // chunk index f = 2c + swap covers 8 distinct bank quads per quarter-warp
+    // (conflict-free LDS.128) and f mod 16 is distinct per half-warp
+    // (conflict-free LDS.64 of the column sums).
+    for (int l0 = 0; l0 < kLanes; l0 += S) {
+      const int32_t row = row_of_lane[l0];
+      if (row < 0) continue;
+      const int64_t g0 = bsr->row_index[row_begin + row], n = s.count[row];
+      std::vector<int64_t> bucket[8];
+      size_t head[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int64_t g = g0; g < g0 + n; ++g) bucket[bsr->group_cols[g] & 7].push_back(g);
+      int64_t left = n;
+      for (int64_t j = 0; j < L && left > 0; ++j) {
+        for (int k = 0; k < S && left > 0; ++k) {
+          const int l = l0 + k, want = (l & 15) >> 1;
+          int b = want;
+          if (head[b] == bucket[b].size()) b = want ^ 4;
+          if (head[b] == bucket[b].size()) {  // most populated remaining bucket
+            b = 0;
+            for (int c = 1; c < 8; ++c)
+              if (bucket[c].size() - head[c] > bucket[b].size() - head[b]) b = c;
+          }
+          deal[(size_t)l * L + j] = bucket[b][head[b]++];
+          --left;
+        }
+      }
+    }
     for (int32_t tau = 0; tau < nt; ++tau) {
       const int32_t t = s.tile0[sl] + tau;
       uint8_t* tile = out + o.tiles + (uint64_t)t * tile_bytes(bits);
@@ -201,23 +229,14 @@ extern "C" int gqsa_pack(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_e
                                (uint32_t)(nt - 1 - tau), 0u, 0u};
       std::memcpy(tile, hdr, sizeof(hdr));
       for (int u = 0; u < kPerLane; ++u) {
-        int quad_load[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         for (int l = 0; l < kLanes; ++l) {
-          if ((l & 7) == 0)
-            for (int q = 0; q < 8; ++q) quad_load[q] = 0;
-          const int32_t row = row_of_lane[l];
-          const int64_t slot = (int64_t)tau * kPerLane + u;    // slot of this lane
-          const int64_t k = slot * S + (l % S);                // k-th group of the row's sequence
-          if (row < 0 || k >= s.count[row]) {  // padding: all zero, reads x chunk 0
-            quad_load[0]++;
+          const int64_t g = deal[(size_t)l * L + (int64_t)tau * kPerLane + u];
+          uint16_t* col = reinterpret_cast<uint16_t*>(tile + off_cols(bits, l, u));
+          if (g < 0) {  // padding: codes, s, z zero; reads this lane's target chunk
+            *col = (uint16_t)(((l & 15) % nchunks) << 4);
             continue;
           }
-          const int64_t g = bsr->row_index[row_begin + row] + (k + rot_of_lane[l]) % s.count[row];
-          // swap bit: first 16-B x chunk in bank quad (2c + swap) mod 8, the
-          // less loaded of the two within the quarter-warp (one LDS.128 phase)
-          const int q0 = (2 * (int)bsr->group_cols[g]) & 7;
-          const uint32_t swap = quad_load[q0 | 1] < quad_load[q0] ? 1u : 0u;
-          quad_load[q0 | (int)swap]++;
+          const uint32_t swap = (uint32_t)(l & 1);
           const uint8_t* src = bsr->codes + g * cb;
           uint8_t* dst = tile + off_codes(bits, l, u);
           if (swap) {
@@ -229,7 +248,6 @@ extern "C" int gqsa_pack(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_e
           uint16_t* sz = reinterpret_cast<uint16_t*>(tile + off_sz(bits) + l * 16 + u * 4);
           sz[0] = bsr->scales_f16[g];
           sz[1] = bsr->zeros_f16[g];
-          uint16_t* col = reinterpret_cast<uint16_t*>(tile + off_cols(bits) + l * 8 + u * 2);
           *col = (uint16_t)(((bsr->group_cols[g] << 1) | swap) << 4);  // byte offset of the first x chunk
         }
       }
@@ -303,7 +321,7 @@ extern "C" int gqsa_unpack(const void* blob, size_t blob_bytes, gqsa_bsr_t* out)
         const uint16_t col = *reinterpret_cast<const uint16_t*>(tile + off_cols(bits) + l * 8 + u * 2);
         const uint8_t* src = tile + off_codes(bits, l, u);
         if (sz[0] == 0) {  // padding (a kept group always has s > 0)
-          if (sz[1] || col) return GQSA_ERR_VALIDATION;
+          if (sz[1] || (col & 15u) || col >= 2u * (uint32_t)d.cols) return GQSA_ERR_VALIDATION;
           for (int i = 0; i < cb; ++i)
             if (src[i]) return GQSA_ERR_VALIDATION;
           continue;

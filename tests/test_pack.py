@@ -96,21 +96,19 @@ def test_tile_fields_match_layout():
     hdr = t0[:16].view(np.uint32)
     assert hdr[0] >> 2 == 0 and hdr[0] & 1 and hdr[1] == -(-int(counts.max()) // 4) - 1
     cols = t0[32 + 1024 + 512:].view(np.uint16)
+    hit = 0
     for u in range(4):
-        for q in range(4):
-            quads = []
-            for lane in range(8 * q, 8 * q + 8):
-                assert int(cols[lane * 4 + u]) % 16 == 0  # byte offset of the first x chunk
-                f = int(cols[lane * 4 + u]) >> 4
-                row = int(perm[lane])
-                g0, g1 = bsr["row_index"][row], bsr["row_index"][row + 1]
-                assert (f >> 1) in set(bsr["group_cols"][g0:g1].tolist())
-                quads.append((2 * (f >> 1) + (f & 1)) % 8)
-            # the swap bits never put more than ceil(n_r/2) lanes of a quarter-warp
-            # on the two bank quads {2r, 2r+1} of residue r = c mod 4
-            res = [x // 2 for x in quads]
-            for r in range(4):
-                assert max(quads.count(2 * r), quads.count(2 * r + 1)) == (res.count(r) + 1) // 2
+        for lane in range(32):
+            field = int(cols[lane * 4 + u])
+            assert field % 16 == 0  # byte offset of the first x chunk
+            f = field >> 4          # chunk index 2c + swap
+            row = int(perm[lane])
+            g0, g1 = bsr["row_index"][row], bsr["row_index"][row + 1]
+            assert (f >> 1) in set(bsr["group_cols"][g0:g1].tolist())
+            assert f & 1 == lane & 1  # swap = lane parity
+            hit += (f % 16 == lane % 16)
+    # bank-aware dealing: early slots almost always get the lane's target chunk
+    assert hit >= 0.9 * 128, hit
 
 
 def test_validation_errors():
@@ -175,4 +173,5 @@ def test_lanes_per_row_rule():
 def test_workspace_size_is_device_independent():
     bsr = synth.make_layer(13, 4096, 4096, sparsity=0.5)
     _, d = gqsa.pack(bsr)
-    assert gqsa.workspace_size(d, 1) == 4096 * 256 and gqsa.workspace_size(d, 8) == 4096 * 2048
+    recs = min(d.num_tiles, 8192)  # one record per possible active warp
+    assert gqsa.workspace_size(d, 1) == recs * 256 and gqsa.workspace_size(d, 8) == recs * 2048
