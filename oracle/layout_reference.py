@@ -49,10 +49,11 @@ def lanes_per_row(n_nz: int, max_len: int) -> int:
 
 def deal_row(cols_of_row, lanes, slots):
     """Bank-aware dealing of one row's kept groups (CSR positions 0..n-1 with
-    group columns cols_of_row) over its lanes: slot by slot, lane l takes the
-    first remaining group whose column c has c mod 8 == (l mod 16) // 2, else
-    c mod 8 == that ^ 4, else the first remaining group of the fullest bucket
-    (lowest bucket index on ties).  Returns {(lane, slot): position}."""
+    group columns cols_of_row) over its lanes: slot by slot j, lane l takes
+    the first remaining group whose column c has c mod 8 == want =
+    (((l mod 8) // 2 + j) mod 4) + 4 * ((l // 8) mod 2), else c mod 8 ==
+    want ^ 4, else the first remaining group of the fullest bucket (lowest
+    bucket index on ties).  Returns {(lane, slot): position}."""
     buckets = [[] for _ in range(8)]
     for k, c in enumerate(cols_of_row):
         buckets[int(c) % 8].append(k)
@@ -63,7 +64,7 @@ def deal_row(cols_of_row, lanes, slots):
         for lane in lanes:
             if left == 0:
                 return out
-            want = (lane % 16) // 2
+            want = (((lane % 8) // 2 + j) % 4) + 4 * ((lane // 8) % 2)
             b = want
             if heads[b] == len(buckets[b]):
                 b = want ^ 4

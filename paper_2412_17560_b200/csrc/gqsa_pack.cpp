@@ -192,11 +192,13 @@ extern "C" int gqsa_pack(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_e
     const int32_t nt = s.tile0[sl + 1] - s.tile0[sl];
     const int64_t L = (int64_t)nt * kPerLane;  // slots per lane
     deal.assign((size_t)kLanes * L, -1);
-    // Bank-aware dealing (kFlagTargetDeal): lane l wants groups whose column
-    // c has c mod 8 == (l mod 16) / 2, read with swap = l mod 2, so the 16-B
-    // chunk index f = 2c + swap covers 8 distinct bank quads per quarter-warp
-    // (conflict-free LDS.128) and f mod 16 is distinct per half-warp
-    // (conflict-free LDS.64 of the column sums).
+    // Bank-aware dealing (kFlagTargetDeal): at slot j lane l wants a group
+    // whose column c has c mod 8 == want8(l, j) = (((l mod 8) / 2 + j) mod 4)
+    // + 4 * ((l / 8) mod 2), read with swap = l mod 2.  The chunk index
+    // f = 2c + swap then covers the 8 bank quads of every quarter-warp once
+    // (conflict-free LDS.128) and 16 distinct f mod 16 per half-warp
+    // (conflict-free LDS.64 of the column sums); the residue a lane wants
+    // rotates with j, so a row's buckets drain evenly.
     for (int l0 = 0; l0 < kLanes; l0 += S) {
       const int32_t row = row_of_lane[l0];
       if (row < 0) continue;
@@ -207,7 +209,8 @@ extern "C" int gqsa_pack(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_e
       int64_t left = n;
       for (int64_t j = 0; j < L && left > 0; ++j) {
         for (int k = 0; k < S && left > 0; ++k) {
-          const int l = l0 + k, want = (l & 15) >> 1;
+          const int l = l0 + k;
+          const int want = (int)((((l & 7) >> 1) + j) & 3) + 4 * ((l >> 3) & 1);
           int b = want;
           if (head[b] == bucket[b].size()) b = want ^ 4;
           if (head[b] == bucket[b].size()) {  // most populated remaining bucket

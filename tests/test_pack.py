@@ -106,8 +106,9 @@ def test_tile_fields_match_layout():
             g0, g1 = bsr["row_index"][row], bsr["row_index"][row + 1]
             assert (f >> 1) in set(bsr["group_cols"][g0:g1].tolist())
             assert f & 1 == lane & 1  # swap = lane parity
-            hit += (f % 16 == lane % 16)
-    # bank-aware dealing: early slots almost always get the lane's target chunk
+            want = (((lane % 8) // 2 + u) % 4) + 4 * ((lane // 8) % 2)
+            hit += ((f >> 1) % 4 == want % 4)  # the lane's target bank quad
+    # bank-aware dealing: early slots almost always get the lane's target quad
     assert hit >= 0.9 * 128, hit
 
 
