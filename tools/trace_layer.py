@@ -96,6 +96,16 @@ def main():
         ch = role[role >= 100] - 100
         print("owner chain length (successor warps) p50/p90/max: %d/%d/%d" % (
             np.median(ch), np.percentile(ch, 90), ch.max()))
+    q, r = divmod(plan.num_tiles, W)
+    ntile = np.array([q + (1 if w < r else 0) for w in range(W)])
+    loop = e[..., 4] - e[..., 3]
+    per = loop / ntile[None, :]
+    print("loop µs per tile (p10/p50/p90/max): %.3f/%.3f/%.3f/%.3f; warps with q+1 tiles: %.0f%%" % (
+        np.percentile(per, 10), np.median(per), np.percentile(per, 90), per.max(), 100 * r / W))
+    sm = np.arange(W) // plan.warps_per_cta
+    per_cta = np.array([np.median(per[:, sm == c]) for c in range(plan.grid)])
+    print("per-CTA median µs/tile: min %.3f max %.3f (spread %.0f%%)" % (
+        per_cta.min(), per_cta.max(), 100 * (per_cta.max() / per_cta.min() - 1)))
     prev_exit = T[:-1, :, 5].max(axis=1)
     rel = T[1:, :, 1].min(axis=1) - prev_exit
     print("PDL release after previous launch's last exit (µs):", " ".join(f"{r:.2f}" for r in rel[:5]))
