@@ -128,8 +128,7 @@ int make_plan(const gqsa_desc_t* d, int B, gqsa_plan_t* pl, const void** kfn) {
   if (occ > sp.ctas) occ = sp.ctas;
   int warps = sms * occ * W;
   if (warps > kMaxWarpsBound) warps = kMaxWarpsBound;
-  const int64_t units = (int64_t)d->num_tiles * kPerLane;  // Stream-K units: 32-group slots
-  const int active = units < warps ? (int)units : warps;
+  const int active = d->num_tiles < warps ? d->num_tiles : warps;
   int grid = (active + W - 1) / W;
   if (grid == 0) {  // nnzg == 0: only empty rows to write
     grid = (d->n_empty + threads - 1) / threads;
@@ -157,8 +156,7 @@ extern "C" int gqsa_workspace_size(const gqsa_desc_t* desc, int32_t batch, size_
   if (!desc || !bytes) return GQSA_ERR_BUFFER;
   if (!desc_ok(desc)) return GQSA_ERR_VALIDATION;
   if (batch < 1 || batch > kMaxBatch) return GQSA_ERR_SHAPE;
-  const int64_t units = (int64_t)desc->num_tiles * kPerLane;
-  const int64_t recs = units < kMaxWarpsBound ? units : kMaxWarpsBound;
+  const int64_t recs = desc->num_tiles < kMaxWarpsBound ? desc->num_tiles : kMaxWarpsBound;
   *bytes = (size_t)(recs > 0 ? recs : 1) * batch * kLanes * kWsSlotBytes;
   return GQSA_OK;
 }
@@ -206,10 +204,8 @@ extern "C" int gqsa_gemm_smallbatch(const gqsa_desc_t* desc, const void* d_blob,
   p.n_empty = desc->n_empty;
   p.active_warps = pl.active_warps;
   p.lanes_per_row = ((uint32_t)desc->flags >> kFlagLanesPerRowShift) & 0xff;
-  // Stream-K units are slots (4 per tile): num_units = part_q * warps + part_r
-  const int64_t units = (int64_t)desc->num_tiles * kPerLane;
-  p.part_q = pl.active_warps ? (int32_t)(units / pl.active_warps) : 0;
-  p.part_r = pl.active_warps ? (int32_t)(units % pl.active_warps) : 0;
+  p.part_q = pl.active_warps ? desc->num_tiles / pl.active_warps : 0;
+  p.part_r = pl.active_warps ? desc->num_tiles % pl.active_warps : 0;
   p.stages = pl.stages;
   p.ring_offset = pl.smem_bytes - pl.ring_bytes - pl.warps_per_cta * kMaxStages * 8;
   p.trace = (g_trace && g_trace_bytes >= (size_t)pl.active_warps * 64) ? g_trace : nullptr;

@@ -347,10 +347,10 @@ __device__ __forceinline__ void store_rows(const KParams& p, float (&v)[kMaxBatc
   }
 }
 
-// Warp that owns slot unit v under the +-1 partition of 4*num_tiles units.
-__device__ __forceinline__ int warp_of_unit(const KParams& p, int v) {
+// Warp that owns tile t under the +-1 partition of num_tiles over active_warps.
+__device__ __forceinline__ int warp_of_tile(const KParams& p, int t) {
   const int big = p.part_r * (p.part_q + 1);
-  return v < big ? v / (p.part_q + 1) : p.part_r + (v - big) / p.part_q;
+  return t < big ? t / (p.part_q + 1) : p.part_r + (t - big) / p.part_q;
 }
 
 // ---------------------------------------------------------------- kernel
@@ -416,19 +416,12 @@ __global__ void __launch_bounds__(max_threads_for(B), 1) gqsa_streamk_kernel(KPa
   const int nthreads = blockDim.x;
   const int gw = blockIdx.x * (nthreads >> 5) + warp;
 
-  // ---- task-centric partition: a contiguous range of SLOT units (one slot =
-  //      32 groups, 4 per tile) per warp, +-1 slot: the work is split evenly
-  //      regardless of rows, slices and tiles.  q, r = divmod(4 * num_tiles,
-  //      warps) come from the host.  The warp streams the tiles its slots lie in.
-  int u_begin = 0, u_end = 0;
-  if (gw < p.active_warps) {
-    u_begin = gw * p.part_q + min(gw, p.part_r);
-    u_end = u_begin + p.part_q + (gw < p.part_r ? 1 : 0);
+  // ---- task-centric partition: contiguous tile range per warp (+-1 tile)
+  int t_begin = 0, t_end = 0;
+  if (gw < p.active_warps) {  // q = num_tiles / warps, r = num_tiles % warps (host)
+    t_begin = gw * p.part_q + min(gw, p.part_r);
+    t_end = t_begin + p.part_q + (gw < p.part_r ? 1 : 0);
   }
-  const int t_begin = u_begin / kPerLane;
-  const int t_end = (u_end + kPerLane - 1) / kPerLane;
-  const int lo_first = u_begin - t_begin * kPerLane;             // first slot of the first tile
-  const int hi_last = u_end - (t_end - 1) * kPerLane;            // end slot of the last tile
   const uint8_t* tiles = p.tiles;
   const int tb = tile_bytes(BITS);
   const int NS = p.stages;
@@ -530,25 +523,20 @@ __global__ void __launch_bounds__(max_threads_for(B), 1) gqsa_streamk_kernel(KPa
   float acc[kMaxBatch];
 #pragma unroll
   for (int b = 0; b < kMaxBatch; ++b) acc[b] = 0.f;
-  // the range starts a slice iff it starts at slot 0 of a FIRST tile
-  bool foreign = !(lo_first == 0 && (hdr0 & kTileFirst));
-  bool closed = false;  // does the range end exactly at the end of a slice?
+  bool foreign = !(hdr0 & kTileFirst);  // slice opened by an earlier warp
+  uint32_t last_hdr = 0;
   int w_last = gw;
   unsigned long long pre[kPre][kMaxBatch];
   int s = 0;
   uint32_t phase = 0;
   trace_point(p, gw, lane, 3);
 
-  // Per-tile work once its registers are loaded: accumulate the lane's groups
-  // in the warp's slots [lo, hi) of the tile, close the slice when its LAST
-  // tile is finished, and (at the warp's final tile, when it owns a slice
-  // continuing downstream) request the fix-up records early.
+  // Per-tile work once its registers are loaded: accumulate the lane's four
+  // groups, close the slice at its LAST tile, and (at the warp's final tile,
+  // when it owns a slice continuing downstream) request the fix-up records.
   auto consume = [&](const TileRegs<BITS>& tr, int t) {
-    const int lo = (t == t_begin) ? lo_first : 0;
-    const int hi = (t == t_end - 1) ? hi_last : kPerLane;
-    const bool ends_slice = (tr.hdr & kTileLast) && hi == kPerLane;
-    if (t == t_end - 1 && !ends_slice && !foreign) {
-      w_last = warp_of_unit(p, (t + (int)tr.rem) * kPerLane + kPerLane - 1);
+    if (t == t_end - 1 && !(tr.hdr & kTileLast) && !foreign) {
+      w_last = warp_of_tile(p, t_end - 1 + (int)tr.rem);
 #pragma unroll
       for (int k = 0; k < kPre; ++k)
 #pragma unroll
@@ -557,16 +545,12 @@ __global__ void __launch_bounds__(max_threads_for(B), 1) gqsa_streamk_kernel(KPa
     }
     if (p.debug_skip_math) {
       acc[0] += __uint_as_float((tr.codes[0].x ^ tr.sz.x ^ tr.cols.x) & 0x3f800000u);
-    } else if (lo == 0 && hi == kPerLane) {
+    } else {
 #pragma unroll
       for (int u = 0; u < kPerLane; ++u) group_accumulate<BITS, B, XSMEM>(p, tr, u, acc);
-    } else {  // a partial tile at either end of the range
-#pragma unroll
-      for (int u = 0; u < kPerLane; ++u)
-        if (u >= lo && u < hi) group_accumulate<BITS, B, XSMEM>(p, tr, u, acc);
     }
-    closed = ends_slice;
-    if (ends_slice) {  // the slice ends in this tile: its rows are complete
+    last_hdr = tr.hdr;
+    if (tr.hdr & kTileLast) {  // the slice ends in this tile: its rows are complete
       if (foreign) publish<B>(p, gw, acc, lane);
       else store_rows<B>(p, acc, row, lane);
 #pragma unroll
@@ -615,7 +599,7 @@ __global__ void __launch_bounds__(max_threads_for(B), 1) gqsa_streamk_kernel(KPa
 
   trace_point(p, gw, lane, 4);
   // ---- a slice left open at the end of the range continues downstream
-  if (!closed) {
+  if (!(last_hdr & kTileLast)) {
     if (foreign) {  // the whole range lies inside a slice owned upstream
       publish<B>(p, gw, acc, lane);
       if (p.trace && lane == 0) p.trace[(int64_t)gw * 8 + 7] = 1;

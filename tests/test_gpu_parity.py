@@ -187,5 +187,5 @@ def test_launch_plan_is_persistent_stream_k():
     _, d = gqsa.pack(bsr)
     p = gqsa.launch_plan(d, 1)
     sms = torch.cuda.get_device_properties(0).multi_processor_count
-    assert p.active_warps == min(4 * d.num_tiles, p.grid * p.warps_per_cta)  # units = slots
+    assert p.active_warps == min(d.num_tiles, p.grid * p.warps_per_cta)
     assert p.grid <= 2 * sms and p.x_in_smem == 1

@@ -174,5 +174,5 @@ def test_lanes_per_row_rule():
 def test_workspace_size_is_device_independent():
     bsr = synth.make_layer(13, 4096, 4096, sparsity=0.5)
     _, d = gqsa.pack(bsr)
-    recs = min(4 * d.num_tiles, 8192)  # one record per possible active warp (units = slots)
+    recs = min(d.num_tiles, 8192)  # one record per possible active warp
     assert gqsa.workspace_size(d, 1) == recs * 256 and gqsa.workspace_size(d, 8) == recs * 2048

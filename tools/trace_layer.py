@@ -96,8 +96,8 @@ def main():
         ch = role[role >= 100] - 100
         print("owner chain length (successor warps) p50/p90/max: %d/%d/%d" % (
             np.median(ch), np.percentile(ch, 90), ch.max()))
-    q, r = divmod(4 * plan.num_tiles, W)  # Stream-K units are slots (4 per tile)
-    ntile = np.array([(q + (1 if w < r else 0)) / 4.0 for w in range(W)])
+    q, r = divmod(plan.num_tiles, W)  # Stream-K units are tiles
+    ntile = np.array([q + (1 if w < r else 0) for w in range(W)], dtype=float)
     loop = e[..., 4] - e[..., 3]
     per = loop / ntile[None, :]
     print("loop µs per tile (p10/p50/p90/max): %.3f/%.3f/%.3f/%.3f; warps with q+1 tiles: %.0f%%" % (
