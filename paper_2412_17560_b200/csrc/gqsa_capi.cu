@@ -89,6 +89,7 @@ SmemPlan smem_plan(const gqsa_desc_t* d, int B) {
   const size_t xbytes = xs ? xb + xc : xc;
   int ns = budget > xbytes ? (int)((budget - xbytes) / ((size_t)W * tb)) : 0;
   if (ns > stages_cap()) ns = stages_cap();
+  ns &= ~1;  // the ring holds tile pairs (one bulk copy + mbarrier per pair)
   if (ns < kMinStages) ns = kMinStages;
   sp.xsmem = xs;
   sp.ctas = c;
@@ -114,8 +115,12 @@ int make_plan(const gqsa_desc_t* d, int B, gqsa_plan_t* pl, const void** kfn) {
     std::lock_guard<std::mutex> lk(g_mu);
     bool& set = g_dev[dev].attr_set[d->bits == 4][B][xsmem];
     if (!set) {
+      // maximum shared-memory carveout: two kernels' CTAs (this launch and
+      // the next, PDL) must fit on one SM at the same time
       if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               kSmemPerSm - 1024 - 1024) != cudaSuccess)
+                               kSmemPerSm - 1024 - 1024) != cudaSuccess ||
+          cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared) != cudaSuccess)
         return GQSA_ERR_CUDA;
       set = true;
     }
@@ -209,8 +214,8 @@ extern "C" int gqsa_gemm_smallbatch(const gqsa_desc_t* desc, const void* d_blob,
   p.stages = pl.stages;
   p.ring_offset = pl.smem_bytes - pl.ring_bytes - pl.warps_per_cta * kMaxStages * 8;
   p.trace = (g_trace && g_trace_bytes >= (size_t)pl.active_warps * 64) ? g_trace : nullptr;
-  static const int skip_math = env_int("GQSA_DEBUG_SKIP_MATH", 0, 0, 1);
-  p.debug_skip_math = skip_math;
+  static const int trigger = env_int("GQSA_PDL_TRIGGER", 0, 0, 2);
+  p.pdl_trigger = trigger;
   if (desc->rows == 0) return GQSA_OK;
 
   cudaLaunchConfig_t cfg = {};

@@ -436,13 +436,20 @@ __global__ void __launch_bounds__(max_threads_for(B), 1) gqsa_streamk_kernel(KPa
   const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(
       smem + p.ring_offset + (size_t)(nthreads >> 5) * NS * tb + (size_t)warp * kMaxStages * 8);
   const uint64_t pol = evict_first_policy();
-  if (lane == 0) {
-    for (int s = 0; s < NS; ++s) mbar_init(bar0 + 8 * s, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int s = 0; s < NS && t_begin + s < t_end; ++s) {
-      mbar_expect_tx(bar0 + 8 * s, tb);
-      bulk_g2s(ring_s + s * tb, tiles + (int64_t)(t_begin + s) * tb, tb, bar0 + 8 * s, pol);
+  // The ring is NP = NS/2 slots of two consecutive tiles: one bulk copy and
+  // one mbarrier per tile pair (the host keeps NS even).
+  const int NP = NS >> 1;
+  auto fill_slot = [&](int slot, int t_first) {  // lane 0 only
+    const int n = min(2, t_end - t_first);
+    if (n > 0) {
+      mbar_expect_tx(bar0 + 8 * slot, n * tb);
+      bulk_g2s(ring_s + slot * 2 * tb, tiles + (int64_t)t_first * tb, n * tb, bar0 + 8 * slot, pol);
     }
+  };
+  if (lane == 0) {
+    for (int s = 0; s < NP; ++s) mbar_init(bar0 + 8 * s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < NP; ++s) fill_slot(s, t_begin + 2 * s);
   }
   __syncwarp();
   int row = -1;  // this lane's row in the first slice (the perm table is part of the blob)
@@ -452,7 +459,7 @@ __global__ void __launch_bounds__(max_threads_for(B), 1) gqsa_streamk_kernel(KPa
     row = __ldg(p.perm + (int64_t)(hdr0 >> 2) * kLanes + lane);
   }
   trace_point(p, gw, lane, 0);
-  pdl_launch_dependents();
+  if (p.pdl_trigger == 0) pdl_launch_dependents();
   pdl_wait();  // x, y, bias and the workspace may belong to the previous kernel
   trace_point(p, gw, lane, 1);
 
@@ -508,6 +515,7 @@ __global__ void __launch_bounds__(max_threads_for(B), 1) gqsa_streamk_kernel(KPa
   }
   trace_point(p, gw, lane, 6);
   __syncthreads();
+  if (p.pdl_trigger == 1) pdl_launch_dependents();
 
   // ---- empty rows get bias (or 0): grid-stride over the empty-row list
   for (int i = blockIdx.x * nthreads + threadIdx.x; i < p.n_empty; i += gridDim.x * nthreads) {
@@ -543,12 +551,8 @@ __global__ void __launch_bounds__(max_threads_for(B), 1) gqsa_streamk_kernel(KPa
         for (int b = 0; b < B; ++b)
           pre[k][b] = (gw + 1 + k <= w_last) ? ld_slot(ws_slot<B>(p, gw + 1 + k, b, lane)) : 0ull;
     }
-    if (p.debug_skip_math) {
-      acc[0] += __uint_as_float((tr.codes[0].x ^ tr.sz.x ^ tr.cols.x) & 0x3f800000u);
-    } else {
 #pragma unroll
-      for (int u = 0; u < kPerLane; ++u) group_accumulate<BITS, B, XSMEM>(p, tr, u, acc);
-    }
+    for (int u = 0; u < kPerLane; ++u) group_accumulate<BITS, B, XSMEM>(p, tr, u, acc);
     last_hdr = tr.hdr;
     if (tr.hdr & kTileLast) {  // the slice ends in this tile: its rows are complete
       if (foreign) publish<B>(p, gw, acc, lane);
@@ -559,41 +563,29 @@ __global__ void __launch_bounds__(max_threads_for(B), 1) gqsa_streamk_kernel(KPa
       if (t + 1 < t_end) row = __ldg(p.perm + (int64_t)((tr.hdr >> 2) + 1) * kLanes + lane);
     }
   };
-  auto refill = [&](int stage, int t_next) {  // lane 0, after __syncwarp
-    if (t_next < t_end) {
-      mbar_expect_tx(bar0 + 8 * stage, tb);
-      bulk_g2s(ring_s + stage * tb, tiles + (int64_t)t_next * tb, tb, bar0 + 8 * stage, pol);
-    }
-  };
-
-  // two tiles per iteration: one ring handshake per pair, and the x gathers
-  // of both tiles can be in flight together
+  // two tiles per iteration: one ring handshake (wait, copy) per pair, and
+  // the x gathers of both tiles can be in flight together
   int t = t_begin;
   for (; t + 1 < t_end; t += 2) {
-    const int s0 = s;
-    const uint32_t ph0 = phase;
-    if (++s == NS) { s = 0; phase ^= 1u; }
-    const int s1 = s;
-    const uint32_t ph1 = phase;
-    if (++s == NS) { s = 0; phase ^= 1u; }
-    mbar_wait(bar0 + 8 * s0, ph0);
-    mbar_wait(bar0 + 8 * s1, ph1);
+    mbar_wait(bar0 + 8 * s, phase);
+    const uint8_t* slot = ring + (size_t)s * 2 * tb;
     TileRegs<BITS> tr0, tr1;
-    read_tile<BITS>(tr0, ring + (size_t)s0 * tb, lane);
-    read_tile<BITS>(tr1, ring + (size_t)s1 * tb, lane);
-    __syncwarp();  // every lane has read both stages: refill them
+    read_tile<BITS>(tr0, slot, lane);
+    read_tile<BITS>(tr1, slot + tb, lane);
+    __syncwarp();  // every lane has read the pair: refill its slot
     if (lane == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      refill(s0, t + NS);
-      refill(s1, t + 1 + NS);
+      fill_slot(s, t + NS);
     }
+    if (++s == NP) { s = 0; phase ^= 1u; }
     consume(tr0, t);
     consume(tr1, t + 1);
+    if (p.pdl_trigger == 2 && t == t_begin) pdl_launch_dependents();
   }
-  if (t < t_end) {
+  if (t < t_end) {  // odd count: the last slot holds one tile
     mbar_wait(bar0 + 8 * s, phase);
     TileRegs<BITS> tr;
-    read_tile<BITS>(tr, ring + (size_t)s * tb, lane);
+    read_tile<BITS>(tr, ring + (size_t)s * 2 * tb, lane);
     consume(tr, t);
   }
 
