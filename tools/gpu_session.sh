@@ -1,6 +1,6 @@
 # ad-hoc GPU experiment driver (edited per session)
 make -s >/dev/null 2>&1
-python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-for st in 2 4; do for s in "4096 4096" "14336 4096" "4096 14336"; do set -- $s; GQSA_STAGES=$st python tools/prof_layer.py --rows $1 --cols $2 --launches 50 --time | grep -v plan | sed "s/^/st=$st /"; done; done > gpurun_out/pair.log 2>&1
-python tools/trace_layer.py --rows 14336 --cols 4096 > gpurun_out/trace_pair.log 2>&1
-cat gpurun_out/pair.log
+python bench.py > gpurun_out/bench.log 2>&1; tail -1 gpurun_out/bench.log
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:gqsa -c 60 --csv --log-file gpurun_out/launches.csv python bench.py --steps 10 --warmup 3 > /dev/null 2>&1
+timeout 400 ncu --set full --clock-control none --import-source on -k regex:gqsa --launch-skip 40 --launch-count 3 -o gpurun_out/bench_full -f python bench.py --steps 10 --warmup 3 > /dev/null 2>&1
+ls -la gpurun_out
