@@ -173,9 +173,11 @@ extern "C" int gqsa_launch_plan(const gqsa_desc_t* desc, int32_t B, gqsa_plan_t*
   return make_plan(desc, B, plan, nullptr);
 }
 
-extern "C" int gqsa_gemm_smallbatch(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_X,
-                                    int32_t B, int64_t ldx, float* d_Y, int64_t ldy,
-                                    const float* d_bias, void* d_ws, size_t ws_bytes, void* stream) {
+extern "C" int gqsa_gemm_partitioned(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_X,
+                                     int32_t B, int64_t ldx, float* d_Y, int64_t ldy,
+                                     const float* d_bias, void* d_ws, size_t ws_bytes,
+                                     int32_t partition, void* stream) {
+  if (partition != GQSA_PARTITION_STREAM_K && partition != GQSA_PARTITION_SLICE_K) return GQSA_ERR_SHAPE;
   if (!desc || !d_blob || !d_X || !d_Y || !d_ws) return GQSA_ERR_BUFFER;
   if (!desc_ok(desc)) return GQSA_ERR_VALIDATION;
   if (B < 1 || B > kMaxBatch) return GQSA_ERR_SHAPE;
@@ -214,6 +216,7 @@ extern "C" int gqsa_gemm_smallbatch(const gqsa_desc_t* desc, const void* d_blob,
   p.stages = pl.stages;
   p.ring_offset = pl.smem_bytes - pl.ring_bytes - pl.warps_per_cta * kMaxStages * 8;
   p.trace = (g_trace && g_trace_bytes >= (size_t)pl.active_warps * 64) ? g_trace : nullptr;
+  p.slice_k = partition == GQSA_PARTITION_SLICE_K ? 1 : 0;
   static const int trigger = env_int("GQSA_PDL_TRIGGER", 0, 0, 2);
   p.pdl_trigger = trigger;
   if (desc->rows == 0) return GQSA_OK;
@@ -232,6 +235,13 @@ extern "C" int gqsa_gemm_smallbatch(const gqsa_desc_t* desc, const void* d_blob,
   if (cudaLaunchKernelExC(&cfg, fn, args) != cudaSuccess) return GQSA_ERR_CUDA;
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return GQSA_OK;
+}
+
+extern "C" int gqsa_gemm_smallbatch(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_X,
+                                    int32_t B, int64_t ldx, float* d_Y, int64_t ldy,
+                                    const float* d_bias, void* d_ws, size_t ws_bytes, void* stream) {
+  return gqsa_gemm_partitioned(desc, d_blob, d_X, B, ldx, d_Y, ldy, d_bias, d_ws, ws_bytes,
+                               GQSA_PARTITION_STREAM_K, stream);
 }
 
 extern "C" int gqsa_gemv(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_x, float* d_y,

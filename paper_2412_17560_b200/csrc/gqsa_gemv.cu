@@ -425,6 +425,17 @@ __global__ void __launch_bounds__(max_threads_for(B), 1) gqsa_streamk_kernel(KPa
   const uint8_t* tiles = p.tiles;
   const int tb = tile_bytes(BITS);
   const int NS = p.stages;
+  if (p.slice_k && t_end > t_begin) {
+    // data-centric partition (Slice-K): the warp owns the slices whose FIRST
+    // tile lies in its Stream-K range, each in full (tile header word 1 =
+    // tiles from this tile to its slice's last tile)
+    const uint2 hb = __ldg(reinterpret_cast<const uint2*>(tiles + (int64_t)t_begin * tb));
+    const uint2 he = __ldg(reinterpret_cast<const uint2*>(tiles + (int64_t)(t_end - 1) * tb));
+    const int b = (hb.x & kTileFirst) ? t_begin : t_begin + (int)hb.y + 1;
+    const int e = t_end + (int)he.y;
+    t_begin = b;
+    t_end = b < t_end ? e : b;
+  }
 
   // ---- weights never depend on the previous kernel: each warp's first NS
   //      tiles are requested (1-D TMA bulk copies into its shared-memory

@@ -36,6 +36,7 @@ struct KParams {
   int32_t stages;          // ring depth NS (tiles) per warp
   int32_t ring_offset;     // shared-memory offset of the TMA ring (after x and the column sums)
   uint64_t* trace;         // optional [active_warps][8] %globaltimer stamps (debug)
+  int32_t slice_k;         // 1: data-centric partition (whole slices per warp, no fix-up)
   int32_t pdl_trigger;     // where the next kernel may launch: 0 before the PDL wait,
                            // 1 after activation staging, 2 after the first tile pair
 };

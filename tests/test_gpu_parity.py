@@ -21,17 +21,17 @@ def _cuda():
     torch.cuda.init()
 
 
-def run(bsr, xbits, bias=None, layer=None, **kw):
+def run(bsr, xbits, bias=None, layer=None, partition=gqsa.PARTITION_STREAM_K, **kw):
     """Pack, upload, run gqsa_gemm_smallbatch (B = rows of x), return y [B][N] float32."""
     L = layer or gqsa.Layer(bsr)
     X = torch.from_numpy(np.ascontiguousarray(xbits)).view(torch.float16).cuda()
     if X.ndim == 1:
         X = X[None]
     b = None if bias is None else torch.from_numpy(bias).cuda()
-    if X.shape[0] == 1 and not kw.get("force_gemm"):
+    if X.shape[0] == 1 and not kw.get("force_gemm") and partition == gqsa.PARTITION_STREAM_K:
         y = L.gemv(X[0], bias=b)[None]
     else:
-        y = L.gemm(X, bias=b)
+        y = L.gemm(X, bias=b, partition=partition)
     torch.cuda.synchronize()
     flags = L.ws.view(torch.int32).view(-1, 16)[:, 15]
     assert int(flags.count_nonzero()) == 0, "every fix-up flag must be left zero"
@@ -92,6 +92,43 @@ def test_exact_integer_mode_bit_exact(rows, cols, bits, sp, mask, B):
     y = run(bsr, x)
     ref = O.gemv(bsr, x)
     assert np.array_equal(y.astype(np.float64), ref), np.argwhere(y != ref)[:5]
+
+
+SLICE_K_CASES = [
+    # rows, cols, bits, sparsity, mask, B
+    (1024, 4096, 4, 0.5, "uniform", 1),
+    (1024, 4096, 2, 0.5, "uniform", 3),
+    (512, 2048, 4, 0.5, "skewed", 1),
+    (300, 1024, 4, 0.3, "row_balanced", 4),
+    (77, 208, 4, 0.2, "uniform", 8),
+    (3, 16384, 4, 0.5, "uniform", 2),     # fewer slices than warps
+    (4096, 16, 4, 0.5, "uniform", 1),
+    (640, 512, 2, 0.9, "uniform", 5),
+]
+
+
+@pytest.mark.parametrize("rows,cols,bits,sp,mask,B", SLICE_K_CASES)
+def test_slice_k_partition_bit_exact(rows, cols, bits, sp, mask, B):
+    """Data-centric partition (App. J baseline): whole slices per warp, no fix-up."""
+    seed = synth.seed_for(f"slicek/{rows}/{cols}/{bits}/{sp}/{mask}/{B}")
+    bsr = synth.make_layer(seed, rows, cols, bits=bits, sparsity=sp, mask=mask, mode="exact_int")
+    x = synth.make_x(seed + 1, B, cols, mode="exact_int")
+    y = run(bsr, x, partition=gqsa.PARTITION_SLICE_K)
+    assert np.array_equal(y.astype(np.float64), O.gemv(bsr, x))
+
+
+@pytest.mark.parametrize("mask", ["uniform", "skewed"])
+def test_slice_k_realistic_and_deterministic(mask):
+    bsr = synth.make_layer(81, 4096, 4096, sparsity=0.5, mask=mask)
+    x = synth.make_x(82, 2, 4096)
+    L = gqsa.Layer(bsr)
+    y = run(bsr, x, layer=L, partition=gqsa.PARTITION_SLICE_K)
+    check_gates(y, O.gemv(bsr, x), abs_bound(bsr, x), f"slice-k {mask}")
+    assert np.array_equal(run(bsr, x, layer=L, partition=gqsa.PARTITION_SLICE_K), y)
+    with pytest.raises(gqsa.GQSAError) as e:
+        X = torch.zeros(1, 4096, dtype=torch.float16, device="cuda")
+        gqsa.gemm_partitioned(L.desc, L.blob, X, torch.empty(1, 4096, device="cuda"), 7, ws=L.ws)
+    assert e.value.status == -1
 
 
 def test_empty_layer_and_bias():
