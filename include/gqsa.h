@@ -181,11 +181,16 @@ int gqsa_gemm_hostio(const gqsa_desc_t* desc, const void* d_blob, const uint16_t
                      float* h_Y, const float* d_bias, void* d_stage, size_t stage_bytes,
                      void* d_ws, size_t ws_bytes, void* stream);
 
-/* Launch plan the next gemv/gemm call will use on the current device:
+/* Launch plan the next gemv/gemm call will use on the current device (for
+ * a split batch: the plan of its first launch):
  * CTAs, warps per CTA, active warps (Stream-K units), tiles.  For tooling. */
 typedef struct {
   int32_t grid, warps_per_cta, active_warps, num_tiles, smem_bytes, x_in_smem;
   int32_t stages, ctas_per_sm, ring_bytes;  /* TMA ring depth per warp, residency, ring size */
+  int32_t batch_per_launch, launches;  /* x of batch_per_launch columns fits in shared memory;
+                                          larger batches run as `launches` launches */
+  int32_t coresident;                  /* 1: CTA uses <= half an SM, so the next PDL launch
+                                          overlaps; 0: the CTA takes the whole SM */
 } gqsa_plan_t;
 int gqsa_launch_plan(const gqsa_desc_t* desc, int32_t B, gqsa_plan_t* plan);
 

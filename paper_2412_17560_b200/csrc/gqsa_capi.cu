@@ -21,7 +21,7 @@ size_t g_trace_bytes = 0;
 
 struct DevInfo {
   int sms = 0;
-  bool attr_set[2][kMaxBatch + 1][2] = {};
+  bool attr_set[2][kMaxBatch + 1] = {};
 };
 std::mutex g_mu;
 DevInfo g_dev[64];
@@ -66,59 +66,76 @@ int warps_per_cta(int B) {
   return B <= 2 ? w1 : 8;
 }
 
-// Shared-memory plan per CTA of W warps: [TMA ring: W x NS tiles][x: B*K fp16
-// (if it fits)][X_c: B*K/G fp32].  By default one CTA per SM that uses at most
-// half of the SM's shared memory, so the next GEMV on the stream (PDL) can be
-// resident at the same time and stream its weights during this one's tail.
+// Shared-memory plan per CTA of W warps: [x: B*K fp16][(P, Q) column sums]
+// [TMA ring: W x NS tiles][ring mbarriers].  Preferred: one CTA per SM using
+// at most half of the SM's shared memory, so the next GEMV on the stream (PDL)
+// is resident at the same time and streams its first tiles during this one's
+// tail.  If x does not leave room for that, the CTA takes the whole SM; if x
+// does not fit at all, the batch is split into launches of `batch` columns.
 struct SmemPlan {
-  bool xsmem;
-  int ctas, stages, warps;
+  bool coresident;
+  int stages, warps, batch, launches;
   size_t ring, total;
 };
+size_t x_bytes(int B, int cols) { return (size_t)B * cols * 2 + (size_t)B * pq_bytes_per_row(B, cols); }
+size_t ring_bytes_for(const gqsa_desc_t* d, int W, int ns) {  // ring + its mbarriers
+  return (size_t)W * ns * tile_bytes(d->bits) + (size_t)W * kMaxStages * 8;
+}
+constexpr size_t kMaxDynSmem = kSmemPerSm - 2048;  // per-CTA limit we request (227 KB - reserve)
+
 SmemPlan smem_plan(const gqsa_desc_t* d, int B) {
   SmemPlan sp{};
+  // largest batch chunk whose x fits next to a minimal ring (default warps,
+  // else 8 warps); cols <= kMaxCols makes Bc = 1 always fit
+  int Bc = B, W = warps_per_cta(B);
+  for (;; --Bc) {
+    W = warps_per_cta(Bc);
+    if (x_bytes(Bc, d->cols) + ring_bytes_for(d, W, kMinStages) <= kMaxDynSmem) break;
+    if (W > 8 && x_bytes(Bc, d->cols) + ring_bytes_for(d, 8, kMinStages) <= kMaxDynSmem) { W = 8; break; }
+    if (Bc == 1) break;
+  }
+  sp.launches = (B + Bc - 1) / Bc;
+  const int Bb = (B + sp.launches - 1) / sp.launches;  // balanced chunks (<= Bc: fits)
+  if (Bb != Bc) W = warps_per_cta(Bb) > W ? W : warps_per_cta(Bb);
+  Bc = Bb;
+  sp.batch = Bc;
   const size_t tb = (size_t)tile_bytes(d->bits);
-  const size_t xc = (size_t)B * d->cols;  // float2 (P, Q) per 16-B chunk: K/8 x 8 B per batch row
-  const size_t xb = (size_t)B * d->cols * 2;
-  const int W = warps_per_cta(B);
-  const int c = ctas_per_sm_cap();
-  const size_t share = (size_t)kSmemPerSm / (c * kCoResidentKernels);
+  const size_t xb = x_bytes(Bc, d->cols);
+  const size_t share = (size_t)kSmemPerSm / (ctas_per_sm_cap() * kCoResidentKernels);
   const size_t budget = share > 2048 ? share - 2048 : 0;  // reserved + static smem
-  const size_t min_ring = (size_t)W * kMinStages * tb;
-  const bool xs = xb + xc + min_ring <= budget || xb + xc <= (size_t)kSmemPerSm / 2;
-  const size_t xbytes = xs ? xb + xc : xc;
-  int ns = budget > xbytes ? (int)((budget - xbytes) / ((size_t)W * tb)) : 0;
-  if (ns > stages_cap()) ns = stages_cap();
-  ns &= ~1;  // the ring holds tile pairs (one bulk copy + mbarrier per pair)
-  if (ns < kMinStages) ns = kMinStages;
-  sp.xsmem = xs;
-  sp.ctas = c;
+  int ns = kMinStages;
+  sp.coresident = xb + ring_bytes_for(d, W, kMinStages) <= budget;
+  if (sp.coresident) {
+    ns = (int)((budget - xb - (size_t)W * kMaxStages * 8) / ((size_t)W * tb));
+    if (ns > stages_cap()) ns = stages_cap();
+    ns &= ~1;  // the ring holds tile pairs (one bulk copy + mbarrier per pair)
+    if (ns < kMinStages) ns = kMinStages;
+  }
   sp.warps = W;
   sp.stages = ns;
   sp.ring = (size_t)W * ns * tb;
-  sp.total = xbytes + sp.ring + (size_t)W * kMaxStages * 8;  // + the ring's mbarriers
+  sp.total = xb + ring_bytes_for(d, W, ns);
   return sp;
 }
 
-// Fill the launch plan; returns a status.
+// Fill the launch plan of the first (or only) batch chunk; returns a status.
 int make_plan(const gqsa_desc_t* d, int B, gqsa_plan_t* pl, const void** kfn) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return GQSA_ERR_CUDA;
   const int sms = device_sms(dev);
   if (sms <= 0) return GQSA_ERR_CUDA;
   const SmemPlan sp = smem_plan(d, B);
-  const bool xsmem = sp.xsmem;
   const size_t smem = sp.total;
-  const void* fn = select_kernel(d->bits, B, xsmem);
+  const void* fn = select_kernel(d->bits, sp.batch);
   if (!fn) return GQSA_ERR_UNSUPPORTED;
   {
     std::lock_guard<std::mutex> lk(g_mu);
-    bool& set = g_dev[dev].attr_set[d->bits == 4][B][xsmem];
+    bool& set = g_dev[dev].attr_set[d->bits == 4][sp.batch];
     if (!set) {
       // maximum shared-memory carveout: two kernels' CTAs (this launch and
       // the next, PDL) must fit on one SM at the same time
-      if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               kSmemPerSm - 1024 - 1024) != cudaSuccess ||
+      if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem) !=
+              cudaSuccess ||
           cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                cudaSharedmemCarveoutMaxShared) != cudaSuccess)
         return GQSA_ERR_CUDA;
@@ -130,7 +147,7 @@ int make_plan(const gqsa_desc_t* d, int B, gqsa_plan_t* pl, const void** kfn) {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem) != cudaSuccess)
     return GQSA_ERR_CUDA;
   if (occ < 1) return GQSA_ERR_UNSUPPORTED;
-  if (occ > sp.ctas) occ = sp.ctas;
+  if (occ > ctas_per_sm_cap()) occ = ctas_per_sm_cap();
   int warps = sms * occ * W;
   if (warps > kMaxWarpsBound) warps = kMaxWarpsBound;
   const int active = d->num_tiles < warps ? d->num_tiles : warps;
@@ -145,10 +162,13 @@ int make_plan(const gqsa_desc_t* d, int B, gqsa_plan_t* pl, const void** kfn) {
   pl->active_warps = active;
   pl->num_tiles = d->num_tiles;
   pl->smem_bytes = (int32_t)smem;
-  pl->x_in_smem = xsmem ? 1 : 0;
+  pl->x_in_smem = 1;
   pl->stages = sp.stages;
   pl->ctas_per_sm = occ;
   pl->ring_bytes = (int32_t)sp.ring;
+  pl->batch_per_launch = sp.batch;
+  pl->launches = sp.launches;
+  pl->coresident = sp.coresident ? 1 : 0;
   if (kfn) *kfn = fn;
   return GQSA_OK;
 }
@@ -157,43 +177,16 @@ inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintp
 
 }  // namespace
 
-extern "C" int gqsa_workspace_size(const gqsa_desc_t* desc, int32_t batch, size_t* bytes) {
-  if (!desc || !bytes) return GQSA_ERR_BUFFER;
-  if (!desc_ok(desc)) return GQSA_ERR_VALIDATION;
-  if (batch < 1 || batch > kMaxBatch) return GQSA_ERR_SHAPE;
-  const int64_t recs = desc->num_tiles < kMaxWarpsBound ? desc->num_tiles : kMaxWarpsBound;
-  *bytes = (size_t)(recs > 0 ? recs : 1) * batch * kLanes * kWsSlotBytes;
-  return GQSA_OK;
-}
-
-extern "C" int gqsa_launch_plan(const gqsa_desc_t* desc, int32_t B, gqsa_plan_t* plan) {
-  if (!desc || !plan) return GQSA_ERR_BUFFER;
-  if (!desc_ok(desc)) return GQSA_ERR_VALIDATION;
-  if (B < 1 || B > kMaxBatch) return GQSA_ERR_SHAPE;
-  return make_plan(desc, B, plan, nullptr);
-}
-
-extern "C" int gqsa_gemm_partitioned(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_X,
-                                     int32_t B, int64_t ldx, float* d_Y, int64_t ldy,
-                                     const float* d_bias, void* d_ws, size_t ws_bytes,
-                                     int32_t partition, void* stream) {
-  if (partition != GQSA_PARTITION_STREAM_K && partition != GQSA_PARTITION_SLICE_K) return GQSA_ERR_SHAPE;
-  if (!desc || !d_blob || !d_X || !d_Y || !d_ws) return GQSA_ERR_BUFFER;
-  if (!desc_ok(desc)) return GQSA_ERR_VALIDATION;
-  if (B < 1 || B > kMaxBatch) return GQSA_ERR_SHAPE;
-  if (ldx < desc->cols || ldx % 8 || ldy < desc->rows) return GQSA_ERR_SHAPE;
-  if (!aligned(d_blob, 256) || !aligned(d_X, 16) || !aligned(d_ws, 16) ||
-      (d_bias && !aligned(d_bias, 4)) || !aligned(d_Y, 4))
-    return GQSA_ERR_BUFFER;
-  size_t need = 0;
-  gqsa_workspace_size(desc, B, &need);
-  if (ws_bytes < need) return GQSA_ERR_BUFFER;
-
+namespace {
+// One launch over Bc batch columns (x of Bc columns fits in shared memory).
+int launch_chunk(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_X, int Bc, int64_t ldx,
+                 float* d_Y, int64_t ldy, const float* d_bias, void* d_ws, int32_t partition,
+                 void* stream) {
   gqsa_plan_t pl;
   const void* fn = nullptr;
-  int st = make_plan(desc, B, &pl, &fn);
+  int st = make_plan(desc, Bc, &pl, &fn);
   if (st) return st;
-
+  if (pl.batch_per_launch != Bc) return GQSA_ERR_UNSUPPORTED;  // unreachable: chunks always fit
   const uint8_t* blob = static_cast<const uint8_t*>(d_blob);
   KParams p;
   p.tiles = blob + desc->off_tiles;
@@ -234,6 +227,51 @@ extern "C" int gqsa_gemm_partitioned(const gqsa_desc_t* desc, const void* d_blob
   void* args[] = {&p};
   if (cudaLaunchKernelExC(&cfg, fn, args) != cudaSuccess) return GQSA_ERR_CUDA;
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  return GQSA_OK;
+}
+}  // namespace
+
+extern "C" int gqsa_workspace_size(const gqsa_desc_t* desc, int32_t batch, size_t* bytes) {
+  if (!desc || !bytes) return GQSA_ERR_BUFFER;
+  if (!desc_ok(desc)) return GQSA_ERR_VALIDATION;
+  if (batch < 1 || batch > kMaxBatch) return GQSA_ERR_SHAPE;
+  const int64_t recs = desc->num_tiles < kMaxWarpsBound ? desc->num_tiles : kMaxWarpsBound;
+  *bytes = (size_t)(recs > 0 ? recs : 1) * batch * kLanes * kWsSlotBytes;
+  return GQSA_OK;
+}
+
+extern "C" int gqsa_launch_plan(const gqsa_desc_t* desc, int32_t B, gqsa_plan_t* plan) {
+  if (!desc || !plan) return GQSA_ERR_BUFFER;
+  if (!desc_ok(desc)) return GQSA_ERR_VALIDATION;
+  if (B < 1 || B > kMaxBatch) return GQSA_ERR_SHAPE;
+  return make_plan(desc, B, plan, nullptr);
+}
+
+extern "C" int gqsa_gemm_partitioned(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_X,
+                                     int32_t B, int64_t ldx, float* d_Y, int64_t ldy,
+                                     const float* d_bias, void* d_ws, size_t ws_bytes,
+                                     int32_t partition, void* stream) {
+  if (partition != GQSA_PARTITION_STREAM_K && partition != GQSA_PARTITION_SLICE_K) return GQSA_ERR_SHAPE;
+  if (!desc || !d_blob || !d_X || !d_Y || !d_ws) return GQSA_ERR_BUFFER;
+  if (!desc_ok(desc)) return GQSA_ERR_VALIDATION;
+  if (B < 1 || B > kMaxBatch) return GQSA_ERR_SHAPE;
+  if (ldx < desc->cols || ldx % 8 || ldy < desc->rows) return GQSA_ERR_SHAPE;
+  if (!aligned(d_blob, 256) || !aligned(d_X, 16) || !aligned(d_ws, 16) ||
+      (d_bias && !aligned(d_bias, 4)) || !aligned(d_Y, 4))
+    return GQSA_ERR_BUFFER;
+  size_t need = 0;
+  gqsa_workspace_size(desc, B, &need);
+  if (ws_bytes < need) return GQSA_ERR_BUFFER;
+
+  gqsa_plan_t pl0;
+  int st = make_plan(desc, B, &pl0, nullptr);
+  if (st) return st;
+  for (int b0 = 0; b0 < B; b0 += pl0.batch_per_launch) {  // batch chunks whose x fits in smem
+    const int Bc = B - b0 < pl0.batch_per_launch ? B - b0 : pl0.batch_per_launch;
+    st = launch_chunk(desc, d_blob, d_X + (int64_t)b0 * ldx, Bc, ldx, d_Y + (int64_t)b0 * ldy, ldy,
+                      d_bias, d_ws, partition, stream);
+    if (st) return st;
+  }
   return GQSA_OK;
 }
 

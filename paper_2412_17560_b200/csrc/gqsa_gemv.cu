@@ -198,8 +198,9 @@ __device__ __forceinline__ uint2 group_words(const TileRegs<BITS>& r, int u) {
 
 // acc[b] += s * sum_t (q_t - z) x_t for the lane's group in slot u (Eq. 3
 // per group, z applied once through the column-group sums).
-//   xs : activations [B][K] fp16 in shared memory (or global when !XSMEM)
-//   pq : per 16-B chunk index f = 2c + swap, float2 (P, Q) with
+//   xs : activations [B][K] fp16 in shared memory
+//   pq : float2 (P, Q) per column group c (B >= 3) or per 16-B chunk index
+//        f = 2c + swap (B <= 2: duplicated, saves one instruction per group), with
 //        P = 1024 X_even + 64 X_odd and Q = X_even + X_odd of column group c
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
   uint4 v;
@@ -214,33 +215,34 @@ __device__ __forceinline__ float2 lds64f(uint32_t a) {
 
 extern __shared__ __align__(128) uint8_t smem[];
 
-template <int BITS, int B, bool XSMEM>
+// Column-sum table entries per column group: 2 (indexed by f = 2c + swap) at
+// batch <= 2, else 1 (indexed by c; halves the table so that larger batches
+// keep x resident in shared memory).
+template <int B>
+constexpr int pq_per_group() { return B <= 2 ? 2 : 1; }
+
+template <int BITS, int B>
 __device__ __forceinline__ void group_accumulate(const KParams& p, const TileRegs<BITS>& tr, int u,
                                                  float (&acc)[kMaxBatch]) {
   // shared-window offsets recomputed here so that they stay in uniform
   // registers ([R + UR] addressing on every LDS)
   const uint32_t xs = (uint32_t)__cvta_generic_to_shared(smem);
-  const uint32_t pq = xs + (XSMEM ? (uint32_t)B * 2u * (uint32_t)p.cols : 0u);
+  const uint32_t pq = xs + (uint32_t)B * 2u * (uint32_t)p.cols;
+  const uint32_t pq_row = (uint32_t)p.cols / kGroup * pq_per_group<B>() * 8u;  // bytes per batch row
   const uint32_t colw = (u < 2) ? tr.cols.x : tr.cols.y;
   const uint32_t xoff0 = (u & 1) ? (colw >> 16) : (colw & 0xffffu);  // byte offset of the first x chunk
   const uint32_t xoff1 = xoff0 ^ 16u;                                  // the other chunk
-  const uint32_t pqoff = xoff0 >> 1;                                   // f * 8
+  const uint32_t pqoff = pq_per_group<B>() == 2 ? xoff0 >> 1 : (xoff0 >> 2) & ~7u;  // f * 8 or c * 8
   const uint2 w = group_words<BITS>(tr, u);
   const uint32_t szw = u == 0 ? tr.sz.x : u == 1 ? tr.sz.y : u == 2 ? tr.sz.z : tr.sz.w;
   const __half2 sz = *reinterpret_cast<const __half2*>(&szw);
   const float s = __low2float(sz), z = __high2float(sz);
 #pragma unroll
   for (int b = 0; b < B; ++b) {
-    uint4 xa, xb;
-    if (XSMEM) {  // x of batch row b at shared offset b * 2K (x is at the start of smem)
-      xa = lds128(xs + b * 2u * (uint32_t)p.cols + xoff0);
-      xb = lds128(xs + b * 2u * (uint32_t)p.cols + xoff1);
-    } else {
-      const uint8_t* xrow = reinterpret_cast<const uint8_t*>(p.X + (int64_t)b * p.ldx);
-      xa = __ldg(reinterpret_cast<const uint4*>(xrow + xoff0));
-      xb = __ldg(reinterpret_cast<const uint4*>(xrow + xoff1));
-    }
-    const float2 X = lds64f(pq + b * (uint32_t)p.cols + pqoff);
+    // x of batch row b at shared offset b * 2K (x is at the start of smem)
+    const uint4 xa = lds128(xs + b * 2u * (uint32_t)p.cols + xoff0);
+    const uint4 xb = lds128(xs + b * 2u * (uint32_t)p.cols + xoff1);
+    const float2 X = lds64f(pq + b * pq_row + pqoff);
     if (BITS == 4) {
       // Offset-folded dequantization: the LOP3 magic leaves
       // 1024 + q (even elements) and 1024 + 16 q (odd elements) as exact fp16;
@@ -409,7 +411,7 @@ __device__ __forceinline__ void read_tile(TileRegs<BITS>& r, const uint8_t* tile
   r.rem = h.y;
 }
 
-template <int BITS, int B, bool XSMEM>
+template <int BITS, int B>
 __global__ void __launch_bounds__(max_threads_for(B), 1) gqsa_streamk_kernel(KParams p) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -440,7 +442,7 @@ __global__ void __launch_bounds__(max_threads_for(B), 1) gqsa_streamk_kernel(KPa
   // ---- weights never depend on the previous kernel: each warp's first NS
   //      tiles are requested (1-D TMA bulk copies into its shared-memory
   //      ring) BEFORE the PDL wait, so they overlap the previous kernel
-  // shared memory: [x: B*K fp16 (XSMEM)][(P,Q): B*K/8 float2][TMA ring: W x NS tiles]
+  // shared memory: [x: B*K fp16][(P,Q): B*K/16*pq_per_group float2][TMA ring: W x NS tiles]
   uint8_t* ring = smem + p.ring_offset + (size_t)warp * NS * tb;
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
   // the ring's mbarriers follow the ring: [W][kMaxStages] u64
@@ -480,7 +482,7 @@ __global__ void __launch_bounds__(max_threads_for(B), 1) gqsa_streamk_kernel(KPa
   //      the same registers: one pass, one barrier.
   const int KG = p.cols / kGroup;
   uint8_t* xs = smem;
-  uint8_t* pq = xs + (XSMEM ? (size_t)B * p.cols * 2 : 0);  // [B][K/8] float2 (P, Q) per chunk index
+  uint8_t* pq = xs + (size_t)B * p.cols * 2;  // [B][K/16 * pq_per_group] float2 (P, Q)
   {
     constexpr int U = 2;  // column groups per thread per round (2 x 32 B in flight)
     for (int i0 = threadIdx.x; i0 < B * KG; i0 += U * nthreads) {
@@ -500,7 +502,7 @@ __global__ void __launch_bounds__(max_threads_for(B), 1) gqsa_streamk_kernel(KPa
         const int i = i0 + k * nthreads;
         if (i < B * KG) {
           const int b = i / KG, c = i - b * KG;
-          if (XSMEM) {
+          {
             uint4* dst = reinterpret_cast<uint4*>(xs + (size_t)b * p.cols * 2) + 2 * c;
             dst[0] = v[k][0];
             dst[1] = v[k][1];
@@ -517,9 +519,10 @@ __global__ void __launch_bounds__(max_threads_for(B), 1) gqsa_streamk_kernel(KPa
           // P = 1024 X_even + 64 X_odd, Q = X_even + X_odd; stored for both
           // chunk orders (swap = 0, 1) of column group c
           const float2 v2 = make_float2(fmaf(1024.f, ae, 64.f * ao), ae + ao);
-          float2* dst = reinterpret_cast<float2*>(pq + (size_t)b * p.cols) + 2 * c;
+          constexpr int PG = pq_per_group<B>();
+          float2* dst = reinterpret_cast<float2*>(pq) + ((size_t)b * KG + c) * PG;
           dst[0] = v2;
-          dst[1] = v2;
+          if (PG == 2) dst[1] = v2;
         }
       }
     }
@@ -563,7 +566,7 @@ __global__ void __launch_bounds__(max_threads_for(B), 1) gqsa_streamk_kernel(KPa
           pre[k][b] = (gw + 1 + k <= w_last) ? ld_slot(ws_slot<B>(p, gw + 1 + k, b, lane)) : 0ull;
     }
 #pragma unroll
-    for (int u = 0; u < kPerLane; ++u) group_accumulate<BITS, B, XSMEM>(p, tr, u, acc);
+    for (int u = 0; u < kPerLane; ++u) group_accumulate<BITS, B>(p, tr, u, acc);
     last_hdr = tr.hdr;
     if (tr.hdr & kTileLast) {  // the slice ends in this tile: its rows are complete
       if (foreign) publish<B>(p, gw, acc, lane);
@@ -618,30 +621,27 @@ __global__ void __launch_bounds__(max_threads_for(B), 1) gqsa_streamk_kernel(KPa
 }
 
 // ---------------------------------------------------------------- launchers
-template <int BITS, int B, bool XSMEM>
+template <int BITS, int B>
 const void* kernel_ptr() {
-  return reinterpret_cast<const void*>(&gqsa_streamk_kernel<BITS, B, XSMEM>);
+  return reinterpret_cast<const void*>(&gqsa_streamk_kernel<BITS, B>);
 }
 
-#define GQSA_KSEL(BITS, XS)                                                              \
-  switch (B) {                                                                         \
-    case 1: return kernel_ptr<BITS, 1, XS>();                                          \
-    case 2: return kernel_ptr<BITS, 2, XS>();                                          \
-    case 3: return kernel_ptr<BITS, 3, XS>();                                          \
-    case 4: return kernel_ptr<BITS, 4, XS>();                                          \
-    case 5: return kernel_ptr<BITS, 5, XS>();                                          \
-    case 6: return kernel_ptr<BITS, 6, XS>();                                          \
-    case 7: return kernel_ptr<BITS, 7, XS>();                                          \
-    case 8: return kernel_ptr<BITS, 8, XS>();                                          \
-    default: return nullptr;                                                           \
+#define GQSA_KSEL(BITS)                         \
+  switch (B) {                                  \
+    case 1: return kernel_ptr<BITS, 1>();       \
+    case 2: return kernel_ptr<BITS, 2>();       \
+    case 3: return kernel_ptr<BITS, 3>();       \
+    case 4: return kernel_ptr<BITS, 4>();       \
+    case 5: return kernel_ptr<BITS, 5>();       \
+    case 6: return kernel_ptr<BITS, 6>();       \
+    case 7: return kernel_ptr<BITS, 7>();       \
+    case 8: return kernel_ptr<BITS, 8>();       \
+    default: return nullptr;                    \
   }
 
-const void* select_kernel(int bits, int B, bool xsmem) {
-  if (bits == 4) {
-    if (xsmem) { GQSA_KSEL(4, true) } else { GQSA_KSEL(4, false) }
-  } else if (bits == 2) {
-    if (xsmem) { GQSA_KSEL(2, true) } else { GQSA_KSEL(2, false) }
-  }
+const void* select_kernel(int bits, int B) {
+  if (bits == 4) { GQSA_KSEL(4) }
+  if (bits == 2) { GQSA_KSEL(2) }
   return nullptr;
 }
 

@@ -41,6 +41,8 @@ struct KParams {
                            // 1 after activation staging, 2 after the first tile pair
 };
 
-const void* select_kernel(int bits, int B, bool xsmem);
+const void* select_kernel(int bits, int B);
+// Bytes of the column-sum table per batch row (see gqsa_gemv.cu pq_per_group).
+inline size_t pq_bytes_per_row(int B, int cols) { return (size_t)cols / 16 * (B <= 2 ? 2 : 1) * 8; }
 
 }  // namespace gqsa

@@ -62,7 +62,7 @@ class Desc(ctypes.Structure):
 class Plan(ctypes.Structure):
     _fields_ = [(k, ctypes.c_int32) for k in
                 ("grid", "warps_per_cta", "active_warps", "num_tiles", "smem_bytes", "x_in_smem",
-                 "stages", "ctas_per_sm", "ring_bytes")]
+                 "stages", "ctas_per_sm", "ring_bytes", "batch_per_launch", "launches", "coresident")]
 
 
 EXPORTS = (

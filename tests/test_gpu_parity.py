@@ -80,7 +80,9 @@ EXACT_CASES = [
     (4096, 16, 4, 0.5, "uniform", 1),     # K = G: many empty rows, 1-group rows
     (5, 64, 4, 0.5, "uniform", 1),        # nnzg < one tile
     (640, 512, 2, 0.9, "uniform", 5),     # mostly-empty rows
-    (2048, 28672, 4, 0.5, "uniform", 4),  # K too large for x in smem at B=4
+    (2048, 28672, 4, 0.5, "uniform", 4),  # x of 4 columns exceeds an SM: 2 launches of 2
+    (1024, 14336, 4, 0.5, "uniform", 8),  # x of 8 columns exceeds an SM: 2 launches of 4
+    (512, 14336, 2, 0.5, "skewed", 3),    # CTA takes the whole SM (no PDL co-residency)
 ]
 
 
@@ -217,6 +219,26 @@ def test_argument_errors():
     with pytest.raises(gqsa.GQSAError) as e:  # misaligned x
         gqsa.gemv(L.desc, L.blob, X.view(-1)[1:257], torch.empty(64, device="cuda"), None, L.ws)
     assert e.value.status == -4
+
+
+def test_launch_plan_batch_split_and_residency():
+    """x (+ column sums) must fit in shared memory: larger batches split into
+    several launches; CTAs that leave no room for the next launch take the SM."""
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    for rows, cols, B, launches, coresident in ((4096, 4096, 1, 1, 1), (4096, 4096, 8, 1, 1),
+                                                 (4096, 14336, 1, 1, 1), (4096, 14336, 4, 1, 0),
+                                                 (4096, 14336, 8, 2, 0), (64, 28672, 4, 2, 0)):
+        bsr = synth.make_layer(rows + cols + B, rows, cols, sparsity=0.5)
+        _, d = gqsa.pack(bsr)
+        p = gqsa.launch_plan(d, B)
+        assert (p.launches, p.coresident) == (launches, coresident), (rows, cols, B, p.launches, p.coresident)
+        assert p.batch_per_launch * p.launches >= B and p.smem_bytes <= 227 * 1024
+        assert p.grid <= sms
+    n0 = gqsa.launch_count()
+    L = gqsa.Layer(synth.make_layer(5, 256, 14336, sparsity=0.5))
+    L.gemm(torch.zeros(8, 14336, dtype=torch.float16, device="cuda"))
+    torch.cuda.synchronize()
+    assert gqsa.launch_count() == n0 + 2
 
 
 def test_launch_plan_is_persistent_stream_k():
