@@ -21,7 +21,7 @@ size_t g_trace_bytes = 0;
 
 struct DevInfo {
   int sms = 0;
-  bool attr_set[2][kMaxBatch + 1] = {};
+  bool attr_set[9][kMaxBatch + 1] = {};
 };
 std::mutex g_mu;
 DevInfo g_dev[64];
@@ -41,7 +41,7 @@ bool lanes_per_row_ok(uint32_t s) { return s >= 1 && s <= 32 && (s & (s - 1)) ==
 
 bool desc_ok(const gqsa_desc_t* d) {
   return d && d->magic == kMagic && d->version == (uint32_t)kVersion && d->group_size == kGroup &&
-         (d->bits == 4 || d->bits == 2) && d->tile_groups == kTileGroups && d->rows >= 0 &&
+         (d->bits == 4 || d->bits == 2 || d->bits == 8) && d->tile_groups == kTileGroups && d->rows >= 0 &&
          d->cols > 0 && d->cols % kGroup == 0 && d->num_tiles >= 0 &&
          lanes_per_row_ok(((uint32_t)d->flags >> kFlagLanesPerRowShift) & 0xff);
 }
@@ -61,9 +61,9 @@ int stages_cap() {
   return cap;
 }
 
-int warps_per_cta(int B) {
+int warps_per_cta(int bits, int B) {
   static int w1 = env_int("GQSA_WARPS", 16, 1, kMaxWarps);
-  return B <= 2 ? w1 : 8;
+  return bits == 8 ? 8 : (B <= 2 ? w1 : 8);  // <= max_threads_for(bits, B) / 32
 }
 
 // Shared-memory plan per CTA of W warps: [x: B*K fp16][(P, Q) column sums]
@@ -87,16 +87,16 @@ SmemPlan smem_plan(const gqsa_desc_t* d, int B) {
   SmemPlan sp{};
   // largest batch chunk whose x fits next to a minimal ring (default warps,
   // else 8 warps); cols <= kMaxCols makes Bc = 1 always fit
-  int Bc = B, W = warps_per_cta(B);
+  int Bc = B, W = warps_per_cta(d->bits, B);
   for (;; --Bc) {
-    W = warps_per_cta(Bc);
+    W = warps_per_cta(d->bits, Bc);
     if (x_bytes(Bc, d->cols) + ring_bytes_for(d, W, kMinStages) <= kMaxDynSmem) break;
     if (W > 8 && x_bytes(Bc, d->cols) + ring_bytes_for(d, 8, kMinStages) <= kMaxDynSmem) { W = 8; break; }
     if (Bc == 1) break;
   }
   sp.launches = (B + Bc - 1) / Bc;
   const int Bb = (B + sp.launches - 1) / sp.launches;  // balanced chunks (<= Bc: fits)
-  if (Bb != Bc) W = warps_per_cta(Bb) > W ? W : warps_per_cta(Bb);
+  if (Bb != Bc) W = warps_per_cta(d->bits, Bb) > W ? W : warps_per_cta(d->bits, Bb);
   Bc = Bb;
   sp.batch = Bc;
   const size_t tb = (size_t)tile_bytes(d->bits);
@@ -130,7 +130,7 @@ int make_plan(const gqsa_desc_t* d, int B, gqsa_plan_t* pl, const void** kfn) {
   if (!fn) return GQSA_ERR_UNSUPPORTED;
   {
     std::lock_guard<std::mutex> lk(g_mu);
-    bool& set = g_dev[dev].attr_set[d->bits == 4][sp.batch];
+    bool& set = g_dev[dev].attr_set[d->bits][sp.batch];
     if (!set) {
       // maximum shared-memory carveout: two kernels' CTAs (this launch and
       // the next, PDL) must fit on one SM at the same time
@@ -147,6 +147,9 @@ int make_plan(const gqsa_desc_t* d, int B, gqsa_plan_t* pl, const void** kfn) {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem) != cudaSuccess)
     return GQSA_ERR_CUDA;
   if (occ < 1) return GQSA_ERR_UNSUPPORTED;
+  // the next launch on the stream (same configuration) can be resident
+  // during this one's tail only if two CTAs fit (shared memory AND registers)
+  const bool coresident = occ >= ctas_per_sm_cap() + 1;
   if (occ > ctas_per_sm_cap()) occ = ctas_per_sm_cap();
   int warps = sms * occ * W;
   if (warps > kMaxWarpsBound) warps = kMaxWarpsBound;
@@ -168,7 +171,7 @@ int make_plan(const gqsa_desc_t* d, int B, gqsa_plan_t* pl, const void** kfn) {
   pl->ring_bytes = (int32_t)sp.ring;
   pl->batch_per_launch = sp.batch;
   pl->launches = sp.launches;
-  pl->coresident = sp.coresident ? 1 : 0;
+  pl->coresident = coresident ? 1 : 0;
   if (kfn) *kfn = fn;
   return GQSA_OK;
 }

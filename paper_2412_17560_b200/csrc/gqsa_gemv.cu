@@ -129,6 +129,17 @@ __device__ __forceinline__ void dot8_w4_raw(uint32_t w, uint32_t x01, uint32_t x
   dd = fhfma<1, 1>(e37, x67, dd);
 }
 
+// Raw dot of one word of four 8-bit codes (element j in byte j) with
+// x[0..3] = (x0, x1) (x2, x3): acc += sum_j (1024 + q_j) x_j, products exact.
+__device__ __forceinline__ void dot4_w8_raw(uint32_t w, uint32_t x01, uint32_t x23, float& acc) {
+  const uint32_t e02 = lop3_and_or(w, 0x00FF00FFu, kMagic1024);       // (1024+q0, 1024+q2)
+  const uint32_t e13 = lop3_and_or(w >> 8, 0x00FF00FFu, kMagic1024);  // (1024+q1, 1024+q3)
+  acc = fhfma<0, 0>(e02, x01, acc);
+  acc = fhfma<0, 1>(e13, x01, acc);
+  acc = fhfma<1, 0>(e02, x23, acc);
+  acc = fhfma<1, 1>(e13, x23, acc);
+}
+
 // Dot of one word of sixteen 2-bit codes (element j at bits 2j..2j+1) with
 // x[0..15] in eight half2 registers.  Masks pick elements (j, j+8).
 __device__ __forceinline__ float dot16_w2(uint32_t w, const uint32_t (&x)[8], float acc) {
@@ -166,8 +177,11 @@ __device__ __forceinline__ float dot16_w2(uint32_t w, const uint32_t (&x)[8], fl
 
 // ---------------------------------------------------------------- tile regs
 template <int BITS>
+constexpr int code_planes() { return BITS == 8 ? 4 : (BITS == 4 ? 2 : 1); }
+
+template <int BITS>
 struct TileRegs {
-  uint4 codes[BITS == 4 ? 2 : 1];  // lane's 4 slots (W4: 2 planes x 16 B)
+  uint4 codes[code_planes<BITS>()];  // lane's 4 slots (W2: 1, W4: 2, W8: 4 planes x 16 B)
   uint4 sz;                        // 4 x (s, z) half pairs
   uint2 cols;                      // 4 x u16 (2c + swap)
   uint32_t hdr;                    // slice << 2 | FIRST | LAST
@@ -186,7 +200,9 @@ __device__ __forceinline__ void load_tile(TileRegs<BITS>& r, const uint8_t* tile
 // Group code word(s) of slot u from the lane's codes.
 template <int BITS>
 __device__ __forceinline__ uint2 group_words(const TileRegs<BITS>& r, int u) {
-  if (BITS == 4) {
+  if (BITS == 8) {
+    return make_uint2(0u, 0u);  // W8 reads the whole 16-B slot (tr.codes[u])
+  } else if (BITS == 4) {
     const uint4& c = r.codes[u >> 1];
     return (u & 1) ? make_uint2(c.z, c.w) : make_uint2(c.x, c.y);
   } else {
@@ -243,7 +259,18 @@ __device__ __forceinline__ void group_accumulate(const KParams& p, const TileReg
     const uint4 xa = lds128(xs + b * 2u * (uint32_t)p.cols + xoff0);
     const uint4 xb = lds128(xs + b * 2u * (uint32_t)p.cols + xoff1);
     const float2 X = lds64f(pq + b * pq_row + pqoff);
-    if (BITS == 4) {
+    if (BITS == 8) {
+      // Every element carries the +1024 offset of the LOP3 magic:
+      //   sum_t (q_t - z) x_t = sum_t (1024 + q_t) x_t - (1024 + z) X.
+      const uint4 c = tr.codes[u];
+      float d0 = 0.f, d1 = 0.f;
+      dot4_w8_raw(c.x, xa.x, xa.y, d0);  // elements 0..3 <-> first x chunk
+      dot4_w8_raw(c.y, xa.z, xa.w, d1);  // 4..7
+      dot4_w8_raw(c.z, xb.x, xb.y, d0);  // 8..11 <-> second x chunk
+      dot4_w8_raw(c.w, xb.z, xb.w, d1);  // 12..15
+      const float t = fmaf(-z, X.y, fmaf(-1024.f, X.y, d0 + d1));
+      acc[b] = fmaf(s, t, acc[b]);
+    } else if (BITS == 4) {
       // Offset-folded dequantization: the LOP3 magic leaves
       // 1024 + q (even elements) and 1024 + 16 q (odd elements) as exact fp16;
       // their products with x are exact in fp32, and the offsets are removed
@@ -402,8 +429,9 @@ __device__ __forceinline__ void trace_point(const KParams& p, int gw, int lane, 
 // One lane's view of a tile that has landed in shared memory.
 template <int BITS>
 __device__ __forceinline__ void read_tile(TileRegs<BITS>& r, const uint8_t* tile, int lane) {
-  r.codes[0] = *reinterpret_cast<const uint4*>(tile + kTileHeaderBytes + lane * 16);
-  if (BITS == 4) r.codes[BITS == 4 ? 1 : 0] = *reinterpret_cast<const uint4*>(tile + kTileHeaderBytes + 512 + lane * 16);
+#pragma unroll
+  for (int pl = 0; pl < code_planes<BITS>(); ++pl)
+    r.codes[pl] = *reinterpret_cast<const uint4*>(tile + kTileHeaderBytes + pl * 512 + lane * 16);
   r.sz = *reinterpret_cast<const uint4*>(tile + off_sz(BITS) + lane * 16);
   r.cols = *reinterpret_cast<const uint2*>(tile + off_cols(BITS) + lane * 8);
   const uint2 h = *reinterpret_cast<const uint2*>(tile);  // broadcast
@@ -412,7 +440,7 @@ __device__ __forceinline__ void read_tile(TileRegs<BITS>& r, const uint8_t* tile
 }
 
 template <int BITS, int B>
-__global__ void __launch_bounds__(max_threads_for(B), 1) gqsa_streamk_kernel(KParams p) {
+__global__ void __launch_bounds__(max_threads_for(BITS, B), min_blocks_for(BITS)) gqsa_streamk_kernel(KParams p) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int nthreads = blockDim.x;
@@ -642,6 +670,7 @@ const void* kernel_ptr() {
 const void* select_kernel(int bits, int B) {
   if (bits == 4) { GQSA_KSEL(4) }
   if (bits == 2) { GQSA_KSEL(2) }
+  if (bits == 8) { GQSA_KSEL(8) }
   return nullptr;
 }
 

@@ -35,7 +35,7 @@ inline bool f16_positive(uint16_t h) { return !(h & 0x8000) && (h & 0x7fff) != 0
 int check_bsr_header(const gqsa_bsr_t* b) {
   if (!b) return GQSA_ERR_BUFFER;
   if (b->rows < 0 || b->cols <= 0 || b->group_size <= 0 || b->nnzg < 0) return GQSA_ERR_SHAPE;
-  if (b->group_size != kGroup || (b->bits != 4 && b->bits != 2)) return GQSA_ERR_UNSUPPORTED;
+  if (b->group_size != kGroup || (b->bits != 4 && b->bits != 2 && b->bits != 8)) return GQSA_ERR_UNSUPPORTED;
   if (b->cols % b->group_size) return GQSA_ERR_SHAPE;
   if (b->cols > kMaxCols) return GQSA_ERR_UNSUPPORTED;  // col field = byte offset in u16
   if (!b->row_index) return GQSA_ERR_BUFFER;
@@ -266,7 +266,7 @@ extern "C" int gqsa_read_desc(const void* blob, size_t blob_bytes, gqsa_desc_t* 
   BlobHeader h;
   std::memcpy(&h, blob, sizeof(h));
   if (h.magic != kMagic || h.version != (uint32_t)kVersion) return GQSA_ERR_VALIDATION;
-  if (h.group_size != kGroup || (h.bits != 4 && h.bits != 2)) return GQSA_ERR_UNSUPPORTED;
+  if (h.group_size != kGroup || (h.bits != 4 && h.bits != 2 && h.bits != 8)) return GQSA_ERR_UNSUPPORTED;
   if (h.tile_groups != kTileGroups || h.tile_bytes != tile_bytes(h.bits)) return GQSA_ERR_VALIDATION;
   if (h.rows < 0 || h.cols <= 0 || h.cols % kGroup || h.cols > kMaxCols || h.nnzg < 0)
     return GQSA_ERR_VALIDATION;

@@ -83,6 +83,11 @@ EXACT_CASES = [
     (2048, 28672, 4, 0.5, "uniform", 4),  # x of 4 columns exceeds an SM: 2 launches of 2
     (1024, 14336, 4, 0.5, "uniform", 8),  # x of 8 columns exceeds an SM: 2 launches of 4
     (512, 14336, 2, 0.5, "skewed", 3),    # CTA takes the whole SM (no PDL co-residency)
+    # W8 (exact-int needs 255*2*4*K < 2^23: K <= 4096)
+    (1024, 4096, 8, 0.5, "uniform", 1),
+    (300, 1024, 8, 0.3, "row_balanced", 4),
+    (77, 208, 8, 0.2, "uniform", 8),
+    (512, 2048, 8, 0.5, "skewed", 2),
 ]
 
 
@@ -165,6 +170,8 @@ REAL_CASES = [
     (4096, 4096, 4, 0.3, "uniform", 8),
     (2048, 5120, 4, 0.5, "row_balanced", 4),
     (1024, 2048, 4, 0.5, "skewed", 1),
+    (4096, 4096, 8, 0.5, "uniform", 1),
+    (2048, 14336, 8, 0.5, "uniform", 2),
 ]
 
 
@@ -223,9 +230,10 @@ def test_argument_errors():
 
 def test_launch_plan_batch_split_and_residency():
     """x (+ column sums) must fit in shared memory: larger batches split into
-    several launches; CTAs that leave no room for the next launch take the SM."""
+    several launches; CTAs that leave no room (shared memory or registers:
+    batch >= 3 kernels use > 128 registers) for the next launch take the SM."""
     sms = torch.cuda.get_device_properties(0).multi_processor_count
-    for rows, cols, B, launches, coresident in ((4096, 4096, 1, 1, 1), (4096, 4096, 8, 1, 1),
+    for rows, cols, B, launches, coresident in ((4096, 4096, 1, 1, 1), (4096, 4096, 8, 1, 0),
                                                  (4096, 14336, 1, 1, 1), (4096, 14336, 4, 1, 0),
                                                  (4096, 14336, 8, 2, 0), (64, 28672, 4, 2, 0)):
         bsr = synth.make_layer(rows + cols + B, rows, cols, sparsity=0.5)

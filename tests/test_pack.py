@@ -52,6 +52,8 @@ CASES = [
     (300, 32, 2, 0.8, "uniform", 6),       # many empty rows, tiny rows
     (8, 64, 4, 1.0, "uniform", 7),         # nnzg = 0
     (1, 4096, 4, 0.5, "uniform", 8),       # all groups in one row
+    (256, 256, 8, 0.5, "uniform", 9),      # W8: four 512-B code planes per tile
+    (37, 208, 8, 0.3, "row_balanced", 10),
 ]
 
 

@@ -1,4 +1,4 @@
 # ad-hoc GPU experiment driver (edited per session)
 make -s >/dev/null 2>&1
 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -15 gpurun_out/pytest_gpu.log
-for s in "4096 4096" "14336 4096" "4096 14336"; do set -- $s; for b in 1 2 4 8; do python tools/prof_layer.py --rows $1 --cols $2 --batch $b --launches 50 --time | grep -v plan; done; done
+python tools/sweep.py --out gpurun_out/r01_sweep > gpurun_out/sweep.log 2>&1; grep "^|" gpurun_out/sweep.log | head -20

@@ -3,7 +3,7 @@
 
     python tools/sweep.py --out profiles/r01_sweep [--quick]
 
-A. W4S50 / W4S30 / W2S50 x batch 1, 2, 4, 8 at the LLaMA-3-8B shapes.
+A. W4S50 / W4S30 / W2S50 / W8S50 x batch 1, 2, 4, 8 at the LLaMA-3-8B shapes.
 B. Partition ablation (App. J): Stream-K versus
    Slice-K on uniform, row-balanced and skewed masks (W4S50, batch 1).
 C. Sparsity sweep at 4096x4096 W4 (Fig. 6 trend): S = 0 .. 0.8,
@@ -86,7 +86,7 @@ def main():
     lines += ["## A. Quantisation setting x batch (Stream-K)", "",
               "| setting | shape | B=1 µs (GB/s) | B=2 | B=4 | B=8 |", "|---|---|---|---|---|---|"]
     batches = [1, 8] if a.quick else [1, 2, 4, 8]
-    for bits, sp in ((4, 0.5), (4, 0.3), (2, 0.5)):
+    for bits, sp in ((4, 0.5), (4, 0.3), (2, 0.5), (8, 0.5)):
         for rows, cols in SHAPES:
             bsr = synth.make_layer(synth.seed_for(f"llama3-8b/{rows}x{cols}/{bits}/{sp}/16/uniform"),
                                    rows, cols, bits=bits, sparsity=sp)
