@@ -440,7 +440,7 @@ __device__ __forceinline__ void read_tile(TileRegs<BITS>& r, const uint8_t* tile
 }
 
 template <int BITS, int B>
-__global__ void __launch_bounds__(max_threads_for(BITS, B), min_blocks_for(BITS)) gqsa_streamk_kernel(KParams p) {
+__global__ void __launch_bounds__(max_threads_for(BITS, B), min_blocks_for(BITS, B)) gqsa_streamk_kernel(KParams p) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int nthreads = blockDim.x;

@@ -21,7 +21,7 @@ constexpr int kCoResidentKernels = 2;    // leave room for the next PDL-launched
 // holds 64 code bytes per lane per tile: 8 warps, <= 128 registers (two CTAs
 // per SM, so the next PDL launch can be resident).
 constexpr int max_threads_for(int bits, int B) { return bits == 8 ? 256 : (B <= 2 ? kMaxThreads : 256); }
-constexpr int min_blocks_for(int bits) { return bits == 8 ? 2 : 1; }
+constexpr int min_blocks_for(int bits, int B) { return (bits == 8 || B > 2) ? 2 : 1; }
 constexpr int kMaxWarpsBound = 8192;     // workspace records (>= any grid we launch)
 constexpr int kWsSlotBytes = 8;          // fix-up slot {partial, flag} per (warp, batch, lane)
 constexpr int kSmemBudget = 200 * 1024;  // above this, x is gathered from L1/L2
