@@ -149,25 +149,31 @@ int gqsa_gemm_smallbatch(const gqsa_desc_t* desc, const void* d_blob, const uint
                          void* d_ws, size_t ws_bytes, void* stream);
 
 /*
- * gqsa_gemm_partitioned: gqsa_gemm_smallbatch with an explicit work
- * partition (PAPER.md:161 and App. J):
- *   GQSA_PARTITION_STREAM_K (task-centric, the default of every other entry
- *     point): equal (+-1 tile) contiguous tile ranges per warp regardless of
- *     row boundaries; rows split across warps are finished by the cross-warp
- *     fix-up.
- *   GQSA_PARTITION_SLICE_K (data-centric, the paper's baseline): a warp owns
- *     whole 32-lane slices (rows) -- those whose first tile falls in its
- *     Stream-K range -- so there is no fix-up, and work per warp varies with
- *     the row lengths.
- * Same arguments, results within the parity gates of each other (the fp32
- * summation order differs); bit-identical across reruns for either mode.
- * Other values of `partition` return GQSA_ERR_SHAPE.
+ * gqsa_gemm_ex: gqsa_gemm_smallbatch with options (NULL = defaults).
+ *   opts->partition (PAPER.md:161 and App. J):
+ *     GQSA_PARTITION_STREAM_K (task-centric, the default): equal (+-1 tile)
+ *       contiguous tile ranges per warp regardless of row boundaries; rows
+ *       split across warps are finished by the cross-warp fix-up.
+ *     GQSA_PARTITION_SLICE_K (data-centric, the paper's baseline): a warp owns
+ *       whole 32-lane slices (rows) -- those whose first tile falls in its
+ *       Stream-K range -- so there is no fix-up, and work per warp varies with
+ *       the row lengths.
+ *     Results agree within the parity gates (the fp32 summation order
+ *     differs); each mode is bit-identical across reruns.
+ *   opts->out_f16: 0 = fp32 Y (default), 1 = fp16 Y (round-to-nearest-even
+ *     of the fp32 result (+ bias)); d_Y then points to uint16 [B][ldy]
+ *     (2-B aligned).
+ * Other option values return GQSA_ERR_SHAPE.
  */
 #define GQSA_PARTITION_STREAM_K 0
 #define GQSA_PARTITION_SLICE_K 1
-int gqsa_gemm_partitioned(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_X,
-                          int32_t B, int64_t ldx, float* d_Y, int64_t ldy, const float* d_bias,
-                          void* d_ws, size_t ws_bytes, int32_t partition, void* stream);
+typedef struct {
+  int32_t partition;  /* GQSA_PARTITION_* */
+  int32_t out_f16;    /* 0: fp32 output, 1: fp16 output */
+} gqsa_options_t;
+int gqsa_gemm_ex(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_X, int32_t B,
+                 int64_t ldx, void* d_Y, int64_t ldy, const float* d_bias, void* d_ws,
+                 size_t ws_bytes, const gqsa_options_t* opts, void* stream);
 
 /*
  * gqsa_gemm_hostio: the end-to-end call with HOST activations and outputs.

@@ -183,7 +183,7 @@ inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintp
 namespace {
 // One launch over Bc batch columns (x of Bc columns fits in shared memory).
 int launch_chunk(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_X, int Bc, int64_t ldx,
-                 float* d_Y, int64_t ldy, const float* d_bias, void* d_ws, int32_t partition,
+                 void* d_Y, int64_t ldy, const float* d_bias, void* d_ws, const gqsa_options_t& o,
                  void* stream) {
   gqsa_plan_t pl;
   const void* fn = nullptr;
@@ -212,7 +212,8 @@ int launch_chunk(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_
   p.stages = pl.stages;
   p.ring_offset = pl.smem_bytes - pl.ring_bytes - pl.warps_per_cta * kMaxStages * 8;
   p.trace = (g_trace && g_trace_bytes >= (size_t)pl.active_warps * 64) ? g_trace : nullptr;
-  p.slice_k = partition == GQSA_PARTITION_SLICE_K ? 1 : 0;
+  p.slice_k = o.partition == GQSA_PARTITION_SLICE_K ? 1 : 0;
+  p.out_f16 = o.out_f16;
   static const int trigger = env_int("GQSA_PDL_TRIGGER", 0, 0, 2);
   p.pdl_trigger = trigger;
   if (desc->rows == 0) return GQSA_OK;
@@ -250,17 +251,18 @@ extern "C" int gqsa_launch_plan(const gqsa_desc_t* desc, int32_t B, gqsa_plan_t*
   return make_plan(desc, B, plan, nullptr);
 }
 
-extern "C" int gqsa_gemm_partitioned(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_X,
-                                     int32_t B, int64_t ldx, float* d_Y, int64_t ldy,
-                                     const float* d_bias, void* d_ws, size_t ws_bytes,
-                                     int32_t partition, void* stream) {
-  if (partition != GQSA_PARTITION_STREAM_K && partition != GQSA_PARTITION_SLICE_K) return GQSA_ERR_SHAPE;
+extern "C" int gqsa_gemm_ex(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_X, int32_t B,
+                            int64_t ldx, void* d_Y, int64_t ldy, const float* d_bias, void* d_ws,
+                            size_t ws_bytes, const gqsa_options_t* opts, void* stream) {
+  const gqsa_options_t o = opts ? *opts : gqsa_options_t{GQSA_PARTITION_STREAM_K, 0};
+  if (o.partition != GQSA_PARTITION_STREAM_K && o.partition != GQSA_PARTITION_SLICE_K) return GQSA_ERR_SHAPE;
+  if (o.out_f16 != 0 && o.out_f16 != 1) return GQSA_ERR_SHAPE;
   if (!desc || !d_blob || !d_X || !d_Y || !d_ws) return GQSA_ERR_BUFFER;
   if (!desc_ok(desc)) return GQSA_ERR_VALIDATION;
   if (B < 1 || B > kMaxBatch) return GQSA_ERR_SHAPE;
   if (ldx < desc->cols || ldx % 8 || ldy < desc->rows) return GQSA_ERR_SHAPE;
   if (!aligned(d_blob, 256) || !aligned(d_X, 16) || !aligned(d_ws, 16) ||
-      (d_bias && !aligned(d_bias, 4)) || !aligned(d_Y, 4))
+      (d_bias && !aligned(d_bias, 4)) || !aligned(d_Y, o.out_f16 ? 2 : 4))
     return GQSA_ERR_BUFFER;
   size_t need = 0;
   gqsa_workspace_size(desc, B, &need);
@@ -271,8 +273,8 @@ extern "C" int gqsa_gemm_partitioned(const gqsa_desc_t* desc, const void* d_blob
   if (st) return st;
   for (int b0 = 0; b0 < B; b0 += pl0.batch_per_launch) {  // batch chunks whose x fits in smem
     const int Bc = B - b0 < pl0.batch_per_launch ? B - b0 : pl0.batch_per_launch;
-    st = launch_chunk(desc, d_blob, d_X + (int64_t)b0 * ldx, Bc, ldx, d_Y + (int64_t)b0 * ldy, ldy,
-                      d_bias, d_ws, partition, stream);
+    void* y0 = static_cast<uint8_t*>(d_Y) + (size_t)b0 * ldy * (o.out_f16 ? 2 : 4);
+    st = launch_chunk(desc, d_blob, d_X + (int64_t)b0 * ldx, Bc, ldx, y0, ldy, d_bias, d_ws, o, stream);
     if (st) return st;
   }
   return GQSA_OK;
@@ -281,8 +283,7 @@ extern "C" int gqsa_gemm_partitioned(const gqsa_desc_t* desc, const void* d_blob
 extern "C" int gqsa_gemm_smallbatch(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_X,
                                     int32_t B, int64_t ldx, float* d_Y, int64_t ldy,
                                     const float* d_bias, void* d_ws, size_t ws_bytes, void* stream) {
-  return gqsa_gemm_partitioned(desc, d_blob, d_X, B, ldx, d_Y, ldy, d_bias, d_ws, ws_bytes,
-                               GQSA_PARTITION_STREAM_K, stream);
+  return gqsa_gemm_ex(desc, d_blob, d_X, B, ldx, d_Y, ldy, d_bias, d_ws, ws_bytes, nullptr, stream);
 }
 
 extern "C" int gqsa_gemv(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_x, float* d_y,

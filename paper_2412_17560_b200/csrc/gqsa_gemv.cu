@@ -362,6 +362,12 @@ __device__ __forceinline__ void collect(const KParams& p, int gw, int w_last, fl
   }
 }
 
+// y element i: fp32, or fp16 rounded to nearest even (PAPER.md:134 step 5).
+__device__ __forceinline__ void store_y(const KParams& p, int64_t i, float v) {
+  if (p.out_f16) reinterpret_cast<__half*>(p.Y)[i] = __float2half_rn(v);
+  else reinterpret_cast<float*>(p.Y)[i] = v;
+}
+
 // Sum over the S lanes of a row (S = lanes per row, a power of two) and store.
 template <int B>
 __device__ __forceinline__ void store_rows(const KParams& p, float (&v)[kMaxBatch], int row, int lane) {
@@ -372,7 +378,7 @@ __device__ __forceinline__ void store_rows(const KParams& p, float (&v)[kMaxBatc
   if (row >= 0 && (lane & (p.lanes_per_row - 1)) == 0) {
     const float bias = p.bias ? __ldg(p.bias + row) : 0.f;
 #pragma unroll
-    for (int b = 0; b < B; ++b) p.Y[(int64_t)b * p.ldy + row] = v[b] + bias;
+    for (int b = 0; b < B; ++b) store_y(p, (int64_t)b * p.ldy + row, v[b] + bias);
   }
 }
 
@@ -564,7 +570,7 @@ __global__ void __launch_bounds__(max_threads_for(BITS, B), min_blocks_for(BITS,
     const int erow = __ldg(p.empty + i);
     const float bias = p.bias ? __ldg(p.bias + erow) : 0.f;
 #pragma unroll
-    for (int b = 0; b < B; ++b) p.Y[(int64_t)b * p.ldy + erow] = bias;
+    for (int b = 0; b < B; ++b) store_y(p, (int64_t)b * p.ldy + erow, bias);
   }
   trace_point(p, gw, lane, 2);
   if (t_end <= t_begin) return;

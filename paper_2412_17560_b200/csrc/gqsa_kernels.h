@@ -31,7 +31,7 @@ struct KParams {
   const int32_t* perm;    // blob + off_nzrow: row of each (slice, lane), -1 = unused
   const int32_t* empty;   // blob + off_empty
   const uint16_t* X;      // [B][ldx] fp16
-  float* Y;               // [B][ldy] fp32
+  void* Y;                // [B][ldy] fp32 (or fp16 when out_f16)
   const float* bias;      // [rows] or null
   uint32_t* ws;           // [active_warps][B][32] 8-B slots, zero between calls
   int64_t ldx, ldy;
@@ -41,6 +41,7 @@ struct KParams {
   int32_t ring_offset;     // shared-memory offset of the TMA ring (after x and the column sums)
   uint64_t* trace;         // optional [active_warps][8] %globaltimer stamps (debug)
   int32_t slice_k;         // 1: data-centric partition (whole slices per warp, no fix-up)
+  int32_t out_f16;         // 1: Y is fp16 (RNE of the fp32 result)
   int32_t pdl_trigger;     // where the next kernel may launch: 0 before the PDL wait,
                            // 1 after activation staging, 2 after the first tile pair
 };

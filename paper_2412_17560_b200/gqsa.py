@@ -67,7 +67,7 @@ class Plan(ctypes.Structure):
 
 EXPORTS = (
     "gqsa_pack_size", "gqsa_pack", "gqsa_read_desc", "gqsa_unpack", "gqsa_workspace_size",
-    "gqsa_gemv", "gqsa_gemm_smallbatch", "gqsa_gemm_partitioned", "gqsa_hostio_stage_size",
+    "gqsa_gemv", "gqsa_gemm_smallbatch", "gqsa_gemm_ex", "gqsa_hostio_stage_size",
     "gqsa_gemm_hostio",
     "gqsa_launch_plan", "gqsa_launch_count", "gqsa_status_string", "gqsa_version",
     "gqsa_debug_trace",
@@ -93,7 +93,7 @@ def lib() -> ctypes.CDLL:
     L.gqsa_workspace_size.argtypes = [ctypes.POINTER(Desc), I32, PSZ]
     L.gqsa_gemv.argtypes = [ctypes.POINTER(Desc), P, P, P, P, P, SZ, P]
     L.gqsa_gemm_smallbatch.argtypes = [ctypes.POINTER(Desc), P, P, I32, I64, P, I64, P, P, SZ, P]
-    L.gqsa_gemm_partitioned.argtypes = [ctypes.POINTER(Desc), P, P, I32, I64, P, I64, P, P, SZ, I32, P]
+    L.gqsa_gemm_ex.argtypes = [ctypes.POINTER(Desc), P, P, I32, I64, P, I64, P, P, SZ, ctypes.POINTER(Options), P]
     L.gqsa_hostio_stage_size.argtypes = [ctypes.POINTER(Desc), I32, PSZ]
     L.gqsa_gemm_hostio.argtypes = [ctypes.POINTER(Desc), P, P, I32, P, P, P, SZ, P, SZ, P]
     L.gqsa_launch_plan.argtypes = [ctypes.POINTER(Desc), I32, ctypes.POINTER(Plan)]
@@ -235,14 +235,20 @@ PARTITION_STREAM_K = 0  # task-centric (default everywhere)
 PARTITION_SLICE_K = 1   # data-centric: whole slices (rows) per warp, no fix-up
 
 
-def gemm_partitioned(desc: Desc, d_blob, X, Y, partition: int, bias=None, ws=None, stream=None) -> None:
-    """gqsa_gemm_partitioned: gemm_smallbatch with an explicit Stream-K / Slice-K partition."""
+class Options(ctypes.Structure):
+    _fields_ = [("partition", ctypes.c_int32), ("out_f16", ctypes.c_int32)]
+
+
+def gemm_ex(desc: Desc, d_blob, X, Y, partition: int = PARTITION_STREAM_K, bias=None, ws=None,
+            stream=None) -> None:
+    """gqsa_gemm_ex: explicit Stream-K / Slice-K partition; Y fp32 or fp16 (RNE)."""
+    import torch
     B = X.shape[0]
-    _check(lib().gqsa_gemm_partitioned(ctypes.byref(desc), d_blob.data_ptr(), X.data_ptr(), B,
-                                       X.stride(0), Y.data_ptr(), Y.stride(0),
-                                       bias.data_ptr() if bias is not None else None,
-                                       ws.data_ptr(), ws.numel(), int(partition), _stream_ptr(stream)),
-           "gqsa_gemm_partitioned")
+    opts = Options(int(partition), 1 if Y.dtype == torch.float16 else 0)
+    _check(lib().gqsa_gemm_ex(ctypes.byref(desc), d_blob.data_ptr(), X.data_ptr(), B, X.stride(0),
+                              Y.data_ptr(), Y.stride(0), bias.data_ptr() if bias is not None else None,
+                              ws.data_ptr(), ws.numel(), ctypes.byref(opts), _stream_ptr(stream)),
+           "gqsa_gemm_ex")
 
 
 def gemm_hostio(desc: Desc, d_blob, h_X, h_Y, stage, ws, bias=None, stream=None) -> None:
@@ -284,12 +290,13 @@ class Layer:
         gemv(self.desc, self.blob, x, y, bias, self.ws, stream)
         return y
 
-    def gemm(self, X, Y=None, bias=None, stream=None, partition: int = PARTITION_STREAM_K):
+    def gemm(self, X, Y=None, bias=None, stream=None, partition: int = PARTITION_STREAM_K,
+             out_dtype=None):
         import torch
         if Y is None:
-            Y = torch.empty(X.shape[0], self.rows, dtype=torch.float32, device=self.device)
-        if partition == PARTITION_STREAM_K:
+            Y = torch.empty(X.shape[0], self.rows, dtype=out_dtype or torch.float32, device=self.device)
+        if partition == PARTITION_STREAM_K and Y.dtype == torch.float32:
             gemm_smallbatch(self.desc, self.blob, X, Y, bias, self.ws, stream)
         else:
-            gemm_partitioned(self.desc, self.blob, X, Y, partition, bias, self.ws, stream)
+            gemm_ex(self.desc, self.blob, X, Y, partition, bias, self.ws, stream)
         return Y

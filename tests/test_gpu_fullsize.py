@@ -22,13 +22,13 @@ def _sample_rows(n, k, seed):
 
 
 @pytest.mark.parametrize("rows,cols", SHAPES_8B)
-@pytest.mark.parametrize("bits,sp", [(4, 0.5), (4, 0.3), (2, 0.5)])
+@pytest.mark.parametrize("bits,sp", [(4, 0.5), (4, 0.3), (2, 0.5), (8, 0.5)])
 def test_llama3_8b_shapes_sampled(rows, cols, bits, sp):
     name = f"llama3-8b/{rows}x{cols}/{bits}/{sp}/16/uniform"
     seed = synth.seed_for(name)
     bsr = synth.make_layer(seed, rows, cols, bits=bits, sparsity=sp)
     L = gqsa.Layer(bsr)
-    for B in (1, 8):
+    for B in (1, 3, 8):  # 4096x14336 at B = 8: two launches of 4
         x = synth.make_x(seed + 1, B, cols)
         X = torch.from_numpy(x).view(torch.float16).cuda()
         y = (L.gemv(X[0])[None] if B == 1 else L.gemm(X)).cpu().numpy()
@@ -55,3 +55,16 @@ def test_full_shape_exact_every_row():
     L = gqsa.Layer(bsr)
     y = L.gemv(torch.from_numpy(x).view(torch.float16).cuda()[0]).cpu().numpy()
     assert np.array_equal(y.astype(np.float64), O.gemv(bsr, x)[0])
+
+
+@pytest.mark.parametrize("mask", ["row_balanced", "skewed"])
+def test_slice_k_full_shape_sampled(mask):
+    """The data-centric partition at a LLaMA shape, in the sweep's launch configuration."""
+    name = f"llama3-8b/14336x4096/4/0.5/16/{mask}"
+    seed = synth.seed_for(name)
+    bsr = synth.make_layer(seed, 14336, 4096, bits=4, sparsity=0.5, mask=mask)
+    L = gqsa.Layer(bsr)
+    x = synth.make_x(seed + 1, 1, 4096)
+    y = L.gemm(torch.from_numpy(x).view(torch.float16).cuda(), partition=gqsa.PARTITION_SLICE_K).cpu().numpy()
+    rs = _sample_rows(14336, 192, seed)
+    check_gates(y[:, rs], O.gemv_rows(bsr, x, rs), abs_bound(bsr, x, rs), name + " slice-k")

@@ -134,8 +134,24 @@ def test_slice_k_realistic_and_deterministic(mask):
     assert np.array_equal(run(bsr, x, layer=L, partition=gqsa.PARTITION_SLICE_K), y)
     with pytest.raises(gqsa.GQSAError) as e:
         X = torch.zeros(1, 4096, dtype=torch.float16, device="cuda")
-        gqsa.gemm_partitioned(L.desc, L.blob, X, torch.empty(1, 4096, device="cuda"), 7, ws=L.ws)
+        gqsa.gemm_ex(L.desc, L.blob, X, torch.empty(1, 4096, device="cuda"), 7, ws=L.ws)
     assert e.value.status == -1
+
+
+@pytest.mark.parametrize("bits,B", [(4, 1), (2, 3), (8, 8)])
+def test_fp16_output_exact(bits, B):
+    """fp16 y (RNE of the fp32 result + bias): in exact-integer mode the fp32
+    value is exact, so y16 == fp16(oracle) bit for bit; empty rows get fp16(bias)."""
+    bsr = synth.make_layer(91 + bits, 700, 1024, bits=bits, sparsity=0.5, mask="skewed", mode="exact_int")
+    x = synth.make_x(92, B, 1024, mode="exact_int")
+    bias = (np.arange(700, dtype=np.float32) * 0.25 - 40.0).astype(np.float32)
+    L = gqsa.Layer(bsr)
+    X = torch.from_numpy(x).view(torch.float16).cuda()
+    for part in (gqsa.PARTITION_STREAM_K, gqsa.PARTITION_SLICE_K):
+        y = L.gemm(X, bias=torch.from_numpy(bias).cuda(), partition=part, out_dtype=torch.float16)
+        torch.cuda.synchronize()
+        ref = O.gemv(bsr, x, bias=bias).astype(np.float16)
+        assert np.array_equal(y.cpu().numpy().view(np.uint16), ref.view(np.uint16))
 
 
 def test_empty_layer_and_bias():

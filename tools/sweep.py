@@ -42,12 +42,12 @@ def measure(bsr, B, partition=gqsa.PARTITION_STREAM_K, reps=20):
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
         for i in range(R):
-            gqsa.gemm_partitioned(desc, blobs[i], X, Y, partition, ws=ws, stream=s)
+            gqsa.gemm_ex(desc, blobs[i], X, Y, partition, ws=ws, stream=s)
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=s):
         for i in range(R):
-            gqsa.gemm_partitioned(desc, blobs[i], X, Y, partition, ws=ws, stream=s)
+            gqsa.gemm_ex(desc, blobs[i], X, Y, partition, ws=ws, stream=s)
     g.replay()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
