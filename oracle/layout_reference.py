@@ -135,7 +135,7 @@ def pack_reference(bsr: dict, row_begin: int = 0, row_end=None) -> bytes:
         for tau in range(nt):
             base = off_tiles + t * tb
             flags = (1 if tau == 0 else 0) | (2 if tau == nt - 1 else 0)
-            struct.pack_into("<IIII", out, base, (s << 2) | flags, nt - 1 - tau, 0, 0)
+            struct.pack_into("<IIII", out, base, (s << 2) | flags, nt - 1 - tau, t - tau, 0)
             for u in range(SLOTS):
                 for lane in range(LANES):
                     g = deal.get((lane, tau * SLOTS + u))

@@ -75,12 +75,14 @@ int warps_per_cta(int bits, int B) {
 struct SmemPlan {
   bool coresident;
   int stages, warps, batch, launches;
-  size_t ring, total;
+  size_t ring, total, fix;
 };
 size_t x_bytes(int B, int cols) { return (size_t)B * cols * 2 + (size_t)B * pq_bytes_per_row(B, cols); }
 size_t ring_bytes_for(const gqsa_desc_t* d, int W, int ns) {  // ring + its mbarriers
   return (size_t)W * ns * tile_bytes(d->bits) + (size_t)W * kMaxStages * 8;
 }
+// intra-CTA fix-up records (batch <= 2; larger batches use the global workspace)
+size_t fix_bytes(int W, int B) { return B <= 2 ? (size_t)W * B * kLanes * kWsSlotBytes : 0; }
 constexpr size_t kMaxDynSmem = kSmemPerSm - 2048;  // per-CTA limit we request (227 KB - reserve)
 
 SmemPlan smem_plan(const gqsa_desc_t* d, int B) {
@@ -100,7 +102,10 @@ SmemPlan smem_plan(const gqsa_desc_t* d, int B) {
   Bc = Bb;
   sp.batch = Bc;
   const size_t tb = (size_t)tile_bytes(d->bits);
-  const size_t xb = x_bytes(Bc, d->cols);
+  // intra-CTA fix-up records, if they fit next to x and a minimal ring
+  size_t fb = fix_bytes(W, Bc);
+  if (x_bytes(Bc, d->cols) + fb + ring_bytes_for(d, W, kMinStages) > kMaxDynSmem) fb = 0;
+  const size_t xb = x_bytes(Bc, d->cols) + fb;  // x, column sums, fix-up records
   const size_t share = (size_t)kSmemPerSm / (ctas_per_sm_cap() * kCoResidentKernels);
   const size_t budget = share > 2048 ? share - 2048 : 0;  // reserved + static smem
   int ns = kMinStages;
@@ -115,6 +120,7 @@ SmemPlan smem_plan(const gqsa_desc_t* d, int B) {
   sp.stages = ns;
   sp.ring = (size_t)W * ns * tb;
   sp.total = xb + ring_bytes_for(d, W, ns);
+  sp.fix = fb;
   return sp;
 }
 
@@ -211,11 +217,20 @@ int launch_chunk(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_
   p.part_r = pl.active_warps ? desc->num_tiles % pl.active_warps : 0;
   p.stages = pl.stages;
   p.ring_offset = pl.smem_bytes - pl.ring_bytes - pl.warps_per_cta * kMaxStages * 8;
+  {
+    static const int fix_local = env_int("GQSA_FIX_LOCAL", 1, 0, 1);
+    const size_t fb = smem_plan(desc, Bc).fix;
+    p.fix_offset = (fb && fix_local) ? p.ring_offset - (int32_t)fb : 0;  // records sit before the ring
+  }
   p.trace = (g_trace && g_trace_bytes >= (size_t)pl.active_warps * 64) ? g_trace : nullptr;
   p.slice_k = o.partition == GQSA_PARTITION_SLICE_K ? 1 : 0;
   p.out_f16 = o.out_f16;
   static const int trigger = env_int("GQSA_PDL_TRIGGER", 0, 0, 2);
   p.pdl_trigger = trigger;
+  static const int xtma = env_int("GQSA_XTMA", 0, 0, 1);
+  p.x_tma = xtma;
+  static const int xrep = env_int("GQSA_XREP", 0, 0, 4096);
+  p.x_rep = xrep;
   if (desc->rows == 0) return GQSA_OK;
 
   cudaLaunchConfig_t cfg = {};

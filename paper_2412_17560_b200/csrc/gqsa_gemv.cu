@@ -299,12 +299,23 @@ __device__ __forceinline__ unsigned long long* ws_slot(const KParams& p, int w, 
   return reinterpret_cast<unsigned long long*>(p.ws) + ((int64_t)w * B + b) * kLanes + lane;
 }
 
+// Intra-CTA records live in shared memory: [W][B][32 lanes] 8-B slots at
+// `fx` (zeroed in the prologue), indexed by the warp's index in its CTA.
+__device__ __forceinline__ uint32_t fx_slot(uint32_t fx, int wl, int B, int b, int lane) {
+  return fx + (uint32_t)(((wl * B + b) * kLanes + lane) * 8);
+}
+
+// local: the owner of the slice is a warp of this CTA (shared-memory record)
 template <int B>
-__device__ __forceinline__ void publish(const KParams& p, int gw, const float (&v)[kMaxBatch], int lane) {
+__device__ __forceinline__ void publish(const KParams& p, int gw, const float (&v)[kMaxBatch], int lane,
+                                        bool local, uint32_t fx, int wl) {
 #pragma unroll
   for (int b = 0; b < B; ++b) {
     const unsigned long long w = (1ull << 32) | __float_as_uint(v[b]);
-    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(ws_slot<B>(p, gw, b, lane)), "l"(w) : "memory");
+    if (local)
+      asm volatile("st.volatile.shared.b64 [%0], %1;" ::"r"(fx_slot(fx, wl, B, b, lane)), "l"(w) : "memory");
+    else
+      asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(ws_slot<B>(p, gw, b, lane)), "l"(w) : "memory");
   }
 }
 
@@ -319,7 +330,21 @@ constexpr int kPre = 2;  // successor records an owner requests before its last 
 
 template <int B>
 __device__ __forceinline__ void collect(const KParams& p, int gw, int w_last, float (&v)[kMaxBatch],
-                                        int lane, unsigned long long (&pre)[kPre][kMaxBatch]) {
+                                        int lane, unsigned long long (&pre)[kPre][kMaxBatch], int wg0,
+                                        uint32_t fx, int cta_w0) {
+  // successors in this CTA (warps gw+1 .. wg0-1): shared-memory records
+  for (int w = gw + 1; w < wg0; ++w) {
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const uint32_t a = fx_slot(fx, w - cta_w0, B, b, lane);
+      unsigned long long s;
+      do {
+        asm volatile("ld.volatile.shared.b64 %0, [%1];" : "=l"(s) : "r"(a) : "memory");
+      } while ((s >> 32) == 0ull);
+      v[b] += __uint_as_float((uint32_t)s);
+    }
+  }
+  gw = wg0 - 1;  // the remaining successors (other CTAs) use global records
   // records requested early (during the owner's last tile): usually ready
 #pragma unroll
   for (int k = 0; k < kPre; ++k) {
@@ -411,6 +436,11 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(bar), "l"(pol)
       : "memory");
 }
+__device__ __forceinline__ void bulk_g2s_plain(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t done = 0;
   while (!done) {
@@ -493,17 +523,33 @@ __global__ void __launch_bounds__(max_threads_for(BITS, B), min_blocks_for(BITS,
       bulk_g2s(ring_s + slot * 2 * tb, tiles + (int64_t)t_first * tb, n * tb, bar0 + 8 * slot, pol);
     }
   };
+  // activation barrier: the last (unused) ring-barrier slot of warp 0
+  const uint32_t barx = (uint32_t)__cvta_generic_to_shared(
+      smem + p.ring_offset + (size_t)(nthreads >> 5) * NS * tb + (size_t)(kMaxStages - 1) * 8);
   if (lane == 0) {
     for (int s = 0; s < NP; ++s) mbar_init(bar0 + 8 * s, 1);
+    if (p.x_tma && threadIdx.x == 0) mbar_init(barx, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int s = 0; s < NP; ++s) fill_slot(s, t_begin + 2 * s);
   }
   __syncwarp();
+  if (p.x_tma) __syncthreads();  // barx initialised before anyone waits on it
   int row = -1;  // this lane's row in the first slice (the perm table is part of the blob)
-  uint32_t hdr0 = 0;
+  uint32_t hdr0 = 0, first0 = 0;
   if (t_end > t_begin) {
-    hdr0 = __ldg(reinterpret_cast<const uint32_t*>(tiles + (int64_t)t_begin * tb));
+    const uint4 h = __ldg(reinterpret_cast<const uint4*>(tiles + (int64_t)t_begin * tb));
+    hdr0 = h.x;
+    first0 = h.z;  // first tile of the slice the range starts in
     row = __ldg(p.perm + (int64_t)(hdr0 >> 2) * kLanes + lane);
+  }
+  // fix-up records of warps of the same CTA go through shared memory
+  const int W = nthreads >> 5;
+  const int cta_w0 = blockIdx.x * W;
+  const int cta_t0 = cta_w0 * p.part_q + min(cta_w0, p.part_r);  // the CTA's first tile
+  const uint32_t fx = p.fix_offset ? (uint32_t)__cvta_generic_to_shared(smem + p.fix_offset) : 0u;
+  if (fx) {
+    for (int i = threadIdx.x; i < W * B * kLanes; i += nthreads)
+      asm volatile("st.shared.b64 [%0], %1;" ::"r"(fx + 8u * i), "l"(0ull) : "memory");
   }
   trace_point(p, gw, lane, 0);
   if (p.pdl_trigger == 0) pdl_launch_dependents();
@@ -515,9 +561,41 @@ __global__ void __launch_bounds__(max_threads_for(BITS, B), min_blocks_for(BITS,
   //      compute the per-column-group sums X_{b,c} (fp32, fixed t order) from
   //      the same registers: one pass, one barrier.
   const int KG = p.cols / kGroup;
+  if (p.x_rep > 1) p.X += (int64_t)(blockIdx.x % p.x_rep) * B * p.ldx;  // experiment: replicated x
   uint8_t* xs = smem;
   uint8_t* pq = xs + (size_t)B * p.cols * 2;  // [B][K/16 * pq_per_group] float2 (P, Q)
-  {
+  if (p.x_tma) {
+    // x arrives by 1-D bulk copies (one request stream per CTA); the column
+    // sums are then computed from shared memory
+    if (threadIdx.x == 0) {
+      const uint32_t row_bytes = 2u * (uint32_t)p.cols;
+      mbar_expect_tx(barx, (uint32_t)B * row_bytes);
+      const uint32_t xs_s = (uint32_t)__cvta_generic_to_shared(xs);
+      for (int b = 0; b < B; ++b)
+        for (uint32_t off = 0; off < row_bytes; off += kBulkChunk)
+          bulk_g2s_plain(xs_s + b * row_bytes + off, reinterpret_cast<const uint8_t*>(p.X + (int64_t)b * p.ldx) + off,
+                         min(kBulkChunk, row_bytes - off), barx);
+    }
+    mbar_wait(barx, 0);
+    for (int i = threadIdx.x; i < B * KG; i += nthreads) {
+      const int b = i / KG, c = i - b * KG;
+      const uint4* src = reinterpret_cast<const uint4*>(xs + (size_t)b * p.cols * 2) + 2 * c;
+      const uint4 v0 = src[0], v1 = src[1];
+      const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+      const uint32_t one = 0x3C003C00u;
+      float ae = 0.f, ao = 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        ae = fhfma<0, 0>(w[e], one, ae);
+        ao = fhfma<1, 0>(w[e], one, ao);
+      }
+      const float2 v2 = make_float2(fmaf(1024.f, ae, 64.f * ao), ae + ao);
+      constexpr int PG = pq_per_group<B>();
+      float2* dst = reinterpret_cast<float2*>(pq) + ((size_t)b * KG + c) * PG;
+      dst[0] = v2;
+      if (PG == 2) dst[1] = v2;
+    }
+  } else {
     constexpr int U = 2;  // column groups per thread per round (2 x 32 B in flight)
     for (int i0 = threadIdx.x; i0 < B * KG; i0 += U * nthreads) {
       uint4 v[U][2];
@@ -590,20 +668,23 @@ __global__ void __launch_bounds__(max_threads_for(BITS, B), min_blocks_for(BITS,
   // Per-tile work once its registers are loaded: accumulate the lane's four
   // groups, close the slice at its LAST tile, and (at the warp's final tile,
   // when it owns a slice continuing downstream) request the fix-up records.
+  const bool local_owner = fx && (int)first0 >= cta_t0;  // owner of the opening slice is in this CTA
+  int wg0 = gw + 1;  // first successor with a global record
   auto consume = [&](const TileRegs<BITS>& tr, int t) {
     if (t == t_end - 1 && !(tr.hdr & kTileLast) && !foreign) {
       w_last = warp_of_tile(p, t_end - 1 + (int)tr.rem);
+      wg0 = fx ? max(gw + 1, min(w_last + 1, cta_w0 + W)) : gw + 1;
 #pragma unroll
       for (int k = 0; k < kPre; ++k)
 #pragma unroll
         for (int b = 0; b < B; ++b)
-          pre[k][b] = (gw + 1 + k <= w_last) ? ld_slot(ws_slot<B>(p, gw + 1 + k, b, lane)) : 0ull;
+          pre[k][b] = (wg0 + k <= w_last) ? ld_slot(ws_slot<B>(p, wg0 + k, b, lane)) : 0ull;
     }
 #pragma unroll
     for (int u = 0; u < kPerLane; ++u) group_accumulate<BITS, B>(p, tr, u, acc);
     last_hdr = tr.hdr;
     if (tr.hdr & kTileLast) {  // the slice ends in this tile: its rows are complete
-      if (foreign) publish<B>(p, gw, acc, lane);
+      if (foreign) publish<B>(p, gw, acc, lane, local_owner, fx, gw - cta_w0);
       else store_rows<B>(p, acc, row, lane);
 #pragma unroll
       for (int b = 0; b < B; ++b) acc[b] = 0.f;
@@ -641,10 +722,10 @@ __global__ void __launch_bounds__(max_threads_for(BITS, B), min_blocks_for(BITS,
   // ---- a slice left open at the end of the range continues downstream
   if (!(last_hdr & kTileLast)) {
     if (foreign) {  // the whole range lies inside a slice owned upstream
-      publish<B>(p, gw, acc, lane);
+      publish<B>(p, gw, acc, lane, local_owner, fx, gw - cta_w0);
       if (p.trace && lane == 0) p.trace[(int64_t)gw * 8 + 7] = 1;
     } else {  // owner: add the successors' partials, then store
-      collect<B>(p, gw, w_last, acc, lane, pre);
+      collect<B>(p, gw, w_last, acc, lane, pre, wg0, fx, cta_w0);
       store_rows<B>(p, acc, row, lane);
       if (p.trace && lane == 0) p.trace[(int64_t)gw * 8 + 7] = 100 + w_last - gw;
     }

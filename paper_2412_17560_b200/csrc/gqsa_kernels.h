@@ -20,8 +20,12 @@ constexpr int kCoResidentKernels = 2;    // leave room for the next PDL-launched
 // Launch bounds: 16+ warps at batch <= 2 (64 registers), 8 warps above.  W8
 // holds 64 code bytes per lane per tile: 8 warps, <= 128 registers (two CTAs
 // per SM, so the next PDL launch can be resident).
-constexpr int max_threads_for(int bits, int B) { return bits == 8 ? 256 : (B <= 2 ? kMaxThreads : 256); }
-constexpr int min_blocks_for(int bits, int B) { return (bits == 8 || B > 2) ? 2 : 1; }
+#ifndef GQSA_B12_THREADS
+#define GQSA_B12_THREADS kMaxThreads
+#define GQSA_B12_MINB 1
+#endif
+constexpr int max_threads_for(int bits, int B) { return bits == 8 ? 256 : (B <= 2 ? GQSA_B12_THREADS : 256); }
+constexpr int min_blocks_for(int bits, int B) { return (bits == 8 || B > 2) ? 2 : GQSA_B12_MINB; }
 constexpr int kMaxWarpsBound = 8192;     // workspace records (>= any grid we launch)
 constexpr int kWsSlotBytes = 8;          // fix-up slot {partial, flag} per (warp, batch, lane)
 constexpr int kSmemBudget = 200 * 1024;  // above this, x is gathered from L1/L2
@@ -44,6 +48,9 @@ struct KParams {
   int32_t out_f16;         // 1: Y is fp16 (RNE of the fp32 result)
   int32_t pdl_trigger;     // where the next kernel may launch: 0 before the PDL wait,
                            // 1 after activation staging, 2 after the first tile pair
+  int32_t x_tma;
+  int32_t x_rep;
+  int32_t fix_offset;      // shared-memory offset of the intra-CTA fix-up records (0: all global)           // experiment: x replicated x_rep times (B*ldx apart), CTA c reads copy c % x_rep           // 1: stage x with 1-D bulk copies (experiment)
 };
 
 const void* select_kernel(int bits, int B);

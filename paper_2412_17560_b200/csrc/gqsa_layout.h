@@ -27,7 +27,7 @@ constexpr int kTileGroups = 128;    // groups (incl. padding) per tile record
 constexpr int kLanes = 32;          // one warp consumes one tile, one lane per row
 constexpr int kPerLane = kTileGroups / kLanes;  // 4 slots per lane per tile
 constexpr int kHeaderBytes = 256;
-constexpr int kTileHeaderBytes = 32;  // u32 (slice<<2 | FIRST | LAST), tiles_to_slice_end; 0[6]
+constexpr int kTileHeaderBytes = 32;  // u32 (slice<<2 | FIRST | LAST), tiles_to_slice_end, slice_first_tile; 0[5]
 constexpr int kSectionAlign = 256;
 constexpr uint32_t kFlagTargetDeal = 4u;     // bank-aware dealing: lane l reads chunk f = 2c+swap,
                                              // f mod 16 == l mod 16 whenever the row allows
@@ -57,10 +57,10 @@ constexpr int kTargetSlots = 64;  // slots per lane of the longest slice (16 til
 // needs at most kTargetSlots slots per lane (short slices -> few warps per
 // slice -> short fix-up chains), and large enough that a layer with fewer
 // than 32 non-empty rows still fills the 32 lanes.
-inline int lanes_per_row_for(int n_nz, int64_t max_len) {
+inline int lanes_per_row_for(int n_nz, int64_t max_len, int target_slots = kTargetSlots) {
   if (n_nz <= 0) return 1;
   int s = 1;
-  while (s < kLanes && (max_len + s - 1) / s > kTargetSlots) s <<= 1;
+  while (s < kLanes && (max_len + s - 1) / s > target_slots) s <<= 1;
   int p = 1;
   while (p < n_nz && p < kLanes) p <<= 1;
   const int s_small = kLanes / p;

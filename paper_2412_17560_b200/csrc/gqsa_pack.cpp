@@ -16,6 +16,7 @@
 //     of its activation slice is read first, balancing shared-memory bank quads.
 // gqsa_unpack is the exact inverse (it re-sorts each row by column).
 #include <algorithm>
+#include <cstdlib>
 #include <cstddef>
 #include <cstring>
 #include <vector>
@@ -86,7 +87,11 @@ Slices make_slices(const gqsa_bsr_t* b, int32_t r0, int32_t r1) {
                    [&](int32_t a, int32_t c) { return s.count[a] > s.count[c]; });
   s.n_nz = (int32_t)s.order.size();
   s.n_empty = (int32_t)s.empty.size();
-  s.lanes_per_row = lanes_per_row_for(s.n_nz, s.n_nz ? s.count[s.order[0]] : 0);
+  static const int target = [] {
+    const char* e = std::getenv("GQSA_TARGET_SLOTS");  // experiment knob
+    return e && std::atoi(e) >= 4 ? std::atoi(e) : kTargetSlots;
+  }();
+  s.lanes_per_row = lanes_per_row_for(s.n_nz, s.n_nz ? s.count[s.order[0]] : 0, target);
   s.rows_per_slice = kLanes / s.lanes_per_row;
   s.num_slices = (s.n_nz + s.rows_per_slice - 1) / s.rows_per_slice;
   s.tile0.resize(s.num_slices + 1);
@@ -226,10 +231,11 @@ extern "C" int gqsa_pack(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_e
     for (int32_t tau = 0; tau < nt; ++tau) {
       const int32_t t = s.tile0[sl] + tau;
       uint8_t* tile = out + o.tiles + (uint64_t)t * tile_bytes(bits);
-      // word 0: slice << 2 | FIRST | LAST; word 1: tiles to the slice's last tile
+      // word 0: slice << 2 | FIRST | LAST; word 1: tiles to the slice's last
+      // tile; word 2: the slice's first tile
       const uint32_t hdr[4] = {((uint32_t)sl << 2) | (tau == 0 ? kTileFirst : 0u) |
                                    (tau == nt - 1 ? kTileLast : 0u),
-                               (uint32_t)(nt - 1 - tau), 0u, 0u};
+                               (uint32_t)(nt - 1 - tau), (uint32_t)s.tile0[sl], 0u};
       std::memcpy(tile, hdr, sizeof(hdr));
       for (int u = 0; u < kPerLane; ++u) {
         for (int l = 0; l < kLanes; ++l) {
@@ -310,13 +316,15 @@ extern "C" int gqsa_unpack(const void* blob, size_t blob_bytes, gqsa_bsr_t* out)
     bool swap;
   };
   std::vector<std::vector<G>> rows(d.rows);
-  int32_t slice = -1;
+  int32_t slice = -1, first = -1;
   for (int32_t t = 0; t < d.num_tiles; ++t) {
     const uint8_t* tile = b + d.off_tiles + (uint64_t)t * d.tile_bytes;
     uint32_t hdr[4];
     std::memcpy(hdr, tile, sizeof(hdr));
     if (hdr[0] & kTileFirst) ++slice;
     if ((int32_t)(hdr[0] >> 2) != slice || slice < 0) return GQSA_ERR_VALIDATION;
+    if (hdr[0] & kTileFirst) first = t;
+    if ((int32_t)hdr[2] != first || hdr[3] != 0u) return GQSA_ERR_VALIDATION;
     for (int u = 0; u < kPerLane; ++u) {
       for (int l = 0; l < kLanes; ++l) {
         const int32_t row = perm[(int64_t)slice * kLanes + l];

@@ -17,7 +17,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libgqsa.so")
+LIB_PATH = os.environ.get("GQSA_LIB_PATH") or os.path.join(_HERE, "lib", "libgqsa.so")
 
 GQSA_OK = 0
 _STATUS = {0: "ok", -1: "shape", -2: "validation", -3: "unsupported", -4: "buffer", -5: "cuda"}

@@ -37,19 +37,22 @@ def main():
     blobs = [torch.from_numpy(blob).cuda() for _ in range(R)]
     ws = torch.zeros(gqsa.workspace_size(desc, a.batch), dtype=torch.uint8, device="cuda")
     X = torch.from_numpy(x).view(torch.float16).cuda()
+    xrep = int(os.environ.get("GQSA_XREP", "0"))
+    if xrep > 1:  # experiment: the kernel reads copy (CTA % xrep) of x
+        X = X.repeat(xrep, 1).contiguous()
     Y = torch.empty(a.batch, a.rows, dtype=torch.float32, device="cuda")
     plan = gqsa.launch_plan(desc, a.batch)
     print(f"plan grid={plan.grid} active_warps={plan.active_warps} tiles={plan.num_tiles} "
           f"smem={plan.smem_bytes} stages={plan.stages} ctas/SM={plan.ctas_per_sm} R={R}", flush=True)
     for i in range(a.launches):
-        gqsa.gemm_smallbatch(desc, blobs[i % R], X, Y, None, ws)
+        gqsa.gemm_smallbatch(desc, blobs[i % R], X[:a.batch], Y, None, ws)
     torch.cuda.synchronize()
     if a.time:
         s = torch.cuda.Stream()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
             for i in range(R):
-                gqsa.gemm_smallbatch(desc, blobs[i % R], X, Y, None, ws)
+                gqsa.gemm_smallbatch(desc, blobs[i % R], X[:a.batch], Y, None, ws)
         g.replay()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
