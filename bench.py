@@ -252,7 +252,19 @@ def run_gpu(args):
         if world > 1:
             dist.all_gather_into_tensor(yfull[i], ys[i].view(-1))
 
+    # chain path: the step's GEMVs in one persistent launch,
+    # each item reading its x only after the previous items completed
+    # (wait_prev = 1: the same sequential semantics as one launch per GEMV)
+    use_chain = args.path == "chain" and world == 1 and B <= 2
+    chain_items = [[(packed[i][1], copies[r][i], xs[i], ys[i], None, 1) for i in range(len(layers))]
+                   for r in range(R)]
+    chain_ws = (torch.zeros(gqsa.chain_workspace_size(chain_items[0], B), dtype=torch.uint8, device=dev)
+                if use_chain else None)
+
     def step(r):
+        if use_chain:
+            gqsa.gemm_chain(chain_items[r], chain_ws)
+            return
         for i in range(len(layers)):
             launch(i, r)
 
@@ -413,16 +425,20 @@ def run_gpu(args):
                    "parallelism": f"rowshard{world}" if world > 1 else "single",
                    "l2": f"weights rotate over {R} device copies of the layer set "
                          f"({R * set_bytes / 2**20:.0f} MiB > 2x L2)",
-                   "timing": "CUDA graphs of gqsa_gemv launches (PDL), CUDA events on the launch stream"},
+                   "path": "gqsa_gemm_chain (one persistent launch per step, grid barrier between layers)"
+                           if use_chain else "one gqsa_gemv launch per layer (PDL)",
+                   "timing": "CUDA graphs of the step's launches (PDL between launches), CUDA events on the "
+                             "launch stream"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
                      "peak_source": peak_src, "frac_of_nominal_8tbs": round(achieved / NOMINAL_HBM_GBS, 4),
-                     "kernel": "gqsa::gqsa_streamk_kernel<4,1,true>",
+                     "kernel": f"gqsa::gqsa_chain_kernel<{bits},{B}>" if use_chain
+                               else f"gqsa::gqsa_streamk_kernel<{bits},{B}>",
                      "algorithmic_bytes_per_step": int(step_bytes)},
         "layers": layer_rows,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": 3 * args.steps,
+        "gpu_launches": (1 if use_chain else len(layers)) * args.steps,
         "clocks": sampler.summary(),
     }
     print(json.dumps(line), flush=True)
@@ -441,6 +457,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rotate", action="store_true")
+    ap.add_argument("--path", default="launches", choices=["chain", "launches"],
+                    help="chain: one gqsa_gemm_chain launch per step; launches: one gqsa_gemv per layer")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -176,6 +176,51 @@ int gqsa_gemm_ex(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_
                  size_t ws_bytes, const gqsa_options_t* opts, void* stream);
 
 /*
+ * gqsa_gemm_chain: a sequence of GEMVs (e.g. the linear layers of a decoder
+ * step) in ONE persistent launch, with the same results as calling
+ * gqsa_gemm_smallbatch on items[0], items[1], ... in order on `stream`.
+ *   items[j].desc / d_blob : the packed layer (all items: the same `bits`)
+ *   items[j].d_X           : device fp16 [B][ldx], ldx >= cols, ldx % 8 == 0
+ *   items[j].d_Y           : device fp32 [B][ldy], ldy >= rows (or fp16 when out_f16)
+ *   items[j].d_bias        : device fp32 [rows] or NULL
+ *   items[j].wait_prev     : 1 = item j may read an earlier item's output, so it
+ *                            reads X only after items 0..j-1 have completed
+ *                            (grid-wide barrier; sequential semantics); 0 = X
+ *                            and Y are independent of earlier items (no barrier)
+ *   items[j].out_f16       : 0 = fp32 Y, 1 = fp16 Y (RNE), e.g. the next item's X
+ *   n in [1, GQSA_MAX_CHAIN], B in {1, 2}, bits in {2, 4}.
+ * Each item computes exactly what the single-GEMV kernel computes (Eq. 3,
+ * PAPER.md:64-69, over the BSR of PAPER.md:95-101, Stream-K partition of
+ * PAPER.md:161); the fp32 summation order of a row may differ from the
+ * single-GEMV launch (different grid), and is fixed for a given chain and
+ * device (bit-identical reruns).  What the chain adds: the
+ * weight stream runs ahead across layer boundaries, so a layer boundary costs
+ * a barrier instead of a kernel launch and an idle memory system.
+ * All CTAs must be co-resident (one per SM; cooperative launch): returns
+ * GQSA_ERR_CUDA if the device cannot host the grid.
+ * Workspace: gqsa_chain_workspace_size bytes, zero-filled once at allocation
+ * (each launch returns it to zero); not shared with concurrent launches.
+ * Errors: GQSA_ERR_SHAPE (n, B, ld*), GQSA_ERR_UNSUPPORTED (mixed bits, bits
+ * 8, x of the widest item does not fit in shared memory), GQSA_ERR_BUFFER
+ * (null / misaligned pointers, small workspace), GQSA_ERR_VALIDATION (desc).
+ */
+#define GQSA_MAX_CHAIN 16
+typedef struct {
+  const gqsa_desc_t* desc;
+  const void* d_blob;
+  const uint16_t* d_X;
+  int64_t ldx;
+  void* d_Y;
+  int64_t ldy;
+  const float* d_bias;
+  int32_t wait_prev;
+  int32_t out_f16;
+} gqsa_chain_item_t;
+int gqsa_chain_workspace_size(const gqsa_chain_item_t* items, int32_t n, int32_t B, size_t* bytes);
+int gqsa_gemm_chain(const gqsa_chain_item_t* items, int32_t n, int32_t B, void* d_ws, size_t ws_bytes,
+                    void* stream);
+
+/*
  * gqsa_gemm_hostio: the end-to-end call with HOST activations and outputs.
  * Copies h_X (pinned or pageable host fp16 [B][cols], dense) into the
  * device staging area d_stage, runs gqsa_gemm_smallbatch, and copies Y back

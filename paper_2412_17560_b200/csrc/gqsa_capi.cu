@@ -225,7 +225,7 @@ int launch_chunk(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_
   p.trace = (g_trace && g_trace_bytes >= (size_t)pl.active_warps * 64) ? g_trace : nullptr;
   p.slice_k = o.partition == GQSA_PARTITION_SLICE_K ? 1 : 0;
   p.out_f16 = o.out_f16;
-  static const int trigger = env_int("GQSA_PDL_TRIGGER", 0, 0, 2);
+  static const int trigger = env_int("GQSA_PDL_TRIGGER", 0, 0, 4);
   p.pdl_trigger = trigger;
   static const int xtma = env_int("GQSA_XTMA", 0, 0, 1);
   p.x_tma = xtma;
@@ -337,6 +337,165 @@ extern "C" int gqsa_gemm_hostio(const gqsa_desc_t* desc, const void* d_blob, con
   if (st) return st;
   if (cudaMemcpyAsync(h_Y, dY, (size_t)B * desc->rows * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
     return GQSA_ERR_CUDA;
+  return GQSA_OK;
+}
+
+// ---------------------------------------------------------------- chain
+namespace {
+struct ChainPlan {
+  int grid, warps, stages, total_warps;
+  size_t smem, ring_offset, fix_offset, rec_bytes;  // rec_bytes: global fix-up records per item
+};
+
+int chain_check(const gqsa_chain_item_t* items, int n, int B) {
+  if (!items) return GQSA_ERR_BUFFER;
+  if (n < 1 || n > kMaxChain || B < 1 || B > 2) return GQSA_ERR_SHAPE;
+  for (int j = 0; j < n; ++j) {
+    const gqsa_desc_t* d = items[j].desc;
+    if (!d) return GQSA_ERR_BUFFER;
+    if (!desc_ok(d)) return GQSA_ERR_VALIDATION;
+    if (d->bits != items[0].desc->bits) return GQSA_ERR_UNSUPPORTED;
+  }
+  if (items[0].desc->bits == 8) return GQSA_ERR_UNSUPPORTED;
+  return GQSA_OK;
+}
+
+int chain_plan(const gqsa_chain_item_t* items, int n, int B, ChainPlan* cpl) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return GQSA_ERR_CUDA;
+  const int sms = device_sms(dev);
+  if (sms <= 0) return GQSA_ERR_CUDA;
+  static const int W = env_int("GQSA_CHAIN_WARPS", 16, 4, kChainThreads / 32);
+  // half = leave half the SM to the next launch (PDL overlap across launches)
+  static const int half = env_int("GQSA_CHAIN_HALF", 0, 0, 1);
+  const int bits = items[0].desc->bits;
+  size_t xb = 0;
+  for (int j = 0; j < n; ++j) {
+    const size_t v = x_bytes(B, items[j].desc->cols);
+    if (v > xb) xb = v;
+  }
+  xb = (xb + 127) / 128 * 128;
+  const size_t fb = fix_bytes(W, B);
+  const size_t budget = half ? (size_t)kSmemPerSm / 2 - 2048 : kMaxDynSmem;
+  const size_t bars = (size_t)W * kMaxStages * 8;
+  const size_t tb = (size_t)tile_bytes(bits);
+  if (xb + fb + bars + (size_t)W * kMinStages * tb > budget) return GQSA_ERR_UNSUPPORTED;
+  int ns = (int)((budget - xb - fb - bars) / ((size_t)W * tb));
+  if (ns > stages_cap()) ns = stages_cap();
+  ns &= ~1;
+  cpl->grid = sms;
+  cpl->warps = W;
+  cpl->stages = ns;
+  cpl->total_warps = sms * W;
+  cpl->fix_offset = xb;
+  cpl->ring_offset = xb + fb;
+  cpl->smem = xb + fb + (size_t)W * ns * tb + bars;
+  cpl->rec_bytes = ((size_t)cpl->total_warps * B * kLanes * kWsSlotBytes + 255) / 256 * 256;
+  return GQSA_OK;
+}
+}  // namespace
+
+extern "C" int gqsa_chain_workspace_size(const gqsa_chain_item_t* items, int32_t n, int32_t B,
+                                         size_t* bytes) {
+  if (!bytes) return GQSA_ERR_BUFFER;
+  int st = chain_check(items, n, B);
+  if (st) return st;
+  ChainPlan cpl;
+  st = chain_plan(items, n, B, &cpl);
+  if (st) return st;
+  *bytes = 256 + (size_t)n * cpl.rec_bytes;
+  return GQSA_OK;
+}
+
+extern "C" int gqsa_gemm_chain(const gqsa_chain_item_t* items, int32_t n, int32_t B, void* d_ws,
+                               size_t ws_bytes, void* stream) {
+  int st = chain_check(items, n, B);
+  if (st) return st;
+  if (!d_ws || !aligned(d_ws, 256)) return GQSA_ERR_BUFFER;
+  for (int j = 0; j < n; ++j) {
+    const gqsa_chain_item_t& it = items[j];
+    if (!it.d_blob || !it.d_X || !it.d_Y) return GQSA_ERR_BUFFER;
+    if (it.ldx < it.desc->cols || it.ldx % 8 || it.ldy < it.desc->rows) return GQSA_ERR_SHAPE;
+    if (it.wait_prev != 0 && it.wait_prev != 1) return GQSA_ERR_SHAPE;
+    if (it.out_f16 != 0 && it.out_f16 != 1) return GQSA_ERR_SHAPE;
+    if (!aligned(it.d_blob, 256) || !aligned(it.d_X, 16) || !aligned(it.d_Y, it.out_f16 ? 2 : 4) ||
+        (it.d_bias && !aligned(it.d_bias, 4)))
+      return GQSA_ERR_BUFFER;
+  }
+  ChainPlan cpl;
+  st = chain_plan(items, n, B, &cpl);
+  if (st) return st;
+  if (ws_bytes < 256 + (size_t)n * cpl.rec_bytes) return GQSA_ERR_BUFFER;
+  const void* fn = select_chain_kernel(items[0].desc->bits, B);
+  if (!fn) return GQSA_ERR_UNSUPPORTED;
+  {
+    static bool set[9][3] = {};
+    std::lock_guard<std::mutex> lk(g_mu);
+    bool& s = set[items[0].desc->bits][B];
+    if (!s) {
+      if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem) != cudaSuccess ||
+          cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared) != cudaSuccess)
+        return GQSA_ERR_CUDA;
+      s = true;
+    }
+  }
+  ChainParams cp;
+  std::memset(&cp, 0, sizeof(cp));
+  uint8_t* ws = static_cast<uint8_t*>(d_ws);
+  cp.counter = reinterpret_cast<uint32_t*>(ws);
+  for (int j = 0; j < n; ++j) {
+    const gqsa_chain_item_t& it = items[j];
+    const gqsa_desc_t* desc = it.desc;
+    const uint8_t* blob = static_cast<const uint8_t*>(it.d_blob);
+    KParams& p = cp.item[j];
+    p.tiles = blob + desc->off_tiles;
+    p.perm = reinterpret_cast<const int32_t*>(blob + desc->off_nzrow);
+    p.empty = reinterpret_cast<const int32_t*>(blob + desc->off_empty);
+    p.X = it.d_X;
+    p.Y = it.d_Y;
+    p.bias = it.d_bias;
+    p.ws = reinterpret_cast<uint32_t*>(ws + 256 + (size_t)j * cpl.rec_bytes);
+    p.ldx = it.ldx;
+    p.ldy = it.ldy;
+    p.rows = desc->rows;
+    p.cols = desc->cols;
+    p.num_tiles = desc->num_tiles;
+    p.n_empty = desc->n_empty;
+    p.active_warps = desc->num_tiles < cpl.total_warps ? desc->num_tiles : cpl.total_warps;
+    p.lanes_per_row = ((uint32_t)desc->flags >> kFlagLanesPerRowShift) & 0xff;
+    p.part_q = p.active_warps ? desc->num_tiles / p.active_warps : 0;
+    p.part_r = p.active_warps ? desc->num_tiles % p.active_warps : 0;
+    p.out_f16 = it.out_f16;
+    cp.wait_prev[j] = j == 0 ? 0 : it.wait_prev;
+  }
+  cp.n = n;
+  cp.stages = cpl.stages;
+  cp.ring_offset = (int32_t)cpl.ring_offset;
+  cp.fix_offset = (int32_t)cpl.fix_offset;
+  cp.total_warps = cpl.total_warps;
+  cp.trace = (g_trace && g_trace_bytes >= (size_t)cpl.total_warps * n * 32) ? g_trace : nullptr;
+
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 32 * cpl.warps, cpl.smem) != cudaSuccess)
+    return GQSA_ERR_CUDA;
+  if (occ < 1) return GQSA_ERR_UNSUPPORTED;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cpl.grid);
+  cfg.blockDim = dim3(32 * cpl.warps);
+  cfg.dynamicSmemBytes = cpl.smem;
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = 1;
+  cfg.attrs = attr;
+  static const int coop = env_int("GQSA_CHAIN_COOP", 1, 0, 1);
+  cfg.numAttrs = coop ? 2 : 1;
+  void* args[] = {&cp};
+  if (cudaLaunchKernelExC(&cfg, fn, args) != cudaSuccess) return GQSA_ERR_CUDA;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   return GQSA_OK;
 }
 

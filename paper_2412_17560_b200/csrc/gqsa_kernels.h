@@ -53,7 +53,25 @@ struct KParams {
   int32_t fix_offset;      // shared-memory offset of the intra-CTA fix-up records (0: all global)           // experiment: x replicated x_rep times (B*ldx apart), CTA c reads copy c % x_rep           // 1: stage x with 1-D bulk copies (experiment)
 };
 
+// Persistent chain kernel (gqsa_chain.cu): one launch runs up to kMaxChain
+// GEMVs in order, one CTA of kChainThreads per SM (cooperative launch).
+constexpr int kMaxChain = 16;
+constexpr int kChainThreads = 512;
+struct ChainParams {
+  KParams item[kMaxChain];        // per item: exactly the per-GEMV kernel's parameters
+  int32_t wait_prev[kMaxChain];   // 1: item j reads X only after items < j completed
+  int32_t n;                      // items
+  int32_t stages;                 // ring depth NS (tiles) per warp
+  int32_t ring_offset;            // shared-memory offset of the TMA ring
+  int32_t fix_offset;             // shared-memory offset of intra-CTA fix-up records (0: none)
+  int32_t total_warps;            // grid * warps per CTA (every warp arrives once per item)
+  uint32_t* counter;              // workspace: CTA arrivals (returned to 0 by the launch's last arrival)
+  uint64_t* trace;                // optional [total_warps][n][4] %globaltimer stamps (debug)
+};
+static_assert(sizeof(ChainParams) <= 4096, "kernel parameter space");
+
 const void* select_kernel(int bits, int B);
+const void* select_chain_kernel(int bits, int B);
 // Bytes of the column-sum table per batch row (see gqsa_gemv.cu pq_per_group).
 inline size_t pq_bytes_per_row(int B, int cols) { return (size_t)cols / 16 * (B <= 2 ? 2 : 1) * 8; }
 

@@ -65,10 +65,20 @@ class Plan(ctypes.Structure):
                  "stages", "ctas_per_sm", "ring_bytes", "batch_per_launch", "launches", "coresident")]
 
 
+class ChainItem(ctypes.Structure):
+    _fields_ = [
+        ("desc", ctypes.POINTER(Desc)), ("d_blob", ctypes.c_void_p),
+        ("d_X", ctypes.c_void_p), ("ldx", ctypes.c_int64),
+        ("d_Y", ctypes.c_void_p), ("ldy", ctypes.c_int64),
+        ("d_bias", ctypes.c_void_p), ("wait_prev", ctypes.c_int32),
+        ("out_f16", ctypes.c_int32),
+    ]
+
+
 EXPORTS = (
     "gqsa_pack_size", "gqsa_pack", "gqsa_read_desc", "gqsa_unpack", "gqsa_workspace_size",
     "gqsa_gemv", "gqsa_gemm_smallbatch", "gqsa_gemm_ex", "gqsa_hostio_stage_size",
-    "gqsa_gemm_hostio",
+    "gqsa_gemm_hostio", "gqsa_chain_workspace_size", "gqsa_gemm_chain",
     "gqsa_launch_plan", "gqsa_launch_count", "gqsa_status_string", "gqsa_version",
     "gqsa_debug_trace",
 )
@@ -97,6 +107,8 @@ def lib() -> ctypes.CDLL:
     L.gqsa_hostio_stage_size.argtypes = [ctypes.POINTER(Desc), I32, PSZ]
     L.gqsa_gemm_hostio.argtypes = [ctypes.POINTER(Desc), P, P, I32, P, P, P, SZ, P, SZ, P]
     L.gqsa_launch_plan.argtypes = [ctypes.POINTER(Desc), I32, ctypes.POINTER(Plan)]
+    L.gqsa_chain_workspace_size.argtypes = [ctypes.POINTER(ChainItem), I32, I32, PSZ]
+    L.gqsa_gemm_chain.argtypes = [ctypes.POINTER(ChainItem), I32, I32, P, SZ, P]
     L.gqsa_launch_count.restype = ctypes.c_uint64
     L.gqsa_debug_trace.argtypes = [P, SZ]
     L.gqsa_status_string.restype = ctypes.c_char_p
@@ -258,6 +270,40 @@ def gemm_hostio(desc: Desc, d_blob, h_X, h_Y, stage, ws, bias=None, stream=None)
                                   h_Y.data_ptr(), bias.data_ptr() if bias is not None else None,
                                   stage.data_ptr(), stage.numel(), ws.data_ptr(), ws.numel(),
                                   _stream_ptr(stream)), "gqsa_gemm_hostio")
+
+
+def _chain_items(items):
+    """items: sequence of (desc, d_blob, X [B][ldx] fp16, Y [B][ldy] fp32 or fp16, bias or None,
+    wait_prev)."""
+    import torch
+    arr = (ChainItem * len(items))()
+    keep = []
+    for j, (desc, d_blob, X, Y, bias, wait_prev) in enumerate(items):
+        keep.append(desc)
+        arr[j] = ChainItem(ctypes.pointer(desc), d_blob.data_ptr(), X.data_ptr(), X.stride(0),
+                           Y.data_ptr(), Y.stride(0), bias.data_ptr() if bias is not None else None,
+                           int(wait_prev), 1 if Y.dtype == torch.float16 else 0)
+    return arr, keep
+
+
+def chain_workspace_size(items, batch: int = 1) -> int:
+    arr, _keep = _chain_items(items)
+    n = ctypes.c_size_t(0)
+    _check(lib().gqsa_chain_workspace_size(arr, len(items), int(batch), ctypes.byref(n)),
+           "gqsa_chain_workspace_size")
+    return n.value
+
+
+def gemm_chain(items, ws, stream=None) -> None:
+    """gqsa_gemm_chain: the GEMVs of ``items`` in order, in one persistent launch.
+
+    items: sequence of (desc, d_blob, X fp16 [B][ldx], Y fp32 [B][ldy], bias or None,
+    wait_prev); ws: zero-initialised uint8 tensor of chain_workspace_size bytes.
+    """
+    arr, _keep = _chain_items(items)
+    B = items[0][2].shape[0]
+    _check(lib().gqsa_gemm_chain(arr, len(items), B, ws.data_ptr(), ws.numel(), _stream_ptr(stream)),
+           "gqsa_gemm_chain")
 
 
 class Layer:

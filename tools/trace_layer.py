@@ -106,6 +106,15 @@ def main():
     per_cta = np.array([np.median(per[:, sm == c]) for c in range(plan.grid)])
     print("per-CTA median µs/tile: min %.3f max %.3f (spread %.0f%%)" % (
         per_cta.min(), per_cta.max(), 100 * (per_cta.max() / per_cta.min() - 1)))
+    ex = T[1:, :, 5]  # exit times [launch][warp]
+    cta_max = np.stack([ex[:, sm == c].max(axis=1) for c in range(plan.grid)], axis=1)
+    cta_med = np.stack([np.median(ex[:, sm == c], axis=1) for c in range(plan.grid)], axis=1)
+    print("exit spread (µs, median over launches): within-CTA max-median %.2f; across CTAs "
+          "(CTA max) p10/p50/max - launch median %.2f/%.2f/%.2f" % (
+              np.median(cta_max - cta_med),
+              np.median(np.percentile(cta_max, 10, axis=1) - np.median(ex, axis=1)),
+              np.median(np.median(cta_max, axis=1) - np.median(ex, axis=1)),
+              np.median(cta_max.max(axis=1) - np.median(ex, axis=1))))
     prev_exit = T[:-1, :, 5].max(axis=1)
     rel = T[1:, :, 1].min(axis=1) - prev_exit
     print("PDL release after previous launch's last exit (µs):", " ".join(f"{r:.2f}" for r in rel[:5]))
