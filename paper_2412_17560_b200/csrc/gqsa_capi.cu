@@ -21,7 +21,7 @@ size_t g_trace_bytes = 0;
 
 struct DevInfo {
   int sms = 0;
-  bool attr_set[9][kMaxBatch + 1] = {};
+  bool attr_set[9][2 * (kMaxBatch + 1)] = {};
 };
 std::mutex g_mu;
 DevInfo g_dev[64];
@@ -61,9 +61,16 @@ int stages_cap() {
   return cap;
 }
 
-int warps_per_cta(int bits, int B) {
+// The FEW kernel variant (12 warps, <= 85 registers) for layers with few
+// tiles per warp; GQSA_FEW=0 disables it (experiments).
+bool few_for(const gqsa_desc_t* d, int B) {
+  static int on = env_int("GQSA_FEW", 1, 0, 1);
+  return on && B <= 2 && (d->bits == 4 || d->bits == 2) && d->num_tiles < kFewTiles;
+}
+int warps_per_cta(const gqsa_desc_t* d, int B) {
   static int w1 = env_int("GQSA_WARPS", 16, 1, kMaxWarps);
-  return bits == 8 ? 8 : (B <= 2 ? w1 : 8);  // <= max_threads_for(bits, B) / 32
+  if (few_for(d, B)) return kFewWarps;
+  return d->bits == 8 ? 8 : (B <= 2 ? w1 : 8);  // <= max_threads_for(bits, B) / 32
 }
 
 // Shared-memory plan per CTA of W warps: [x: B*K fp16][(P, Q) column sums]
@@ -89,16 +96,16 @@ SmemPlan smem_plan(const gqsa_desc_t* d, int B) {
   SmemPlan sp{};
   // largest batch chunk whose x fits next to a minimal ring (default warps,
   // else 8 warps); cols <= kMaxCols makes Bc = 1 always fit
-  int Bc = B, W = warps_per_cta(d->bits, B);
+  int Bc = B, W = warps_per_cta(d, B);
   for (;; --Bc) {
-    W = warps_per_cta(d->bits, Bc);
+    W = warps_per_cta(d, Bc);
     if (x_bytes(Bc, d->cols) + ring_bytes_for(d, W, kMinStages) <= kMaxDynSmem) break;
     if (W > 8 && x_bytes(Bc, d->cols) + ring_bytes_for(d, 8, kMinStages) <= kMaxDynSmem) { W = 8; break; }
     if (Bc == 1) break;
   }
   sp.launches = (B + Bc - 1) / Bc;
   const int Bb = (B + sp.launches - 1) / sp.launches;  // balanced chunks (<= Bc: fits)
-  if (Bb != Bc) W = warps_per_cta(d->bits, Bb) > W ? W : warps_per_cta(d->bits, Bb);
+  if (Bb != Bc) W = warps_per_cta(d, Bb) > W ? W : warps_per_cta(d, Bb);
   Bc = Bb;
   sp.batch = Bc;
   const size_t tb = (size_t)tile_bytes(d->bits);
@@ -132,11 +139,11 @@ int make_plan(const gqsa_desc_t* d, int B, gqsa_plan_t* pl, const void** kfn) {
   if (sms <= 0) return GQSA_ERR_CUDA;
   const SmemPlan sp = smem_plan(d, B);
   const size_t smem = sp.total;
-  const void* fn = select_kernel(d->bits, sp.batch);
+  const void* fn = select_kernel(d->bits, sp.batch, few_for(d, sp.batch));
   if (!fn) return GQSA_ERR_UNSUPPORTED;
   {
     std::lock_guard<std::mutex> lk(g_mu);
-    bool& set = g_dev[dev].attr_set[d->bits][sp.batch];
+    bool& set = g_dev[dev].attr_set[d->bits][sp.batch + (few_for(d, sp.batch) ? kMaxBatch + 1 : 0)];
     if (!set) {
       // maximum shared-memory carveout: two kernels' CTAs (this launch and
       // the next, PDL) must fit on one SM at the same time

@@ -24,8 +24,18 @@ constexpr int kCoResidentKernels = 2;    // leave room for the next PDL-launched
 #define GQSA_B12_THREADS kMaxThreads
 #define GQSA_B12_MINB 1
 #endif
-constexpr int max_threads_for(int bits, int B) { return bits == 8 ? 256 : (B <= 2 ? GQSA_B12_THREADS : 256); }
-constexpr int min_blocks_for(int bits, int B) { return (bits == 8 || B > 2) ? 2 : GQSA_B12_MINB; }
+// FEW: the variant for layers with few tiles per warp (small layers, e.g.
+// 4096x4096 at S50): 12 warps per CTA with up to 85 registers (two CTAs per
+// SM for PDL co-residency).  Measured (B200): 4096x4096 W4S50 B=1 5.13 ->
+// 4.47 us; no change on 14336x4096 / 4096x14336, which keep 16 warps.
+constexpr int kFewWarps = 12;
+constexpr int kFewTiles = 148 * 16 * 4;  // below ~4 tiles per warp of a 16-warp grid
+constexpr int max_threads_for(int bits, int B, bool few = false) {
+  return few ? 32 * kFewWarps : bits == 8 ? 256 : (B <= 2 ? GQSA_B12_THREADS : 256);
+}
+constexpr int min_blocks_for(int bits, int B, bool few = false) {
+  return few ? 2 : (bits == 8 || B > 2) ? 2 : GQSA_B12_MINB;
+}
 constexpr int kMaxWarpsBound = 8192;     // workspace records (>= any grid we launch)
 constexpr int kWsSlotBytes = 8;          // fix-up slot {partial, flag} per (warp, batch, lane)
 constexpr int kSmemBudget = 200 * 1024;  // above this, x is gathered from L1/L2
@@ -70,7 +80,7 @@ struct ChainParams {
 };
 static_assert(sizeof(ChainParams) <= 4096, "kernel parameter space");
 
-const void* select_kernel(int bits, int B);
+const void* select_kernel(int bits, int B, bool few);
 const void* select_chain_kernel(int bits, int B);
 // Bytes of the column-sum table per batch row (see gqsa_gemv.cu pq_per_group).
 inline size_t pq_bytes_per_row(int B, int cols) { return (size_t)cols / 16 * (B <= 2 ? 2 : 1) * 8; }

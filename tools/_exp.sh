@@ -1,3 +1,7 @@
 make -s >/dev/null 2>&1
-ncu --set full --import-source on --clock-control none -k regex:gqsa_streamk -s 6 -c 1 -o gpurun_out/l14336 python tools/prof_layer.py --rows 14336 --cols 4096 --launches 8 > gpurun_out/ncu.log 2>&1
-tail -3 gpurun_out/ncu.log
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
+for cfg in "GQSA_FEW=1" "GQSA_FEW=0"; do
+  env $cfg timeout 300 python bench.py --steps 5000 --warmup 100 --no-cpu-baseline --e2e-steps 10 2>gpurun_out/err.txt | python -c "
+import json,sys
+d=json.loads(sys.stdin.readline()); print('$cfg', d['value'], d['us_per_step'], [l['us'] for l in d['layers']])" || tail -5 gpurun_out/err.txt
+done
