@@ -113,7 +113,8 @@ SmemPlan smem_plan(const gqsa_desc_t* d, int B) {
   size_t fb = fix_bytes(W, Bc);
   if (x_bytes(Bc, d->cols) + fb + ring_bytes_for(d, W, kMinStages) > kMaxDynSmem) fb = 0;
   const size_t xb = x_bytes(Bc, d->cols) + fb;  // x, column sums, fix-up records
-  const size_t share = (size_t)kSmemPerSm / (ctas_per_sm_cap() * kCoResidentKernels);
+  static const int cores = env_int("GQSA_CORESIDENT", kCoResidentKernels, 1, 4);  // experiments
+  const size_t share = (size_t)kSmemPerSm / (ctas_per_sm_cap() * cores);
   const size_t budget = share > 2048 ? share - 2048 : 0;  // reserved + static smem
   int ns = kMinStages;
   sp.coresident = xb + ring_bytes_for(d, W, kMinStages) <= budget;
