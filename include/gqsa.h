@@ -82,6 +82,33 @@ typedef struct {
   const uint16_t* zeros_f16;
 } gqsa_bsr_t;
 
+/*
+ * Offline compression front-end (host; PAPER.md:74-93 [Eq. 4, §3.2, Fig. 3],
+ * 50-63 [Eq. 1-2]): dense W -> plain BSR of the kept, quantized groups.
+ *   W          : host fp32 [rows][cols] (row-major, nn.Linear layout), finite.
+ *   hinv_diag  : host fp64 [cols], diag(H^-1) of the layer's Hessian estimate
+ *                (finite, > 0); Eq. 4 saliency s = W^2 / hinv_diag^2.
+ *   sparsity   : S in [0, 1): exactly floor(S * rows*cols/G) groups (the
+ *                lowest mean saliency of the layer; ties -> lower (row, group)
+ *                index) are pruned.
+ *   bits       : 2, 4 or 8;  group_size: G (any divisor of cols; the packer
+ *                and kernels take G = 16).
+ *   out        : caller-allocated arrays: row_index int32[rows+1];
+ *                group_cols/scales_f16/zeros_f16 [nnzg]; codes
+ *                ceil(nnzg*G*bits/8) bytes, where nnzg = gqsa_compress_nnzg();
+ *                scalar fields are filled in.  Quantization per kept group by
+ *                Eq. 1-2 in fp64 (ties away from zero), s and z stored as
+ *                fp16 (round to nearest even); constant groups: DESIGN.md R9.
+ *   group_saliency : optional host fp64 [rows][cols/G] out (the group scores), or NULL.
+ * Deterministic (fixed fp64 evaluation order).  Errors: GQSA_ERR_SHAPE (dims,
+ * cols % G, S outside [0,1)), GQSA_ERR_UNSUPPORTED (bits, cols/G > 65536),
+ * GQSA_ERR_VALIDATION (non-finite W, hinv_diag <= 0 or non-finite, s or z
+ * not representable in fp16), GQSA_ERR_BUFFER (null pointers).
+ */
+int gqsa_compress_nnzg(int32_t rows, int32_t cols, int32_t group_size, double sparsity, int64_t* nnzg);
+int gqsa_compress(const float* W, int32_t rows, int32_t cols, int32_t group_size, int32_t bits,
+                  const double* hinv_diag, double sparsity, gqsa_bsr_t* out, double* group_saliency);
+
 /* Host copy of a packed blob's header (filled by gqsa_pack / gqsa_read_desc). */
 typedef struct {
   uint32_t magic, version;

@@ -125,8 +125,9 @@ def build_gqs(W, keep, G: int, bits: int) -> dict:
             z16.append(z)
             group_cols.append(g)
         row_index.append(len(group_cols))
-    sh = np.array(s16, dtype=np.float64).astype(np.float16)
-    zh = np.array(z16, dtype=np.float64).astype(np.float16)
+    with np.errstate(over="ignore"):
+        sh = np.array(s16, dtype=np.float64).astype(np.float16)
+        zh = np.array(z16, dtype=np.float64).astype(np.float16)
     if not (np.all(np.isfinite(sh)) and np.all(np.isfinite(zh)) and np.all(sh > 0)):
         raise ValueError("scale/zero not representable in fp16 (reading R8)")
     # low bits first: element e of the stream at bits [e*n, e*n+n)

@@ -79,6 +79,7 @@ EXPORTS = (
     "gqsa_pack_size", "gqsa_pack", "gqsa_read_desc", "gqsa_unpack", "gqsa_workspace_size",
     "gqsa_gemv", "gqsa_gemm_smallbatch", "gqsa_gemm_ex", "gqsa_hostio_stage_size",
     "gqsa_gemm_hostio", "gqsa_chain_workspace_size", "gqsa_gemm_chain",
+    "gqsa_compress_nnzg", "gqsa_compress",
     "gqsa_launch_plan", "gqsa_launch_count", "gqsa_status_string", "gqsa_version",
     "gqsa_debug_trace",
 )
@@ -107,6 +108,8 @@ def lib() -> ctypes.CDLL:
     L.gqsa_hostio_stage_size.argtypes = [ctypes.POINTER(Desc), I32, PSZ]
     L.gqsa_gemm_hostio.argtypes = [ctypes.POINTER(Desc), P, P, I32, P, P, P, SZ, P, SZ, P]
     L.gqsa_launch_plan.argtypes = [ctypes.POINTER(Desc), I32, ctypes.POINTER(Plan)]
+    L.gqsa_compress_nnzg.argtypes = [I32, I32, I32, ctypes.c_double, ctypes.POINTER(ctypes.c_int64)]
+    L.gqsa_compress.argtypes = [P, I32, I32, I32, I32, P, ctypes.c_double, ctypes.POINTER(BSR), P]
     L.gqsa_chain_workspace_size.argtypes = [ctypes.POINTER(ChainItem), I32, I32, PSZ]
     L.gqsa_gemm_chain.argtypes = [ctypes.POINTER(ChainItem), I32, I32, P, SZ, P]
     L.gqsa_launch_count.restype = ctypes.c_uint64

@@ -34,7 +34,8 @@ from typing import Optional
 
 import numpy as np
 
-__all__ = ["seed_for", "make_layer", "make_x", "pack_bits", "bsr_from_parts", "shard_rows"]
+__all__ = ["seed_for", "make_layer", "make_x", "pack_bits", "bsr_from_parts", "shard_rows",
+           "make_dense", "make_calib"]
 
 
 def seed_for(name: str) -> int:
@@ -170,6 +171,29 @@ def make_x(seed: int, batch: int, cols: int, mode: str = "realistic") -> np.ndar
     else:
         raise ValueError(f"unknown x mode {mode!r}")
     return x.astype(np.float16).view(np.uint16)
+
+
+def make_dense(seed: int, rows: int, cols: int) -> np.ndarray:
+    """A dense fp32 weight matrix [rows][cols] for the compression front-end:
+    W[r, :] ~ N(0, sigma_r^2), sigma_r = 0.02 * 10^U(-1,1) (per-row channel
+    imbalance), plus 0.1 % of input columns x4 (salient input
+    channels, the structure Fig. 1 shows)."""
+    rng = np.random.default_rng(seed)
+    sigma = 0.02 * 10.0 ** rng.uniform(-1.0, 1.0, size=rows)
+    W = rng.standard_normal((rows, cols)) * sigma[:, None]
+    ch = rng.choice(cols, size=max(1, cols // 1000), replace=False)
+    W[:, ch] *= 4.0
+    return W.astype(np.float32)
+
+
+def make_calib(seed: int, n: int, cols: int) -> np.ndarray:
+    """Calibration activations [n][cols] fp32: N(0,1) with 0.5 % of the
+    channels x20 (activation outliers, as make_x)."""
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((n, cols))
+    ch = rng.choice(cols, size=max(1, int(round(0.005 * cols))), replace=False)
+    X[:, ch] *= 20.0
+    return X.astype(np.float32)
 
 
 def shard_rows(rows: int, world: int, rank: int) -> tuple:
