@@ -62,31 +62,6 @@ constexpr uint32_t kBulkChunk = 32768u;     // bytes per 1-D bulk copy
 constexpr uint32_t kMagic1024 = 0x64006400u;   // half2(1024, 1024)
 constexpr uint32_t kNeg1024 = 0xE400E400u;     // half2(-1024, -1024)
 
-// Dot product of one word of eight 4-bit codes (elements j = 0..7 at bits
-// 4j..4j+3) with x[0..7] held as half2 (x0,x1) (x2,x3) (x4,x5) (x6,x7).
-// Every code becomes an exact fp16 integer; every product is exact in fp32.
-__device__ __forceinline__ float dot8_w4(uint32_t w, uint32_t x01, uint32_t x23, uint32_t x45,
-                                         uint32_t x67, float acc) {
-  const uint32_t kM1 = 0x000F000Fu, kM2 = 0x00F000F0u;
-  const uint32_t k116 = 0x2C002C00u;   // half2(1/16)
-  const uint32_t kN64 = 0xD400D400u;   // half2(-64)
-  const uint32_t w8 = w >> 8;
-  const uint32_t e04 = hadd2(lop3_and_or(w, kM1, kMagic1024), kNeg1024);          // (e0, e4)
-  const uint32_t e15 = hfma2(lop3_and_or(w, kM2, kMagic1024), k116, kN64);        // (e1, e5)
-  const uint32_t e26 = hadd2(lop3_and_or(w8, kM1, kMagic1024), kNeg1024);         // (e2, e6)
-  const uint32_t e37 = hfma2(lop3_and_or(w8, kM2, kMagic1024), k116, kN64);       // (e3, e7)
-  // products are exact; only the fp32 adds round
-  acc = fhfma<0, 0>(e04, x01, acc);
-  acc = fhfma<0, 1>(e15, x01, acc);
-  acc = fhfma<0, 0>(e26, x23, acc);
-  acc = fhfma<0, 1>(e37, x23, acc);
-  acc = fhfma<1, 0>(e04, x45, acc);
-  acc = fhfma<1, 1>(e15, x45, acc);
-  acc = fhfma<1, 0>(e26, x67, acc);
-  acc = fhfma<1, 1>(e37, x67, acc);
-  return acc;
-}
-
 // Raw (offset-carrying) dot of one word of eight 4-bit codes with x[0..7]:
 // de += sum_{j even} (1024 + e_j) x_j,  dd += sum_{j odd} (1024 + 16 e_j) x_j.
 // Each LOP3 makes two exact fp16 values; each product is exact in fp32.
@@ -118,39 +93,67 @@ __device__ __forceinline__ void dot4_w8_raw(uint32_t w, uint32_t x01, uint32_t x
   acc = fhfma<1, 1>(e13, x23, acc);
 }
 
-// Dot of one word of sixteen 2-bit codes (element j at bits 2j..2j+1) with
-// x[0..15] in eight half2 registers.  Masks pick elements (j, j+8).
-__device__ __forceinline__ float dot16_w2(uint32_t w, const uint32_t (&x)[8], float acc) {
+// Raw (offset-carrying) dot of one word of sixteen 2-bit codes with x[0..15]
+// (low 16-bit half <-> x chunk xa, high half <-> xb): element e lands in set
+// j = e mod 4 as the exact fp16 1024 + 4^j q_e (one LOP3 per pair, no
+// HADD2/HFMA2), and d[j] += sum_{e in set j} (1024 + 4^j q_e) x_e with exact
+// products.  The offsets are removed once per group with the set sums.
+__device__ __forceinline__ void dot16_w2_raw(uint32_t w, const uint4& xa, const uint4& xb, float& d0,
+                                             float& d1, float& d2, float& d3) {
   const uint32_t w8 = w >> 8;
-  // scale constants: 1/4, 1/16, 1/64 and offsets -256, -64, -16 (exact fp16)
-  const uint32_t k14 = 0x34003400u, kN256 = 0xDC00DC00u;
-  const uint32_t k116 = 0x2C002C00u, kN64 = 0xD400D400u;
-  const uint32_t k164 = 0x24002400u, kN16 = 0xCC00CC00u;
-  const uint32_t a0 = hadd2(lop3_and_or(w, 0x00030003u, kMagic1024), kNeg1024);     // (e0, e8)
-  const uint32_t a1 = hfma2(lop3_and_or(w, 0x000C000Cu, kMagic1024), k14, kN256);  // (e1, e9)
-  const uint32_t a2 = hfma2(lop3_and_or(w, 0x00300030u, kMagic1024), k116, kN64);  // (e2, e10)
-  const uint32_t a3 = hfma2(lop3_and_or(w, 0x00C000C0u, kMagic1024), k164, kN16);  // (e3, e11)
-  const uint32_t b0 = hadd2(lop3_and_or(w8, 0x00030003u, kMagic1024), kNeg1024);    // (e4, e12)
-  const uint32_t b1 = hfma2(lop3_and_or(w8, 0x000C000Cu, kMagic1024), k14, kN256); // (e5, e13)
-  const uint32_t b2 = hfma2(lop3_and_or(w8, 0x00300030u, kMagic1024), k116, kN64); // (e6, e14)
-  const uint32_t b3 = hfma2(lop3_and_or(w8, 0x00C000C0u, kMagic1024), k164, kN16); // (e7, e15)
-  acc = fhfma<0, 0>(a0, x[0], acc);
-  acc = fhfma<0, 1>(a1, x[0], acc);
-  acc = fhfma<0, 0>(a2, x[1], acc);
-  acc = fhfma<0, 1>(a3, x[1], acc);
-  acc = fhfma<0, 0>(b0, x[2], acc);
-  acc = fhfma<0, 1>(b1, x[2], acc);
-  acc = fhfma<0, 0>(b2, x[3], acc);
-  acc = fhfma<0, 1>(b3, x[3], acc);
-  acc = fhfma<1, 0>(a0, x[4], acc);
-  acc = fhfma<1, 1>(a1, x[4], acc);
-  acc = fhfma<1, 0>(a2, x[5], acc);
-  acc = fhfma<1, 1>(a3, x[5], acc);
-  acc = fhfma<1, 0>(b0, x[6], acc);
-  acc = fhfma<1, 1>(b1, x[6], acc);
-  acc = fhfma<1, 0>(b2, x[7], acc);
-  acc = fhfma<1, 1>(b3, x[7], acc);
-  return acc;
+  const uint32_t r0 = lop3_and_or(w, 0x00030003u, kMagic1024);   // (e0, e8)   x1
+  const uint32_t r1 = lop3_and_or(w, 0x000C000Cu, kMagic1024);   // (e1, e9)   x4
+  const uint32_t r2 = lop3_and_or(w, 0x00300030u, kMagic1024);   // (e2, e10)  x16
+  const uint32_t r3 = lop3_and_or(w, 0x00C000C0u, kMagic1024);   // (e3, e11)  x64
+  const uint32_t q0 = lop3_and_or(w8, 0x00030003u, kMagic1024);  // (e4, e12)
+  const uint32_t q1 = lop3_and_or(w8, 0x000C000Cu, kMagic1024);  // (e5, e13)
+  const uint32_t q2 = lop3_and_or(w8, 0x00300030u, kMagic1024);  // (e6, e14)
+  const uint32_t q3 = lop3_and_or(w8, 0x00C000C0u, kMagic1024);  // (e7, e15)
+  d0 = fhfma<0, 0>(r0, xa.x, d0);
+  d1 = fhfma<0, 1>(r1, xa.x, d1);
+  d2 = fhfma<0, 0>(r2, xa.y, d2);
+  d3 = fhfma<0, 1>(r3, xa.y, d3);
+  d0 = fhfma<0, 0>(q0, xa.z, d0);
+  d1 = fhfma<0, 1>(q1, xa.z, d1);
+  d2 = fhfma<0, 0>(q2, xa.w, d2);
+  d3 = fhfma<0, 1>(q3, xa.w, d3);
+  d0 = fhfma<1, 0>(r0, xb.x, d0);
+  d1 = fhfma<1, 1>(r1, xb.x, d1);
+  d2 = fhfma<1, 0>(r2, xb.y, d2);
+  d3 = fhfma<1, 1>(r3, xb.y, d3);
+  d0 = fhfma<1, 0>(q0, xb.z, d0);
+  d1 = fhfma<1, 1>(q1, xb.z, d1);
+  d2 = fhfma<1, 0>(q2, xb.w, d2);
+  d3 = fhfma<1, 1>(q3, xb.w, d3);
+}
+
+// Column-group sums of one group's 16 activations w[0..7] = (x0,x1) .. (x14,x15)
+// (t ascending within each sum): (P, Q) with Q = sum_t x_t and P the offset
+// the raw dot products carry: W4 / W8 P = 1024 X_even + 64 X_odd (W8 uses
+// only Q and the plain 1024 X = 1024 Q - ... see group_accumulate), W2
+// P = 1024 X_0 + 256 X_1 + 64 X_2 + 16 X_3 with X_j = sum_{t = j mod 4} x_t.
+template <int BITS>
+__device__ __forceinline__ float2 column_sums(const uint32_t (&w)[8]) {
+  const uint32_t one = 0x3C003C00u;  // half2(1, 1): x * 1 is exact, one FHFMA per element
+  if (BITS == 2) {
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      a0 = fhfma<0, 0>(w[2 * i], one, a0);
+      a1 = fhfma<1, 0>(w[2 * i], one, a1);
+      a2 = fhfma<0, 0>(w[2 * i + 1], one, a2);
+      a3 = fhfma<1, 0>(w[2 * i + 1], one, a3);
+    }
+    return make_float2(fmaf(1024.f, a0, fmaf(256.f, a1, fmaf(64.f, a2, 16.f * a3))), (a0 + a1) + (a2 + a3));
+  } else {
+    float ae = 0.f, ao = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {  // even t = 0, 2, .., 14 and odd t = 1, .., 15, in order
+      ae = fhfma<0, 0>(w[e], one, ae);
+      ao = fhfma<1, 0>(w[e], one, ao);
+    }
+    return make_float2(fmaf(1024.f, ae, 64.f * ao), ae + ao);
+  }
 }
 
 // ---------------------------------------------------------------- tile regs
@@ -260,10 +263,13 @@ __device__ __forceinline__ void group_accumulate(const KParams& p, const TileReg
       const float t = fmaf(-z, X.y, fmaf(dd, 0.0625f, de) - X.x);
       acc[b] = fmaf(s, t, acc[b]);
     } else {
-      // 16-bit half h of the word holds the elements of x chunk h
-      const uint32_t xr[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-      const float dot = dot16_w2(w.x, xr, 0.f);
-      acc[b] = fmaf(s, fmaf(-z, X.y, dot), acc[b]);
+      // Offset-folded W2 (as W4): sum_t (q_t - z) x_t =
+      //   D0 + D1/4 + D2/16 + D3/64 - (1024 X_0 + 256 X_1 + 64 X_2 + 16 X_3) - z X
+      float d0 = 0.f, d1 = 0.f, d2 = 0.f, d3 = 0.f;
+      dot16_w2_raw(w.x, xa, xb, d0, d1, d2, d3);
+      const float dsum = fmaf(d3, 0.015625f, fmaf(d2, 0.0625f, fmaf(d1, 0.25f, d0)));
+      const float t = fmaf(-z, X.y, dsum - X.x);
+      acc[b] = fmaf(s, t, acc[b]);
     }
   }
 }
@@ -460,7 +466,7 @@ __device__ __forceinline__ void read_tile(TileRegs<BITS>& r, const uint8_t* tile
 // COHERENT: x may have been written earlier in the SAME launch (chain
 // kernel), so it is read through L2 only (ld.global.cg), never through the
 // non-coherent L1/texture path.
-template <int B, bool COHERENT = false>
+template <int BITS, int B, bool COHERENT = false>
 __device__ __forceinline__ void stage_activations(const KParams& p, uint8_t* xs, uint8_t* pq, int KG,
                                                   int nthreads) {
   constexpr int U = 2;  // column groups per thread per round (2 x 32 B in flight)
@@ -488,16 +494,8 @@ __device__ __forceinline__ void stage_activations(const KParams& p, uint8_t* xs,
         }
         const uint32_t w[8] = {v[k][0].x, v[k][0].y, v[k][0].z, v[k][0].w,
                                v[k][1].x, v[k][1].y, v[k][1].z, v[k][1].w};
-        const uint32_t one = 0x3C003C00u;  // half2(1, 1): x * 1 is exact, one FHFMA per element
-        float ae = 0.f, ao = 0.f;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {  // even t = 0, 2, .., 14 and odd t = 1, .., 15, in order
-          ae = fhfma<0, 0>(w[e], one, ae);
-          ao = fhfma<1, 0>(w[e], one, ao);
-        }
-        // P = 1024 X_even + 64 X_odd, Q = X_even + X_odd; stored for both
-        // chunk orders (swap = 0, 1) of column group c
-        const float2 v2 = make_float2(fmaf(1024.f, ae, 64.f * ao), ae + ao);
+        // (P, Q) of column group c, stored for both chunk orders (swap = 0, 1)
+        const float2 v2 = column_sums<BITS>(w);
         constexpr int PG = pq_per_group<B>();
         float2* dst = reinterpret_cast<float2*>(pq) + ((size_t)b * KG + c) * PG;
         dst[0] = v2;

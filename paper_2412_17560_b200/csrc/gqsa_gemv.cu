@@ -137,21 +137,14 @@ __global__ void __launch_bounds__(max_threads_for(BITS, B, FEW), min_blocks_for(
       const uint4* src = reinterpret_cast<const uint4*>(xs + (size_t)b * p.cols * 2) + 2 * c;
       const uint4 v0 = src[0], v1 = src[1];
       const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-      const uint32_t one = 0x3C003C00u;
-      float ae = 0.f, ao = 0.f;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        ae = fhfma<0, 0>(w[e], one, ae);
-        ao = fhfma<1, 0>(w[e], one, ao);
-      }
-      const float2 v2 = make_float2(fmaf(1024.f, ae, 64.f * ao), ae + ao);
+      const float2 v2 = column_sums<BITS>(w);
       constexpr int PG = pq_per_group<B>();
       float2* dst = reinterpret_cast<float2*>(pq) + ((size_t)b * KG + c) * PG;
       dst[0] = v2;
       if (PG == 2) dst[1] = v2;
     }
   } else {
-    stage_activations<B>(p, xs, pq, KG, nthreads);
+    stage_activations<BITS, B>(p, xs, pq, KG, nthreads);
   }
   trace_point(p, gw, lane, 6);
   __syncthreads();

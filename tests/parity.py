@@ -4,10 +4,27 @@ import numpy as np
 from oracle import gqsa_oracle as O
 
 
+# Offset each element carries through the kernel's folded dot products before
+# it is removed once per group (DESIGN.md §6 step 4, §7): W4 even t 1024, odd
+# t 1024/16; W2 t mod 4 = j: 1024/4^j; W8 1024.
+def _fold_offsets(bits: int, G: int) -> np.ndarray:
+    t = np.arange(G)
+    if bits == 4:
+        return np.where(t % 2 == 0, 1024.0, 64.0)
+    if bits == 2:
+        return 1024.0 / 4.0 ** (t % 4)
+    return np.full(G, 1024.0)
+
+
+FOLD_REL = 2.0 ** -23 / 1e-5  # fold error: 2 roundings (2^-24) of o_t|x_t| per group, in G2 units
+
+
 def abs_bound(bsr: dict, x_bits: np.ndarray, rows=None) -> np.ndarray:
-    """A_r = sum_g |s_g| (sum_t |q_t x_t| + |z_g| sum_t |x_t|) per row (and
-    batch): the magnitude the fp32 kernel's rounding errors scale with
-    (DESIGN.md §7).  Returns [B][len(rows)]."""
+    """G2's scale per row (and batch): A_r + FOLD_REL * F_r with
+    A_r = sum_g |s_g| (sum_t |q_t x_t| + |z_g| sum_t |x_t|), the magnitude of
+    the terms the fp32 kernel adds, and F_r = sum_g |s_g| sum_t o_t |x_t|, the
+    magnitude of the fold offsets o_t it carries and removes once per group
+    (so |dy_r| <= 1e-5 A_r + 2^-23 F_r).  Returns [B][len(rows)]."""
     G, n = int(bsr["group_size"]), int(bsr["bits"])
     X = np.asarray(x_bits).view(np.float16).astype(np.float64)
     if X.ndim == 1:
@@ -19,6 +36,7 @@ def abs_bound(bsr: dict, x_bits: np.ndarray, rows=None) -> np.ndarray:
     rows = np.arange(int(bsr["rows"])) if rows is None else np.asarray(rows)
     out = np.zeros((X.shape[0], rows.size))
     t = np.arange(G)
+    off = _fold_offsets(n, G)
     codes = np.asarray(bsr["codes"], np.uint8)
     for j, r in enumerate(rows):
         g0, g1 = int(ri[r]), int(ri[r + 1])
@@ -31,6 +49,7 @@ def abs_bound(bsr: dict, x_bits: np.ndarray, rows=None) -> np.ndarray:
         for b in range(X.shape[0]):
             ax = np.abs(X[b][idx])
             out[b, j] = np.sum(s[g0:g1] * ((q * ax).sum(1) + z[g0:g1] * ax.sum(1)))
+            out[b, j] += FOLD_REL * np.sum(s[g0:g1] * (ax * off).sum(1))
     return out
 
 
