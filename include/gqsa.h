@@ -260,6 +260,25 @@ int gqsa_gemm_hostio(const gqsa_desc_t* desc, const void* d_blob, const uint16_t
                      float* h_Y, const float* d_bias, void* d_stage, size_t stage_bytes,
                      void* d_ws, size_t ws_bytes, void* stream);
 
+/*
+ * gqsa_gemm_multi_hostio: n INDEPENDENT layers with host I/O in one call --
+ * the end-to-end path of a decode step whose activations live on the host:
+ * ONE host->device copy of all inputs, one gqsa_gemm_smallbatch launch per
+ * layer (PDL-chained on `stream`), ONE device->host copy of all outputs.
+ *   descs[j], d_blobs[j], d_ws[j], ws_bytes[j] : layer j (as gqsa_gemm_smallbatch)
+ *   h_X : host fp16, the concatenation of the n inputs [B][cols_j] (dense,
+ *         layer 0 first); pinned memory makes the copy asynchronous
+ *   h_Y : host fp32, the concatenation of the n outputs [B][rows_j]
+ *   d_stage : device buffer of gqsa_multi_hostio_stage_size bytes (256-B aligned)
+ * Returns after enqueueing; synchronize `stream` before reading h_Y.  Each
+ * layer reads only its own input segment (no dependency between layers).
+ * Errors as gqsa_gemm_smallbatch, plus GQSA_ERR_SHAPE for n < 1.
+ */
+int gqsa_multi_hostio_stage_size(const gqsa_desc_t* const* descs, int32_t n, int32_t B, size_t* bytes);
+int gqsa_gemm_multi_hostio(const gqsa_desc_t* const* descs, const void* const* d_blobs, int32_t n, int32_t B,
+                           const uint16_t* h_X, float* h_Y, void* d_stage, size_t stage_bytes,
+                           void* const* d_ws, const size_t* ws_bytes, void* stream);
+
 /* Launch plan the next gemv/gemm call will use on the current device (for
  * a split batch: the plan of its first launch):
  * CTAs, warps per CTA, active warps (Stream-K units), tiles.  For tooling. */

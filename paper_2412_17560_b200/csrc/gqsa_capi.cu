@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "../../include/gqsa.h"
 #include "gqsa_kernels.h"
@@ -132,6 +133,29 @@ SmemPlan smem_plan(const gqsa_desc_t* d, int B) {
   return sp;
 }
 
+// Resident CTAs per SM for (kernel, block, dynamic smem), memoised: the
+// occupancy query costs microseconds of host time per launch otherwise.
+bool cached_occupancy(int dev, const void* fn, int threads, size_t smem, int* occ) {
+  struct Key {
+    int dev;
+    const void* fn;
+    int threads;
+    size_t smem;
+  };
+  static std::vector<std::pair<Key, int>> cache;
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (const auto& e : cache)
+    if (e.first.dev == dev && e.first.fn == fn && e.first.threads == threads && e.first.smem == smem) {
+      *occ = e.second;
+      return true;
+    }
+  int v = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, fn, threads, smem) != cudaSuccess) return false;
+  if (cache.size() < 4096) cache.push_back({Key{dev, fn, threads, smem}, v});
+  *occ = v;
+  return true;
+}
+
 // Fill the launch plan of the first (or only) batch chunk; returns a status.
 int make_plan(const gqsa_desc_t* d, int B, gqsa_plan_t* pl, const void** kfn) {
   int dev = 0;
@@ -158,8 +182,7 @@ int make_plan(const gqsa_desc_t* d, int B, gqsa_plan_t* pl, const void** kfn) {
   }
   const int W = sp.warps, threads = 32 * sp.warps;
   int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem) != cudaSuccess)
-    return GQSA_ERR_CUDA;
+  if (!cached_occupancy(dev, fn, threads, smem, &occ)) return GQSA_ERR_CUDA;
   if (occ < 1) return GQSA_ERR_UNSUPPORTED;
   // the next launch on the stream (same configuration) can be resident
   // during this one's tail only if two CTAs fit (shared memory AND registers)
@@ -196,13 +219,19 @@ inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintp
 
 namespace {
 // One launch over Bc batch columns (x of Bc columns fits in shared memory).
+// `plan0`/`fn0`: the caller's plan when it was made for exactly Bc columns.
 int launch_chunk(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_X, int Bc, int64_t ldx,
                  void* d_Y, int64_t ldy, const float* d_bias, void* d_ws, const gqsa_options_t& o,
-                 void* stream) {
+                 void* stream, const gqsa_plan_t* plan0 = nullptr, const void* fn0 = nullptr) {
   gqsa_plan_t pl;
   const void* fn = nullptr;
-  int st = make_plan(desc, Bc, &pl, &fn);
-  if (st) return st;
+  if (plan0 && fn0 && plan0->launches == 1 && plan0->batch_per_launch == Bc) {
+    pl = *plan0;
+    fn = fn0;
+  } else {
+    int st = make_plan(desc, Bc, &pl, &fn);
+    if (st) return st;
+  }
   if (pl.batch_per_launch != Bc) return GQSA_ERR_UNSUPPORTED;  // unreachable: chunks always fit
   const uint8_t* blob = static_cast<const uint8_t*>(d_blob);
   KParams p;
@@ -292,12 +321,14 @@ extern "C" int gqsa_gemm_ex(const gqsa_desc_t* desc, const void* d_blob, const u
   if (ws_bytes < need) return GQSA_ERR_BUFFER;
 
   gqsa_plan_t pl0;
-  int st = make_plan(desc, B, &pl0, nullptr);
+  const void* fn0 = nullptr;
+  int st = make_plan(desc, B, &pl0, &fn0);
   if (st) return st;
   for (int b0 = 0; b0 < B; b0 += pl0.batch_per_launch) {  // batch chunks whose x fits in smem
     const int Bc = B - b0 < pl0.batch_per_launch ? B - b0 : pl0.batch_per_launch;
     void* y0 = static_cast<uint8_t*>(d_Y) + (size_t)b0 * ldy * (o.out_f16 ? 2 : 4);
-    st = launch_chunk(desc, d_blob, d_X + (int64_t)b0 * ldx, Bc, ldx, y0, ldy, d_bias, d_ws, o, stream);
+    st = launch_chunk(desc, d_blob, d_X + (int64_t)b0 * ldx, Bc, ldx, y0, ldy, d_bias, d_ws, o, stream, &pl0,
+                      fn0);
     if (st) return st;
   }
   return GQSA_OK;
@@ -504,6 +535,65 @@ extern "C" int gqsa_gemm_chain(const gqsa_chain_item_t* items, int32_t n, int32_
   void* args[] = {&cp};
   if (cudaLaunchKernelExC(&cfg, fn, args) != cudaSuccess) return GQSA_ERR_CUDA;
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  return GQSA_OK;
+}
+
+// Stage layout: [x_0 .. x_{n-1}: B*cols_j fp16 each, 16-B aligned][y_0 .. y_{n-1}: B*rows_j fp32]
+namespace {
+int multi_layout(const gqsa_desc_t* const* descs, int n, int B, size_t* x_off, size_t* y_off,
+                 size_t* x_bytes_total, size_t* y_bytes_total) {
+  if (!descs) return GQSA_ERR_BUFFER;
+  if (n < 1 || B < 1 || B > kMaxBatch) return GQSA_ERR_SHAPE;
+  size_t xo = 0;
+  for (int j = 0; j < n; ++j) {
+    if (!descs[j]) return GQSA_ERR_BUFFER;
+    if (!desc_ok(descs[j])) return GQSA_ERR_VALIDATION;
+    if (x_off) x_off[j] = xo;
+    xo += (size_t)B * descs[j]->cols * 2;  // cols % 16 == 0: segments stay 32-B aligned
+  }
+  const size_t y0 = (xo + 255) / 256 * 256;
+  size_t yo = y0;
+  for (int j = 0; j < n; ++j) {
+    if (y_off) y_off[j] = yo;
+    yo += (size_t)B * descs[j]->rows * 4;
+  }
+  if (x_bytes_total) *x_bytes_total = xo;
+  if (y_bytes_total) *y_bytes_total = yo - y0;
+  return GQSA_OK;
+}
+}  // namespace
+
+extern "C" int gqsa_multi_hostio_stage_size(const gqsa_desc_t* const* descs, int32_t n, int32_t B, size_t* bytes) {
+  if (!bytes) return GQSA_ERR_BUFFER;
+  size_t xt = 0, yt = 0;
+  const int st = multi_layout(descs, n, B, nullptr, nullptr, &xt, &yt);
+  if (st) return st;
+  *bytes = (xt + 255) / 256 * 256 + yt;
+  return GQSA_OK;
+}
+
+extern "C" int gqsa_gemm_multi_hostio(const gqsa_desc_t* const* descs, const void* const* d_blobs, int32_t n,
+                                      int32_t B, const uint16_t* h_X, float* h_Y, void* d_stage,
+                                      size_t stage_bytes, void* const* d_ws, const size_t* ws_bytes,
+                                      void* stream) {
+  if (!d_blobs || !h_X || !h_Y || !d_stage || !d_ws || !ws_bytes) return GQSA_ERR_BUFFER;
+  if (n > 4096) return GQSA_ERR_SHAPE;
+  std::vector<size_t> xo((size_t)(n > 0 ? n : 1)), yo((size_t)(n > 0 ? n : 1));
+  size_t xt = 0, yt = 0;
+  int st = multi_layout(descs, n, B, xo.data(), yo.data(), &xt, &yt);
+  if (st) return st;
+  if (stage_bytes < (xt + 255) / 256 * 256 + yt || !aligned(d_stage, 256)) return GQSA_ERR_BUFFER;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint8_t* stage = static_cast<uint8_t*>(d_stage);
+  if (cudaMemcpyAsync(stage, h_X, xt, cudaMemcpyHostToDevice, s) != cudaSuccess) return GQSA_ERR_CUDA;
+  for (int j = 0; j < n; ++j) {
+    const gqsa_desc_t* d = descs[j];
+    st = gqsa_gemm_smallbatch(d, d_blobs[j], reinterpret_cast<const uint16_t*>(stage + xo[j]), B, d->cols,
+                              reinterpret_cast<float*>(stage + yo[j]), d->rows, nullptr, d_ws[j], ws_bytes[j],
+                              stream);
+    if (st) return st;
+  }
+  if (cudaMemcpyAsync(h_Y, stage + yo[0], yt, cudaMemcpyDeviceToHost, s) != cudaSuccess) return GQSA_ERR_CUDA;
   return GQSA_OK;
 }
 

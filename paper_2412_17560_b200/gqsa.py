@@ -79,7 +79,7 @@ EXPORTS = (
     "gqsa_pack_size", "gqsa_pack", "gqsa_read_desc", "gqsa_unpack", "gqsa_workspace_size",
     "gqsa_gemv", "gqsa_gemm_smallbatch", "gqsa_gemm_ex", "gqsa_hostio_stage_size",
     "gqsa_gemm_hostio", "gqsa_chain_workspace_size", "gqsa_gemm_chain",
-    "gqsa_compress_nnzg", "gqsa_compress",
+    "gqsa_compress_nnzg", "gqsa_compress", "gqsa_multi_hostio_stage_size", "gqsa_gemm_multi_hostio",
     "gqsa_launch_plan", "gqsa_launch_count", "gqsa_status_string", "gqsa_version",
     "gqsa_debug_trace",
 )
@@ -108,6 +108,10 @@ def lib() -> ctypes.CDLL:
     L.gqsa_hostio_stage_size.argtypes = [ctypes.POINTER(Desc), I32, PSZ]
     L.gqsa_gemm_hostio.argtypes = [ctypes.POINTER(Desc), P, P, I32, P, P, P, SZ, P, SZ, P]
     L.gqsa_launch_plan.argtypes = [ctypes.POINTER(Desc), I32, ctypes.POINTER(Plan)]
+    PDESC = ctypes.POINTER(ctypes.POINTER(Desc))
+    L.gqsa_multi_hostio_stage_size.argtypes = [PDESC, I32, I32, PSZ]
+    L.gqsa_gemm_multi_hostio.argtypes = [PDESC, ctypes.POINTER(P), I32, I32, P, P, P, SZ, ctypes.POINTER(P),
+                                         ctypes.POINTER(SZ), P]
     L.gqsa_compress_nnzg.argtypes = [I32, I32, I32, ctypes.c_double, ctypes.POINTER(ctypes.c_int64)]
     L.gqsa_compress.argtypes = [P, I32, I32, I32, I32, P, ctypes.c_double, ctypes.POINTER(BSR), P]
     L.gqsa_chain_workspace_size.argtypes = [ctypes.POINTER(ChainItem), I32, I32, PSZ]
@@ -225,8 +229,12 @@ def debug_trace(buf=None) -> None:
 
 def _stream_ptr(stream) -> int:
     import torch
-    s = torch.cuda.current_stream() if stream is None else stream
-    return int(s.cuda_stream)
+    if stream is not None:
+        return int(stream.cuda_stream)
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)  # ~10x cheaper than current_stream()
+    if raw is not None:
+        return int(raw(torch.cuda.current_device()))
+    return int(torch.cuda.current_stream().cuda_stream)
 
 
 def gemv(desc: Desc, d_blob, x, y, bias=None, ws=None, stream=None) -> None:
@@ -307,6 +315,43 @@ def gemm_chain(items, ws, stream=None) -> None:
     B = items[0][2].shape[0]
     _check(lib().gqsa_gemm_chain(arr, len(items), B, ws.data_ptr(), ws.numel(), _stream_ptr(stream)),
            "gqsa_gemm_chain")
+
+
+def _desc_array(descs):
+    arr = (ctypes.POINTER(Desc) * len(descs))()
+    for j, d in enumerate(descs):
+        arr[j] = ctypes.pointer(d)
+    return arr
+
+
+def multi_hostio_stage_size(descs, batch: int = 1) -> int:
+    n = ctypes.c_size_t(0)
+    _check(lib().gqsa_multi_hostio_stage_size(_desc_array(descs), len(descs), int(batch), ctypes.byref(n)),
+           "gqsa_multi_hostio_stage_size")
+    return n.value
+
+
+class MultiHostIO:
+    """A prepared gqsa_gemm_multi_hostio call (argument arrays built once):
+    n independent layers, host (pinned) fp16 inputs concatenated in h_X, fp32
+    outputs concatenated into h_Y; one copy each way per call."""
+
+    def __init__(self, descs, d_blobs, h_X, h_Y, stage, ws_list, batch: int = 1):
+        n = len(descs)
+        self._keep = (descs, d_blobs, h_X, h_Y, stage, ws_list)
+        self._args = (_desc_array(descs), (ctypes.c_void_p * n)(*[b.data_ptr() for b in d_blobs]), n, int(batch),
+                      h_X.data_ptr(), h_Y.data_ptr(), stage.data_ptr(), stage.numel(),
+                      (ctypes.c_void_p * n)(*[w.data_ptr() for w in ws_list]),
+                      (ctypes.c_size_t * n)(*[w.numel() for w in ws_list]))
+        self._fn = lib().gqsa_gemm_multi_hostio
+
+    def __call__(self, stream=None) -> None:
+        _check(self._fn(*self._args, _stream_ptr(stream)), "gqsa_gemm_multi_hostio")
+
+
+def gemm_multi_hostio(descs, d_blobs, h_X, h_Y, stage, ws_list, batch: int = 1, stream=None) -> None:
+    """gqsa_gemm_multi_hostio (one-shot form of :class:`MultiHostIO`)."""
+    MultiHostIO(descs, d_blobs, h_X, h_Y, stage, ws_list, batch)(stream)
 
 
 class Layer:

@@ -228,6 +228,32 @@ def test_hostio_end_to_end_path():
     assert np.array_equal(hY.numpy().astype(np.float64), O.gemv(bsr, x))
 
 
+def test_multi_hostio_end_to_end_path():
+    """gqsa_gemm_multi_hostio: one H2D copy of concatenated inputs, one launch
+    per layer, one D2H copy of concatenated outputs (bench.py's e2e path)."""
+    shapes = [(300, 1024), (77, 208), (1024, 4096)]
+    for B in (1, 2):
+        layers, xs, refs = [], [], []
+        for i, (n, k) in enumerate(shapes):
+            seed = synth.seed_for(f"multi/{i}/{n}/{k}/{B}")
+            bsr = synth.make_layer(seed, n, k, sparsity=0.5, mode="exact_int")
+            x = synth.make_x(seed + 1, B, k, mode="exact_int")
+            layers.append(gqsa.Layer(bsr))
+            xs.append(x.reshape(-1))
+            refs.append(O.gemv(bsr, x))
+        descs = [L.desc for L in layers]
+        hX = torch.from_numpy(np.concatenate(xs)).view(torch.float16).pin_memory()
+        hY = torch.full((sum(B * n for n, _ in shapes),), float("nan"), dtype=torch.float32).pin_memory()
+        stage = torch.empty(gqsa.multi_hostio_stage_size(descs, B), dtype=torch.uint8, device="cuda")
+        gqsa.gemm_multi_hostio(descs, [L.blob for L in layers], hX, hY, stage, [L.ws for L in layers], batch=B)
+        torch.cuda.synchronize()
+        got = hY.numpy().astype(np.float64)
+        off = 0
+        for (n, _), ref in zip(shapes, refs):
+            assert np.array_equal(got[off:off + B * n].reshape(B, n), ref)
+            off += B * n
+
+
 def test_argument_errors():
     bsr = synth.make_layer(61, 64, 256, sparsity=0.5)
     L = gqsa.Layer(bsr)
