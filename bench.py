@@ -377,7 +377,6 @@ def run_gpu(args):
         hY = torch.empty(sum(B * d.rows for d in descs), dtype=torch.float32).pin_memory()
         stage = torch.empty(gqsa.multi_hostio_stage_size(descs, B), dtype=torch.uint8, device=dev)
         ne = min(args.steps, args.e2e_steps)
-
         calls = [gqsa.MultiHostIO(descs, copies[r], hX, hY, stage, ws, batch=B) for r in range(R)]
 
         def e2e_step(k):
@@ -399,244 +398,6 @@ def run_gpu(args):
                "h2d_bytes_per_step": int(hX.numel() * 2), "d2h_bytes_per_step": int(hY.numel() * 4),
                "steps": ne, "ms_per_step": e_ms / ne, "wall_ms_per_step": wall * 1e3 / ne,
                "api": "gqsa_gemm_multi_hostio (1 H2D + per-layer launches + 1 D2H, stream sync per step)"}
-
-    if rank != 0:
-        return
-    from oracle import gqsa_oracle as O
-    layers = make_layers(4, 0.5, args.batch)
-    total_steps = args.steps + args.warmup
-    budget = float(os.environ.get("GQSA_REF_BUDGET_S", "90"))
-    per_step = budget / max(total_steps, 1)
-    # a bounded row sample per layer, sized from a quick calibration
-    t0 = time.perf_counter()
-    O.gemv_rows(layers[0]["bsr"], layers[0]["x"], np.arange(64))
-    per_row = (time.perf_counter() - t0) / 64
-    rows_per_layer = int(max(1, min(4096, per_step / (per_row * 3 * 3.5))))
-    rng = np.random.default_rng(0)
-    samples = []
-    for L in layers:
-        ri = L["bsr"]["row_index"]
-        rs = np.sort(rng.choice(L["rows"], size=min(rows_per_layer, L["rows"]), replace=False))
-        nnz = int(np.sum(ri[rs + 1] - ri[rs]))
-        b = nnz * (16 * 4 // 8 + 6) + 4 * (len(rs) + 1) + 2 * L["cols"] + 4 * len(rs)
-        samples.append((L, rs, b))
-    for _ in range(args.warmup):
-        for L, rs, _b in samples:
-            O.gemv_rows(L["bsr"], L["x"], rs)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        for L, rs, _b in samples:
-            O.gemv_rows(L["bsr"], L["x"], rs)
-    dt = time.perf_counter() - t0
-    step_bytes = sum(b for _, _, b in samples)
-    value = step_bytes * args.steps / dt / 1e9
-    sample = (f"{rows_per_layer} random output rows of each of 4096x4096, 14336x4096, 4096x14336 "
-              f"(W4S50, B={args.batch}) per step; bytes counted per sampled row")
-    line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded; DESIGN.md §4 recipe)",
-        "config": {"workload": "llama3-8b-layer-shapes-w4s50-b1", "global_batch": args.batch,
-                   "seq_len": 1, "parallelism": "host-cpu"},
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
-        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-
-
-# ----------------------------------------------------------------------------- GPU arm
-def run_gpu(args):
-    import torch
-    import torch.distributed as dist
-
-    from paper_2412_17560_b200 import gqsa
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-
-    bits, sp, B = 4, 0.5, args.batch
-    layers = make_layers(bits, sp, B, world, rank)
-    hbm_peak, peak_src = peaks()
-
-    # pack this rank's row shard of every layer; R device copies for L2 rotation
-    packed = []
-    set_bytes = 0
-    for L in layers:
-        blob, desc = gqsa.pack(L["bsr"], L["lo"], L["hi"])
-        packed.append((blob, desc))
-        set_bytes += blob.size
-    R = max(2, math.ceil(2.2 * L2_BYTES / max(set_bytes, 1)) + 1) if not args.no_rotate else 1
-    ws = []
-    copies = []  # copies[r][i] = device blob of layer i
-    for r in range(R):
-        row = []
-        for blob, desc in packed:
-            row.append(torch.from_numpy(blob).to(dev))
-        copies.append(row)
-    for blob, desc in packed:
-        ws.append(torch.zeros(gqsa.workspace_size(desc, B), dtype=torch.uint8, device=dev))
-    xs = [torch.from_numpy(L["x"]).view(torch.float16).to(dev) for L in layers]
-    ys = [torch.empty(B, d.rows, dtype=torch.float32, device=dev) for _, d in packed]
-    yfull = [torch.empty(world * B * d.rows, dtype=torch.float32, device=dev) if world > 1 else None
-             for _, d in packed]
-
-    def launch(i, r):
-        _, desc = packed[i]
-        if B == 1:
-            gqsa.gemv(desc, copies[r][i], xs[i][0], ys[i][0], None, ws[i])
-        else:
-            gqsa.gemm_smallbatch(desc, copies[r][i], xs[i], ys[i], None, ws[i])
-        if world > 1:
-            dist.all_gather_into_tensor(yfull[i], ys[i].view(-1))
-
-    # chain path: the step's GEMVs in one persistent launch,
-    # each item reading its x only after the previous items completed
-    # (wait_prev = 1: the same sequential semantics as one launch per GEMV)
-    use_chain = args.path == "chain" and world == 1 and B <= 2
-    chain_items = [[(packed[i][1], copies[r][i], xs[i], ys[i], None, 1) for i in range(len(layers))]
-                   for r in range(R)]
-    chain_ws = (torch.zeros(gqsa.chain_workspace_size(chain_items[0], B), dtype=torch.uint8, device=dev)
-                if use_chain else None)
-
-    def step(r):
-        if use_chain:
-            gqsa.gemm_chain(chain_items[r], chain_ws)
-            return
-        for i in range(len(layers)):
-            launch(i, r)
-
-    stream = torch.cuda.Stream(device=dev)
-    torch.cuda.synchronize()
-    # eager warm-up (also the first launches: attribute set-up, module load)
-    with torch.cuda.stream(stream):
-        for r in range(R):
-            step(r)
-    torch.cuda.synchronize()
-
-    def capture(nsteps, start=0):
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
-            for k in range(nsteps):
-                step((start + k) % R)
-        return g
-
-    use_graph = world == 1  # NCCL collectives stay eager under torchrun
-    graphs = {}
-
-    def run_steps(n):
-        if use_graph:
-            if R not in graphs:
-                graphs[R] = capture(R)
-            for _ in range(n // R):
-                graphs[R].replay()
-            if n % R:
-                if n % R not in graphs:
-                    graphs[n % R] = capture(n % R)
-                graphs[n % R].replay()
-        else:
-            for k in range(n):
-                step(k % R)
-
-    with torch.cuda.stream(stream):
-        run_steps(max(args.warmup, 3))
-        if use_graph and args.steps % R:
-            graphs.setdefault(args.steps % R, capture(args.steps % R))
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sampler = ClockSampler(local)
-    torch.cuda.synchronize()
-    with sampler:
-        e0.record(stream)
-        with torch.cuda.stream(stream):
-            run_steps(args.steps)
-        e1.record(stream)
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    ms_step = ms / args.steps
-
-    # counted bytes: every rank's shard (sum over ranks) + the all-gathered y
-    step_bytes_rank = sum(counted_bytes(d.rows, d.cols, d.nnzg, bits, B) for _, d in packed)
-    if world > 1:
-        t = torch.tensor([step_bytes_rank], dtype=torch.float64, device=dev)
-        dist.all_reduce(t)
-        step_bytes = float(t.item())
-    else:
-        step_bytes = float(step_bytes_rank)
-    value = step_bytes * args.steps / (ms * 1e-3) / 1e9
-
-    # ---- per-layer device time (dominant kernel per shape), outside the timed region
-    layer_rows = []
-    if world == 1:
-        for i, L in enumerate(layers):
-            _, desc = packed[i]
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                for r in range(R):
-                    if B == 1:
-                        gqsa.gemv(desc, copies[r][i], xs[i][0], ys[i][0], None, ws[i])
-                    else:
-                        gqsa.gemm_smallbatch(desc, copies[r][i], xs[i], ys[i], None, ws[i])
-            for _ in range(3):
-                g.replay()
-            reps = max(10, 2000 // R)
-            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            a.record(stream)
-            with torch.cuda.stream(stream):
-                for _ in range(reps):
-                    g.replay()
-            b_.record(stream)
-            torch.cuda.synchronize()
-            us = a.elapsed_time(b_) * 1e3 / (reps * R)
-            cb = counted_bytes(desc.rows, desc.cols, desc.nnzg, bits, B)
-            layer_rows.append({"shape": f"{desc.rows}x{desc.cols}", "role": L["name"],
-                               "nnzg": desc.nnzg, "counted_bytes": cb, "us": round(us, 3),
-                               "gbs": round(cb / us / 1e3, 1),
-                               "frac_of_8tbs": round(cb / us / 1e3 / NOMINAL_HBM_GBS, 4),
-                               "frac_of_measured": round(cb / us / 1e3 / hbm_peak, 4)})
-
-    # ---- end to end through the public C ABI with host buffers (pinned)
-    e2e = None
-    if world == 1:
-        hX = [torch.from_numpy(L["x"]).view(torch.float16).pin_memory() for L in layers]
-        hY = [torch.empty(B, d.rows, dtype=torch.float32).pin_memory() for _, d in packed]
-        stage = [torch.empty(gqsa.hostio_stage_size(d, B), dtype=torch.uint8, device=dev) for _, d in packed]
-        ne = min(args.steps, args.e2e_steps)
-        for k in range(3):
-            with torch.cuda.stream(stream):
-                for i in range(len(layers)):
-                    gqsa.gemm_hostio(packed[i][1], copies[k % R][i], hX[i], hY[i], stage[i], ws[i])
-            stream.synchronize()
-        a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0 = time.perf_counter()
-        a.record(stream)
-        for k in range(ne):
-            with torch.cuda.stream(stream):
-                for i in range(len(layers)):
-                    gqsa.gemm_hostio(packed[i][1], copies[k % R][i], hX[i], hY[i], stage[i], ws[i])
-            stream.synchronize()  # the caller reads y every step
-        b_.record(stream)
-        stream.synchronize()
-        wall = time.perf_counter() - t0
-        e_ms = a.elapsed_time(b_)
-        e2e = {"value": step_bytes * ne / (e_ms * 1e-3) / 1e9, "unit": "GB/s",
-               "h2d_bytes_per_step": int(sum(2 * B * d.cols for _, d in packed)),
-               "d2h_bytes_per_step": int(sum(4 * B * d.rows for _, d in packed)),
-               "steps": ne, "ms_per_step": e_ms / ne, "wall_ms_per_step": wall * 1e3 / ne}
 
     if rank != 0:
         if world > 1:
