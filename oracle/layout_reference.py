@@ -29,17 +29,22 @@ def tile_bytes(bits: int) -> int:
     return 32 + T * 16 * bits // 8 + T * 4 + T * 2
 
 
-TARGET_SLOTS = 64
+def target_slots(nnzg: int) -> int:
+    """Slots per lane of the longest slice: 16 when the layer
+    has under 1.6 tiles (of 128 groups) per warp of a 148 x 16-warp grid, 32
+    under 4, else 64."""
+    tpw = nnzg / 128.0 / (148.0 * 16.0)
+    return 16 if tpw < 1.6 else 32 if tpw < 4.0 else 64
 
 
-def lanes_per_row(n_nz: int, max_len: int) -> int:
+def lanes_per_row(n_nz: int, max_len: int, target: int = 64) -> int:
     """S = the larger of (a) the smallest power of two with
-    ceil(max_len / S) <= 64 slots per lane and (b) 32 / (next power of two
-    >= n_nz) when fewer than 32 rows are non-empty; capped at 32."""
+    ceil(max_len / S) <= target slots per lane and (b) 32 / (next power of
+    two >= n_nz) when fewer than 32 rows are non-empty; capped at 32."""
     if n_nz <= 0:
         return 1
     s = 1
-    while s < LANES and -(-max_len // s) > TARGET_SLOTS:
+    while s < LANES and -(-max_len // s) > target:
         s *= 2
     p = 1
     while p < n_nz and p < LANES:
@@ -87,7 +92,7 @@ def pack_reference(bsr: dict, row_begin: int = 0, row_end=None) -> bytes:
     nz = [r for r in range(rows) if counts[r] > 0]
     nz.sort(key=lambda r: (-counts[r], r))          # count descending, then row
     empty = [r for r in range(rows) if counts[r] == 0]
-    S = lanes_per_row(len(nz), counts[nz[0]] if nz else 0)
+    S = lanes_per_row(len(nz), counts[nz[0]] if nz else 0, target_slots(nnzg))
     rps = LANES // S                                # rows per slice
     n_slices = -(-len(nz) // rps)
     slice_tiles = []

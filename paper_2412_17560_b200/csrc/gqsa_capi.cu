@@ -507,6 +507,10 @@ extern "C" int gqsa_gemm_chain(const gqsa_chain_item_t* items, int32_t n, int32_
     p.part_r = p.active_warps ? desc->num_tiles % p.active_warps : 0;
     p.out_f16 = it.out_f16;
     cp.wait_prev[j] = j == 0 ? 0 : it.wait_prev;
+    cp.reuse_x[j] = (j > 0 && !cp.wait_prev[j] && it.d_X == items[j - 1].d_X && it.ldx == items[j - 1].ldx &&
+                     it.desc->cols == items[j - 1].desc->cols)
+                        ? 1
+                        : 0;
   }
   cp.n = n;
   cp.stages = cpl.stages;

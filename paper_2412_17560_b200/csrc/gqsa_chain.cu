@@ -133,8 +133,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) gqsa_chain_kernel(const __gr
     uint8_t* xs = smem;
     uint8_t* pq = xs + (size_t)B * p.cols * 2;
     if (cp.trace && lane == 0) cp.trace[((int64_t)gw * cp.n + j) * 4 + 0] = globaltimer();
-    stage_activations<BITS, B, true>(p, xs, pq, KG, nthreads);
-    __syncthreads();
+    if (!cp.reuse_x[j]) {  // else: same X as item j-1 and no wait: x and (P, Q) are in place
+      stage_activations<BITS, B, true>(p, xs, pq, KG, nthreads);
+      __syncthreads();
+    }
     if (cp.trace && lane == 0) cp.trace[((int64_t)gw * cp.n + j) * 4 + 1] = globaltimer();
     for (int i = blockIdx.x * nthreads + threadIdx.x; i < p.n_empty; i += gridDim.x * nthreads) {
       const int erow = __ldg(p.empty + i);

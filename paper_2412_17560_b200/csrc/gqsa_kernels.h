@@ -70,6 +70,7 @@ constexpr int kChainThreads = 512;
 struct ChainParams {
   KParams item[kMaxChain];        // per item: exactly the per-GEMV kernel's parameters
   int32_t wait_prev[kMaxChain];   // 1: item j reads X only after items < j completed
+  int32_t reuse_x[kMaxChain];     // 1: item j has item j-1's X (and no wait): skip restaging
   int32_t n;                      // items
   int32_t stages;                 // ring depth NS (tiles) per warp
   int32_t ring_offset;            // shared-memory offset of the TMA ring

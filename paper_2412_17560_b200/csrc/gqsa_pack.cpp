@@ -87,10 +87,13 @@ Slices make_slices(const gqsa_bsr_t* b, int32_t r0, int32_t r1) {
                    [&](int32_t a, int32_t c) { return s.count[a] > s.count[c]; });
   s.n_nz = (int32_t)s.order.size();
   s.n_empty = (int32_t)s.empty.size();
-  static const int target = [] {
-    const char* e = std::getenv("GQSA_TARGET_SLOTS");  // experiment knob
-    return e && std::atoi(e) >= 4 ? std::atoi(e) : kTargetSlots;
+  static const int target_env = [] {
+    const char* e = std::getenv("GQSA_TARGET_SLOTS");  // experiment knob (overrides the rule)
+    return e && std::atoi(e) >= 4 ? std::atoi(e) : 0;
   }();
+  int64_t nnz_range = 0;
+  for (int32_t r : s.order) nnz_range += s.count[r];
+  const int target = target_env ? target_env : target_slots_for(nnz_range);
   s.lanes_per_row = lanes_per_row_for(s.n_nz, s.n_nz ? s.count[s.order[0]] : 0, target);
   s.rows_per_slice = kLanes / s.lanes_per_row;
   s.num_slices = (s.n_nz + s.rows_per_slice - 1) / s.rows_per_slice;

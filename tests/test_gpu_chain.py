@@ -145,6 +145,23 @@ def test_chain_realistic_gates_llama_shapes(shapes, bits, sp, B):
         assert torch.equal(it[3], f), "chain reruns must be bit-identical"
 
 
+def test_chain_shared_input_reuse():
+    """Items reading the SAME X without waiting (q/k/v, gate/up of a decoder
+    layer) reuse the staged activations; results stay exact."""
+    x = synth.make_x(31, 2, 4096, mode="exact_int")
+    X = _x(x)
+    items, refs = [], []
+    for i, (rows, wait) in enumerate(((512, 1), (128, 0), (128, 0), (700, 1), (300, 0))):
+        bsr = synth.make_layer(40 + i, rows, 4096, sparsity=0.5, mode="exact_int")
+        desc, d_blob = _dev_blob(bsr)
+        Y = torch.full((2, rows), float("nan"), dtype=torch.float32, device="cuda")
+        items.append((desc, d_blob, X, Y, None, wait))
+        refs.append(O.gemv(bsr, x))
+    run_chain(items)
+    for it, ref in zip(items, refs):
+        assert np.array_equal(it[3].cpu().numpy().astype(np.float64), ref)
+
+
 def test_chain_bias_and_fp16_output():
     bsr = synth.make_layer(7, 1000, 2048, sparsity=0.5, mode="exact_int")
     x = synth.make_x(8, 2, 2048, mode="exact_int")

@@ -7,7 +7,10 @@ E. LLaMA-3-8B decoder LINEAR STACK per token (32 layers x q, k, v, o, gate,
    up, down = 224 GEMVs) at W4S30 / W4S50 / W2S50, B = 1, 2, 4, 8: one CUDA
    graph of the whole stack (PDL between launches), µs per token, counted GB/s.
    Also the merged form production servers use (vLLM-style fused qkv
-   6144x4096 and gate_up 28672x4096: 128 GEMVs per token).
+   6144x4096 and gate_up 28672x4096: 128 GEMVs per token), and both forms as
+   one gqsa_gemm_chain launch per decoder layer (k, v and up read the input
+   of the item before them, so they do not wait; the other items wait for
+   every earlier item; B <= 2).
 F. Qwen2.5-14B (5120 / 13824, 48 layers) W4S50 and LLaMA-3.1-70B (8192 /
    28672) W4S50 row shards: the per-rank GEMV of a P-way row split
    (N/P x K) measured on this GPU, P = 1, 2, 4, 8 (Qwen) and P = 8 (70B).
@@ -38,8 +41,14 @@ LLAMA3_8B = [("q", 4096, 4096), ("k", 1024, 4096), ("v", 1024, 4096), ("o", 4096
 LLAMA3_8B_MERGED = [("qkv", 6144, 4096), ("o", 4096, 4096), ("gate_up", 28672, 4096), ("down", 4096, 14336)]
 
 
-def time_stack(mats, n_layers, bits, sp, B, reps=20):
-    """mats: [(name, rows, cols)] of one decoder layer; returns µs per token and bytes."""
+# wait_prev per item of one decoder layer's chain: k, v read q's input and up
+# reads gate's input (independent of the previous item); the others wait.
+CHAIN_WAIT = {"q": 1, "k": 0, "v": 0, "o": 1, "gate": 1, "up": 0, "down": 1, "qkv": 1, "gate_up": 1}
+
+
+def time_stack(mats, n_layers, bits, sp, B, reps=20, chain=False):
+    """mats: [(name, rows, cols)] of one decoder layer; returns µs per token and bytes.
+    chain: one gqsa_gemm_chain launch per decoder layer instead of one launch per GEMV."""
     dev = torch.device("cuda")
     packed = []
     for name, rows, cols in mats:
@@ -49,13 +58,27 @@ def time_stack(mats, n_layers, bits, sp, B, reps=20):
         packed.append((blob, desc))
     copies = [[torch.from_numpy(b).to(dev) for b, _ in packed] for _ in range(n_layers)]
     ws = [torch.zeros(gqsa.workspace_size(d, B), dtype=torch.uint8, device=dev) for _, d in packed]
-    xs = [torch.from_numpy(synth.make_x(synth.seed_for(f"stack-x/{c}/{B}"), B, c)).view(torch.float16).to(dev)
-          for _, _, c in mats]
+    # q/k/v (qkv) read the same input, gate/up (gate_up) too
+    src = {"q": "attn", "k": "attn", "v": "attn", "qkv": "attn", "o": "o", "gate": "mlp", "up": "mlp",
+           "gate_up": "mlp", "down": "down"}
+    xin = {}
+    for name, _, c in mats:
+        if src[name] not in xin:
+            xin[src[name]] = torch.from_numpy(synth.make_x(synth.seed_for(f"stack-x/{src[name]}/{c}/{B}"), B, c)
+                                              ).view(torch.float16).to(dev)
+    xs = [xin[src[name]] for name, _, _ in mats]
     ys = [torch.empty(B, r, dtype=torch.float32, device=dev) for _, r, _ in mats]
     s = torch.cuda.Stream()
+    if chain:
+        items = [[(d, copies[L][i], xs[i], ys[i], None, CHAIN_WAIT[mats[i][0]]) for i, (_, d) in enumerate(packed)]
+                 for L in range(n_layers)]
+        cws = torch.zeros(gqsa.chain_workspace_size(items[0], B), dtype=torch.uint8, device=dev)
 
     def token():
         for L in range(n_layers):
+            if chain:
+                gqsa.gemm_chain(items[L], cws, stream=s)
+                continue
             for i, (_, d) in enumerate(packed):
                 gqsa.gemm_smallbatch(d, copies[L][i], xs[i], ys[i], None, ws[i], stream=s)
 
@@ -76,7 +99,7 @@ def time_stack(mats, n_layers, bits, sp, B, reps=20):
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / reps
     nb = n_layers * sum(counted_bytes(d.rows, d.cols, d.nnzg, bits, B) for _, d in packed)
-    launches = n_layers * len(packed)
+    launches = n_layers * (1 if chain else len(packed))
     del copies
     torch.cuda.empty_cache()
     return us, nb, launches
@@ -124,11 +147,16 @@ def main():
              f"GB/s = counted bytes / µs; frac = GB/s / {peak:.1f} ({src}). One CUDA graph per token, "
              "PDL between launches, weights in 32 (48) distinct device copies (HBM-resident, >> L2).", "",
              "## E. LLaMA-3-8B decoder linear stack per token (SURVEY §8(d) C3)", "",
-             "| setting | form | GEMVs | B | µs / token | GB per token | GB/s | frac |", "|---|---|---|---|---|---|---|---|"]
+             "| setting | form | launches | B | µs / token | GB per token | GB/s | frac |", "|---|---|---|---|---|---|---|---|"]
     for bits, sp in ((4, 0.3), (4, 0.5), (2, 0.5)):
-        for form, mats in (("separate q/k/v, gate/up", LLAMA3_8B), ("merged qkv, gate_up", LLAMA3_8B_MERGED)):
+        for form, mats, chain in (("separate q/k/v, gate/up", LLAMA3_8B, False),
+                                  ("merged qkv, gate_up", LLAMA3_8B_MERGED, False),
+                                  ("separate, 1 chain launch per layer", LLAMA3_8B, True),
+                                  ("merged, 1 chain launch per layer", LLAMA3_8B_MERGED, True)):
             for B in batches:
-                us, nb, nl = time_stack(mats, 32, bits, sp, B)
+                if chain and B > 2:
+                    continue
+                us, nb, nl = time_stack(mats, 32, bits, sp, B, chain=chain)
                 r = dict(section="E", setting=f"W{bits}S{int(sp * 100)}", form=form, B=B, us=round(us, 1),
                          bytes=nb, launches=nl, gbs=round(nb / us / 1e3, 1), frac=round(nb / us / 1e3 / peak, 4))
                 recs.append(r)
