@@ -262,12 +262,6 @@ int launch_chunk(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_
   p.trace = (g_trace && g_trace_bytes >= (size_t)pl.active_warps * 64) ? g_trace : nullptr;
   p.slice_k = o.partition == GQSA_PARTITION_SLICE_K ? 1 : 0;
   p.out_f16 = o.out_f16;
-  static const int trigger = env_int("GQSA_PDL_TRIGGER", 0, 0, 4);
-  p.pdl_trigger = trigger;
-  static const int xtma = env_int("GQSA_XTMA", 0, 0, 1);
-  p.x_tma = xtma;
-  static const int xrep = env_int("GQSA_XREP", 0, 0, 4096);
-  p.x_rep = xrep;
   if (desc->rows == 0) return GQSA_OK;
 
   cudaLaunchConfig_t cfg = {};

@@ -58,7 +58,6 @@ __device__ __forceinline__ uint32_t hfma2(uint32_t a, uint32_t b, uint32_t c) {
   return d;
 }
 
-constexpr uint32_t kBulkChunk = 32768u;     // bytes per 1-D bulk copy
 constexpr uint32_t kMagic1024 = 0x64006400u;   // half2(1024, 1024)
 constexpr uint32_t kNeg1024 = 0xE400E400u;     // half2(-1024, -1024)
 
@@ -419,11 +418,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       "%4;" ::"r"(dst),
       "l"(src), "r"(bytes), "r"(bar), "l"(pol)
       : "memory");
-}
-__device__ __forceinline__ void bulk_g2s_plain(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(bar)
-               : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t done = 0;

@@ -78,17 +78,12 @@ __global__ void __launch_bounds__(max_threads_for(BITS, B, FEW), min_blocks_for(
       bulk_g2s(ring_s + slot * 2 * tb, tiles + (int64_t)t_first * tb, n * tb, bar0 + 8 * slot, pol);
     }
   };
-  // activation barrier: the last (unused) ring-barrier slot of warp 0
-  const uint32_t barx = (uint32_t)__cvta_generic_to_shared(
-      smem + p.ring_offset + (size_t)(nthreads >> 5) * NS * tb + (size_t)(kMaxStages - 1) * 8);
   if (lane == 0) {
     for (int s = 0; s < NP; ++s) mbar_init(bar0 + 8 * s, 1);
-    if (p.x_tma && threadIdx.x == 0) mbar_init(barx, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int s = 0; s < NP; ++s) fill_slot(s, t_begin + 2 * s);
   }
   __syncwarp();
-  if (p.x_tma) __syncthreads();  // barx initialised before anyone waits on it
   int row = -1;  // this lane's row in the first slice (the perm table is part of the blob)
   uint32_t hdr0 = 0, first0 = 0;
   if (t_end > t_begin) {
@@ -107,7 +102,9 @@ __global__ void __launch_bounds__(max_threads_for(BITS, B, FEW), min_blocks_for(
       asm volatile("st.shared.b64 [%0], %1;" ::"r"(fx + 8u * i), "l"(0ull) : "memory");
   }
   trace_point(p, gw, lane, 0);
-  if (p.pdl_trigger == 0) pdl_launch_dependents();
+  // let the next launch on the stream become resident now (it needs half an
+  // SM: measured best; later triggers delay its weight prefetch)
+  pdl_launch_dependents();
   pdl_wait();  // x, y, bias and the workspace may belong to the previous kernel
   trace_point(p, gw, lane, 1);
 
@@ -116,39 +113,11 @@ __global__ void __launch_bounds__(max_threads_for(BITS, B, FEW), min_blocks_for(
   //      compute the per-column-group sums X_{b,c} (fp32, fixed t order) from
   //      the same registers: one pass, one barrier.
   const int KG = p.cols / kGroup;
-  if (p.x_rep > 1) p.X += (int64_t)(blockIdx.x % p.x_rep) * B * p.ldx;  // experiment: replicated x
   uint8_t* xs = smem;
   uint8_t* pq = xs + (size_t)B * p.cols * 2;  // [B][K/16 * pq_per_group] float2 (P, Q)
-  if (p.x_tma) {
-    // x arrives by 1-D bulk copies (one request stream per CTA); the column
-    // sums are then computed from shared memory
-    if (threadIdx.x == 0) {
-      const uint32_t row_bytes = 2u * (uint32_t)p.cols;
-      mbar_expect_tx(barx, (uint32_t)B * row_bytes);
-      const uint32_t xs_s = (uint32_t)__cvta_generic_to_shared(xs);
-      for (int b = 0; b < B; ++b)
-        for (uint32_t off = 0; off < row_bytes; off += kBulkChunk)
-          bulk_g2s_plain(xs_s + b * row_bytes + off, reinterpret_cast<const uint8_t*>(p.X + (int64_t)b * p.ldx) + off,
-                         min(kBulkChunk, row_bytes - off), barx);
-    }
-    mbar_wait(barx, 0);
-    for (int i = threadIdx.x; i < B * KG; i += nthreads) {
-      const int b = i / KG, c = i - b * KG;
-      const uint4* src = reinterpret_cast<const uint4*>(xs + (size_t)b * p.cols * 2) + 2 * c;
-      const uint4 v0 = src[0], v1 = src[1];
-      const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-      const float2 v2 = column_sums<BITS>(w);
-      constexpr int PG = pq_per_group<B>();
-      float2* dst = reinterpret_cast<float2*>(pq) + ((size_t)b * KG + c) * PG;
-      dst[0] = v2;
-      if (PG == 2) dst[1] = v2;
-    }
-  } else {
-    stage_activations<BITS, B>(p, xs, pq, KG, nthreads);
-  }
+  stage_activations<BITS, B>(p, xs, pq, KG, nthreads);
   trace_point(p, gw, lane, 6);
   __syncthreads();
-  if (p.pdl_trigger == 1) pdl_launch_dependents();
 
   // ---- empty rows get bias (or 0): grid-stride over the empty-row list
   for (int i = blockIdx.x * nthreads + threadIdx.x; i < p.n_empty; i += gridDim.x * nthreads) {
@@ -220,8 +189,6 @@ __global__ void __launch_bounds__(max_threads_for(BITS, B, FEW), min_blocks_for(
     if (++s == NP) { s = 0; phase ^= 1u; }
     consume(tr0, t);
     consume(tr1, t + 1);
-    if (p.pdl_trigger == 2 && t == t_begin) pdl_launch_dependents();
-    if (p.pdl_trigger == 3 && t + NS + 2 >= t_end) pdl_launch_dependents();  // no refill left
   }
   if (t < t_end) {  // odd count: the last slot holds one tile
     mbar_wait(bar0 + 8 * s, phase);
@@ -231,7 +198,6 @@ __global__ void __launch_bounds__(max_threads_for(BITS, B, FEW), min_blocks_for(
   }
 
   trace_point(p, gw, lane, 4);
-  if (p.pdl_trigger >= 3) pdl_launch_dependents();
   // ---- a slice left open at the end of the range continues downstream
   if (!(last_hdr & kTileLast)) {
     if (foreign) {  // the whole range lies inside a slice owned upstream

@@ -56,11 +56,7 @@ struct KParams {
   uint64_t* trace;         // optional [active_warps][8] %globaltimer stamps (debug)
   int32_t slice_k;         // 1: data-centric partition (whole slices per warp, no fix-up)
   int32_t out_f16;         // 1: Y is fp16 (RNE of the fp32 result)
-  int32_t pdl_trigger;     // where the next kernel may launch: 0 before the PDL wait,
-                           // 1 after activation staging, 2 after the first tile pair
-  int32_t x_tma;
-  int32_t x_rep;
-  int32_t fix_offset;      // shared-memory offset of the intra-CTA fix-up records (0: all global)           // experiment: x replicated x_rep times (B*ldx apart), CTA c reads copy c % x_rep           // 1: stage x with 1-D bulk copies (experiment)
+  int32_t fix_offset;      // shared-memory offset of the intra-CTA fix-up records (0: all global)
 };
 
 // Persistent chain kernel (gqsa_chain.cu): one launch runs up to kMaxChain

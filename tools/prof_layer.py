@@ -37,9 +37,6 @@ def main():
     blobs = [torch.from_numpy(blob).cuda() for _ in range(R)]
     ws = torch.zeros(gqsa.workspace_size(desc, a.batch), dtype=torch.uint8, device="cuda")
     X = torch.from_numpy(x).view(torch.float16).cuda()
-    xrep = int(os.environ.get("GQSA_XREP", "0"))
-    if xrep > 1:  # experiment: the kernel reads copy (CTA % xrep) of x
-        X = X.repeat(xrep, 1).contiguous()
     Y = torch.empty(a.batch, a.rows, dtype=torch.float32, device="cuda")
     plan = gqsa.launch_plan(desc, a.batch)
     print(f"plan grid={plan.grid} active_warps={plan.active_warps} tiles={plan.num_tiles} "
