@@ -214,8 +214,13 @@ def run_gpu(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    fused = args.allgather == "fused"
+    if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
+        os.environ["NCCL_DEBUG"] = "WARN"  # NCCL's version banner goes to stdout: keep it to the JSON line
+    if world > 1 or fused:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
 
     bits, sp, B = 4, 0.5, args.batch
     layers = make_layers(bits, sp, B, world, rank)
@@ -243,8 +248,25 @@ def run_gpu(args):
     yfull = [torch.empty(world * B * d.rows, dtype=torch.float32, device=dev) if world > 1 else None
              for _, d in packed]
 
+    # fused all-gather: each rank's GEMV stores its rows
+    # straight into every rank's full y (symmetric memory, NVLink P2P), then a
+    # symmetric-memory barrier orders the step; no NCCL data movement
+    if fused:
+        import torch.distributed._symmetric_memory as symm_mem
+        gname = dist.group.WORLD.group_name
+        if hasattr(symm_mem, "enable_symm_mem_for_group"):
+            symm_mem.enable_symm_mem_for_group(gname)
+        yf = [symm_mem.empty((B, L["rows"]), dtype=torch.float32, device=dev) for L in layers]
+        hdl = [symm_mem.rendezvous(t, gname) for t in yf]
+        peers = [[h.get_buffer(p, (B, L["rows"]), torch.float32) for p in range(world)]
+                 for h, L in zip(hdl, layers)]
+
     def launch(i, r):
         _, desc = packed[i]
+        if fused:
+            gqsa.gemm_allgather(desc, copies[r][i], xs[i], peers[i], row_offset=layers[i]["lo"], ws=ws[i])
+            hdl[i].barrier(channel=0)
+            return
         if B == 1:
             gqsa.gemv(desc, copies[r][i], xs[i][0], ys[i][0], None, ws[i])
         else:
@@ -283,7 +305,7 @@ def run_gpu(args):
                 step((start + k) % R)
         return g
 
-    use_graph = world == 1  # NCCL collectives stay eager under torchrun
+    use_graph = world == 1 and not fused  # collectives stay eager
     graphs = {}
 
     def run_steps(n):
@@ -427,6 +449,7 @@ def run_gpu(args):
         "config": {"workload": "llama3-8b-layer-shapes-w4s50-b1 (4096x4096, 14336x4096, 4096x14336)",
                    "global_batch": B, "seq_len": 1, "group_size": 16, "bits": bits, "sparsity": sp,
                    "parallelism": f"rowshard{world}" if world > 1 else "single",
+                   "allgather": (args.allgather if (world > 1 or fused) else None),
                    "l2": f"weights rotate over {R} device copies of the layer set "
                          f"({R * set_bytes / 2**20:.0f} MiB > 2x L2)",
                    "path": "gqsa_gemm_chain (one persistent launch per step, grid barrier between layers)"
@@ -446,7 +469,7 @@ def run_gpu(args):
         "clocks": sampler.summary(),
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 
@@ -461,6 +484,9 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rotate", action="store_true")
+    ap.add_argument("--allgather", default="nccl", choices=["nccl", "fused"],
+                    help="row-shard output exchange: NCCL all_gather, or the fused GEMV epilogue storing "
+                         "into every rank's y over symmetric memory (gqsa_gemm_allgather)")
     ap.add_argument("--path", default="launches", choices=["chain", "launches"],
                     help="chain: one gqsa_gemm_chain launch per step; launches: one gqsa_gemv per layer")
     args = ap.parse_args()

@@ -203,6 +203,26 @@ int gqsa_gemm_ex(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_
                  size_t ws_bytes, const gqsa_options_t* opts, void* stream);
 
 /*
+ * gqsa_gemm_allgather: the row-sharded GEMM of one rank with the all-gather
+ * FUSED into its epilogue: every output element
+ * of this rank's shard (global rows [row_offset, row_offset + desc->rows)) is
+ * stored directly into each of the n_peers full-length outputs d_peer_Y[k]
+ * ([B][ldy], fp32 or fp16 when out_f16) -- the ranks' y buffers mapped into
+ * this device's address space (NVLink P2P / symmetric memory; on one GPU
+ * they may simply be local buffers).  No NCCL call: the transfer overlaps
+ * the GEMV tile by tile.  The kernel ends with a system-scope fence; the
+ * caller orders consumers after ALL ranks' launches (e.g. a symmetric-memory
+ * barrier on each rank's stream) before reading the gathered y.
+ *   desc/d_blob : this rank's shard (gqsa_pack(row_begin, row_end)).
+ *   d_bias      : this shard's bias [desc->rows] or NULL.
+ * Errors: GQSA_ERR_SHAPE (n_peers not in [1, 8], B, ldy < row_offset + rows,
+ * ldx), GQSA_ERR_BUFFER (null / misaligned pointers, small workspace).
+ */
+int gqsa_gemm_allgather(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_X, int32_t B, int64_t ldx,
+                        void* const* d_peer_Y, int32_t n_peers, int64_t ldy, int32_t row_offset, int32_t out_f16,
+                        const float* d_bias, void* d_ws, size_t ws_bytes, void* stream);
+
+/*
  * gqsa_gemm_chain: a sequence of GEMVs (e.g. the linear layers of a decoder
  * step) in ONE persistent launch, with the same results as calling
  * gqsa_gemm_smallbatch on items[0], items[1], ... in order on `stream`.

@@ -219,10 +219,18 @@ inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintp
 
 namespace {
 // One launch over Bc batch columns (x of Bc columns fits in shared memory).
+// Fused all-gather destinations of one launch (n == 0: plain Y).
+struct Peers {
+  int n = 0;
+  int32_t row_offset = 0;
+  void* y[kMaxPeers] = {};
+};
+
 // `plan0`/`fn0`: the caller's plan when it was made for exactly Bc columns.
 int launch_chunk(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_X, int Bc, int64_t ldx,
                  void* d_Y, int64_t ldy, const float* d_bias, void* d_ws, const gqsa_options_t& o,
-                 void* stream, const gqsa_plan_t* plan0 = nullptr, const void* fn0 = nullptr) {
+                 void* stream, const gqsa_plan_t* plan0 = nullptr, const void* fn0 = nullptr,
+                 const Peers* peers = nullptr) {
   gqsa_plan_t pl;
   const void* fn = nullptr;
   if (plan0 && fn0 && plan0->launches == 1 && plan0->batch_per_launch == Bc) {
@@ -234,7 +242,7 @@ int launch_chunk(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_
   }
   if (pl.batch_per_launch != Bc) return GQSA_ERR_UNSUPPORTED;  // unreachable: chunks always fit
   const uint8_t* blob = static_cast<const uint8_t*>(d_blob);
-  KParams p;
+  KParams p{};
   p.tiles = blob + desc->off_tiles;
   p.perm = reinterpret_cast<const int32_t*>(blob + desc->off_nzrow);
   p.empty = reinterpret_cast<const int32_t*>(blob + desc->off_empty);
@@ -262,6 +270,13 @@ int launch_chunk(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_
   p.trace = (g_trace && g_trace_bytes >= (size_t)pl.active_warps * 64) ? g_trace : nullptr;
   p.slice_k = o.partition == GQSA_PARTITION_SLICE_K ? 1 : 0;
   p.out_f16 = o.out_f16;
+  if (peers && peers->n) {
+    p.n_peers = peers->n;
+    p.row_offset = peers->row_offset;
+    for (int k = 0; k < peers->n; ++k)  // chunk b0 is folded into d_Y's offset from peer 0
+      p.peer_y[k] = reinterpret_cast<uint64_t>(peers->y[k]) +
+                    (reinterpret_cast<uintptr_t>(d_Y) - reinterpret_cast<uintptr_t>(peers->y[0]));
+  }
   if (desc->rows == 0) return GQSA_OK;
 
   cudaLaunchConfig_t cfg = {};
@@ -323,6 +338,42 @@ extern "C" int gqsa_gemm_ex(const gqsa_desc_t* desc, const void* d_blob, const u
     void* y0 = static_cast<uint8_t*>(d_Y) + (size_t)b0 * ldy * (o.out_f16 ? 2 : 4);
     st = launch_chunk(desc, d_blob, d_X + (int64_t)b0 * ldx, Bc, ldx, y0, ldy, d_bias, d_ws, o, stream, &pl0,
                       fn0);
+    if (st) return st;
+  }
+  return GQSA_OK;
+}
+
+extern "C" int gqsa_gemm_allgather(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_X, int32_t B,
+                                   int64_t ldx, void* const* d_peer_Y, int32_t n_peers, int64_t ldy,
+                                   int32_t row_offset, int32_t out_f16, const float* d_bias, void* d_ws,
+                                   size_t ws_bytes, void* stream) {
+  if (!desc || !d_blob || !d_X || !d_peer_Y || !d_ws) return GQSA_ERR_BUFFER;
+  if (!desc_ok(desc)) return GQSA_ERR_VALIDATION;
+  if (n_peers < 1 || n_peers > kMaxPeers || B < 1 || B > kMaxBatch || (out_f16 != 0 && out_f16 != 1))
+    return GQSA_ERR_SHAPE;
+  if (row_offset < 0 || ldy < (int64_t)row_offset + desc->rows || ldx < desc->cols || ldx % 8) return GQSA_ERR_SHAPE;
+  for (int k = 0; k < n_peers; ++k)
+    if (!d_peer_Y[k] || !aligned(d_peer_Y[k], out_f16 ? 2 : 4)) return GQSA_ERR_BUFFER;
+  if (!aligned(d_blob, 256) || !aligned(d_X, 16) || !aligned(d_ws, 16) || (d_bias && !aligned(d_bias, 4)))
+    return GQSA_ERR_BUFFER;
+  size_t need = 0;
+  gqsa_workspace_size(desc, B, &need);
+  if (ws_bytes < need) return GQSA_ERR_BUFFER;
+  const gqsa_options_t o{GQSA_PARTITION_STREAM_K, out_f16};
+  gqsa_plan_t pl0;
+  const void* fn0 = nullptr;
+  int st = make_plan(desc, B, &pl0, &fn0);
+  if (st) return st;
+  Peers peers;
+  peers.n = n_peers;
+  peers.row_offset = row_offset;
+  for (int k = 0; k < n_peers; ++k) peers.y[k] = d_peer_Y[k];
+  const size_t es = out_f16 ? 2 : 4;
+  for (int b0 = 0; b0 < B; b0 += pl0.batch_per_launch) {
+    const int Bc = B - b0 < pl0.batch_per_launch ? B - b0 : pl0.batch_per_launch;
+    void* y0 = static_cast<uint8_t*>(d_peer_Y[0]) + (size_t)b0 * ldy * es;
+    st = launch_chunk(desc, d_blob, d_X + (int64_t)b0 * ldx, Bc, ldx, y0, ldy, d_bias, d_ws, o, stream, &pl0, fn0,
+                      &peers);
     if (st) return st;
   }
   return GQSA_OK;

@@ -372,6 +372,14 @@ __device__ __forceinline__ void collect(const KParams& p, int gw, int w_last, fl
 
 // y element i: fp32, or fp16 rounded to nearest even (PAPER.md:134 step 5).
 __device__ __forceinline__ void store_y(const KParams& p, int64_t i, float v) {
+  if (p.n_peers) {  // fused all-gather: this shard's rows land in every rank's full y
+#pragma unroll 1
+    for (int k = 0; k < p.n_peers; ++k) {
+      if (p.out_f16) reinterpret_cast<__half*>(p.peer_y[k])[i + p.row_offset] = __float2half_rn(v);
+      else reinterpret_cast<float*>(p.peer_y[k])[i + p.row_offset] = v;
+    }
+    return;
+  }
   if (p.out_f16) reinterpret_cast<__half*>(p.Y)[i] = __float2half_rn(v);
   else reinterpret_cast<float*>(p.Y)[i] = v;
 }

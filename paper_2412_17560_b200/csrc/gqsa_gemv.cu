@@ -127,7 +127,10 @@ __global__ void __launch_bounds__(max_threads_for(BITS, B, FEW), min_blocks_for(
     for (int b = 0; b < B; ++b) store_y(p, (int64_t)b * p.ldy + erow, bias);
   }
   trace_point(p, gw, lane, 2);
-  if (t_end <= t_begin) return;
+  if (t_end <= t_begin) {
+    if (p.n_peers) __threadfence_system();
+    return;
+  }
 
   // ---- stream the warp's tile range; lane = one row of the current slice
   float acc[kMaxBatch];
@@ -212,6 +215,7 @@ __global__ void __launch_bounds__(max_threads_for(BITS, B, FEW), min_blocks_for(
     p.trace[(int64_t)gw * 8 + 7] = 0;
   }
   trace_point(p, gw, lane, 5);
+  if (p.n_peers) __threadfence_system();  // peer stores visible before the launch completes
 }
 
 // ---------------------------------------------------------------- launchers

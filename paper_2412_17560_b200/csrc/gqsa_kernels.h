@@ -10,6 +10,7 @@ constexpr int kMaxStages = 8;            // tiles in flight per warp (shared-mem
 constexpr int kMinStages = 2;
 constexpr int kSmemPerSm = 228 * 1024;   // shared memory per SM (incl. 1 KB reserved per CTA)
 constexpr int kMaxBatch = 8;
+constexpr int kMaxPeers = 8;            // ranks of a fused all-gather (one NVLink domain)
 constexpr int kMaxCtasPerSm = 1;         // default residency: one CTA of up to 16 warps per SM
 constexpr int kCoResidentKernels = 2;    // leave room for the next PDL-launched GEMV
 // Register budget: 4 resident CTAs (64 regs/thread) at batch 1 -- the HBM
@@ -57,6 +58,13 @@ struct KParams {
   int32_t slice_k;         // 1: data-centric partition (whole slices per warp, no fix-up)
   int32_t out_f16;         // 1: Y is fp16 (RNE of the fp32 result)
   int32_t fix_offset;      // shared-memory offset of the intra-CTA fix-up records (0: all global)
+  // Fused all-gather epilogue (gqsa_gemm_allgather): when n_peers > 0 every
+  // output element is stored into each peer's full-length Y (peer pointers,
+  // e.g. NVLink P2P / symmetric memory) at global row row_offset + row,
+  // instead of into Y.
+  int32_t n_peers;
+  int32_t row_offset;
+  uint64_t peer_y[kMaxPeers];
 };
 
 // Persistent chain kernel (gqsa_chain.cu): one launch runs up to kMaxChain

@@ -80,6 +80,7 @@ EXPORTS = (
     "gqsa_gemv", "gqsa_gemm_smallbatch", "gqsa_gemm_ex", "gqsa_hostio_stage_size",
     "gqsa_gemm_hostio", "gqsa_chain_workspace_size", "gqsa_gemm_chain",
     "gqsa_compress_nnzg", "gqsa_compress", "gqsa_multi_hostio_stage_size", "gqsa_gemm_multi_hostio",
+    "gqsa_gemm_allgather",
     "gqsa_launch_plan", "gqsa_launch_count", "gqsa_status_string", "gqsa_version",
     "gqsa_debug_trace",
 )
@@ -112,6 +113,8 @@ def lib() -> ctypes.CDLL:
     L.gqsa_multi_hostio_stage_size.argtypes = [PDESC, I32, I32, PSZ]
     L.gqsa_gemm_multi_hostio.argtypes = [PDESC, ctypes.POINTER(P), I32, I32, P, P, P, SZ, ctypes.POINTER(P),
                                          ctypes.POINTER(SZ), P]
+    L.gqsa_gemm_allgather.argtypes = [ctypes.POINTER(Desc), P, P, I32, I64, ctypes.POINTER(P), I32, I64, I32, I32,
+                                      P, P, SZ, P]
     L.gqsa_compress_nnzg.argtypes = [I32, I32, I32, ctypes.c_double, ctypes.POINTER(ctypes.c_int64)]
     L.gqsa_compress.argtypes = [P, I32, I32, I32, I32, P, ctypes.c_double, ctypes.POINTER(BSR), P]
     L.gqsa_chain_workspace_size.argtypes = [ctypes.POINTER(ChainItem), I32, I32, PSZ]
@@ -329,6 +332,20 @@ def multi_hostio_stage_size(descs, batch: int = 1) -> int:
     _check(lib().gqsa_multi_hostio_stage_size(_desc_array(descs), len(descs), int(batch), ctypes.byref(n)),
            "gqsa_multi_hostio_stage_size")
     return n.value
+
+
+def gemm_allgather(desc: Desc, d_blob, X, peer_Y, row_offset: int, bias=None, ws=None, stream=None) -> None:
+    """gqsa_gemm_allgather: this rank's shard GEMM storing its rows directly into
+    every tensor of ``peer_Y`` (each the full [B][ldy] output, same dtype,
+    fp32 or fp16) at global rows row_offset + r."""
+    import torch
+    n = len(peer_Y)
+    ptrs = (ctypes.c_void_p * n)(*[t.data_ptr() for t in peer_Y])
+    out16 = 1 if peer_Y[0].dtype == torch.float16 else 0
+    _check(lib().gqsa_gemm_allgather(ctypes.byref(desc), d_blob.data_ptr(), X.data_ptr(), X.shape[0], X.stride(0),
+                                     ptrs, n, peer_Y[0].stride(0), int(row_offset), out16,
+                                     bias.data_ptr() if bias is not None else None, ws.data_ptr(), ws.numel(),
+                                     _stream_ptr(stream)), "gqsa_gemm_allgather")
 
 
 class MultiHostIO:

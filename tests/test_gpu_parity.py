@@ -298,3 +298,31 @@ def test_launch_plan_is_persistent_stream_k():
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     assert p.active_warps == min(d.num_tiles, p.grid * p.warps_per_cta)
     assert p.grid <= 2 * sms and p.x_in_smem == 1
+
+
+@pytest.mark.parametrize("rows,cols,B,P,f16", [(1000, 2048, 1, 2, False), (4096, 4096, 2, 4, False),
+                                               (2048, 14336, 8, 2, False), (512, 1024, 3, 8, True)])
+def test_fused_allgather_epilogue_simulated_ranks(rows, cols, B, P, f16):
+    """gqsa_gemm_allgather on one GPU with P simulated ranks: each rank's row
+    shard stores its rows into ALL P full-length outputs (here local buffers
+    standing for the peers' NVLink-mapped y); every output must equal the
+    oracle's full result exactly (exact-integer mode; fp16 output = RNE)."""
+    seed = synth.seed_for(f"allgather/{rows}/{cols}/{B}/{P}")
+    bsr = synth.make_layer(seed, rows, cols, sparsity=0.5, mode="exact_int")
+    x = synth.make_x(seed + 1, B, cols, mode="exact_int")
+    X = torch.from_numpy(x).view(torch.float16).cuda()
+    dt = torch.float16 if f16 else torch.float32
+    Ys = [torch.full((B, rows), float("nan"), dtype=dt, device="cuda") for _ in range(P)]
+    for r in range(P):
+        lo, hi = synth.shard_rows(rows, P, r)
+        blob, desc = gqsa.pack(bsr, lo, hi)
+        ws = torch.zeros(gqsa.workspace_size(desc, B), dtype=torch.uint8, device="cuda")
+        gqsa.gemm_allgather(desc, torch.from_numpy(blob).cuda(), X, Ys, row_offset=lo, ws=ws)
+    torch.cuda.synchronize()
+    ref = O.gemv(bsr, x)
+    for Y in Ys:
+        got = Y.cpu().numpy()
+        if f16:
+            assert np.array_equal(got, ref.astype(np.float16))
+        else:
+            assert np.array_equal(got.astype(np.float64), ref)
