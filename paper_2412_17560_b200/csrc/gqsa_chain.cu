@@ -188,11 +188,14 @@ __global__ void __launch_bounds__(kChainThreads, 1) gqsa_chain_kernel(const __gr
         if (two) read_tile<BITS>(tr1, slot + tb, lane);
         __syncwarp();  // every lane has read the slot: refill it (possibly with the next item's tiles)
         if (lane == 0) {
-      // No fence.proxy.async here: the slot's generic-proxy READS (above,
-      // completed into registers before __syncwarp returns) precede the
-      // bulk copy's async-proxy WRITES in program order; the same
-      // consumer-release pattern CUTLASS pipelines use (an mbarrier arrive,
-      // no proxy fence).  Measured: the MEMBAR it emitted cost 2% per step.
+      // Generic-proxy reads of the slot, then an async-proxy (TMA) write to
+      // it.  By default no fence.proxy.async (its MEMBAR cost 2 % per step):
+      // the reads return within tens of cycles, the copy's first write lands
+      // a global round trip (>= 0.5 us) later.  That is a timing argument,
+      // not a memory-model guarantee; -DGQSA_PROXY_FENCE restores the fence.
+#ifdef GQSA_PROXY_FENCE
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
           fill_slot(s);
         }
         if (++s == NP) { s = 0; phase ^= 1u; }
