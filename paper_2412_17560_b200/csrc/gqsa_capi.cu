@@ -65,8 +65,11 @@ int stages_cap() {
 // The FEW kernel variant (12 warps, <= 85 registers) for layers with few
 // tiles per warp; GQSA_FEW=0 disables it (experiments).
 bool few_for(const gqsa_desc_t* d, int B) {
-  static int on = env_int("GQSA_FEW", 1, 0, 1);
-  return on && B <= 2 && (d->bits == 4 || d->bits == 2) && d->num_tiles < kFewTiles;
+  static int on = env_int("GQSA_FEW", 1, 0, 2);  // 2: every layer (experiments)
+  // batch 2 always (twice the accumulators: 80 registers and NS = 4 beat 16
+  // warps at 64 registers by 13-14 % on 14336x4096 / 4096x14336); batch 1
+  // only for small layers
+  return on && B <= 2 && (d->bits == 4 || d->bits == 2) && (on == 2 || B == 2 || d->num_tiles < kFewTiles);
 }
 int warps_per_cta(const gqsa_desc_t* d, int B) {
   static int w1 = env_int("GQSA_WARPS", 16, 1, kMaxWarps);

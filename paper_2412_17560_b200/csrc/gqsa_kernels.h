@@ -25,10 +25,10 @@ constexpr int kCoResidentKernels = 2;    // leave room for the next PDL-launched
 #define GQSA_B12_THREADS kMaxThreads
 #define GQSA_B12_MINB 1
 #endif
-// FEW: the variant for layers with few tiles per warp (small layers, e.g.
-// 4096x4096 at S50): 12 warps per CTA with up to 85 registers (two CTAs per
-// SM for PDL co-residency).  Measured (B200): 4096x4096 W4S50 B=1 5.13 ->
-// 4.47 us; no change on 14336x4096 / 4096x14336, which keep 16 warps.
+// FEW: 12 warps per CTA with up to 85 registers (two CTAs per SM for PDL
+// co-residency), for batch 1 on layers with few tiles per warp (e.g.
+// 4096x4096 at S50: 5.13 -> 4.47 us; 14336x4096 / 4096x14336 unchanged, they
+// keep 16 warps) and for every batch-2 layer (-13..14 %).
 constexpr int kFewWarps = 12;
 constexpr int kFewTiles = 148 * 16 * 4;  // below ~4 tiles per warp of a 16-warp grid
 constexpr int max_threads_for(int bits, int B, bool few = false) {
