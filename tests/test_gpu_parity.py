@@ -326,3 +326,58 @@ def test_fused_allgather_epilogue_simulated_ranks(rows, cols, B, P, f16):
             assert np.array_equal(got, ref.astype(np.float16))
         else:
             assert np.array_equal(got.astype(np.float64), ref)
+
+
+def test_pdl_dependent_launch_chain_reads_producer_output():
+    """Back-to-back launches where launch k reads, as its x, the fp16 output
+    launch k-1 just wrote (Programmatic Dependent Launch: weights are
+    prefetched before griddepcontrol.wait, x only after it).  Inputs start as
+    NaN, so a launch that read x early would produce NaN; every layer must
+    match the oracle on the activations its producer left, in a CUDA graph
+    replayed several times."""
+    dims = [4096, 1024, 4096, 2048, 4096, 14336, 4096]
+    bsrs = [synth.make_layer(synth.seed_for(f"pdl/{i}"), dims[i + 1], dims[i], sparsity=0.5)
+            for i in range(len(dims) - 1)]
+    layers = [gqsa.Layer(b) for b in bsrs]
+    bufs = [torch.full((1, d), float("nan"), dtype=torch.float16, device="cuda") for d in dims]
+    x0 = synth.make_x(77, 1, dims[0])
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for i, L in enumerate(layers):
+            gqsa.gemm_ex(L.desc, L.blob, bufs[i], bufs[i + 1], ws=L.ws, stream=s)
+    for rep in range(3):
+        for b in bufs[1:]:
+            b.fill_(float("nan"))
+        bufs[0].copy_(torch.from_numpy(x0).view(torch.float16))
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        for i, b in enumerate(bsrs):
+            xin = bufs[i].cpu().numpy().view(np.uint16)
+            y = bufs[i + 1].cpu().numpy().astype(np.float64)
+            assert np.isfinite(y).all(), (rep, i)
+            ref = O.gemv(b, xin)
+            assert np.all(np.abs(y - ref) <= 2.0 ** -10 * np.abs(ref) + 1e-5 * abs_bound(b, xin)), (rep, i)
+
+
+def test_concurrent_streams_share_one_blob():
+    """One packed blob used by two streams at once, each with its own
+    workspace (include/gqsa.h ownership rules): results stay bit-exact."""
+    bsr = synth.make_layer(91, 2048, 4096, sparsity=0.5, mode="exact_int")
+    blob, desc = gqsa.pack(bsr)
+    d_blob = torch.from_numpy(blob).cuda()
+    xs = [synth.make_x(92 + k, 2, 4096, mode="exact_int") for k in range(2)]
+    X = [torch.from_numpy(x).view(torch.float16).cuda() for x in xs]
+    refs = [O.gemv(bsr, x) for x in xs]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    wss = [torch.zeros(gqsa.workspace_size(desc, 2), dtype=torch.uint8, device="cuda") for _ in range(2)]
+    Ys = [[torch.empty(2, 2048, dtype=torch.float32, device="cuda") for _ in range(20)] for _ in range(2)]
+    torch.cuda.synchronize()
+    for it in range(20):
+        for k in range(2):
+            gqsa.gemm_smallbatch(desc, d_blob, X[k], Ys[k][it], None, wss[k], stream=streams[k])
+    torch.cuda.synchronize()
+    for k in range(2):
+        for Y in Ys[k]:
+            assert np.array_equal(Y.cpu().numpy().astype(np.float64), refs[k])
