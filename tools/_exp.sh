@@ -1,6 +1,6 @@
 make -s >/dev/null 2>&1
-timeout 600 python -m pytest tests/test_gpu_chain.py -q > gpurun_out/t.log 2>&1; tail -1 gpurun_out/t.log
-timeout 300 python tools/trace_chain.py 2>&1 | tail -4
-for P in chain launches; do timeout 300 python bench.py --path $P --steps 5000 --warmup 100 --no-cpu-baseline --e2e-steps 10 2>/dev/null | tail -1 | python -c "
-import json,sys; d=json.loads(sys.stdin.readline()); print('$P', d['value'], d['us_per_step'])"; done
-timeout 1500 python tools/stack_bench.py --batches 1 --out gpurun_out/stk > gpurun_out/stack.log 2>&1; grep "^| W4S50" gpurun_out/stack.log
+for cfg in "GQSA_CTAS_PER_SM=1" "GQSA_CTAS_PER_SM=2 GQSA_WARPS=8 GQSA_FEW=0"; do
+  env $cfg timeout 300 python bench.py --steps 5000 --warmup 100 --no-cpu-baseline --e2e-steps 10 2>gpurun_out/err.txt | tail -1 | python -c "
+import json,sys
+d=json.loads(sys.stdin.readline()); print('$cfg', d['value'], d['us_per_step'], [l['us'] for l in d['layers']])" || tail -3 gpurun_out/err.txt
+done
