@@ -1,6 +1,2 @@
 make -s >/dev/null 2>&1
-for cfg in "GQSA_CTAS_PER_SM=1" "GQSA_CTAS_PER_SM=2 GQSA_WARPS=8 GQSA_FEW=0"; do
-  env $cfg timeout 300 python bench.py --steps 5000 --warmup 100 --no-cpu-baseline --e2e-steps 10 2>gpurun_out/err.txt | tail -1 | python -c "
-import json,sys
-d=json.loads(sys.stdin.readline()); print('$cfg', d['value'], d['us_per_step'], [l['us'] for l in d['layers']])" || tail -3 gpurun_out/err.txt
-done
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:gqsa -s 27 -c 60 --csv --log-file gpurun_out/launches.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 2 > gpurun_out/bench_ncu.log 2>&1; tail -1 gpurun_out/bench_ncu.log
