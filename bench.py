@@ -212,6 +212,8 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("GQSA_SHARE_DEVICE") == "1":  # test hook: several ranks on one GPU (gloo)
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     fused = args.allgather == "fused"
@@ -220,7 +222,11 @@ def run_gpu(args):
     if world > 1 or fused:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
-        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
+        backend = os.environ.get("GQSA_DIST_BACKEND", "nccl")  # gloo: test hook for the plumbing
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
+        else:
+            dist.init_process_group(backend, rank=rank, world_size=world)
 
     bits, sp, B = 4, 0.5, args.batch
     layers = make_layers(bits, sp, B, world, rank)

@@ -1,2 +1,2 @@
 make -s >/dev/null 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:gqsa -s 27 -c 60 --csv --log-file gpurun_out/launches.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 2 > gpurun_out/bench_ncu.log 2>&1; tail -1 gpurun_out/bench_ncu.log
+timeout 900 python -m pytest tests/test_gpu_bench_multirank.py -q > gpurun_out/t.log 2>&1; tail -3 gpurun_out/t.log; grep -E "^E " gpurun_out/t.log | head -10
