@@ -387,9 +387,21 @@ def run_gpu(args):
             b_.record(stream)
             torch.cuda.synchronize()
             us = a.elapsed_time(b_) * 1e3 / (reps * R)
+            # spread over 50 replays (each R launches; an event between replays
+            # breaks the PDL overlap at the replay boundary, so these sit a
+            # little above the back-to-back mean "us")
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(51)]
+            with torch.cuda.stream(stream):
+                evs[0].record(stream)
+                for k in range(50):
+                    g.replay()
+                    evs[k + 1].record(stream)
+            torch.cuda.synchronize()
+            per = np.array([evs[k].elapsed_time(evs[k + 1]) * 1e3 / R for k in range(50)])
             cb = counted_bytes(desc.rows, desc.cols, desc.nnzg, bits, B)
             layer_rows.append({"shape": f"{desc.rows}x{desc.cols}", "role": L["name"],
                                "nnzg": desc.nnzg, "counted_bytes": cb, "us": round(us, 3),
+                               "replay_us_p10_p50_p90": [round(float(np.percentile(per, q)), 3) for q in (10, 50, 90)],
                                "gbs": round(cb / us / 1e3, 1),
                                "frac_of_8tbs": round(cb / us / 1e3 / NOMINAL_HBM_GBS, 4),
                                "frac_of_measured": round(cb / us / 1e3 / hbm_peak, 4)})

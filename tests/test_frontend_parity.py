@@ -102,3 +102,16 @@ def test_compress_errors():
     with pytest.raises(gqsa.GQSAError) as e:
         frontend.compress(np.zeros((4, 30), np.float32), np.ones(30), 0.5, 4)
     assert e.value.status == -1
+
+
+def test_compress_g8_is_plain_bsr_but_not_packable():
+    """The front-end handles any G dividing K (plain BSR, checked against the
+    oracle); the packer and kernels take G = 16 only (GQSA_ERR_UNSUPPORTED)."""
+    W = synth.make_dense(31, 16, 128)
+    d = np.ones(128)
+    ref, _, _ = F.compress_layer(W, d, 0.5, 4, 8)
+    got = frontend.compress(W, d, 0.5, 4, 8)
+    _same_bsr(got, ref)
+    with pytest.raises(gqsa.GQSAError) as e:
+        gqsa.pack(got)
+    assert e.value.status == -3

@@ -197,3 +197,23 @@ def test_chain_argument_errors():
     with pytest.raises(gqsa.GQSAError) as e:
         gqsa.gemm_chain([(desc, d_blob, X, Y, None, 1)], ws[:64])
     assert e.value.status == -4
+
+
+def test_chain_max_items_and_ws_reuse():
+    """16 items (GQSA_MAX_CHAIN), alternating dependent / independent, reused
+    workspace over several launches: exact results every time."""
+    items, refs = [], []
+    for i in range(16):
+        rows, cols = (128 + 64 * (i % 5), 256 * (1 + i % 3))
+        bsr = synth.make_layer(100 + i, rows, cols, sparsity=0.5, mode="exact_int")
+        x = synth.make_x(200 + i, 1, cols, mode="exact_int")
+        desc, d_blob = _dev_blob(bsr)
+        items.append((desc, d_blob, _x(x), torch.empty(1, rows, dtype=torch.float32, device="cuda"), None, i % 2))
+        refs.append(O.gemv(bsr, x))
+    ws = run_chain(items)
+    for _ in range(3):
+        for it in items:
+            it[3].fill_(float("nan"))
+        run_chain(items, ws)
+        for it, ref in zip(items, refs):
+            assert np.array_equal(it[3].cpu().numpy().astype(np.float64), ref)
