@@ -88,7 +88,13 @@ struct SmemPlan {
   int stages, warps, batch, launches;
   size_t ring, total, fix;
 };
-size_t x_bytes(int B, int cols) { return (size_t)B * cols * 2 + (size_t)B * pq_bytes_per_row(B, cols); }
+// x and its column sums, rounded up to 128 B: the fix-up records and the
+// TMA ring that follow must stay 16-B aligned (bulk-copy destinations; e.g.
+// B = 3, K = 208 gives 1560 B unrounded).
+size_t x_bytes(int B, int cols) {
+  const size_t v = (size_t)B * cols * 2 + (size_t)B * pq_bytes_per_row(B, cols);
+  return (v + 127) / 128 * 128;
+}
 size_t ring_bytes_for(const gqsa_desc_t* d, int W, int ns) {  // ring + its mbarriers
   return (size_t)W * ns * tile_bytes(d->bits) + (size_t)W * kMaxStages * 8;
 }

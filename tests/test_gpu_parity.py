@@ -75,6 +75,8 @@ EXACT_CASES = [
     (512, 2048, 4, 0.5, "skewed", 1),
     (300, 1024, 4, 0.3, "row_balanced", 4),
     (77, 208, 4, 0.2, "uniform", 8),      # ragged tile tail, odd rows
+    (77, 208, 2, 0.5, "uniform", 3),      # x + column sums of 1560 B: ring alignment (sanitizer find)
+    (41, 48, 4, 0.5, "uniform", 5),       # K = 48: 3 column groups, odd batch
     (3, 16384, 4, 0.5, "uniform", 2),     # few long rows: rows span many warps
     (1, 32768, 4, 0.5, "uniform", 1),     # one row over 32 lanes (S = 32), max K
     (4096, 16, 4, 0.5, "uniform", 1),     # K = G: many empty rows, 1-group rows

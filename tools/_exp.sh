@@ -1,4 +1,3 @@
 make -s >/dev/null 2>&1
-timeout 900 python -m pytest tests -m gpu -q > gpurun_out/t.log 2>&1; tail -2 gpurun_out/t.log; grep -E "^E |FAILED" gpurun_out/t.log | head
-timeout 600 python bench.py --steps 5000 --warmup 100 --no-cpu-baseline --e2e-steps 200 2>/dev/null | grep "^{" | python -c "
-import json,sys; d=json.loads(sys.stdin.readline()); print(d['value'], [(l['us'], l['us_p10_p50_p90']) for l in d['layers']])"
+GQSA_FIX_LOCAL=0 timeout 1500 compute-sanitizer --tool racecheck --racecheck-report hazard --print-limit 200 python tools/sanitize_small.py > gpurun_out/racecheck2.log 2>&1; echo racecheck rc=$?; tail -2 gpurun_out/racecheck2.log
+grep -E "^=========     (Read|Write) Thread" gpurun_out/racecheck2.log | sed 's/Thread ([0-9,]*)//; s/+0x[0-9a-f]*//' | sort | uniq -c | head -20

@@ -1,0 +1,46 @@
+"""Small launches of every kernel family for compute-sanitizer (memcheck /
+racecheck / synccheck): gemv, small-batch GEMM (split and co-resident
+plans), Slice-K, fp16 output, chain, fused all-gather.  Exits non-zero on a
+mismatch against the oracle (exact-integer mode)."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from oracle import gqsa_oracle as O  # noqa: E402
+from paper_2412_17560_b200 import gqsa, synth  # noqa: E402
+
+ok = True
+for rows, cols, bits, B, mask in ((300, 1024, 4, 1, "uniform"), (77, 208, 2, 3, "uniform"),
+                                  (512, 2048, 4, 2, "skewed"), (64, 4096, 8, 1, "uniform"),
+                                  (128, 14336, 4, 8, "uniform"), (5, 64, 4, 1, "uniform")):
+    bsr = synth.make_layer(rows + cols, rows, cols, bits=bits, sparsity=0.5, mask=mask, mode="exact_int")
+    x = synth.make_x(rows, B, cols, mode="exact_int")
+    L = gqsa.Layer(bsr)
+    X = torch.from_numpy(x).view(torch.float16).cuda()
+    ref = O.gemv(bsr, x)
+    for part in (gqsa.PARTITION_STREAM_K, gqsa.PARTITION_SLICE_K):
+        y = L.gemm(X, partition=part).cpu().numpy().astype(np.float64)
+        ok &= np.array_equal(y, ref)
+    y16 = L.gemm(X, out_dtype=torch.float16, partition=gqsa.PARTITION_SLICE_K).cpu().numpy()
+    ok &= np.array_equal(y16, ref.astype(np.float16))
+    if bits != 8 and B <= 2:
+        Y = torch.empty(B, rows, dtype=torch.float32, device="cuda")
+        items = [(L.desc, L.blob, X, Y, None, 1)]
+        ws = torch.zeros(gqsa.chain_workspace_size(items, B), dtype=torch.uint8, device="cuda")
+        gqsa.gemm_chain(items, ws)
+        ok &= np.array_equal(Y.cpu().numpy().astype(np.float64), ref)
+    Ys = [torch.zeros(B, rows, dtype=torch.float32, device="cuda") for _ in range(2)]
+    for r in range(2):
+        lo, hi = synth.shard_rows(rows, 2, r)
+        blob, desc = gqsa.pack(bsr, lo, hi)
+        wsr = torch.zeros(gqsa.workspace_size(desc, B), dtype=torch.uint8, device="cuda")
+        gqsa.gemm_allgather(desc, torch.from_numpy(blob).cuda(), X, Ys, row_offset=lo, ws=wsr)
+    for Yk in Ys:
+        ok &= np.array_equal(Yk.cpu().numpy().astype(np.float64), ref)
+    torch.cuda.synchronize()
+print("sanitize_small:", "ok" if ok else "MISMATCH")
+sys.exit(0 if ok else 1)
