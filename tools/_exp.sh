@@ -1,3 +1,2 @@
 make -s >/dev/null 2>&1
-GQSA_FIX_LOCAL=0 timeout 1500 compute-sanitizer --tool racecheck --racecheck-report hazard --print-limit 200 python tools/sanitize_small.py > gpurun_out/racecheck2.log 2>&1; echo racecheck rc=$?; tail -2 gpurun_out/racecheck2.log
-grep -E "^=========     (Read|Write) Thread" gpurun_out/racecheck2.log | sed 's/Thread ([0-9,]*)//; s/+0x[0-9a-f]*//' | sort | uniq -c | head -20
+timeout 1500 python -m pytest tests/test_gpu_fuzz.py -q -x > gpurun_out/t.log 2>&1; tail -2 gpurun_out/t.log; grep -E "^E |FAILED" gpurun_out/t.log | head -5
