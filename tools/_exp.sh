@@ -1,2 +1,2 @@
 make -s >/dev/null 2>&1
-timeout 1500 python -m pytest tests/test_gpu_fuzz.py -q -x > gpurun_out/t.log 2>&1; tail -2 gpurun_out/t.log; grep -E "^E |FAILED" gpurun_out/t.log | head -5
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:gqsa -s 27 -c 60 --csv --log-file gpurun_out/launches.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 2 > gpurun_out/bench_ncu.log 2>&1; tail -1 gpurun_out/bench_ncu.log
