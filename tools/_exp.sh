@@ -1,2 +1,2 @@
 make -s >/dev/null 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:gqsa -s 27 -c 60 --csv --log-file gpurun_out/launches.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 2 > gpurun_out/bench_ncu.log 2>&1; tail -1 gpurun_out/bench_ncu.log
+timeout 1800 python tools/stack_bench.py --out gpurun_out/r01_stack > gpurun_out/stack.log 2>&1; grep -A20 "## G" gpurun_out/r01_stack.md

@@ -176,6 +176,16 @@ def main():
                 recs.append(r)
                 print(json.dumps(r), flush=True)
                 lines.append(f"| {model} | {name} | {n}x{k} | {P} | {n // P}x{k} | {us:.2f} | {r['gbs']:.0f} |")
+    lines += ["", "## G. Qwen2.5-14B full matrices, W4S50, B = 1 / 2 / 4 / 8 on one GPU (SURVEY §8(d) C4, P = 1)", "",
+              "| matrix | N x K | B | µs | GB/s |", "|---|---|---|---|---|"]
+    for name, n, k in qwen:
+        for B in batches:
+            us, nb = time_layer(n, k, 4, 0.5, B)
+            r = dict(section="G", model="Qwen2.5-14B", matrix=name, N=n, K=k, B=B, us=round(us, 3), bytes=nb,
+                     gbs=round(nb / us / 1e3, 1))
+            recs.append(r)
+            print(json.dumps(r), flush=True)
+            lines.append(f"| {name} | {n}x{k} | {B} | {us:.2f} | {r['gbs']:.0f} |")
     lines.append("")
     if a.out:
         open(a.out + ".md", "w").write("\n".join(lines) + "\n")
