@@ -23,6 +23,7 @@ size_t g_trace_bytes = 0;
 struct DevInfo {
   int sms = 0;
   bool attr_set[9][2 * (kMaxBatch + 1)] = {};
+  bool chain_attr_set[9][3] = {};
 };
 std::mutex g_mu;
 DevInfo g_dev[64];
@@ -522,9 +523,10 @@ extern "C" int gqsa_gemm_chain(const gqsa_chain_item_t* items, int32_t n, int32_
   const void* fn = select_chain_kernel(items[0].desc->bits, B);
   if (!fn) return GQSA_ERR_UNSUPPORTED;
   {
-    static bool set[9][3] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return GQSA_ERR_CUDA;
     std::lock_guard<std::mutex> lk(g_mu);
-    bool& s = set[items[0].desc->bits][B];
+    bool& s = g_dev[dev].chain_attr_set[items[0].desc->bits][B];
     if (!s) {
       if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem) != cudaSuccess ||
           cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,

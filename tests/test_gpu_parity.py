@@ -235,25 +235,36 @@ def test_multi_hostio_end_to_end_path():
     per layer, one D2H copy of concatenated outputs (bench.py's e2e path)."""
     shapes = [(300, 1024), (77, 208), (1024, 4096)]
     for B in (1, 2):
-        layers, xs, refs = [], [], []
+        layers, xs, refs, xs2, refs2 = [], [], [], [], []
         for i, (n, k) in enumerate(shapes):
             seed = synth.seed_for(f"multi/{i}/{n}/{k}/{B}")
             bsr = synth.make_layer(seed, n, k, sparsity=0.5, mode="exact_int")
             x = synth.make_x(seed + 1, B, k, mode="exact_int")
+            x2 = synth.make_x(seed + 2, B, k, mode="exact_int")
             layers.append(gqsa.Layer(bsr))
             xs.append(x.reshape(-1))
+            xs2.append(x2.reshape(-1))
             refs.append(O.gemv(bsr, x))
+            refs2.append(O.gemv(bsr, x2))
         descs = [L.desc for L in layers]
         hX = torch.from_numpy(np.concatenate(xs)).view(torch.float16).pin_memory()
         hY = torch.full((sum(B * n for n, _ in shapes),), float("nan"), dtype=torch.float32).pin_memory()
         stage = torch.empty(gqsa.multi_hostio_stage_size(descs, B), dtype=torch.uint8, device="cuda")
-        gqsa.gemm_multi_hostio(descs, [L.blob for L in layers], hX, hY, stage, [L.ws for L in layers], batch=B)
-        torch.cuda.synchronize()
-        got = hY.numpy().astype(np.float64)
-        off = 0
-        for (n, _), ref in zip(shapes, refs):
-            assert np.array_equal(got[off:off + B * n].reshape(B, n), ref)
-            off += B * n
+        # default stream (eager) once, then a side stream three times: the
+        # library captures a CUDA graph on the first call and replays it
+        # (fresh host inputs each time: the graph's copies read them at replay)
+        side = torch.cuda.Stream()
+        for k, st in enumerate([None, side, side, side]):
+            hX.copy_(torch.from_numpy(np.concatenate(xs) if k % 2 == 0 else np.concatenate(xs2)).view(torch.float16))
+            hY.fill_(float("nan"))
+            gqsa.gemm_multi_hostio(descs, [L.blob for L in layers], hX, hY, stage, [L.ws for L in layers], batch=B,
+                                   stream=st)
+            torch.cuda.synchronize()
+            got = hY.numpy().astype(np.float64)
+            off = 0
+            for (n, _), ref, ref2 in zip(shapes, refs, refs2):
+                assert np.array_equal(got[off:off + B * n].reshape(B, n), ref if k % 2 == 0 else ref2), (k, n)
+                off += B * n
 
 
 def test_argument_errors():
