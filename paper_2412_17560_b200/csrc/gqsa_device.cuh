@@ -13,20 +13,6 @@
 namespace gqsa {
 
 // ---------------------------------------------------------------- PTX helpers
-__device__ __forceinline__ uint4 ldg_stream128(const void* p) {
-  uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p));
-  return v;
-}
-__device__ __forceinline__ uint2 ldg_stream64(const void* p) {
-  uint2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v2.u32 {%0,%1}, [%2];"
-               : "=r"(v.x), "=r"(v.y)
-               : "l"(p));
-  return v;
-}
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -168,14 +154,6 @@ struct TileRegs {
   uint32_t rem;                    // tiles from this one to its slice's last tile
 };
 
-template <int BITS>
-__device__ __forceinline__ void load_tile(TileRegs<BITS>& r, const uint8_t* tile, int lane) {
-  r.codes[0] = ldg_stream128(tile + kTileHeaderBytes + lane * 16);
-  if (BITS == 4) r.codes[BITS == 4 ? 1 : 0] = ldg_stream128(tile + kTileHeaderBytes + 512 + lane * 16);
-  r.sz = ldg_stream128(tile + off_sz(BITS) + lane * 16);
-  r.cols = ldg_stream64(tile + off_cols(BITS) + lane * 8);
-  r.hdr = __ldg(reinterpret_cast<const uint32_t*>(tile));  // broadcast within the warp
-}
 
 // Group code word(s) of slot u from the lane's codes.
 template <int BITS>

@@ -1,4 +1,4 @@
-// gqsa_gemv.cu -- sm_100a Stream-K group-sparse W4/W2 GEMV / small-batch GEMM.
+// gqsa_gemv.cu -- sm_100a Stream-K group-sparse W2/W4/W8 GEMV / small-batch GEMM.
 //
 // Computes, for every batch column b < B and output row r (PAPER.md:64-69
 // [Eq. 3], 95-101 [§3.2 BSR], 134 [§3.5]):
@@ -13,15 +13,19 @@
 //  * Task-centric partition (PAPER.md:161 Stream-K, App. J): the
 //    tile stream (128 groups per tile) is cut into contiguous, equal (+-1
 //    tile) ranges, one per WARP, regardless of row or slice boundaries.
-//  * Weights stream HBM -> registers with 128-bit L1::no_allocate loads,
-//    double-buffered per warp; the first tiles are requested BEFORE
-//    griddepcontrol.wait so they overlap the previous kernel (PDL).
+//  * Weights stream HBM -> shared memory through a per-warp ring of 1-D TMA
+//    bulk copies (tile pairs, one mbarrier per pair, evict-first L2 policy);
+//    the first pairs are requested BEFORE griddepcontrol.wait so they overlap
+//    the previous kernel (PDL; this CTA uses at most half an SM so the next
+//    launch is resident during its tail).
 //  * Activations are staged in shared memory once per CTA, together with the
-//    per-column-group sums X_{b,c} (fp32).
-//  * Dequantization: LOP3 magic (0x6400 = fp16 1024) turns 4-bit (2-bit)
-//    fields into exact fp16 integers; FHFMA (fma.rn.f32.f16) multiplies the
-//    exact fp16 code by fp16 x and accumulates in fp32 (products exact).
-//    No tensor cores: batch-1 GEMV is bandwidth-bound.
+//    per-column-group sums (P, Q) the offset-folded dequantization needs.
+//  * Dequantization: LOP3 magic (0x6400 = fp16 1024) turns code fields into
+//    exact fp16 (1024 + 2^k q); FHFMA (fma.rn.f32.f16) multiplies them by fp16
+//    x with exact products and fp32 accumulation; the offsets are removed once
+//    per group with (P, Q).  No tensor cores: the rows of a warp hold groups
+//    at unrelated columns, and batch 1 is bandwidth-bound
+//    (PAPER.md:9, 134).
 //  * Fix-up: a slice split across warps is finished by the warp that owns its
 //    first tile, which adds the per-lane partials its successors publish
 //    (64-bit {value, flag} slots, no fences), in warp order: deterministic.
