@@ -1,2 +1,3 @@
 make -s >/dev/null 2>&1
-timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/t.log 2>&1; tail -2 gpurun_out/t.log; grep -E "^E |FAILED" gpurun_out/t.log | head -5
+for rep in 1 2 3; do for f in 1 2; do for sh in "14336 4096" "4096 14336"; do set -- $sh
+GQSA_FEW=$f timeout 300 python tools/prof_layer.py --rows $1 --cols $2 --launches 1 --time 2>&1 | tail -1 | sed "s/^/FEW=$f /"; done; done; done
