@@ -1,3 +1,2 @@
 make -s >/dev/null 2>&1
-for rep in 1 2 3; do for f in 1 2; do for sh in "14336 4096" "4096 14336"; do set -- $sh
-GQSA_FEW=$f timeout 300 python tools/prof_layer.py --rows $1 --cols $2 --launches 1 --time 2>&1 | tail -1 | sed "s/^/FEW=$f /"; done; done; done
+timeout 3000 compute-sanitizer --tool memcheck --print-limit 10 python -m pytest tests/test_gpu_parity.py tests/test_gpu_frontend.py -q -x > gpurun_out/memcheck_par.log 2>&1; echo rc=$?; tail -4 gpurun_out/memcheck_par.log
