@@ -72,3 +72,38 @@ def compress(W, hinv_diag, sparsity: float, bits: int = 4, G: int = 16,
            "codes": out["codes"][:(n * G * bits + 7) // 8],
            "scales_f16": out["scales_f16"][:n], "zeros_f16": out["zeros_f16"][:n]}
     return (bsr, sal) if return_saliency else bsr
+
+
+def concat_rows(bsrs) -> dict:
+    """Stack plain-BSR layers with the same K, G and bits along the output
+    dimension (rows of bsrs[0] first): the merged q/k/v or gate/up matrix of a
+    decoder layer, so one GEMV launch serves what were several (production
+    servers merge them the same way; tools/stack_bench.py "merged").  Pure
+    data movement: codes are re-packed bit-exactly, row offsets rebased."""
+    b0 = bsrs[0]
+    G, n, K = int(b0["group_size"]), int(b0["bits"]), int(b0["cols"])
+    for b in bsrs:
+        if (int(b["group_size"]), int(b["bits"]), int(b["cols"])) != (G, n, K):
+            raise ValueError("concat_rows: layers differ in K, G or bits")
+    rows = sum(int(b["rows"]) for b in bsrs)
+    ri = [np.zeros(1, np.int64)]
+    off = 0
+    bits = []
+    for b in bsrs:
+        r = np.asarray(b["row_index"], np.int64)
+        ri.append(r[1:] + off)
+        off += int(r[-1])
+        nb = int(b["nnzg"]) * G * n
+        bits.append(np.unpackbits(np.asarray(b["codes"], np.uint8), bitorder="little")[:nb])
+    allbits = np.concatenate(bits) if bits else np.zeros(0, np.uint8)
+    pad = (-allbits.size) % 8
+    if pad:
+        allbits = np.concatenate([allbits, np.zeros(pad, np.uint8)])
+    return {
+        "rows": rows, "cols": K, "group_size": G, "bits": n, "nnzg": off,
+        "row_index": np.concatenate(ri).astype(np.int32),
+        "group_cols": np.concatenate([np.asarray(b["group_cols"], np.uint16) for b in bsrs]),
+        "codes": np.packbits(allbits, bitorder="little"),
+        "scales_f16": np.concatenate([np.asarray(b["scales_f16"], np.uint16) for b in bsrs]),
+        "zeros_f16": np.concatenate([np.asarray(b["zeros_f16"], np.uint16) for b in bsrs]),
+    }

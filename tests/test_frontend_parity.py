@@ -115,3 +115,25 @@ def test_compress_g8_is_plain_bsr_but_not_packable():
     with pytest.raises(gqsa.GQSAError) as e:
         gqsa.pack(got)
     assert e.value.status == -3
+
+
+def test_concat_rows_merges_layers_exactly():
+    """frontend.concat_rows (merged q/k/v, gate/up): the merged BSR's rows are
+    the inputs' rows in order, bit for bit, and its oracle GEMV is the
+    concatenation of the inputs' GEMVs."""
+    from oracle import gqsa_oracle as O
+    parts = [synth.make_layer(60 + i, r, 512, bits=b, sparsity=0.5) for i, (r, b) in
+             enumerate(((64, 4), (16, 4), (16, 4)))]
+    merged = frontend.concat_rows(parts)
+    assert merged["rows"] == 96 and merged["nnzg"] == sum(p["nnzg"] for p in parts)
+    lo = 0
+    for p in parts:
+        sl = synth.slice_rows(merged, lo, lo + p["rows"])
+        _same_bsr(sl, p)
+        lo += p["rows"]
+    x = synth.make_x(5, 2, 512)
+    assert np.array_equal(O.gemv(merged, x), np.concatenate([O.gemv(p, x) for p in parts], axis=1))
+    blob, desc = gqsa.pack(merged)
+    _same_bsr(gqsa.unpack(blob), merged)
+    with pytest.raises(ValueError):
+        frontend.concat_rows([parts[0], synth.make_layer(1, 8, 256)])
