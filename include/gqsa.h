@@ -48,7 +48,7 @@ typedef enum {
   GQSA_OK = 0,
   GQSA_ERR_SHAPE = -1,       /* dims mismatch, cols % G != 0, B not in [1,8], bad row range */
   GQSA_ERR_VALIDATION = -2,  /* BSR invariant violated (see gqsa_pack) or inconsistent blob */
-  GQSA_ERR_UNSUPPORTED = -3, /* bits not in {2,4,8}, G != 16, cols > 32768 */
+  GQSA_ERR_UNSUPPORTED = -3, /* (bits, G) not in {2,4,8} x {16} or {4} x {8,32}; cols > 32768 */
   GQSA_ERR_BUFFER = -4,      /* null pointer, blob/workspace too small, misaligned device pointer */
   GQSA_ERR_CUDA = -5         /* CUDA launch / copy failure */
 } gqsa_status_t;
@@ -56,7 +56,9 @@ typedef enum {
 /*
  * Plain host BSR.
  *   rows, cols    : N (out_features) and K (in_features) of W[N][K].
- *   group_size    : G, the sparse AND quantization group, 16 in v1.
+ *   group_size    : G, the sparse AND quantization group: 16 (the
+ *                   paper's default) for every width; 8 or 32 for
+ *                   W4 (the group-size sweep; the chain kernel takes 16 only).
  *   bits          : n, code width: 4 or 2 (the paper's W4/W2), or 8 (W8, the
  *                   paper's other deployed setting).
  *   nnzg          : number of kept groups = row_index[rows].

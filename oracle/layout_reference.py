@@ -24,9 +24,9 @@ def _align(v: int, a: int = ALIGN) -> int:
     return -(-v // a) * a
 
 
-def tile_bytes(bits: int) -> int:
+def tile_bytes(bits: int, G: int = 16) -> int:
     # 32 B tile header + codes (T*G*n/8) + s/z (T*4) + columns (T*2)
-    return 32 + T * 16 * bits // 8 + T * 4 + T * 2
+    return 32 + T * G * bits // 8 + T * 4 + T * 2
 
 
 def target_slots(nnzg: int) -> int:
@@ -100,7 +100,7 @@ def pack_reference(bsr: dict, row_begin: int = 0, row_end=None) -> bytes:
         slots = -(-counts[nz[s * rps]] // S)        # the slice's longest row sets its length
         slice_tiles.append(-(-slots // SLOTS))
     num_tiles = sum(slice_tiles)
-    tb = tile_bytes(n)
+    tb = tile_bytes(n, G)
     off_ri = HDR
     off_perm = _align(off_ri + 4 * (rows + 1))
     off_em = _align(off_perm + 4 * LANES * n_slices)
@@ -110,7 +110,8 @@ def pack_reference(bsr: dict, row_begin: int = 0, row_end=None) -> bytes:
     out = bytearray(total)
     struct.pack_into("<IIiiiiqiiiiiiiiQQQQQ", out, 0,
                      MAGIC, VERSION, rows, K, G, n, nnzg, T, num_tiles, len(nz), len(empty),
-                     tb, 4 | (S << 8), row_begin, row_end, off_ri, off_perm, off_em, off_tiles, total)
+                     tb, (4 if G == 16 else 0) | (S << 8), row_begin, row_end, off_ri, off_perm, off_em,
+                     off_tiles, total)
     struct.pack_into(f"<{rows + 1}i", out, off_ri, *[v - g0 for v in ri_all[row_begin:row_end + 1]])
     if empty:
         struct.pack_into(f"<{len(empty)}i", out, off_em, *empty)
@@ -135,7 +136,11 @@ def pack_reference(bsr: dict, row_begin: int = 0, row_end=None) -> bytes:
             row = lane_row[l0]
             if row >= 0:
                 gr = ri_all[row_begin + row]
-                for key, pos in deal_row(gcols[gr:gr + counts[row]], range(l0, l0 + S), nt * SLOTS).items():
+                if G == 16:
+                    dealt = deal_row(gcols[gr:gr + counts[row]], range(l0, l0 + S), nt * SLOTS)
+                else:  # G = 8 / 32: CSR order, round robin over the row's S lanes
+                    dealt = {(l0 + p % S, p // S): p for p in range(counts[row])}
+                for key, pos in dealt.items():
                     deal[key] = gr + pos
         for tau in range(nt):
             base = off_tiles + t * tb
@@ -145,17 +150,22 @@ def pack_reference(bsr: dict, row_begin: int = 0, row_end=None) -> bytes:
                 for lane in range(LANES):
                     g = deal.get((lane, tau * SLOTS + u))
                     off_col = base + 32 + codes_total + T * 4 + lane * 8 + u * 2
-                    if g is None:  # padding: reads the lane's target chunk
-                        struct.pack_into("<H", out, off_col, ((lane % 16) % (K // 8)) << 4)
+                    if g is None:  # padding: reads the lane's target chunk (G = 16) or chunk 0
+                        struct.pack_into("<H", out, off_col, ((lane % 16) % (K // 8)) << 4 if G == 16 else 0)
                         continue
-                    swap = lane % 2
+                    swap = lane % 2 if G == 16 else lane % 4 if G == 32 else 0
                     gb = bytes(codes[g * cb:(g + 1) * cb])
-                    if swap:
+                    if G == 32:   # the lane reads chunks rot, rot+1, .. (mod 4): words in that order
+                        gb = b"".join(gb[4 * ((k + swap) % 4):4 * ((k + swap) % 4) + 4] for k in range(4))
+                    elif swap:
                         gb = gb[cb // 2:] + gb[:cb // 2]
                     off_c = base + 32 + (u // per_plane) * 512 + lane * 16 + (u % per_plane) * cb
                     out[off_c:off_c + cb] = gb
                     struct.pack_into("<HH", out, base + 32 + codes_total + lane * 16 + u * 4,
                                      int(sc[g]), int(zr[g]))
-                    struct.pack_into("<H", out, off_col, ((int(gcols[g]) << 1) | swap) << 4)
+                    # byte offset of the group's first 16-B x chunk: 2c + swap (G = 16), c (G = 8), 4c (G = 32)
+                    field = (((int(gcols[g]) << 1) | swap) << 4 if G == 16 else
+                             (int(gcols[g]) << 4) if G == 8 else (((int(gcols[g]) << 2) | swap) << 4))
+                    struct.pack_into("<H", out, off_col, field)
             t += 1
     return bytes(out)

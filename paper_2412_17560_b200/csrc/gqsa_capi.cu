@@ -22,7 +22,7 @@ size_t g_trace_bytes = 0;
 
 struct DevInfo {
   int sms = 0;
-  bool attr_set[9][2 * (kMaxBatch + 1)] = {};
+  bool attr_set[27][2 * (kMaxBatch + 1)] = {};  // [bits + 9 * (G = 8: 1, 32: 2)][batch (+ FEW)]
   bool chain_attr_set[9][3] = {};
 };
 std::mutex g_mu;
@@ -42,9 +42,9 @@ int device_sms(int dev) {
 bool lanes_per_row_ok(uint32_t s) { return s >= 1 && s <= 32 && (s & (s - 1)) == 0; }
 
 bool desc_ok(const gqsa_desc_t* d) {
-  return d && d->magic == kMagic && d->version == (uint32_t)kVersion && d->group_size == kGroup &&
-         (d->bits == 4 || d->bits == 2 || d->bits == 8) && d->tile_groups == kTileGroups && d->rows >= 0 &&
-         d->cols > 0 && d->cols % kGroup == 0 && d->num_tiles >= 0 &&
+  return d && d->magic == kMagic && d->version == (uint32_t)kVersion && group_supported(d->bits, d->group_size) &&
+         d->tile_groups == kTileGroups && d->rows >= 0 && d->cols > 0 && d->cols % d->group_size == 0 &&
+         d->num_tiles >= 0 &&
          lanes_per_row_ok(((uint32_t)d->flags >> kFlagLanesPerRowShift) & 0xff);
 }
 
@@ -70,7 +70,9 @@ bool few_for(const gqsa_desc_t* d, int B) {
   // batch 2 always (twice the accumulators: 80 registers and NS = 4 beat 16
   // warps at 64 registers by 13-14 % on 14336x4096 / 4096x14336); batch 1
   // only for small layers
-  return on && B <= 2 && (d->bits == 4 || d->bits == 2) && (on == 2 || B == 2 || d->num_tiles < kFewTiles);
+  if (d->group_size == 32) return B <= 2;  // four code planes per tile: needs the FEW register budget
+  return on && d->group_size == kGroup && B <= 2 && (d->bits == 4 || d->bits == 2) &&
+         (on == 2 || B == 2 || d->num_tiles < kFewTiles);
 }
 int warps_per_cta(const gqsa_desc_t* d, int B) {
   static int w1 = env_int("GQSA_WARPS", 16, 1, kMaxWarps);
@@ -92,12 +94,12 @@ struct SmemPlan {
 // x and its column sums, rounded up to 128 B: the fix-up records and the
 // TMA ring that follow must stay 16-B aligned (bulk-copy destinations; e.g.
 // B = 3, K = 208 gives 1560 B unrounded).
-size_t x_bytes(int B, int cols) {
-  const size_t v = (size_t)B * cols * 2 + (size_t)B * pq_bytes_per_row(B, cols);
+size_t x_bytes(int B, int cols, int G = kGroup) {
+  const size_t v = (size_t)B * cols * 2 + (size_t)B * pq_bytes_per_row(B, cols, G);
   return (v + 127) / 128 * 128;
 }
 size_t ring_bytes_for(const gqsa_desc_t* d, int W, int ns) {  // ring + its mbarriers
-  return (size_t)W * ns * tile_bytes(d->bits) + (size_t)W * kMaxStages * 8;
+  return (size_t)W * ns * tile_bytes(d->bits, d->group_size) + (size_t)W * kMaxStages * 8;
 }
 // intra-CTA fix-up records (batch <= 2; larger batches use the global workspace)
 size_t fix_bytes(int W, int B) { return B <= 2 ? (size_t)W * B * kLanes * kWsSlotBytes : 0; }
@@ -110,8 +112,11 @@ SmemPlan smem_plan(const gqsa_desc_t* d, int B) {
   int Bc = B, W = warps_per_cta(d, B);
   for (;; --Bc) {
     W = warps_per_cta(d, Bc);
-    if (x_bytes(Bc, d->cols) + ring_bytes_for(d, W, kMinStages) <= kMaxDynSmem) break;
-    if (W > 8 && x_bytes(Bc, d->cols) + ring_bytes_for(d, 8, kMinStages) <= kMaxDynSmem) { W = 8; break; }
+    if (x_bytes(Bc, d->cols, d->group_size) + ring_bytes_for(d, W, kMinStages) <= kMaxDynSmem) break;
+    if (W > 8 && x_bytes(Bc, d->cols, d->group_size) + ring_bytes_for(d, 8, kMinStages) <= kMaxDynSmem) {
+      W = 8;
+      break;
+    }
     if (Bc == 1) break;
   }
   sp.launches = (B + Bc - 1) / Bc;
@@ -119,11 +124,11 @@ SmemPlan smem_plan(const gqsa_desc_t* d, int B) {
   if (Bb != Bc) W = warps_per_cta(d, Bb) > W ? W : warps_per_cta(d, Bb);
   Bc = Bb;
   sp.batch = Bc;
-  const size_t tb = (size_t)tile_bytes(d->bits);
+  const size_t tb = (size_t)tile_bytes(d->bits, d->group_size);
   // intra-CTA fix-up records, if they fit next to x and a minimal ring
   size_t fb = fix_bytes(W, Bc);
-  if (x_bytes(Bc, d->cols) + fb + ring_bytes_for(d, W, kMinStages) > kMaxDynSmem) fb = 0;
-  const size_t xb = x_bytes(Bc, d->cols) + fb;  // x, column sums, fix-up records
+  if (x_bytes(Bc, d->cols, d->group_size) + fb + ring_bytes_for(d, W, kMinStages) > kMaxDynSmem) fb = 0;
+  const size_t xb = x_bytes(Bc, d->cols, d->group_size) + fb;  // x, column sums, fix-up records
   static const int cores = env_int("GQSA_CORESIDENT", kCoResidentKernels, 1, 4);  // experiments
   const size_t share = (size_t)kSmemPerSm / (ctas_per_sm_cap() * cores);
   const size_t budget = share > 2048 ? share - 2048 : 0;  // reserved + static smem
@@ -174,11 +179,12 @@ int make_plan(const gqsa_desc_t* d, int B, gqsa_plan_t* pl, const void** kfn) {
   if (sms <= 0) return GQSA_ERR_CUDA;
   const SmemPlan sp = smem_plan(d, B);
   const size_t smem = sp.total;
-  const void* fn = select_kernel(d->bits, sp.batch, few_for(d, sp.batch));
+  const void* fn = select_kernel(d->bits, d->group_size, sp.batch, few_for(d, sp.batch));
   if (!fn) return GQSA_ERR_UNSUPPORTED;
   {
     std::lock_guard<std::mutex> lk(g_mu);
-    bool& set = g_dev[dev].attr_set[d->bits][sp.batch + (few_for(d, sp.batch) ? kMaxBatch + 1 : 0)];
+    bool& set = g_dev[dev].attr_set[d->bits + (d->group_size == 8 ? 9 : d->group_size == 32 ? 18 : 0)]
+                                   [sp.batch + (few_for(d, sp.batch) ? kMaxBatch + 1 : 0)];
     if (!set) {
       // maximum shared-memory carveout: two kernels' CTAs (this launch and
       // the next, PDL) must fit on one SM at the same time
@@ -448,7 +454,7 @@ int chain_check(const gqsa_chain_item_t* items, int n, int B) {
     const gqsa_desc_t* d = items[j].desc;
     if (!d) return GQSA_ERR_BUFFER;
     if (!desc_ok(d)) return GQSA_ERR_VALIDATION;
-    if (d->bits != items[0].desc->bits) return GQSA_ERR_UNSUPPORTED;
+    if (d->bits != items[0].desc->bits || d->group_size != kGroup) return GQSA_ERR_UNSUPPORTED;
   }
   if (items[0].desc->bits == 8) return GQSA_ERR_UNSUPPORTED;
   return GQSA_OK;

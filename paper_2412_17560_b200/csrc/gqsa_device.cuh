@@ -117,8 +117,8 @@ __device__ __forceinline__ void dot16_w2_raw(uint32_t w, const uint4& xa, const 
 // the raw dot products carry: W4 / W8 P = 1024 X_even + 64 X_odd (W8 uses
 // only Q and the plain 1024 X = 1024 Q - ... see group_accumulate), W2
 // P = 1024 X_0 + 256 X_1 + 64 X_2 + 16 X_3 with X_j = sum_{t = j mod 4} x_t.
-template <int BITS>
-__device__ __forceinline__ float2 column_sums(const uint32_t (&w)[8]) {
+template <int BITS, int G = kGroup>
+__device__ __forceinline__ float2 column_sums(const uint32_t* w) {
   const uint32_t one = 0x3C003C00u;  // half2(1, 1): x * 1 is exact, one FHFMA per element
   if (BITS == 2) {
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
@@ -133,7 +133,7 @@ __device__ __forceinline__ float2 column_sums(const uint32_t (&w)[8]) {
   } else {
     float ae = 0.f, ao = 0.f;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {  // even t = 0, 2, .., 14 and odd t = 1, .., 15, in order
+    for (int e = 0; e < G / 2; ++e) {  // even t = 0, 2, .. and odd t = 1, 3, .., in order
       ae = fhfma<0, 0>(w[e], one, ae);
       ao = fhfma<1, 0>(w[e], one, ao);
     }
@@ -142,12 +142,14 @@ __device__ __forceinline__ float2 column_sums(const uint32_t (&w)[8]) {
 }
 
 // ---------------------------------------------------------------- tile regs
-template <int BITS>
-constexpr int code_planes() { return BITS == 8 ? 4 : (BITS == 4 ? 2 : 1); }
+// 16-B code planes per lane per tile: 4 slots x G*n/8 bytes (W2: 1, W4: 2,
+// W8: 4 at G = 16; W4: 1 at G = 8, 4 at G = 32).
+template <int BITS, int G = kGroup>
+constexpr int code_planes() { return G * BITS / 32; }
 
-template <int BITS>
+template <int BITS, int G = kGroup>
 struct TileRegs {
-  uint4 codes[code_planes<BITS>()];  // lane's 4 slots (W2: 1, W4: 2, W8: 4 planes x 16 B)
+  uint4 codes[code_planes<BITS, G>()];  // the lane's 4 slots
   uint4 sz;                        // 4 x (s, z) half pairs
   uint2 cols;                      // 4 x u16 (2c + swap)
   uint32_t hdr;                    // slice << 2 | FIRST | LAST
@@ -156,9 +158,12 @@ struct TileRegs {
 
 
 // Group code word(s) of slot u from the lane's codes.
-template <int BITS>
-__device__ __forceinline__ uint2 group_words(const TileRegs<BITS>& r, int u) {
-  if (BITS == 8) {
+template <int BITS, int G = kGroup>
+__device__ __forceinline__ uint2 group_words(const TileRegs<BITS, G>& r, int u) {
+  if (G == 8 || G == 32) {  // W4: G = 8 one word per slot; G = 32 reads the whole plane (codes[u])
+    const uint4& c = r.codes[0];
+    return G == 8 ? make_uint2(u == 0 ? c.x : u == 1 ? c.y : u == 2 ? c.z : c.w, 0u) : make_uint2(0u, 0u);
+  } else if (BITS == 8) {
     return make_uint2(0u, 0u);  // W8 reads the whole 16-B slot (tr.codes[u])
   } else if (BITS == 4) {
     const uint4& c = r.codes[u >> 1];
@@ -192,31 +197,56 @@ extern __shared__ __align__(128) uint8_t smem[];
 // Column-sum table entries per column group: 2 (indexed by f = 2c + swap) at
 // batch <= 2, else 1 (indexed by c; halves the table so that larger batches
 // keep x resident in shared memory).
-template <int B>
-constexpr int pq_per_group() { return B <= 2 ? 2 : 1; }
+template <int B, int G = kGroup>
+constexpr int pq_per_group() { return (G == kGroup && B <= 2) ? 2 : 1; }
 
-template <int BITS, int B>
-__device__ __forceinline__ void group_accumulate(const KParams& p, const TileRegs<BITS>& tr, int u,
+template <int BITS, int B, int G = kGroup>
+__device__ __forceinline__ void group_accumulate(const KParams& p, const TileRegs<BITS, G>& tr, int u,
                                                  float (&acc)[kMaxBatch]) {
   // shared-window offsets recomputed here so that they stay in uniform
   // registers ([R + UR] addressing on every LDS)
   const uint32_t xs = (uint32_t)__cvta_generic_to_shared(smem);
   const uint32_t pq = xs + (uint32_t)B * 2u * (uint32_t)p.cols;
-  const uint32_t pq_row = (uint32_t)p.cols / kGroup * pq_per_group<B>() * 8u;  // bytes per batch row
+  const uint32_t pq_row = (uint32_t)p.cols / G * pq_per_group<B, G>() * 8u;  // bytes per batch row
   const uint32_t colw = (u < 2) ? tr.cols.x : tr.cols.y;
   const uint32_t xoff0 = (u & 1) ? (colw >> 16) : (colw & 0xffffu);  // byte offset of the first x chunk
-  const uint32_t xoff1 = xoff0 ^ 16u;                                  // the other chunk
-  const uint32_t pqoff = pq_per_group<B>() == 2 ? xoff0 >> 1 : (xoff0 >> 2) & ~7u;  // f * 8 or c * 8
-  const uint2 w = group_words<BITS>(tr, u);
+  const uint32_t xoff1 = xoff0 ^ 16u;                                  // the other chunk (G = 16)
+  // (P, Q) entry: G = 16, B <= 2: per chunk index f (f * 8 = xoff0 / 2); else
+  // per column group c (c * 8 = xoff0 / 4 at G = 16, xoff0 / 2 at G = 8, xoff0 / 8 at G = 32)
+  const uint32_t pqoff = G == 8 ? xoff0 >> 1
+                         : G == 32 ? (xoff0 >> 3) & ~7u
+                                   : (pq_per_group<B, G>() == 2 ? xoff0 >> 1 : (xoff0 >> 2) & ~7u);
+  const uint2 w = group_words<BITS, G>(tr, u);
   const uint32_t szw = u == 0 ? tr.sz.x : u == 1 ? tr.sz.y : u == 2 ? tr.sz.z : tr.sz.w;
   const __half2 sz = *reinterpret_cast<const __half2*>(&szw);
   const float s = __low2float(sz), z = __high2float(sz);
 #pragma unroll
   for (int b = 0; b < B; ++b) {
     // x of batch row b at shared offset b * 2K (x is at the start of smem)
-    const uint4 xa = lds128(xs + b * 2u * (uint32_t)p.cols + xoff0);
-    const uint4 xb = lds128(xs + b * 2u * (uint32_t)p.cols + xoff1);
+    const uint32_t xrow = xs + b * 2u * (uint32_t)p.cols;
     const float2 X = lds64f(pq + b * pq_row + pqoff);
+    if (G == 8) {  // W4, one chunk: sum_t (q_t - z) x_t = D_even + D_odd/16 - P - z Q
+      const uint4 xa = lds128(xrow + xoff0);
+      float de = 0.f, dd = 0.f;
+      dot8_w4_raw(w.x, xa.x, xa.y, xa.z, xa.w, de, dd);
+      acc[b] = fmaf(s, fmaf(-z, X.y, fmaf(dd, 0.0625f, de) - X.x), acc[b]);
+      continue;
+    }
+    if (G == 32) {  // W4, four chunks from the lane's rotation: (xoff0 + 16k) mod 64 within the group
+      const uint4 c = tr.codes[u];
+      const uint32_t gb = xrow + (xoff0 & ~63u);
+      const uint4 x0 = lds128(gb + (xoff0 & 63u)), x1 = lds128(gb + ((xoff0 + 16u) & 63u));
+      const uint4 x2 = lds128(gb + ((xoff0 + 32u) & 63u)), x3 = lds128(gb + ((xoff0 + 48u) & 63u));
+      float de = 0.f, dd = 0.f;
+      dot8_w4_raw(c.x, x0.x, x0.y, x0.z, x0.w, de, dd);
+      dot8_w4_raw(c.y, x1.x, x1.y, x1.z, x1.w, de, dd);
+      dot8_w4_raw(c.z, x2.x, x2.y, x2.z, x2.w, de, dd);
+      dot8_w4_raw(c.w, x3.x, x3.y, x3.z, x3.w, de, dd);
+      acc[b] = fmaf(s, fmaf(-z, X.y, fmaf(dd, 0.0625f, de) - X.x), acc[b]);
+      continue;
+    }
+    const uint4 xa = lds128(xrow + xoff0);
+    const uint4 xb = lds128(xrow + xoff1);
     if (BITS == 8) {
       // Every element carries the +1024 offset of the LOP3 magic:
       //   sum_t (q_t - z) x_t = sum_t (1024 + q_t) x_t - (1024 + z) X.
@@ -427,13 +457,13 @@ __device__ __forceinline__ void trace_point(const KParams& p, int gw, int lane, 
 }
 
 // One lane's view of a tile that has landed in shared memory.
-template <int BITS>
-__device__ __forceinline__ void read_tile(TileRegs<BITS>& r, const uint8_t* tile, int lane) {
+template <int BITS, int G = kGroup>
+__device__ __forceinline__ void read_tile(TileRegs<BITS, G>& r, const uint8_t* tile, int lane) {
 #pragma unroll
-  for (int pl = 0; pl < code_planes<BITS>(); ++pl)
+  for (int pl = 0; pl < code_planes<BITS, G>(); ++pl)
     r.codes[pl] = *reinterpret_cast<const uint4*>(tile + kTileHeaderBytes + pl * 512 + lane * 16);
-  r.sz = *reinterpret_cast<const uint4*>(tile + off_sz(BITS) + lane * 16);
-  r.cols = *reinterpret_cast<const uint2*>(tile + off_cols(BITS) + lane * 8);
+  r.sz = *reinterpret_cast<const uint4*>(tile + off_sz(BITS, G) + lane * 16);
+  r.cols = *reinterpret_cast<const uint2*>(tile + off_cols(BITS, G) + lane * 8);
   const uint2 h = *reinterpret_cast<const uint2*>(tile);  // broadcast
   r.hdr = h.x;
   r.rem = h.y;
@@ -446,20 +476,21 @@ __device__ __forceinline__ void read_tile(TileRegs<BITS>& r, const uint8_t* tile
 // COHERENT: x may have been written earlier in the SAME launch (chain
 // kernel), so it is read through L2 only (ld.global.cg), never through the
 // non-coherent L1/texture path.
-template <int BITS, int B, bool COHERENT = false>
+template <int BITS, int B, bool COHERENT = false, int G = kGroup>
 __device__ __forceinline__ void stage_activations(const KParams& p, uint8_t* xs, uint8_t* pq, int KG,
                                                   int nthreads) {
-  constexpr int U = 2;  // column groups per thread per round (2 x 32 B in flight)
+  constexpr int NC = G / 8;  // 16-B chunks per column group
+  constexpr int U = NC >= 4 ? 1 : 2;  // column groups per thread per round in flight
   for (int i0 = threadIdx.x; i0 < B * KG; i0 += U * nthreads) {
-    uint4 v[U][2];
+    uint4 v[U][NC];
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       const int i = i0 + k * nthreads;
       if (i < B * KG) {
         const int b = i / KG, c = i - b * KG;
-        const uint4* src = reinterpret_cast<const uint4*>(p.X + (int64_t)b * p.ldx) + 2 * c;
-        v[k][0] = COHERENT ? __ldcg(src) : __ldg(src);
-        v[k][1] = COHERENT ? __ldcg(src + 1) : __ldg(src + 1);
+        const uint4* src = reinterpret_cast<const uint4*>(p.X + (int64_t)b * p.ldx) + NC * c;
+#pragma unroll
+        for (int h = 0; h < NC; ++h) v[k][h] = COHERENT ? __ldcg(src + h) : __ldg(src + h);
       }
     }
 #pragma unroll
@@ -467,19 +498,22 @@ __device__ __forceinline__ void stage_activations(const KParams& p, uint8_t* xs,
       const int i = i0 + k * nthreads;
       if (i < B * KG) {
         const int b = i / KG, c = i - b * KG;
-        {
-          uint4* dst = reinterpret_cast<uint4*>(xs + (size_t)b * p.cols * 2) + 2 * c;
-          dst[0] = v[k][0];
-          dst[1] = v[k][1];
+        uint4* dst = reinterpret_cast<uint4*>(xs + (size_t)b * p.cols * 2) + NC * c;
+        uint32_t w[4 * NC];
+#pragma unroll
+        for (int h = 0; h < NC; ++h) {
+          dst[h] = v[k][h];
+          w[4 * h] = v[k][h].x;
+          w[4 * h + 1] = v[k][h].y;
+          w[4 * h + 2] = v[k][h].z;
+          w[4 * h + 3] = v[k][h].w;
         }
-        const uint32_t w[8] = {v[k][0].x, v[k][0].y, v[k][0].z, v[k][0].w,
-                               v[k][1].x, v[k][1].y, v[k][1].z, v[k][1].w};
-        // (P, Q) of column group c, stored for both chunk orders (swap = 0, 1)
-        const float2 v2 = column_sums<BITS>(w);
-        constexpr int PG = pq_per_group<B>();
-        float2* dst = reinterpret_cast<float2*>(pq) + ((size_t)b * KG + c) * PG;
-        dst[0] = v2;
-        if (PG == 2) dst[1] = v2;
+        // (P, Q) of column group c, stored for both chunk orders (swap = 0, 1) at G = 16, B <= 2
+        const float2 v2 = column_sums<BITS, G>(w);
+        constexpr int PG = pq_per_group<B, G>();
+        float2* pdst = reinterpret_cast<float2*>(pq) + ((size_t)b * KG + c) * PG;
+        pdst[0] = v2;
+        if (PG == 2) pdst[1] = v2;
       }
     }
   }

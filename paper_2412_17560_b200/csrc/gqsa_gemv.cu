@@ -33,7 +33,7 @@
 
 namespace gqsa {
 
-template <int BITS, int B, bool FEW>
+template <int BITS, int B, bool FEW, int G = kGroup>
 __global__ void __launch_bounds__(max_threads_for(BITS, B, FEW), min_blocks_for(BITS, B, FEW))
     gqsa_streamk_kernel(KParams p) {
   const int lane = threadIdx.x & 31;
@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(max_threads_for(BITS, B, FEW), min_blocks_for(
     t_end = t_begin + p.part_q + (gw < p.part_r ? 1 : 0);
   }
   const uint8_t* tiles = p.tiles;
-  const int tb = tile_bytes(BITS);
+  const int tb = tile_bytes(BITS, G);
   const int NS = p.stages;
   if (p.slice_k && t_end > t_begin) {
     // data-centric partition (Slice-K): the warp owns the slices whose FIRST
@@ -116,10 +116,10 @@ __global__ void __launch_bounds__(max_threads_for(BITS, B, FEW), min_blocks_for(
   //      through the TMA unit, whose queue holds the weight ring fills) and
   //      compute the per-column-group sums X_{b,c} (fp32, fixed t order) from
   //      the same registers: one pass, one barrier.
-  const int KG = p.cols / kGroup;
+  const int KG = p.cols / G;
   uint8_t* xs = smem;
   uint8_t* pq = xs + (size_t)B * p.cols * 2;  // [B][K/16 * pq_per_group] float2 (P, Q)
-  stage_activations<BITS, B>(p, xs, pq, KG, nthreads);
+  stage_activations<BITS, B, false, G>(p, xs, pq, KG, nthreads);
   trace_point(p, gw, lane, 6);
   __syncthreads();
 
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(max_threads_for(BITS, B, FEW), min_blocks_for(
   // when it owns a slice continuing downstream) request the fix-up records.
   const bool local_owner = fx && (int)first0 >= cta_t0;  // owner of the opening slice is in this CTA
   int wg0 = gw + 1;  // first successor with a global record
-  auto consume = [&](const TileRegs<BITS>& tr, int t) {
+  auto consume = [&](const TileRegs<BITS, G>& tr, int t) {
     if (t == t_end - 1 && !(tr.hdr & kTileLast) && !foreign) {
       w_last = warp_of_tile(p, t_end - 1 + (int)tr.rem);
       wg0 = fx ? max(gw + 1, min(w_last + 1, cta_w0 + W)) : gw + 1;
@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(max_threads_for(BITS, B, FEW), min_blocks_for(
           pre[k][b] = (wg0 + k <= w_last) ? ld_slot(ws_slot<B>(p, wg0 + k, b, lane)) : 0ull;
     }
 #pragma unroll
-    for (int u = 0; u < kPerLane; ++u) group_accumulate<BITS, B>(p, tr, u, acc);
+    for (int u = 0; u < kPerLane; ++u) group_accumulate<BITS, B, G>(p, tr, u, acc);
     last_hdr = tr.hdr;
     if (tr.hdr & kTileLast) {  // the slice ends in this tile: its rows are complete
       if (foreign) publish<B>(p, gw, acc, lane, local_owner, fx, gw - cta_w0);
@@ -181,9 +181,9 @@ __global__ void __launch_bounds__(max_threads_for(BITS, B, FEW), min_blocks_for(
   for (; t + 1 < t_end; t += 2) {
     mbar_wait(bar0 + 8 * s, phase);
     const uint8_t* slot = ring + (size_t)s * 2 * tb;
-    TileRegs<BITS> tr0, tr1;
-    read_tile<BITS>(tr0, slot, lane);
-    read_tile<BITS>(tr1, slot + tb, lane);
+    TileRegs<BITS, G> tr0, tr1;
+    read_tile<BITS, G>(tr0, slot, lane);
+    read_tile<BITS, G>(tr1, slot + tb, lane);
     __syncwarp();  // every lane has read the pair: refill its slot
     if (lane == 0) {
       // Generic-proxy reads of the slot, then an async-proxy (TMA) write to
@@ -202,8 +202,8 @@ __global__ void __launch_bounds__(max_threads_for(BITS, B, FEW), min_blocks_for(
   }
   if (t < t_end) {  // odd count: the last slot holds one tile
     mbar_wait(bar0 + 8 * s, phase);
-    TileRegs<BITS> tr;
-    read_tile<BITS>(tr, ring + (size_t)s * 2 * tb, lane);
+    TileRegs<BITS, G> tr;
+    read_tile<BITS, G>(tr, ring + (size_t)s * 2 * tb, lane);
     consume(tr, t);
   }
 
@@ -226,9 +226,9 @@ __global__ void __launch_bounds__(max_threads_for(BITS, B, FEW), min_blocks_for(
 }
 
 // ---------------------------------------------------------------- launchers
-template <int BITS, int B, bool FEW = false>
+template <int BITS, int B, bool FEW = false, int G = kGroup>
 const void* kernel_ptr() {
-  return reinterpret_cast<const void*>(&gqsa_streamk_kernel<BITS, B, FEW>);
+  return reinterpret_cast<const void*>(&gqsa_streamk_kernel<BITS, B, FEW, G>);
 }
 
 #define GQSA_KSEL(BITS)                         \
@@ -244,7 +244,27 @@ const void* kernel_ptr() {
     default: return nullptr;                    \
   }
 
-const void* select_kernel(int bits, int B, bool few) {
+#define GQSA_KSEL_G(G)                                  \
+  switch (B) {                                          \
+    case 1: return kernel_ptr<4, 1, false, G>();        \
+    case 2: return kernel_ptr<4, 2, false, G>();        \
+    case 3: return kernel_ptr<4, 3, false, G>();        \
+    case 4: return kernel_ptr<4, 4, false, G>();        \
+    case 5: return kernel_ptr<4, 5, false, G>();        \
+    case 6: return kernel_ptr<4, 6, false, G>();        \
+    case 7: return kernel_ptr<4, 7, false, G>();        \
+    case 8: return kernel_ptr<4, 8, false, G>();        \
+    default: return nullptr;                            \
+  }
+
+const void* select_kernel(int bits, int G, int B, bool few) {
+  if (G != kGroup) {  // W4 at G = 8 / 32 (group-size sweep)
+    if (bits != 4) return nullptr;
+    if (G == 32 && few && B <= 2) return B == 1 ? kernel_ptr<4, 1, true, 32>() : kernel_ptr<4, 2, true, 32>();
+    if (G == 8) { GQSA_KSEL_G(8) }
+    if (G == 32) { GQSA_KSEL_G(32) }
+    return nullptr;
+  }
   if (few && B <= 2 && (bits == 4 || bits == 2)) {
     if (bits == 4) return B == 1 ? kernel_ptr<4, 1, true>() : kernel_ptr<4, 2, true>();
     return B == 1 ? kernel_ptr<2, 1, true>() : kernel_ptr<2, 2, true>();

@@ -85,9 +85,11 @@ struct ChainParams {
 };
 static_assert(sizeof(ChainParams) <= 4096, "kernel parameter space");
 
-const void* select_kernel(int bits, int B, bool few);
+const void* select_kernel(int bits, int G, int B, bool few);
 const void* select_chain_kernel(int bits, int B);
 // Bytes of the column-sum table per batch row (see gqsa_gemv.cu pq_per_group).
-inline size_t pq_bytes_per_row(int B, int cols) { return (size_t)cols / 16 * (B <= 2 ? 2 : 1) * 8; }
+inline size_t pq_bytes_per_row(int B, int cols, int G = 16) {
+  return (size_t)cols / G * ((G == 16 && B <= 2) ? 2 : 1) * 8;
+}
 
 }  // namespace gqsa

@@ -36,19 +36,39 @@ constexpr int kMaxCols = 32768;              // column field = byte offset (2c+s
 constexpr uint32_t kTileFirst = 1u;          // tile header flags
 constexpr uint32_t kTileLast = 2u;
 
+// Group sizes: G = 16 for every bit width (the paper's default);
+// G = 8 and G = 32 for W4 (the group-size sweep).
+__host__ __device__ constexpr bool group_supported(int bits, int G) {
+  return G == kGroup ? (bits == 2 || bits == 4 || bits == 8) : (bits == 4 && (G == 8 || G == 32));
+}
 // Bytes of one group's codes (G*n/8).
-__host__ __device__ constexpr int group_code_bytes(int bits) { return kGroup * bits / 8; }
-// Codes plane: each lane owns 16 B per plane -> 16/cb groups per plane.
-__host__ __device__ constexpr int groups_per_plane(int bits) { return 16 / group_code_bytes(bits); }
-__host__ __device__ constexpr int codes_bytes(int bits) { return kTileGroups * group_code_bytes(bits); }
-__host__ __device__ constexpr int off_sz(int bits) { return kTileHeaderBytes + codes_bytes(bits); }
-__host__ __device__ constexpr int off_cols(int bits) { return off_sz(bits) + kTileGroups * 4; }
-__host__ __device__ constexpr int tile_bytes(int bits) { return off_cols(bits) + kTileGroups * 2; }
+__host__ __device__ constexpr int group_code_bytes(int bits, int G = kGroup) { return G * bits / 8; }
+// Codes plane: each lane owns 16 B per plane -> 16/cb groups per plane (cb <= 16).
+__host__ __device__ constexpr int groups_per_plane(int bits, int G = kGroup) { return 16 / group_code_bytes(bits, G); }
+__host__ __device__ constexpr int codes_bytes(int bits, int G = kGroup) { return kTileGroups * group_code_bytes(bits, G); }
+__host__ __device__ constexpr int off_sz(int bits, int G = kGroup) { return kTileHeaderBytes + codes_bytes(bits, G); }
+__host__ __device__ constexpr int off_cols(int bits, int G = kGroup) { return off_sz(bits, G) + kTileGroups * 4; }
+__host__ __device__ constexpr int tile_bytes(int bits, int G = kGroup) { return off_cols(bits, G) + kTileGroups * 2; }
 
 // Offset (within a tile) of the code bytes of the group in lane l, slot u.
-__host__ __device__ constexpr int off_codes(int bits, int lane, int u) {
-  return kTileHeaderBytes + (u / groups_per_plane(bits)) * 512 + lane * 16 +
-         (u % groups_per_plane(bits)) * group_code_bytes(bits);
+__host__ __device__ constexpr int off_codes_g(int bits, int G, int lane, int u) {
+  return kTileHeaderBytes + (u / groups_per_plane(bits, G)) * 512 + lane * 16 +
+         (u % groups_per_plane(bits, G)) * group_code_bytes(bits, G);
+}
+__host__ __device__ constexpr int off_codes(int bits, int lane, int u) { return off_codes_g(bits, kGroup, lane, u); }
+
+// Column field of a kept group at group column c: the byte offset of the
+// first 16-B activation chunk the lane reads.  G = 16: chunk 2c + swap
+// (swap = lane parity); G = 8: chunk c; G = 32: chunk
+// 4c + rot, rot = lane mod 4 -- the lane reads the group's four chunks
+// rot, rot+1, .. (mod 4) and its code words are stored in that order, so the
+// lanes of a quarter-warp spread over the bank quads.
+__host__ __device__ constexpr uint32_t col_field(int G, uint32_t c, uint32_t rot) {
+  return G == 16 ? (((c << 1) | rot) << 4) : G == 8 ? (c << 4) : (((c << 2) | rot) << 4);
+}
+// Rotation (G = 32) / swap (G = 16) of lane l; 0 for G = 8.
+__host__ __device__ constexpr uint32_t lane_rot(int G, int lane) {
+  return G == 16 ? (uint32_t)(lane & 1) : G == 32 ? (uint32_t)(lane & 3) : 0u;
 }
 
 constexpr int kTargetSlots = 64;  // slots per lane of the longest slice (16 tiles)
@@ -78,8 +98,8 @@ inline int lanes_per_row_for(int n_nz, int64_t max_len, int target_slots = kTarg
 }
 
 // Offset (within a tile) of the column field of lane l, slot u.
-__host__ __device__ constexpr int off_cols(int bits, int lane, int u) {
-  return off_cols(bits) + lane * 8 + u * 2;
+__host__ __device__ constexpr int off_cols_g(int bits, int G, int lane, int u) {
+  return off_cols(bits, G) + lane * 8 + u * 2;
 }
 
 // On-blob header; the first 104 bytes mirror gqsa_desc_t field-for-field.

@@ -36,7 +36,7 @@ inline bool f16_positive(uint16_t h) { return !(h & 0x8000) && (h & 0x7fff) != 0
 int check_bsr_header(const gqsa_bsr_t* b) {
   if (!b) return GQSA_ERR_BUFFER;
   if (b->rows < 0 || b->cols <= 0 || b->group_size <= 0 || b->nnzg < 0) return GQSA_ERR_SHAPE;
-  if (b->group_size != kGroup || (b->bits != 4 && b->bits != 2 && b->bits != 8)) return GQSA_ERR_UNSUPPORTED;
+  if (!group_supported(b->bits, b->group_size)) return GQSA_ERR_UNSUPPORTED;
   if (b->cols % b->group_size) return GQSA_ERR_SHAPE;
   if (b->cols > kMaxCols) return GQSA_ERR_UNSUPPORTED;  // col field = byte offset in u16
   if (!b->row_index) return GQSA_ERR_BUFFER;
@@ -114,13 +114,13 @@ struct Offsets {
   uint64_t ri, perm, empty, tiles, total;
 };
 
-Offsets offsets(const Slices& s, int bits) {
+Offsets offsets(const Slices& s, int bits, int G) {
   Offsets o;
   o.ri = kHeaderBytes;
   o.perm = align_up(o.ri + 4ull * (s.rows + 1), kSectionAlign);
   o.empty = align_up(o.perm + 4ull * kLanes * s.num_slices, kSectionAlign);
   o.tiles = align_up(o.empty + 4ull * s.n_empty, kSectionAlign);
-  o.total = align_up(o.tiles + (uint64_t)s.num_tiles * tile_bytes(bits), kSectionAlign);
+  o.total = align_up(o.tiles + (uint64_t)s.num_tiles * tile_bytes(bits, G), kSectionAlign);
   return o;
 }
 
@@ -139,7 +139,7 @@ extern "C" int gqsa_pack_size(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t 
   if (!blob_bytes) return GQSA_ERR_BUFFER;
   if (row_begin < 0 || row_end < row_begin || row_end > bsr->rows) return GQSA_ERR_SHAPE;
   if ((st = validate(bsr, row_begin, row_end))) return st;
-  *blob_bytes = (size_t)offsets(make_slices(bsr, row_begin, row_end), bsr->bits).total;
+  *blob_bytes = (size_t)offsets(make_slices(bsr, row_begin, row_end), bsr->bits, bsr->group_size).total;
   return GQSA_OK;
 }
 
@@ -151,27 +151,28 @@ extern "C" int gqsa_pack(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_e
   if (row_begin < 0 || row_end < row_begin || row_end > bsr->rows) return GQSA_ERR_SHAPE;
   if ((st = validate(bsr, row_begin, row_end))) return st;
   const Slices s = make_slices(bsr, row_begin, row_end);
-  const Offsets o = offsets(s, bsr->bits);
+  const Offsets o = offsets(s, bsr->bits, bsr->group_size);
   if (blob_bytes < o.total) return GQSA_ERR_BUFFER;
   uint8_t* out = static_cast<uint8_t*>(blob);
   std::memset(out, 0, o.total);
   const int64_t g_begin = bsr->row_index[row_begin];
-  const int bits = bsr->bits, cb = group_code_bytes(bits), S = s.lanes_per_row;
+  const int bits = bsr->bits, G = bsr->group_size, cb = group_code_bytes(bits, G), S = s.lanes_per_row;
+  const int tb = tile_bytes(bits, G);
 
   BlobHeader h{};
   h.magic = kMagic;
   h.version = kVersion;
   h.rows = s.rows;
   h.cols = bsr->cols;
-  h.group_size = kGroup;
+  h.group_size = G;
   h.bits = bits;
   h.nnzg = (int64_t)bsr->row_index[row_end] - g_begin;
   h.tile_groups = kTileGroups;
   h.num_tiles = s.num_tiles;
   h.n_nzrows = s.n_nz;
   h.n_empty = s.n_empty;
-  h.tile_bytes = tile_bytes(bits);
-  h.flags = (int32_t)(kFlagTargetDeal | ((uint32_t)S << kFlagLanesPerRowShift));
+  h.tile_bytes = tb;
+  h.flags = (int32_t)((G == kGroup ? kFlagTargetDeal : 0u) | ((uint32_t)S << kFlagLanesPerRowShift));
   h.row_begin = row_begin;
   h.row_end = row_end;
   h.off_row_index = o.ri;
@@ -211,6 +212,10 @@ extern "C" int gqsa_pack(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_e
       const int32_t row = row_of_lane[l0];
       if (row < 0) continue;
       const int64_t g0 = bsr->row_index[row_begin + row], n = s.count[row];
+      if (G != kGroup) {  // G = 8 / 32: CSR order, round robin over the row's lanes
+        for (int64_t p = 0; p < n; ++p) deal[(size_t)(l0 + p % S) * L + p / S] = g0 + p;
+        continue;
+      }
       std::vector<int64_t> bucket[8];
       size_t head[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       for (int64_t g = g0; g < g0 + n; ++g) bucket[bsr->group_cols[g] & 7].push_back(g);
@@ -233,7 +238,7 @@ extern "C" int gqsa_pack(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_e
     }
     for (int32_t tau = 0; tau < nt; ++tau) {
       const int32_t t = s.tile0[sl] + tau;
-      uint8_t* tile = out + o.tiles + (uint64_t)t * tile_bytes(bits);
+      uint8_t* tile = out + o.tiles + (uint64_t)t * tb;
       // word 0: slice << 2 | FIRST | LAST; word 1: tiles to the slice's last
       // tile; word 2: the slice's first tile
       const uint32_t hdr[4] = {((uint32_t)sl << 2) | (tau == 0 ? kTileFirst : 0u) |
@@ -243,24 +248,26 @@ extern "C" int gqsa_pack(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_e
       for (int u = 0; u < kPerLane; ++u) {
         for (int l = 0; l < kLanes; ++l) {
           const int64_t g = deal[(size_t)l * L + (int64_t)tau * kPerLane + u];
-          uint16_t* col = reinterpret_cast<uint16_t*>(tile + off_cols(bits, l, u));
-          if (g < 0) {  // padding: codes, s, z zero; reads this lane's target chunk
-            *col = (uint16_t)(((l & 15) % nchunks) << 4);
+          uint16_t* col = reinterpret_cast<uint16_t*>(tile + off_cols_g(bits, G, l, u));
+          if (g < 0) {  // padding: codes, s, z zero; reads this lane's target chunk (G = 16) or chunk 0
+            *col = G == kGroup ? (uint16_t)(((l & 15) % nchunks) << 4) : (uint16_t)0;
             continue;
           }
-          const uint32_t swap = (uint32_t)(l & 1);
+          const uint32_t swap = lane_rot(G, l);
           const uint8_t* src = bsr->codes + g * cb;
-          uint8_t* dst = tile + off_codes(bits, l, u);
-          if (swap) {
+          uint8_t* dst = tile + off_codes_g(bits, G, l, u);
+          if (G == 32) {  // code word k <- the group's word (k + rot) mod 4 (chunk read order)
+            for (int k = 0; k < 4; ++k) std::memcpy(dst + 4 * k, src + 4 * ((k + swap) & 3), 4);
+          } else if (swap) {
             std::memcpy(dst, src + cb / 2, cb / 2);
             std::memcpy(dst + cb / 2, src, cb / 2);
           } else {
             std::memcpy(dst, src, cb);
           }
-          uint16_t* sz = reinterpret_cast<uint16_t*>(tile + off_sz(bits) + l * 16 + u * 4);
+          uint16_t* sz = reinterpret_cast<uint16_t*>(tile + off_sz(bits, G) + l * 16 + u * 4);
           sz[0] = bsr->scales_f16[g];
           sz[1] = bsr->zeros_f16[g];
-          *col = (uint16_t)(((bsr->group_cols[g] << 1) | swap) << 4);  // byte offset of the first x chunk
+          *col = (uint16_t)col_field(G, bsr->group_cols[g], swap);  // byte offset of the first x chunk
         }
       }
     }
@@ -275,9 +282,9 @@ extern "C" int gqsa_read_desc(const void* blob, size_t blob_bytes, gqsa_desc_t* 
   BlobHeader h;
   std::memcpy(&h, blob, sizeof(h));
   if (h.magic != kMagic || h.version != (uint32_t)kVersion) return GQSA_ERR_VALIDATION;
-  if (h.group_size != kGroup || (h.bits != 4 && h.bits != 2 && h.bits != 8)) return GQSA_ERR_UNSUPPORTED;
-  if (h.tile_groups != kTileGroups || h.tile_bytes != tile_bytes(h.bits)) return GQSA_ERR_VALIDATION;
-  if (h.rows < 0 || h.cols <= 0 || h.cols % kGroup || h.cols > kMaxCols || h.nnzg < 0)
+  if (!group_supported(h.bits, h.group_size)) return GQSA_ERR_UNSUPPORTED;
+  if (h.tile_groups != kTileGroups || h.tile_bytes != tile_bytes(h.bits, h.group_size)) return GQSA_ERR_VALIDATION;
+  if (h.rows < 0 || h.cols <= 0 || h.cols % h.group_size || h.cols > kMaxCols || h.nnzg < 0)
     return GQSA_ERR_VALIDATION;
   if (h.n_nzrows < 0 || h.n_empty < 0 || h.n_nzrows + h.n_empty != h.rows) return GQSA_ERR_VALIDATION;
   if (h.nnzg < h.n_nzrows || h.num_tiles < 0) return GQSA_ERR_VALIDATION;
@@ -310,13 +317,14 @@ extern "C" int gqsa_unpack(const void* blob, size_t blob_bytes, gqsa_bsr_t* out)
   const int32_t* ri = reinterpret_cast<const int32_t*>(b + d.off_row_index);
   const int32_t* perm = reinterpret_cast<const int32_t*>(b + d.off_nzrow);
   const int32_t* em = reinterpret_cast<const int32_t*>(b + d.off_empty);
-  const int bits = d.bits, cb = group_code_bytes(bits);
+  const int bits = d.bits, GS = d.group_size, cb = group_code_bytes(bits, GS);
   const int S = ((uint32_t)d.flags >> kFlagLanesPerRowShift) & 0xff;
 
   struct G {
     uint16_t col, s, z;
     const uint8_t* codes;
-    bool swap;
+    bool swap;     // G = 16: halves exchanged
+    uint32_t rot;  // G = 32: code words rotated
   };
   std::vector<std::vector<G>> rows(d.rows);
   int32_t slice = -1, first = -1;
@@ -331,9 +339,9 @@ extern "C" int gqsa_unpack(const void* blob, size_t blob_bytes, gqsa_bsr_t* out)
     for (int u = 0; u < kPerLane; ++u) {
       for (int l = 0; l < kLanes; ++l) {
         const int32_t row = perm[(int64_t)slice * kLanes + l];
-        const uint16_t* sz = reinterpret_cast<const uint16_t*>(tile + off_sz(bits) + l * 16 + u * 4);
-        const uint16_t col = *reinterpret_cast<const uint16_t*>(tile + off_cols(bits) + l * 8 + u * 2);
-        const uint8_t* src = tile + off_codes(bits, l, u);
+        const uint16_t* sz = reinterpret_cast<const uint16_t*>(tile + off_sz(bits, GS) + l * 16 + u * 4);
+        const uint16_t col = *reinterpret_cast<const uint16_t*>(tile + off_cols_g(bits, GS, l, u));
+        const uint8_t* src = tile + off_codes_g(bits, GS, l, u);
         if (sz[0] == 0) {  // padding (a kept group always has s > 0)
           if (sz[1] || (col & 15u) || col >= 2u * (uint32_t)d.cols) return GQSA_ERR_VALIDATION;
           for (int i = 0; i < cb; ++i)
@@ -342,7 +350,14 @@ extern "C" int gqsa_unpack(const void* blob, size_t blob_bytes, gqsa_bsr_t* out)
         }
         if (row < 0 || row >= d.rows) return GQSA_ERR_VALIDATION;
         if (col & 15u) return GQSA_ERR_VALIDATION;
-        rows[row].push_back(G{(uint16_t)(col >> 5), sz[0], sz[1], src, ((col >> 4) & 1u) != 0});
+        if (GS == kGroup) {
+          rows[row].push_back(G{(uint16_t)(col >> 5), sz[0], sz[1], src, ((col >> 4) & 1u) != 0, 0});
+        } else if (GS == 8) {
+          rows[row].push_back(G{(uint16_t)(col >> 4), sz[0], sz[1], src, false, 0});
+        } else {
+          if (((col >> 4) & 3u) != lane_rot(GS, l)) return GQSA_ERR_VALIDATION;
+          rows[row].push_back(G{(uint16_t)(col >> 6), sz[0], sz[1], src, false, (col >> 4) & 3u});
+        }
       }
     }
   }
@@ -365,7 +380,9 @@ extern "C" int gqsa_unpack(const void* blob, size_t blob_bytes, gqsa_bsr_t* out)
       o_s[acc] = g.s;
       o_z[acc] = g.z;
       uint8_t* dst = o_codes + acc * cb;
-      if (g.swap) {
+      if (GS == 32) {  // stored word k is the group's word (k + rot) mod 4
+        for (int k = 0; k < 4; ++k) std::memcpy(dst + 4 * ((k + g.rot) & 3), g.codes + 4 * k, 4);
+      } else if (g.swap) {
         std::memcpy(dst, g.codes + cb / 2, cb / 2);
         std::memcpy(dst + cb / 2, g.codes, cb / 2);
       } else {

@@ -104,16 +104,23 @@ def test_compress_errors():
     assert e.value.status == -1
 
 
-def test_compress_g8_is_plain_bsr_but_not_packable():
+def test_compress_other_group_sizes():
     """The front-end handles any G dividing K (plain BSR, checked against the
-    oracle); the packer and kernels take G = 16 only (GQSA_ERR_UNSUPPORTED)."""
+    oracle); the packer takes G = 8 / 32 at W4 (round trip) and rejects them
+    at other widths (GQSA_ERR_UNSUPPORTED)."""
     W = synth.make_dense(31, 16, 128)
     d = np.ones(128)
-    ref, _, _ = F.compress_layer(W, d, 0.5, 4, 8)
-    got = frontend.compress(W, d, 0.5, 4, 8)
-    _same_bsr(got, ref)
+    for G in (8, 32):
+        ref, _, _ = F.compress_layer(W, d, 0.5, 4, G)
+        got = frontend.compress(W, d, 0.5, 4, G)
+        _same_bsr(got, ref)
+        blob, desc = gqsa.pack(got)
+        assert desc.group_size == G
+        _same_bsr(gqsa.unpack(blob), got)
+    got2 = frontend.compress(W, d, 0.5, 2, 8)
+    _same_bsr(got2, F.compress_layer(W, d, 0.5, 2, 8)[0])
     with pytest.raises(gqsa.GQSAError) as e:
-        gqsa.pack(got)
+        gqsa.pack(got2)
     assert e.value.status == -3
 
 

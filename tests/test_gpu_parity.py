@@ -394,3 +394,42 @@ def test_concurrent_streams_share_one_blob():
     for k in range(2):
         for Y in Ys[k]:
             assert np.array_equal(Y.cpu().numpy().astype(np.float64), refs[k])
+
+
+G_EXACT = [
+    # rows, cols, G, sparsity, mask, B
+    (300, 1024, 8, 0.5, "uniform", 1),
+    (77, 264, 8, 0.2, "uniform", 2),
+    (512, 2048, 8, 0.5, "skewed", 3),
+    (1024, 4096, 8, 0.5, "uniform", 8),
+    (300, 1024, 32, 0.5, "uniform", 1),
+    (77, 224, 32, 0.2, "uniform", 2),
+    (512, 2048, 32, 0.5, "row_balanced", 4),
+    (1024, 4096, 32, 0.5, "uniform", 8),
+    (3, 16384, 32, 0.5, "uniform", 1),
+    (2048, 14336, 32, 0.5, "uniform", 2),
+]
+
+
+@pytest.mark.parametrize("rows,cols,G,sp,mask,B", G_EXACT)
+def test_group_size_8_32_exact(rows, cols, G, sp, mask, B):
+    """W4 at G = 8 and G = 32 (the group-size sweep): bit-exact in exact-integer
+    mode, Stream-K and Slice-K."""
+    seed = synth.seed_for(f"gexact/{rows}/{cols}/{G}/{sp}/{mask}/{B}")
+    bsr = synth.make_layer(seed, rows, cols, G=G, bits=4, sparsity=sp, mask=mask, mode="exact_int")
+    x = synth.make_x(seed + 1, B, cols, mode="exact_int")
+    ref = O.gemv(bsr, x)
+    L = gqsa.Layer(bsr)
+    X = torch.from_numpy(x).view(torch.float16).cuda()
+    for part in (gqsa.PARTITION_STREAM_K, gqsa.PARTITION_SLICE_K):
+        y = L.gemm(X, partition=part)
+        torch.cuda.synchronize()
+        assert np.array_equal(y.cpu().numpy().astype(np.float64), ref), part
+
+
+@pytest.mark.parametrize("G", [8, 32])
+def test_group_size_realistic_gates(G):
+    bsr = synth.make_layer(synth.seed_for(f"greal/{G}"), 4096, 4096, G=G, bits=4, sparsity=0.5)
+    x = synth.make_x(3, 2, 4096)
+    y = run(bsr, x)
+    check_gates(y, O.gemv(bsr, x), abs_bound(bsr, x), f"G{G}")

@@ -55,6 +55,15 @@ CASES = [
     (256, 256, 8, 0.5, "uniform", 9),      # W8: four 512-B code planes per tile
     (37, 208, 8, 0.3, "row_balanced", 10),
 ]
+# W4 at group sizes 8 and 32 (SURVEY §8(f) NEXT-1 group-size sweep)
+G_CASES = [
+    # rows, cols, G, sparsity, mask, seed
+    (256, 512, 8, 0.5, "uniform", 21),
+    (37, 264, 8, 0.3, "row_balanced", 22),
+    (64, 1024, 32, 0.5, "skewed", 23),
+    (3, 4096, 32, 0.5, "uniform", 24),
+    (40, 96, 32, 0.0, "uniform", 25),
+]
 
 
 @pytest.mark.parametrize("rows,cols,bits,sp,mask,seed", CASES)
@@ -64,6 +73,26 @@ def test_roundtrip_and_reference_bytes(rows, cols, bits, sp, mask, seed):
     assert desc.blob_bytes == blob.size and desc.nnzg == bsr["nnzg"]
     assert bytes(blob) == pack_reference(bsr)
     _eq_bsr(gqsa.unpack(blob), bsr)
+
+
+@pytest.mark.parametrize("rows,cols,G,sp,mask,seed", G_CASES)
+def test_group_sizes_roundtrip_and_reference_bytes(rows, cols, G, sp, mask, seed):
+    bsr = synth.make_layer(seed, rows, cols, G=G, bits=4, sparsity=sp, mask=mask)
+    blob, desc = gqsa.pack(bsr)
+    assert desc.group_size == G and desc.tile_bytes == 32 + 128 * G // 2 + 512 + 256
+    assert bytes(blob) == pack_reference(bsr)
+    _eq_bsr(gqsa.unpack(blob), bsr)
+
+
+def test_group_size_rejections():
+    bsr = synth.make_layer(26, 16, 128, G=8, bits=2, sparsity=0.5)
+    with pytest.raises(gqsa.GQSAError) as e:
+        gqsa.pack(bsr)
+    assert e.value.status == -3
+    bsr = synth.make_layer(27, 16, 128, G=64, bits=4, sparsity=0.5)
+    with pytest.raises(gqsa.GQSAError) as e:
+        gqsa.pack(bsr)
+    assert e.value.status == -3
 
 
 def test_shard_ranges_rebase_and_reassemble():

@@ -1,5 +1,5 @@
 make -s >/dev/null 2>&1
-for b in 2 8; do timeout 600 python bench.py --batch $b --steps 2000 --warmup 20 --no-cpu-baseline --e2e-steps 50 2>gpurun_out/err.txt | grep "^{" | python -c "
-import json,sys; d=json.loads(sys.stdin.readline()); print('B=$b', d['value'], d['us_per_step'], [l['us'] for l in d['layers']], d['e2e']['value'])" || tail -3 gpurun_out/err.txt; done
-for p in chain; do timeout 600 python bench.py --path chain --batch 2 --steps 2000 --warmup 20 --no-cpu-baseline --e2e-steps 50 2>gpurun_out/err.txt | grep "^{" | python -c "
-import json,sys; d=json.loads(sys.stdin.readline()); print('chain B=2', d['value'], d['us_per_step'])" || tail -3 gpurun_out/err.txt; done
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/t.log 2>&1; tail -2 gpurun_out/t.log; grep -E "^E |FAILED" gpurun_out/t.log | head -5
+timeout 900 python tools/sweep.py --sections H --out gpurun_out/sweepH > /dev/null 2>&1; grep "^|" gpurun_out/sweepH.md
+timeout 600 python bench.py --steps 5000 --warmup 100 --no-cpu-baseline --e2e-steps 200 2>/dev/null | grep "^{" | python -c "
+import json,sys; d=json.loads(sys.stdin.readline()); print(d['value'], [l['us'] for l in d['layers']])"

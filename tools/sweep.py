@@ -8,6 +8,7 @@ B. Partition ablation (App. J): Stream-K versus
    Slice-K on uniform, row-balanced and skewed masks (W4S50, batch 1).
 C. Sparsity sweep at 4096x4096 W4 (Fig. 6 trend): S = 0 .. 0.8,
    speed-up over this build's own S = 0 (dense-equivalent) launch.
+H. Group size G = 8 / 16 / 32 at W4S50, B = 1.
 D. Saliency-selected masks (the method's own front-end, PAPER.md:74-93:
    Eq. 4 + group means + exact-count pruning, frontend.compress) on synthetic
    dense layers with per-row scale imbalance and calibration activations with
@@ -73,7 +74,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None, help="write <out>.md and <out>.jsonl")
     ap.add_argument("--quick", action="store_true", help="batch 1 and 8 only")
-    ap.add_argument("--sections", default="ABCD", help="subset of A, B, C, D to run")
+    ap.add_argument("--sections", default="ABCDH", help="subset of A, B, C, D, H to run")
     a = ap.parse_args()
     peak, src = peaks()
     recs = []
@@ -162,6 +163,25 @@ def main():
             lines.append(f"| {rows}x{cols} | {lens.min()}/{lens.mean():.0f}/{lens.max()} | "
                          f"{int((lens == 0).sum())} | {rs['us']:.2f} ({rs['gbs']:.0f}) | {rk['us']:.2f} | "
                          f"{rk['us'] / rs['us']:.2f}x | {tc:.2f} |")
+        lines.append("")
+
+    if "H" in a.sections:  # group size, W4S50, B = 1
+        lines += ["## H. Group size G = 8 / 16 / 32, W4S50, B = 1", "",
+                  "Counted bytes per kept group: G/2 code bytes + 6 (s, z, column): 1.25 / 0.875 / 0.69 B per "
+                  "weight. The paper keeps G = 16 (PAPER.md:170).", "",
+                  "| shape | G = 8 µs (GB/s) | G = 16 | G = 32 |", "|---|---|---|---|"]
+        for rows, cols in SHAPES:
+            cells = []
+            for G in (8, 16, 32):
+                bsr = synth.make_layer(synth.seed_for(f"sweep-g/{rows}x{cols}/{G}"), rows, cols, G=G, bits=4,
+                                       sparsity=0.5)
+                r = measure(bsr, 1)
+                r["group_size"] = G
+                nb = int(bsr["nnzg"]) * (G // 2 + 6) + 4 * (rows + 1) + 2 * cols + 4 * rows
+                r["counted_bytes"], r["gbs"] = nb, round(nb / r["us"] / 1e3, 1)
+                emit("H", r)
+                cells.append(f"{r['us']:.2f} ({r['gbs']:.0f})")
+            lines.append(f"| {rows}x{cols} | " + " | ".join(cells) + " |")
         lines.append("")
 
     if a.out:
