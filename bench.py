@@ -6,24 +6,35 @@ configs[1] -- 4096x4096, 14336x4096, 4096x14336 at W4S50, G=16, batch 1 --
 i.e. every row of SURVEY §8(a) over one batch of synthetic input.  value =
 counted (compressed, algorithmic) bytes of all steps / device time, in GB/s.
 
+The step runs as ONE gqsa_gemm_grouped launch (the three GEMVs are
+independent; `--path launches` runs one gqsa_gemv per layer instead).
+
 Timing: the weights rotate over R device copies of the layer set (> 2x the
 126 MB L2), so every launch streams from HBM.  K steps are replayed from CUDA
-graphs, bracketed by barrier + synchronize, timed with CUDA events on the
-launching stream (max over ranks).  Clocks / throttle reasons are sampled
-through NVML during the timed region.
+graphs (every graph of the timed region replayed during warm-up), bracketed
+by barrier + synchronize, timed with CUDA events on the launching stream (max
+over ranks).  Clocks / throttle reasons are sampled through NVML during the
+timed region.
 
 N > 1 (torchrun, NCCL): every rank owns rows [N*r/P, N*(r+1)/P) of each layer
 (output-row sharding), runs its GEMV, then all-gathers y over
-NVLink (torch.distributed.all_gather_into_tensor).  Total work is fixed:
-"scaling": "strong".
+NVLink (torch.distributed.all_gather_into_tensor), all captured in CUDA
+graphs.  Total work is fixed: "scaling": "strong".  The line adds the split
+of SURVEY §8(e): per-rank kernel µs, all-gather µs, end-to-end µs and the
+kernel-only aggregate GB/s.
 
 --impl reference: the CPU fp64 oracle (oracle/), the tier's reference arm,
 timed on the host on a bounded row sample of the same workload (rank 0 only).
 """
+import os
+
+# the CPU legs (oracle) run single-threaded: set before numpy is imported
+for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
 import argparse
 import json
 import math
-import os
 import sys
 import threading
 import time
@@ -128,29 +139,76 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- cpu baseline
-def cpu_oracle_baseline(layers, budget_s=12.0, max_reps=50):
-    """The fp64 oracle as it stands, single process (numpy, 1 core), on whole
-    layers of the workload, repeated until ~budget_s of CPU work."""
+def host_info():
+    """nproc, the CPU model (lscpu "Model name" / /proc/cpuinfo) of the box."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+class pinned_core:
+    """Pin this process to one host core while the oracle is timed (restores the mask)."""
+
+    def __init__(self):
+        self.core, self.prev = None, None
+
+    def __enter__(self):
+        try:
+            self.prev = os.sched_getaffinity(0)
+            self.core = min(self.prev)
+            os.sched_setaffinity(0, {self.core})
+        except (AttributeError, OSError):
+            self.core = None
+        return self
+
+    def __exit__(self, *a):
+        if self.prev is not None:
+            os.sched_setaffinity(0, self.prev)
+
+
+def cpu_oracle_baseline(layers, budget_s=12.0, max_reps=50, gpu_y=None):
+    """The fp64 oracle as it stands, single process (numpy, 1 core: affinity
+    pinned, BLAS/OpenMP threads 1), on whole layers of the workload, repeated
+    until ~budget_s of CPU work.  Its first result per layer also checks the
+    GPU output of the same layer (``gpu_y``: name -> [B][rows]) against the
+    north-star gate G1 (max|dy| <= 1e-3 ||y||_2) and G3 (||dy||_2 <= 1e-4 ||y||_2)."""
     from oracle import gqsa_oracle as O
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
     done_bytes, t_total, reps = 0, 0.0, 0
+    parity = {}
+    pin = pinned_core()
+    pin.__enter__()
     names = []
     while t_total < budget_s and reps < max_reps:
         for L in layers:
             bsr = L["bsr"]
             t0 = time.perf_counter()
-            O.gemv(bsr, L["x"])
+            y_ref = O.gemv(bsr, L["x"])
             t_total += time.perf_counter() - t0
+            if gpu_y is not None and L["name"] not in parity:
+                d = np.abs(np.asarray(gpu_y[L["name"]], np.float64) - y_ref)
+                nrm = float(np.linalg.norm(y_ref))
+                g1, g3 = float(d.max()) / nrm, float(np.linalg.norm(d)) / nrm
+                parity[L["name"]] = {"g1_maxabs_over_l2": g1, "g3_l2_rel": g3,
+                                     "ok": bool(np.all(np.isfinite(d)) and g1 <= 1e-3 and g3 <= 1e-4)}
             done_bytes += counted_bytes(L["rows"], L["cols"], bsr["nnzg"], bsr["bits"], L["x"].shape[0])
             names.append(L["name"])
             if t_total >= budget_s:
                 break
         reps += 1
+    pin.__exit__()
     return {
         "value": done_bytes / t_total / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+        "pinned_core": pin.core, **host_info(),
         "sample": f"{len(names)} whole-layer oracle GEMVs ({', '.join(sorted(set(names)))}) of the "
                   f"same synthetic workload, {t_total:.1f} s of single-core numpy fp64",
         "seconds": round(t_total, 2),
+        "gpu_parity": parity or None,
     }
 
 
@@ -203,6 +261,63 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- GPU arm
+class StepTimer:
+    """Times K steps replayed from CUDA graphs on `stream` with CUDA events.
+
+    The graphs are exactly the ones the timed region replays -- one of `period`
+    steps (a multiple of the weight-rotation period R) and one of the
+    remainder -- and both are replayed during warm-up, so the timed region pays
+    no first-replay upload.  A short device sleep precedes the start event so
+    that the host has queued the replays before the GPU reaches them (no
+    launch gaps inside the timed region)."""
+
+    def __init__(self, torch, stream, step, R, steps, warmup, use_graph=True):
+        self.torch, self.stream, self.step, self.steps = torch, stream, step, steps
+        self.use_graph = use_graph
+        self.period = R * max(1, -(-120 // R)) if steps > 120 else steps
+        self.rem = steps % self.period
+        if use_graph:
+            self.g_full = self._capture(self.period, 0)
+            self.g_rem = self._capture(self.rem, 0) if self.rem else None
+        self.warm = max(warmup, 3)
+        with torch.cuda.stream(stream):
+            if use_graph:
+                for _ in range(max(1, -(-self.warm // self.period))):
+                    self.g_full.replay()
+                if self.g_rem is not None:
+                    self.g_rem.replay()
+            else:
+                for k in range(self.warm):
+                    step(k)
+        torch.cuda.synchronize()
+
+    def _capture(self, n, start):
+        g = self.torch.cuda.CUDAGraph()
+        with self.torch.cuda.graph(g, stream=self.stream):
+            for k in range(n):
+                self.step(start + k)
+        return g
+
+    def run(self):
+        """Returns milliseconds for `steps` steps (device time, CUDA events)."""
+        torch = self.torch
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(self.stream):
+            torch.cuda._sleep(200_000)  # ~0.1 ms: the host queues the replays meanwhile
+            e0.record(self.stream)
+            if self.use_graph:
+                for _ in range(self.steps // self.period):
+                    self.g_full.replay()
+                if self.g_rem is not None:
+                    self.g_rem.replay()
+            else:
+                for k in range(self.steps):
+                    self.step(k)
+            e1.record(self.stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -217,8 +332,8 @@ def run_gpu(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     fused = args.allgather == "fused"
-    if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
-        os.environ["NCCL_DEBUG"] = "WARN"  # NCCL's version banner goes to stdout: keep it to the JSON line
+    if os.environ.get("NCCL_DEBUG") and not os.environ.get("NCCL_DEBUG_FILE"):
+        os.environ["NCCL_DEBUG_FILE"] = "/dev/stderr"  # NCCL's log to stderr: stdout carries the JSON line
     if world > 1 or fused:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
@@ -227,6 +342,7 @@ def run_gpu(args):
             dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
         else:
             dist.init_process_group(backend, rank=rank, world_size=world)
+    nccl = dist.is_initialized() and dist.get_backend() == "nccl"
 
     bits, sp, B = 4, 0.5, args.batch
     layers = make_layers(bits, sp, B, world, rank)
@@ -240,19 +356,13 @@ def run_gpu(args):
         packed.append((blob, desc))
         set_bytes += blob.size
     R = max(2, math.ceil(2.2 * L2_BYTES / max(set_bytes, 1)) + 1) if not args.no_rotate else 1
-    ws = []
-    copies = []  # copies[r][i] = device blob of layer i
-    for r in range(R):
-        row = []
-        for blob, desc in packed:
-            row.append(torch.from_numpy(blob).to(dev))
-        copies.append(row)
-    for blob, desc in packed:
-        ws.append(torch.zeros(gqsa.workspace_size(desc, B), dtype=torch.uint8, device=dev))
+    copies = [[torch.from_numpy(blob).to(dev) for blob, _ in packed] for _ in range(R)]
+    descs = [d for _, d in packed]
+    ws = torch.zeros(gqsa.workspace_size(descs[0], B), dtype=torch.uint8, device=dev)
     xs = [torch.from_numpy(L["x"]).view(torch.float16).to(dev) for L in layers]
-    ys = [torch.empty(B, d.rows, dtype=torch.float32, device=dev) for _, d in packed]
+    ys = [torch.empty(B, d.rows, dtype=torch.float32, device=dev) for d in descs]
     yfull = [torch.empty(world * B * d.rows, dtype=torch.float32, device=dev) if world > 1 else None
-             for _, d in packed]
+             for d in descs]
 
     # fused all-gather: each rank's GEMV stores its rows
     # straight into every rank's full y (symmetric memory, NVLink P2P), then a
@@ -267,94 +377,66 @@ def run_gpu(args):
         peers = [[h.get_buffer(p, (B, L["rows"]), torch.float32) for p in range(world)]
                  for h, L in zip(hdl, layers)]
 
-    def launch(i, r):
-        _, desc = packed[i]
+    path = "launches" if fused else args.path
+    grouped = [gqsa.Grouped([(descs[i], copies[r][i], xs[i], ys[i], None) for i in range(len(layers))], ws,
+                            x_ready=args.x_ready) for r in range(R)]
+
+    def gemvs(r):
+        """The step's sparse GEMVs (this rank's shards)."""
         if fused:
-            gqsa.gemm_allgather(desc, copies[r][i], xs[i], peers[i], row_offset=layers[i]["lo"], ws=ws[i])
-            hdl[i].barrier(channel=0)
-            return
-        if B == 1:
-            gqsa.gemv(desc, copies[r][i], xs[i][0], ys[i][0], None, ws[i])
+            for i in range(len(layers)):
+                gqsa.gemm_allgather(descs[i], copies[r][i], xs[i], peers[i], row_offset=layers[i]["lo"], ws=ws)
+                hdl[i].barrier(channel=0)
+        elif path == "grouped":
+            grouped[r]()
         else:
-            gqsa.gemm_smallbatch(desc, copies[r][i], xs[i], ys[i], None, ws[i])
-        if world > 1:
-            dist.all_gather_into_tensor(yfull[i], ys[i].view(-1))
+            for i in range(len(layers)):
+                if B == 1:
+                    gqsa.gemv(descs[i], copies[r][i], xs[i][0], ys[i][0], None, ws)
+                else:
+                    gqsa.gemm_smallbatch(descs[i], copies[r][i], xs[i], ys[i], None, ws)
 
-    # chain path: the step's GEMVs in one persistent launch,
-    # each item reading its x only after the previous items completed
-    # (wait_prev = 1: the same sequential semantics as one launch per GEMV)
-    use_chain = args.path == "chain" and world == 1 and B <= 2
-    chain_items = [[(packed[i][1], copies[r][i], xs[i], ys[i], None, 1) for i in range(len(layers))]
-                   for r in range(R)]
-    chain_ws = (torch.zeros(gqsa.chain_workspace_size(chain_items[0], B), dtype=torch.uint8, device=dev)
-                if use_chain else None)
+    def gathers():
+        """The step's exchange: all-gather of every layer's y shard over NCCL (N > 1)."""
+        if world > 1 and not fused:
+            for i in range(len(layers)):
+                dist.all_gather_into_tensor(yfull[i], ys[i].view(-1))
 
-    def step(r):
-        if use_chain:
-            gqsa.gemm_chain(chain_items[r], chain_ws)
-            return
-        for i in range(len(layers)):
-            launch(i, r)
+    def step(k):
+        gemvs(k % R)
+        gathers()
 
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.synchronize()
-    # eager warm-up (also the first launches: attribute set-up, module load)
-    with torch.cuda.stream(stream):
+    with torch.cuda.stream(stream):  # eager first launches (attributes, module load, NCCL comms)
         for r in range(R):
             step(r)
     torch.cuda.synchronize()
-
-    def capture(nsteps, start=0):
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
-            for k in range(nsteps):
-                step((start + k) % R)
-        return g
-
-    use_graph = world == 1 and not fused  # collectives stay eager
-    graphs = {}
-
-    def run_steps(n):
-        if use_graph:
-            if R not in graphs:
-                graphs[R] = capture(R)
-            for _ in range(n // R):
-                graphs[R].replay()
-            if n % R:
-                if n % R not in graphs:
-                    graphs[n % R] = capture(n % R)
-                graphs[n % R].replay()
-        else:
-            for k in range(n):
-                step(k % R)
-
-    with torch.cuda.stream(stream):
-        run_steps(max(args.warmup, 3))
-        if use_graph and args.steps % R:
-            graphs.setdefault(args.steps % R, capture(args.steps % R))
-    torch.cuda.synchronize()
+    # NCCL collectives are graph-capturable; symmetric-memory barriers and the
+    # gloo test hook stay eager
+    use_graph = not fused and (world == 1 or nccl)
+    timer = StepTimer(torch, stream, step, R, args.steps, args.warmup, use_graph)
     if world > 1:
         dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(local)
-    torch.cuda.synchronize()
     with sampler:
-        e0.record(stream)
-        with torch.cuda.stream(stream):
-            run_steps(args.steps)
-        e1.record(stream)
-        torch.cuda.synchronize()
+        ms = timer.run()
     if world > 1:
         dist.barrier()
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    ms_step = ms / args.steps
 
-    # counted bytes: every rank's shard (sum over ranks) + the all-gathered y
-    step_bytes_rank = sum(counted_bytes(d.rows, d.cols, d.nnzg, bits, B) for _, d in packed)
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ms = max_over_ranks(ms)
+    ms_step = ms / args.steps
+    warm = timer.warm
+
+    # counted bytes: every rank's shard (sum over ranks)
+    step_bytes_rank = sum(counted_bytes(d.rows, d.cols, d.nnzg, bits, B) for d in descs)
     if world > 1:
         t = torch.tensor([step_bytes_rank], dtype=torch.float64, device=dev)
         dist.all_reduce(t)
@@ -363,61 +445,55 @@ def run_gpu(args):
         step_bytes = float(step_bytes_rank)
     value = step_bytes * args.steps / (ms * 1e-3) / 1e9
 
-    # ---- per-layer device time (dominant kernel per shape), outside the timed region
+    # ---- multi-GPU split: kernels alone and the exchange alone,
+    #      each timed like the step (graphs, max over ranks)
+    split = None
+    if world > 1 and not fused:
+        ksteps = min(args.steps, 2000)
+        kt = StepTimer(torch, stream, lambda k: gemvs(k % R), R, ksteps, args.warmup, use_graph)
+        dist.barrier()
+        k_ms = max_over_ranks(kt.run()) / ksteps
+        gt = StepTimer(torch, stream, lambda k: gathers(), 1, ksteps, args.warmup, use_graph)
+        dist.barrier()
+        g_ms = max_over_ranks(gt.run()) / ksteps
+        split = {"per_rank_kernel_us": round(k_ms * 1e3, 3), "allgather_us": round(g_ms * 1e3, 3),
+                 "end_to_end_us": round(ms_step * 1e3, 3),
+                 "kernel_only_aggregate_gbs": round(step_bytes / (k_ms * 1e-3) / 1e9, 1),
+                 "allgather_bytes_per_rank": int(sum(B * d.rows * 4 for d in descs)),
+                 "nccl": nccl}
+
+    # ---- per-layer device time (one launch per layer), outside the timed region
     layer_rows = []
     if world == 1:
         for i, L in enumerate(layers):
-            _, desc = packed[i]
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                for r in range(R):
-                    if B == 1:
-                        gqsa.gemv(desc, copies[r][i], xs[i][0], ys[i][0], None, ws[i])
-                    else:
-                        gqsa.gemm_smallbatch(desc, copies[r][i], xs[i], ys[i], None, ws[i])
-            for _ in range(3):
-                g.replay()
-            reps = max(10, 2000 // R)
-            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            a.record(stream)
-            with torch.cuda.stream(stream):
-                for _ in range(reps):
-                    g.replay()
-            b_.record(stream)
-            torch.cuda.synchronize()
-            us = a.elapsed_time(b_) * 1e3 / (reps * R)
-            # spread over 50 replays (each R launches; an event between replays
-            # breaks the PDL overlap at the replay boundary, so these sit a
-            # little above the back-to-back mean "us")
-            evs = [torch.cuda.Event(enable_timing=True) for _ in range(51)]
-            with torch.cuda.stream(stream):
-                evs[0].record(stream)
-                for k in range(50):
-                    g.replay()
-                    evs[k + 1].record(stream)
-            torch.cuda.synchronize()
-            per = np.array([evs[k].elapsed_time(evs[k + 1]) * 1e3 / R for k in range(50)])
-            cb = counted_bytes(desc.rows, desc.cols, desc.nnzg, bits, B)
-            layer_rows.append({"shape": f"{desc.rows}x{desc.cols}", "role": L["name"],
-                               "nnzg": desc.nnzg, "counted_bytes": cb, "us": round(us, 3),
-                               "replay_us_p10_p50_p90": [round(float(np.percentile(per, q)), 3) for q in (10, 50, 90)],
+            d = descs[i]
+
+            def one(k, i=i):
+                if B == 1:
+                    gqsa.gemv(d, copies[k % R][i], xs[i][0], ys[i][0], None, ws)
+                else:
+                    gqsa.gemm_smallbatch(d, copies[k % R][i], xs[i], ys[i], None, ws)
+            reps = max(R, (2000 // R) * R)
+            lt = StepTimer(torch, stream, one, R, reps, 3 * R, True)
+            us = lt.run() * 1e3 / reps
+            cb = counted_bytes(d.rows, d.cols, d.nnzg, bits, B)
+            layer_rows.append({"shape": f"{d.rows}x{d.cols}", "role": L["name"], "nnzg": d.nnzg,
+                               "counted_bytes": cb, "blob_bytes": int(d.blob_bytes), "us": round(us, 3),
                                "gbs": round(cb / us / 1e3, 1),
                                "frac_of_8tbs": round(cb / us / 1e3 / NOMINAL_HBM_GBS, 4),
                                "frac_of_measured": round(cb / us / 1e3 / hbm_peak, 4)})
 
     # ---- end to end through the public C ABI with host buffers (pinned):
     #      gqsa_gemm_multi_hostio = one H2D copy of the step's inputs, the
-    #      step's GEMV launches, one D2H copy of its outputs; the caller
-    #      synchronises and reads y every step
+    #      step's GEMVs as one grouped launch, one D2H copy of its outputs; the
+    #      caller synchronises and reads y every step
     e2e = None
     if world == 1:
-        descs = [d for _, d in packed]
         hX = torch.from_numpy(np.concatenate([L["x"].reshape(-1) for L in layers])).view(torch.float16).pin_memory()
         hY = torch.empty(sum(B * d.rows for d in descs), dtype=torch.float32).pin_memory()
         stage = torch.empty(gqsa.multi_hostio_stage_size(descs, B), dtype=torch.uint8, device=dev)
         ne = min(args.steps, args.e2e_steps)
-        calls = [gqsa.MultiHostIO(descs, copies[r], hX, hY, stage, ws, batch=B) for r in range(R)]
+        calls = [gqsa.MultiHostIO(descs, copies[r], hX, hY, stage, [ws], batch=B) for r in range(R)]
 
         def e2e_step(k):
             calls[k % R](stream)
@@ -437,28 +513,33 @@ def run_gpu(args):
         e2e = {"value": step_bytes * ne / (e_ms * 1e-3) / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": int(hX.numel() * 2), "d2h_bytes_per_step": int(hY.numel() * 4),
                "steps": ne, "ms_per_step": e_ms / ne, "wall_ms_per_step": wall * 1e3 / ne,
-               "api": "gqsa_gemm_multi_hostio (1 H2D + per-layer launches + 1 D2H, stream sync per step)"}
+               "api": "gqsa_gemm_multi_hostio (1 H2D + one grouped launch + 1 D2H, stream sync per step)"}
 
+    # ---- outputs of the timed step, for the parity check in the cpu_baseline leg
+    with torch.cuda.stream(stream):
+        step(0)
+    torch.cuda.synchronize()
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_oracle_baseline(layers, budget_s=args.cpu_budget)
+        gpu_y = None if fused else {L["name"]: ys[i].cpu().numpy() for i, L in enumerate(layers)}
+        cpu = cpu_oracle_baseline(layers, budget_s=args.cpu_budget, gpu_y=gpu_y)
 
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            tr = json.load(open(tp))
-            traffic = tr.get("step_dram_bytes")
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    achieved = step_bytes / (ms_step * 1e-3) / 1e9 / world if world > 1 else value
+    n_launch = (1 if path == "grouped" else len(layers)) * args.steps
+    achieved = value if world == 1 else step_bytes / world / (ms_step * 1e-3) / 1e9
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
-        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_step,
+        "steps": args.steps, "warmup": warm, "ms_per_step": ms_step,
         "us_per_step": round(ms_step * 1e3, 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "u4xf16->f32",
@@ -468,22 +549,26 @@ def run_gpu(args):
                    "global_batch": B, "seq_len": 1, "group_size": 16, "bits": bits, "sparsity": sp,
                    "parallelism": f"rowshard{world}" if world > 1 else "single",
                    "allgather": (args.allgather if (world > 1 or fused) else None),
-                   "l2": f"weights rotate over {R} device copies of the layer set "
+                   "l2": f"inputs larger than L2: weights rotate over {R} device copies of the layer set "
                          f"({R * set_bytes / 2**20:.0f} MiB > 2x L2)",
-                   "path": "gqsa_gemm_chain (one persistent launch per step, grid barrier between layers)"
-                           if use_chain else "one gqsa_gemv launch per layer (PDL)",
-                   "timing": "CUDA graphs of the step's launches (PDL between launches), CUDA events on the "
-                             "launch stream"},
+                   "path": {"grouped": "one gqsa_gemm_grouped launch per step (the 3 independent GEMVs "
+                                       "share one Stream-K partition)",
+                            "launches": "one gqsa_gemv launch per layer (PDL)"}[path],
+                   "x_ready": bool(args.x_ready),
+                   "timing": "CUDA graphs of the step (all graphs replayed in warm-up), CUDA events on the "
+                             "launch stream, device sleep before the start event"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
                      "peak_source": peak_src, "frac_of_nominal_8tbs": round(achieved / NOMINAL_HBM_GBS, 4),
-                     "kernel": f"gqsa::gqsa_chain_kernel<{bits},{B}>" if use_chain
-                               else f"gqsa::gqsa_streamk_kernel<{bits},{B}>",
-                     "algorithmic_bytes_per_step": int(step_bytes)},
+                     "kernel": f"gqsa::gqsa_stream_kernel<{bits},{B},16>",
+                     "algorithmic_bytes_per_step": int(step_bytes),
+                     "note": "achieved = algorithmic bytes of the step / device time of the step; the step is "
+                             + ("ONE launch of the dominant kernel" if path == "grouped" else "3 launches")},
         "layers": layer_rows,
+        "multi_gpu": split,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": (1 if use_chain else len(layers)) * args.steps,
+        "gpu_launches": n_launch,
         "clocks": sampler.summary(),
     }
     print(json.dumps(line), flush=True)
@@ -505,8 +590,11 @@ def main():
     ap.add_argument("--allgather", default="nccl", choices=["nccl", "fused"],
                     help="row-shard output exchange: NCCL all_gather, or the fused GEMV epilogue storing "
                          "into every rank's y over symmetric memory (gqsa_gemm_allgather)")
-    ap.add_argument("--path", default="launches", choices=["chain", "launches"],
-                    help="chain: one gqsa_gemm_chain launch per step; launches: one gqsa_gemv per layer")
+    ap.add_argument("--path", default="grouped", choices=["grouped", "launches"],
+                    help="grouped: the step's GEMVs in one gqsa_gemm_grouped launch; launches: one gqsa_gemv "
+                         "per layer")
+    ap.add_argument("--x-ready", type=int, default=0, choices=[0, 1],
+                    help="declare x not produced by the previous kernel (staged before the PDL wait)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -20,14 +20,16 @@
  * never allocates or frees device memory and keeps no pointer past a call.
  * A packed blob is immutable and may be shared by concurrent calls on
  * different streams, each with its OWN workspace.  A workspace
- * must be zero-filled once when allocated; every call returns each 64-B
- * record's flag word to zero (the partial-sum words are scratch).
+ * must be zero-filled once when allocated; every call leaves it zero again
+ * (fix-up counters and record flags; the partial-sum words are scratch).
+ * Forward progress never depends on CTA co-residency: no thread waits for a
+ * thread that has not already written what it waits for.
  *
  * Errors: every int-returning function returns GQSA_OK (0) or a negative
  * gqsa_status_t.  Errors raised during asynchronous device execution surface
  * at the next stream synchronisation (CUDA convention).
  *
- * Byte layout of the packed blob: DESIGN.md §5 ("LAYOUT v2").
+ * Byte layout of the packed blob: DESIGN.md §5 ("LAYOUT v3").
  */
 #ifndef GQSA_H_
 #define GQSA_H_
@@ -40,15 +42,16 @@ extern "C" {
 #endif
 
 #define GQSA_MAGIC 0x41535147u   /* bytes "GQSA" little-endian */
-#define GQSA_VERSION 2
-#define GQSA_TILE_GROUPS 128     /* kept groups per tile record (LAYOUT v1) */
+#define GQSA_VERSION 3
+#define GQSA_TILE_GROUPS 128     /* kept groups per tile record */
+#define GQSA_MAX_COLS 32736      /* K limit: the u16 column field addresses 2K + 64 bytes */
 #define GQSA_MAX_BATCH 8
 
 typedef enum {
   GQSA_OK = 0,
   GQSA_ERR_SHAPE = -1,       /* dims mismatch, cols % G != 0, B not in [1,8], bad row range */
   GQSA_ERR_VALIDATION = -2,  /* BSR invariant violated (see gqsa_pack) or inconsistent blob */
-  GQSA_ERR_UNSUPPORTED = -3, /* (bits, G) not in {2,4,8} x {16} or {4} x {8,32}; cols > 32768 */
+  GQSA_ERR_UNSUPPORTED = -3, /* (bits, G) not in {2,4,8} x {16} or {4} x {8,32}; cols > GQSA_MAX_COLS */
   GQSA_ERR_BUFFER = -4,      /* null pointer, blob/workspace too small, misaligned device pointer */
   GQSA_ERR_CUDA = -5         /* CUDA launch / copy failure */
 } gqsa_status_t;
@@ -58,7 +61,7 @@ typedef enum {
  *   rows, cols    : N (out_features) and K (in_features) of W[N][K].
  *   group_size    : G, the sparse AND quantization group: 16 (the
  *                   paper's default) for every width; 8 or 32 for
- *                   W4 (the group-size sweep; the chain kernel takes 16 only).
+ *                   W4 only (the group-size sweep).
  *   bits          : n, code width: 4 or 2 (the paper's W4/W2), or 8 (W8, the
  *                   paper's other deployed setting).
  *   nnzg          : number of kept groups = row_index[rows].
@@ -94,7 +97,7 @@ typedef struct {
  *                lowest mean saliency of the layer; ties -> lower (row, group)
  *                index) are pruned.
  *   bits       : 2, 4 or 8;  group_size: G (any divisor of cols; the packer
- *                and kernels take G = 16).
+ *                and kernels take G = 16 for every width, G = 8 / 32 for W4).
  *   out        : caller-allocated arrays: row_index int32[rows+1];
  *                group_cols/scales_f16/zeros_f16 [nnzg]; codes
  *                ceil(nnzg*G*bits/8) bytes, where nnzg = gqsa_compress_nnzg();
@@ -120,7 +123,8 @@ typedef struct {
   int32_t n_nzrows, n_empty;
   int32_t tile_bytes, flags;
   int32_t row_begin, row_end;     /* source row range this blob was packed from */
-  uint64_t off_row_index, off_nzrow, off_empty, off_tiles, blob_bytes;
+  int32_t num_slices, reserved0;
+  uint64_t off_row_index, off_perm, off_empty, off_slice_tile0, off_tile_slice, off_tiles, blob_bytes;
 } gqsa_desc_t;
 
 /*
@@ -149,8 +153,10 @@ int gqsa_read_desc(const void* blob, size_t blob_bytes, gqsa_desc_t* desc);
  * ceil(nnzg*G*n/8) bytes. */
 int gqsa_unpack(const void* blob, size_t blob_bytes, gqsa_bsr_t* out);
 
-/* Workspace bytes a gemv/gemm call needs for `batch` columns on the current
- * device (cross-warp fix-up records).  Zero-fill once. */
+/* Workspace bytes a gemv/gemm (or grouped) call needs for `batch` columns on
+ * the current device: per-warp fix-up arrival counters and partial-sum records
+ * (DESIGN.md §6).  It depends on the batch and the device's SM count, not on
+ * the layer.  Zero-fill once; every call leaves it zero. */
 int gqsa_workspace_size(const gqsa_desc_t* desc, int32_t batch, size_t* bytes);
 
 /*
@@ -163,7 +169,8 @@ int gqsa_workspace_size(const gqsa_desc_t* desc, int32_t batch, size_t* bytes);
  *   stream : cudaStream_t (NULL = legacy default stream).
  * Asynchronous; graph-capturable.  Uses Programmatic Dependent Launch so that
  * weight fetch overlaps the previous kernel on the stream; activations are
- * read only after the previous kernel completes.
+ * read only after the previous kernel completes (unless the caller declares
+ * them ready, gqsa_options_t.x_ready).
  */
 int gqsa_gemv(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_x, float* d_y,
               const float* d_bias, void* d_ws, size_t ws_bytes, void* stream);
@@ -192,6 +199,12 @@ int gqsa_gemm_smallbatch(const gqsa_desc_t* desc, const void* d_blob, const uint
  *   opts->out_f16: 0 = fp32 Y (default), 1 = fp16 Y (round-to-nearest-even
  *     of the fp32 result (+ bias)); d_Y then points to uint16 [B][ldy]
  *     (2-B aligned).
+ *   opts->x_ready: 0 (default) = X may be written by the previous kernel on
+ *     the stream, so it is read after that kernel completes; 1 = the caller
+ *     guarantees X is NOT written by the previous kernel (e.g. several
+ *     GEMVs of one input, or inputs copied before an earlier launch), so the
+ *     kernel stages X while the previous kernel drains.  Y, bias and the
+ *     workspace are always touched only after the previous kernel completes.
  * Other option values return GQSA_ERR_SHAPE.
  */
 #define GQSA_PARTITION_STREAM_K 0
@@ -199,6 +212,8 @@ int gqsa_gemm_smallbatch(const gqsa_desc_t* desc, const void* d_blob, const uint
 typedef struct {
   int32_t partition;  /* GQSA_PARTITION_* */
   int32_t out_f16;    /* 0: fp32 output, 1: fp16 output */
+  int32_t x_ready;    /* 1: X is not produced by the previous kernel on the stream */
+  int32_t reserved;   /* 0 */
 } gqsa_options_t;
 int gqsa_gemm_ex(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_X, int32_t B,
                  int64_t ldx, void* d_Y, int64_t ldy, const float* d_bias, void* d_ws,
@@ -225,35 +240,27 @@ int gqsa_gemm_allgather(const gqsa_desc_t* desc, const void* d_blob, const uint1
                         const float* d_bias, void* d_ws, size_t ws_bytes, void* stream);
 
 /*
- * gqsa_gemm_chain: a sequence of GEMVs (e.g. the linear layers of a decoder
- * step) in ONE persistent launch, with the same results as calling
- * gqsa_gemm_smallbatch on items[0], items[1], ... in order on `stream`.
- *   items[j].desc / d_blob : the packed layer (all items: the same `bits`)
- *   items[j].d_X           : device fp16 [B][ldx], ldx >= cols, ldx % 8 == 0
- *   items[j].d_Y           : device fp32 [B][ldy], ldy >= rows (or fp16 when out_f16)
+ * gqsa_gemm_grouped: n INDEPENDENT GEMMs (e.g. the q/k/v or gate/up
+ * projections of a decoder step, or the step's layers when their inputs are
+ * ready) in ONE launch: Y_j[b] = W_hat_j X_j[b] (+ bias_j), j < n.  The tile
+ * streams of all items are concatenated and cut into equal (+-1 tile) ranges
+ * per warp (PAPER.md:161 Stream-K over the total work), so the step pays one
+ * launch, one activation staging and one tail instead of n.
+ *   items[j].desc / d_blob : packed layer j (all items: the same bits and G)
+ *   items[j].d_X           : device fp16 [B][ldx], ldx >= cols, ldx % 8 == 0, 16-B aligned
+ *   items[j].d_Y           : device fp32 [B][ldy] (fp16 when opts->out_f16), ldy >= rows
  *   items[j].d_bias        : device fp32 [rows] or NULL
- *   items[j].wait_prev     : 1 = item j may read an earlier item's output, so it
- *                            reads X only after items 0..j-1 have completed
- *                            (grid-wide barrier; sequential semantics); 0 = X
- *                            and Y are independent of earlier items (no barrier)
- *   items[j].out_f16       : 0 = fp32 Y, 1 = fp16 Y (RNE), e.g. the next item's X
- *   n in [1, GQSA_MAX_CHAIN], B in {1, 2}, bits in {2, 4}.
- * Each item computes exactly what the single-GEMV kernel computes (Eq. 3,
- * PAPER.md:64-69, over the BSR of PAPER.md:95-101, Stream-K partition of
- * PAPER.md:161); the fp32 summation order of a row may differ from the
- * single-GEMV launch (different grid), and is fixed for a given chain and
- * device (bit-identical reruns).  What the chain adds: the
- * weight stream runs ahead across layer boundaries, so a layer boundary costs
- * a barrier instead of a kernel launch and an idle memory system.
- * All CTAs must be co-resident (one per SM; cooperative launch): returns
- * GQSA_ERR_CUDA if the device cannot host the grid.
- * Workspace: gqsa_chain_workspace_size bytes, zero-filled once at allocation
- * (each launch returns it to zero); not shared with concurrent launches.
- * Errors: GQSA_ERR_SHAPE (n, B, ld*), GQSA_ERR_UNSUPPORTED (mixed bits, bits
- * 8, x of the widest item does not fit in shared memory), GQSA_ERR_BUFFER
- * (null / misaligned pointers, small workspace), GQSA_ERR_VALIDATION (desc).
+ *   n in [1, GQSA_MAX_ITEMS], 1 <= B <= 8; opts as gqsa_gemm_ex (NULL = defaults).
+ * No item may read another item's output (they run concurrently).  Each
+ * item's result equals gqsa_gemm_ex on it alone up to the fp32 summation
+ * order (bit-identical reruns for a fixed item list and device).  Items whose
+ * activations do not fit in shared memory together run as several launches.
+ * Workspace: gqsa_workspace_size(items[0].desc, B) bytes.
+ * Errors: GQSA_ERR_SHAPE (n, B, ld*, options), GQSA_ERR_UNSUPPORTED (mixed
+ * bits / G), GQSA_ERR_BUFFER (null / misaligned pointers, small workspace),
+ * GQSA_ERR_VALIDATION (desc).
  */
-#define GQSA_MAX_CHAIN 16
+#define GQSA_MAX_ITEMS 8
 typedef struct {
   const gqsa_desc_t* desc;
   const void* d_blob;
@@ -262,12 +269,9 @@ typedef struct {
   void* d_Y;
   int64_t ldy;
   const float* d_bias;
-  int32_t wait_prev;
-  int32_t out_f16;
-} gqsa_chain_item_t;
-int gqsa_chain_workspace_size(const gqsa_chain_item_t* items, int32_t n, int32_t B, size_t* bytes);
-int gqsa_gemm_chain(const gqsa_chain_item_t* items, int32_t n, int32_t B, void* d_ws, size_t ws_bytes,
-                    void* stream);
+} gqsa_gemm_item_t;
+int gqsa_gemm_grouped(const gqsa_gemm_item_t* items, int32_t n, int32_t B, const gqsa_options_t* opts,
+                      void* d_ws, size_t ws_bytes, void* stream);
 
 /*
  * gqsa_gemm_hostio: the end-to-end call with HOST activations and outputs.
@@ -285,9 +289,11 @@ int gqsa_gemm_hostio(const gqsa_desc_t* desc, const void* d_blob, const uint16_t
 /*
  * gqsa_gemm_multi_hostio: n INDEPENDENT layers with host I/O in one call --
  * the end-to-end path of a decode step whose activations live on the host:
- * ONE host->device copy of all inputs, one gqsa_gemm_smallbatch launch per
- * layer (PDL-chained on `stream`), ONE device->host copy of all outputs.
- *   descs[j], d_blobs[j], d_ws[j], ws_bytes[j] : layer j (as gqsa_gemm_smallbatch)
+ * ONE host->device copy of all inputs, the layers as gqsa_gemm_grouped
+ * launches (one per GQSA_MAX_ITEMS layers), ONE device->host copy of all
+ * outputs.
+ *   descs[j], d_blobs[j] : layer j; d_ws[0] / ws_bytes[0]: the workspace
+ *   (gqsa_workspace_size; the other entries are ignored)
  *   h_X : host fp16, the concatenation of the n inputs [B][cols_j] (dense,
  *         layer 0 first); pinned memory makes the copy asynchronous
  *   h_Y : host fp32, the concatenation of the n outputs [B][rows_j]
@@ -306,11 +312,10 @@ int gqsa_gemm_multi_hostio(const gqsa_desc_t* const* descs, const void* const* d
  * CTAs, warps per CTA, active warps (Stream-K units), tiles.  For tooling. */
 typedef struct {
   int32_t grid, warps_per_cta, active_warps, num_tiles, smem_bytes, x_in_smem;
-  int32_t stages, ctas_per_sm, ring_bytes;  /* TMA ring depth per warp, residency, ring size */
+  int32_t stages, ctas_per_sm, ring_bytes;  /* tiles in flight per warp (register buffers), 1, 0 */
   int32_t batch_per_launch, launches;  /* x of batch_per_launch columns fits in shared memory;
                                           larger batches run as `launches` launches */
-  int32_t coresident;                  /* 1: CTA uses <= half an SM, so the next PDL launch
-                                          overlaps; 0: the CTA takes the whole SM */
+  int32_t coresident;                  /* always 0: one CTA per SM owns the SM */
 } gqsa_plan_t;
 int gqsa_launch_plan(const gqsa_desc_t* desc, int32_t B, gqsa_plan_t* plan);
 
@@ -319,7 +324,7 @@ uint64_t gqsa_launch_count(void);
 
 /* Profiling hook: while set, every launch writes, per active warp w, eight
  * uint64 %globaltimer stamps at d_buf[8w .. 8w+7] (0 start, 1 after the PDL
- * wait, 2 activations staged, 3 first tile landed, 4 tile loop done, 5 exit)
+ * wait, 2 activations staged, 3 tile loop start, 4 tile loop done, 5 exit)
  * when bytes >= 64 * active_warps.  d_buf = NULL turns it off (default).
  * The buffer is caller-owned device memory; not for production use. */
 int gqsa_debug_trace(void* d_buf, size_t bytes);

@@ -1,4 +1,4 @@
-"""Independent Python implementation of the packed-blob LAYOUT v2 -- TEST
+"""Independent Python implementation of the packed-blob LAYOUT v3 -- TEST
 INFRASTRUCTURE ONLY (same import rules as gqsa_oracle.py).
 
 Written from the prose specification in DESIGN.md §5, not from the C++
@@ -12,7 +12,7 @@ import struct
 import numpy as np
 
 MAGIC = 0x41535147
-VERSION = 2
+VERSION = 3
 T = 128          # groups per tile (4 slots x 32 lanes)
 LANES = 32
 SLOTS = 4
@@ -25,8 +25,8 @@ def _align(v: int, a: int = ALIGN) -> int:
 
 
 def tile_bytes(bits: int, G: int = 16) -> int:
-    # 32 B tile header + codes (T*G*n/8) + s/z (T*4) + columns (T*2)
-    return 32 + T * G * bits // 8 + T * 4 + T * 2
+    # codes (T*G*n/8) + s/z (T*4) + columns (T*2); no per-tile header
+    return T * G * bits // 8 + T * 4 + T * 2
 
 
 def target_slots(nnzg: int) -> int:
@@ -104,17 +104,24 @@ def pack_reference(bsr: dict, row_begin: int = 0, row_end=None) -> bytes:
     off_ri = HDR
     off_perm = _align(off_ri + 4 * (rows + 1))
     off_em = _align(off_perm + 4 * LANES * n_slices)
-    off_tiles = _align(off_em + 4 * len(empty))
+    off_st0 = _align(off_em + 4 * len(empty))
+    off_ts = _align(off_st0 + 4 * (n_slices + 1))
+    off_tiles = _align(off_ts + 4 * num_tiles)
     total = _align(off_tiles + num_tiles * tb)
 
     out = bytearray(total)
-    struct.pack_into("<IIiiiiqiiiiiiiiQQQQQ", out, 0,
+    struct.pack_into("<IIiiiiqiiiiiiiiiiQQQQQQQ", out, 0,
                      MAGIC, VERSION, rows, K, G, n, nnzg, T, num_tiles, len(nz), len(empty),
-                     tb, (4 if G == 16 else 0) | (S << 8), row_begin, row_end, off_ri, off_perm, off_em,
-                     off_tiles, total)
+                     tb, (4 if G == 16 else 0) | (S << 8), row_begin, row_end, n_slices, 0,
+                     off_ri, off_perm, off_em, off_st0, off_ts, off_tiles, total)
     struct.pack_into(f"<{rows + 1}i", out, off_ri, *[v - g0 for v in ri_all[row_begin:row_end + 1]])
     if empty:
         struct.pack_into(f"<{len(empty)}i", out, off_em, *empty)
+    # slice tables: first tile of each slice (+ the total), and the slice of each tile
+    first = [sum(slice_tiles[:s]) for s in range(n_slices + 1)]
+    struct.pack_into(f"<{n_slices + 1}i", out, off_st0, *first)
+    if num_tiles:
+        struct.pack_into(f"<{num_tiles}i", out, off_ts, *[s for s in range(n_slices) for _ in range(slice_tiles[s])])
 
     cb = G * n // 8
     codes = np.asarray(bsr["codes"], np.uint8)
@@ -144,14 +151,12 @@ def pack_reference(bsr: dict, row_begin: int = 0, row_end=None) -> bytes:
                     deal[key] = gr + pos
         for tau in range(nt):
             base = off_tiles + t * tb
-            flags = (1 if tau == 0 else 0) | (2 if tau == nt - 1 else 0)
-            struct.pack_into("<IIII", out, base, (s << 2) | flags, nt - 1 - tau, t - tau, 0)
             for u in range(SLOTS):
                 for lane in range(LANES):
                     g = deal.get((lane, tau * SLOTS + u))
-                    off_col = base + 32 + codes_total + T * 4 + lane * 8 + u * 2
-                    if g is None:  # padding: reads the lane's target chunk (G = 16) or chunk 0
-                        struct.pack_into("<H", out, off_col, ((lane % 16) % (K // 8)) << 4 if G == 16 else 0)
+                    off_col = base + codes_total + T * 4 + lane * 8 + u * 2
+                    if g is None:  # padding: s = z = 0, codes 0, reads the zero block after x (byte 2K)
+                        struct.pack_into("<H", out, off_col, 2 * K)
                         continue
                     swap = lane % 2 if G == 16 else lane % 4 if G == 32 else 0
                     gb = bytes(codes[g * cb:(g + 1) * cb])
@@ -159,9 +164,9 @@ def pack_reference(bsr: dict, row_begin: int = 0, row_end=None) -> bytes:
                         gb = b"".join(gb[4 * ((k + swap) % 4):4 * ((k + swap) % 4) + 4] for k in range(4))
                     elif swap:
                         gb = gb[cb // 2:] + gb[:cb // 2]
-                    off_c = base + 32 + (u // per_plane) * 512 + lane * 16 + (u % per_plane) * cb
+                    off_c = base + (u // per_plane) * 512 + lane * 16 + (u % per_plane) * cb
                     out[off_c:off_c + cb] = gb
-                    struct.pack_into("<HH", out, base + 32 + codes_total + lane * 16 + u * 4,
+                    struct.pack_into("<HH", out, base + codes_total + lane * 16 + u * 4,
                                      int(sc[g]), int(zr[g]))
                     # byte offset of the group's first 16-B x chunk: 2c + swap (G = 16), c (G = 8), 4c (G = 32)
                     field = (((int(gcols[g]) << 1) | swap) << 4 if G == 16 else

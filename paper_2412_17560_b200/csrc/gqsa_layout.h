@@ -1,11 +1,13 @@
-// gqsa_layout.h -- LAYOUT v2 of the packed GQSA blob (product-internal).
+// gqsa_layout.h -- LAYOUT v3 of the packed GQSA blob (product-internal).
 //
 // The blob is the paper's BSR (rowIndex / groups / values +
 // per-group scale and zero) re-laid out offline for the B200
 // kernel as a sliced-ELL stream of 128-group tiles (4 slots x 32 lanes, one
-// lane per row): every warp-level load is a fully-coalesced 512-B (codes,
-// s/z) or 256-B (columns) request, and a lane accumulates its row without
-// cross-lane reductions.  Full description: DESIGN.md §5.
+// lane per row): every warp-level load of a tile is a fully coalesced,
+// 128-B-aligned 512-B (codes, s/z) or 256-B (columns) request straight into
+// registers, and a lane accumulates its row without cross-lane reductions.
+// Slice boundaries live in two small side tables instead of per-tile headers,
+// so a tile is an exact multiple of 128 B.  Full description: DESIGN.md §5.
 #pragma once
 #include <stdint.h>
 
@@ -21,23 +23,24 @@
 namespace gqsa {
 
 constexpr uint32_t kMagic = 0x41535147u;  // "GQSA"
-constexpr int kVersion = 2;
-constexpr int kGroup = 16;          // G (v1/v2)
+constexpr int kVersion = 3;
+constexpr int kGroup = 16;          // G (the paper's default)
 constexpr int kTileGroups = 128;    // groups (incl. padding) per tile record
 constexpr int kLanes = 32;          // one warp consumes one tile, one lane per row
 constexpr int kPerLane = kTileGroups / kLanes;  // 4 slots per lane per tile
 constexpr int kHeaderBytes = 256;
-constexpr int kTileHeaderBytes = 32;  // u32 (slice<<2 | FIRST | LAST), tiles_to_slice_end, slice_first_tile; 0[5]
 constexpr int kSectionAlign = 256;
-constexpr uint32_t kFlagTargetDeal = 4u;     // bank-aware dealing: lane l reads chunk f = 2c+swap,
-                                             // f mod 16 == l mod 16 whenever the row allows
+constexpr uint32_t kFlagTargetDeal = 4u;     // bank-aware dealing (G = 16)
 constexpr int kFlagLanesPerRowShift = 8;     // flags bits 8..15: lanes per row S
-constexpr int kMaxCols = 32768;              // column field = byte offset (2c+swap)*16 < 65536
-constexpr uint32_t kTileFirst = 1u;          // tile header flags
-constexpr uint32_t kTileLast = 2u;
+// The column field is the byte offset of a 16-B activation chunk in a u16;
+// padding entries point at a 64-B zero block right after the K activations
+// of each batch row (offset 2K), so 2K + 64 <= 65536.
+constexpr int kMaxCols = 32736;
+// Bytes of zero padding after each staged activation row (>= one G = 32 group).
+constexpr int kXPadBytes = 64;
 
-// Group sizes: G = 16 for every bit width (the paper's default);
-// G = 8 and G = 32 for W4 (the group-size sweep).
+// Group sizes: G = 16 for every bit width; G = 8 and G = 32 for W4 (the
+// group-size sweep).
 __host__ __device__ constexpr bool group_supported(int bits, int G) {
   return G == kGroup ? (bits == 2 || bits == 4 || bits == 8) : (bits == 4 && (G == 8 || G == 32));
 }
@@ -45,17 +48,25 @@ __host__ __device__ constexpr bool group_supported(int bits, int G) {
 __host__ __device__ constexpr int group_code_bytes(int bits, int G = kGroup) { return G * bits / 8; }
 // Codes plane: each lane owns 16 B per plane -> 16/cb groups per plane (cb <= 16).
 __host__ __device__ constexpr int groups_per_plane(int bits, int G = kGroup) { return 16 / group_code_bytes(bits, G); }
+__host__ __device__ constexpr int code_planes(int bits, int G = kGroup) { return G * bits / 32; }
 __host__ __device__ constexpr int codes_bytes(int bits, int G = kGroup) { return kTileGroups * group_code_bytes(bits, G); }
-__host__ __device__ constexpr int off_sz(int bits, int G = kGroup) { return kTileHeaderBytes + codes_bytes(bits, G); }
+__host__ __device__ constexpr int off_sz(int bits, int G = kGroup) { return codes_bytes(bits, G); }
 __host__ __device__ constexpr int off_cols(int bits, int G = kGroup) { return off_sz(bits, G) + kTileGroups * 4; }
 __host__ __device__ constexpr int tile_bytes(int bits, int G = kGroup) { return off_cols(bits, G) + kTileGroups * 2; }
+static_assert(tile_bytes(4) % 128 == 0 && tile_bytes(2) % 128 == 0 && tile_bytes(8) % 128 == 0 &&
+                  tile_bytes(4, 8) % 128 == 0 && tile_bytes(4, 32) % 128 == 0,
+              "tiles are whole 128-B lines");
 
 // Offset (within a tile) of the code bytes of the group in lane l, slot u.
 __host__ __device__ constexpr int off_codes_g(int bits, int G, int lane, int u) {
-  return kTileHeaderBytes + (u / groups_per_plane(bits, G)) * 512 + lane * 16 +
-         (u % groups_per_plane(bits, G)) * group_code_bytes(bits, G);
+  return (u / groups_per_plane(bits, G)) * 512 + lane * 16 + (u % groups_per_plane(bits, G)) * group_code_bytes(bits, G);
 }
-__host__ __device__ constexpr int off_codes(int bits, int lane, int u) { return off_codes_g(bits, kGroup, lane, u); }
+// Offset (within a tile) of the (s, z) pair of lane l, slot u.
+__host__ __device__ constexpr int off_sz_g(int bits, int G, int lane, int u) { return off_sz(bits, G) + lane * 16 + u * 4; }
+// Offset (within a tile) of the column field of lane l, slot u.
+__host__ __device__ constexpr int off_cols_g(int bits, int G, int lane, int u) {
+  return off_cols(bits, G) + lane * 8 + u * 2;
+}
 
 // Column field of a kept group at group column c: the byte offset of the
 // first 16-B activation chunk the lane reads.  G = 16: chunk 2c + swap
@@ -70,23 +81,23 @@ __host__ __device__ constexpr uint32_t col_field(int G, uint32_t c, uint32_t rot
 __host__ __device__ constexpr uint32_t lane_rot(int G, int lane) {
   return G == 16 ? (uint32_t)(lane & 1) : G == 32 ? (uint32_t)(lane & 3) : 0u;
 }
+// Column field of a padding entry: the zero block after the activations.
+__host__ __device__ constexpr uint32_t pad_field(int cols) { return 2u * (uint32_t)cols; }
 
 constexpr int kTargetSlots = 64;  // slots per lane of the longest slice (16 tiles)
 
 // Target slots per lane for a layer of nnzg kept groups: short slices when the
 // layer has few tiles per warp of a B200 grid (148 SMs x 16 warps), so a
 // slice spans few warps and the fix-up chain stays short; long slices (less
-// tile padding) otherwise.  Measured (W4S50, B = 1): 1024x4096 4.28 -> 2.92 us
-// (16), 4096x4096 4.49 -> 4.13 us (32), 14336x4096 best at 64.
+// tile padding) otherwise.
 inline int target_slots_for(int64_t nnzg) {
   const double tiles_per_warp = (double)nnzg / kTileGroups / (148.0 * 16.0);
   return tiles_per_warp < 1.6 ? 16 : tiles_per_warp < 4.0 ? 32 : kTargetSlots;
 }
 
 // Lanes per row S (a power of two <= 32): large enough that the longest row
-// needs at most kTargetSlots slots per lane (short slices -> few warps per
-// slice -> short fix-up chains), and large enough that a layer with fewer
-// than 32 non-empty rows still fills the 32 lanes.
+// needs at most target_slots slots per lane, and large enough that a layer
+// with fewer than 32 non-empty rows still fills the 32 lanes.
 inline int lanes_per_row_for(int n_nz, int64_t max_len, int target_slots = kTargetSlots) {
   if (n_nz <= 0) return 1;
   int s = 1;
@@ -97,12 +108,7 @@ inline int lanes_per_row_for(int n_nz, int64_t max_len, int target_slots = kTarg
   return s > s_small ? s : s_small;
 }
 
-// Offset (within a tile) of the column field of lane l, slot u.
-__host__ __device__ constexpr int off_cols_g(int bits, int G, int lane, int u) {
-  return off_cols(bits, G) + lane * 8 + u * 2;
-}
-
-// On-blob header; the first 104 bytes mirror gqsa_desc_t field-for-field.
+// On-blob header; the first 128 bytes mirror gqsa_desc_t field-for-field.
 struct BlobHeader {
   uint32_t magic, version;
   int32_t rows, cols, group_size, bits;
@@ -111,8 +117,9 @@ struct BlobHeader {
   int32_t n_nzrows, n_empty;
   int32_t tile_bytes, flags;
   int32_t row_begin, row_end;
-  uint64_t off_row_index, off_nzrow, off_empty, off_tiles, blob_bytes;
-  uint8_t reserved[kHeaderBytes - 104];
+  int32_t num_slices, reserved0;
+  uint64_t off_row_index, off_perm, off_empty, off_slice_tile0, off_tile_slice, off_tiles, blob_bytes;
+  uint8_t reserved[kHeaderBytes - 128];
 };
 static_assert(sizeof(BlobHeader) == kHeaderBytes, "header size");
 

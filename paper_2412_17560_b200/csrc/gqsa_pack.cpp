@@ -1,4 +1,4 @@
-// gqsa_pack.cpp -- host packer, unpacker and validator for LAYOUT v2.
+// gqsa_pack.cpp -- host packer, unpacker and validator for LAYOUT v3.
 //
 // Offline pre-processing ("quantized weights are grouped by size
 // G and saved ... along with scaling factors and zero points"): the plain BSR
@@ -12,6 +12,9 @@
 //     a hashed rotation, go round-robin over its S lanes;
 //   * a slice's slots are cut into 128-group TILES (4 slots x 32 lanes) whose
 //     per-lane payloads are 16-B vectors (codes, s/z) and 8-B vectors (columns);
+//     slice boundaries are kept in side tables (slice_tile0, tile_slice);
+//   * padding entries (s = z = 0, codes 0) point at the zero block after the
+//     staged activations, so they contribute exactly 0 for any input x;
 //   * per (slot, quarter-warp) the swap bit of each group picks which 16-B half
 //     of its activation slice is read first, balancing shared-memory bank quads.
 // gqsa_unpack is the exact inverse (it re-sorts each row by column).
@@ -38,7 +41,7 @@ int check_bsr_header(const gqsa_bsr_t* b) {
   if (b->rows < 0 || b->cols <= 0 || b->group_size <= 0 || b->nnzg < 0) return GQSA_ERR_SHAPE;
   if (!group_supported(b->bits, b->group_size)) return GQSA_ERR_UNSUPPORTED;
   if (b->cols % b->group_size) return GQSA_ERR_SHAPE;
-  if (b->cols > kMaxCols) return GQSA_ERR_UNSUPPORTED;  // col field = byte offset in u16
+  if (b->cols > kMaxCols) return GQSA_ERR_UNSUPPORTED;  // col field = byte offset in u16 (+ zero block)
   if (!b->row_index) return GQSA_ERR_BUFFER;
   if (b->nnzg > 0 && (!b->group_cols || !b->codes || !b->scales_f16 || !b->zeros_f16))
     return GQSA_ERR_BUFFER;
@@ -111,7 +114,7 @@ Slices make_slices(const gqsa_bsr_t* b, int32_t r0, int32_t r1) {
 }
 
 struct Offsets {
-  uint64_t ri, perm, empty, tiles, total;
+  uint64_t ri, perm, empty, st0, ts, tiles, total;
 };
 
 Offsets offsets(const Slices& s, int bits, int G) {
@@ -119,14 +122,16 @@ Offsets offsets(const Slices& s, int bits, int G) {
   o.ri = kHeaderBytes;
   o.perm = align_up(o.ri + 4ull * (s.rows + 1), kSectionAlign);
   o.empty = align_up(o.perm + 4ull * kLanes * s.num_slices, kSectionAlign);
-  o.tiles = align_up(o.empty + 4ull * s.n_empty, kSectionAlign);
+  o.st0 = align_up(o.empty + 4ull * s.n_empty, kSectionAlign);
+  o.ts = align_up(o.st0 + 4ull * (s.num_slices + 1), kSectionAlign);
+  o.tiles = align_up(o.ts + 4ull * s.num_tiles, kSectionAlign);
   o.total = align_up(o.tiles + (uint64_t)s.num_tiles * tile_bytes(bits, G), kSectionAlign);
   return o;
 }
 
 void fill_desc(const BlobHeader& h, gqsa_desc_t* d) {
   static_assert(offsetof(gqsa_desc_t, blob_bytes) == offsetof(BlobHeader, blob_bytes), "desc mirror");
-  static_assert(sizeof(gqsa_desc_t) == 104, "desc size");
+  static_assert(sizeof(gqsa_desc_t) == 128, "desc size");
   std::memcpy(d, &h, sizeof(gqsa_desc_t));
 }
 
@@ -175,9 +180,12 @@ extern "C" int gqsa_pack(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_e
   h.flags = (int32_t)((G == kGroup ? kFlagTargetDeal : 0u) | ((uint32_t)S << kFlagLanesPerRowShift));
   h.row_begin = row_begin;
   h.row_end = row_end;
+  h.num_slices = s.num_slices;
   h.off_row_index = o.ri;
-  h.off_nzrow = o.perm;
+  h.off_perm = o.perm;
   h.off_empty = o.empty;
+  h.off_slice_tile0 = o.st0;
+  h.off_tile_slice = o.ts;
   h.off_tiles = o.tiles;
   h.blob_bytes = o.total;
   std::memcpy(out, &h, sizeof(h));
@@ -188,8 +196,13 @@ extern "C" int gqsa_pack(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_e
   for (int64_t i = 0; i < (int64_t)kLanes * s.num_slices; ++i) perm[i] = -1;
   int32_t* em = reinterpret_cast<int32_t*>(out + o.empty);
   for (int32_t i = 0; i < s.n_empty; ++i) em[i] = s.empty[i];
+  int32_t* st0 = reinterpret_cast<int32_t*>(out + o.st0);
+  int32_t* ts = reinterpret_cast<int32_t*>(out + o.ts);
+  for (int32_t sl = 0; sl <= s.num_slices; ++sl) st0[sl] = s.tile0[sl];
+  for (int32_t sl = 0; sl < s.num_slices; ++sl)
+    for (int32_t t = s.tile0[sl]; t < s.tile0[sl + 1]; ++t) ts[t] = sl;
 
-  const int nchunks = bsr->cols / 8;  // 16-B activation chunks per batch row
+  const uint16_t padf = (uint16_t)pad_field(bsr->cols);  // the zero block after x
   std::vector<int64_t> deal;          // [lane][slot] source group, -1 = padding
   for (int32_t sl = 0; sl < s.num_slices; ++sl) {
     int32_t row_of_lane[kLanes];
@@ -239,18 +252,12 @@ extern "C" int gqsa_pack(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_e
     for (int32_t tau = 0; tau < nt; ++tau) {
       const int32_t t = s.tile0[sl] + tau;
       uint8_t* tile = out + o.tiles + (uint64_t)t * tb;
-      // word 0: slice << 2 | FIRST | LAST; word 1: tiles to the slice's last
-      // tile; word 2: the slice's first tile
-      const uint32_t hdr[4] = {((uint32_t)sl << 2) | (tau == 0 ? kTileFirst : 0u) |
-                                   (tau == nt - 1 ? kTileLast : 0u),
-                               (uint32_t)(nt - 1 - tau), (uint32_t)s.tile0[sl], 0u};
-      std::memcpy(tile, hdr, sizeof(hdr));
       for (int u = 0; u < kPerLane; ++u) {
         for (int l = 0; l < kLanes; ++l) {
           const int64_t g = deal[(size_t)l * L + (int64_t)tau * kPerLane + u];
           uint16_t* col = reinterpret_cast<uint16_t*>(tile + off_cols_g(bits, G, l, u));
-          if (g < 0) {  // padding: codes, s, z zero; reads this lane's target chunk (G = 16) or chunk 0
-            *col = G == kGroup ? (uint16_t)(((l & 15) % nchunks) << 4) : (uint16_t)0;
+          if (g < 0) {  // padding: codes, s, z zero; reads the zero block (contributes exactly 0)
+            *col = padf;
             continue;
           }
           const uint32_t swap = lane_rot(G, l);
@@ -264,7 +271,7 @@ extern "C" int gqsa_pack(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_e
           } else {
             std::memcpy(dst, src, cb);
           }
-          uint16_t* sz = reinterpret_cast<uint16_t*>(tile + off_sz(bits, G) + l * 16 + u * 4);
+          uint16_t* sz = reinterpret_cast<uint16_t*>(tile + off_sz_g(bits, G, l, u));
           sz[0] = bsr->scales_f16[g];
           sz[1] = bsr->zeros_f16[g];
           *col = (uint16_t)col_field(G, bsr->group_cols[g], swap);  // byte offset of the first x chunk
@@ -291,12 +298,25 @@ extern "C" int gqsa_read_desc(const void* blob, size_t blob_bytes, gqsa_desc_t* 
   const int S = (int)((uint32_t)h.flags >> kFlagLanesPerRowShift) & 0xff;
   if (S < 1 || S > kLanes || (S & (S - 1))) return GQSA_ERR_VALIDATION;
   const int64_t slices = (h.n_nzrows + kLanes / S - 1) / (kLanes / S);
-  if (h.off_row_index < (uint64_t)kHeaderBytes || h.off_nzrow < h.off_row_index + 4ull * (h.rows + 1) ||
-      h.off_empty < h.off_nzrow + 4ull * kLanes * slices || h.off_tiles < h.off_empty + 4ull * h.n_empty ||
-      h.off_tiles % kSectionAlign ||
+  if (h.num_slices != slices || h.num_tiles < slices) return GQSA_ERR_VALIDATION;
+  if (h.off_row_index < (uint64_t)kHeaderBytes || h.off_perm < h.off_row_index + 4ull * (h.rows + 1) ||
+      h.off_empty < h.off_perm + 4ull * kLanes * slices || h.off_slice_tile0 < h.off_empty + 4ull * h.n_empty ||
+      h.off_tile_slice < h.off_slice_tile0 + 4ull * (slices + 1) ||
+      h.off_tiles < h.off_tile_slice + 4ull * h.num_tiles || h.off_tiles % kSectionAlign ||
       h.blob_bytes < h.off_tiles + (uint64_t)h.num_tiles * h.tile_bytes)
     return GQSA_ERR_VALIDATION;
   if (h.blob_bytes > blob_bytes) return GQSA_ERR_BUFFER;
+  // slice tables: slice_tile0 is a strictly increasing cover of [0, num_tiles)
+  // and tile_slice its inverse (the kernel trusts both)
+  const uint8_t* b = static_cast<const uint8_t*>(blob);
+  const int32_t* st0 = reinterpret_cast<const int32_t*>(b + h.off_slice_tile0);
+  const int32_t* ts = reinterpret_cast<const int32_t*>(b + h.off_tile_slice);
+  if (st0[0] != 0 || st0[slices] != h.num_tiles) return GQSA_ERR_VALIDATION;
+  for (int64_t sl = 0; sl < slices; ++sl) {
+    if (st0[sl + 1] <= st0[sl]) return GQSA_ERR_VALIDATION;
+    for (int32_t t = st0[sl]; t < st0[sl + 1]; ++t)
+      if (ts[t] != (int32_t)sl) return GQSA_ERR_VALIDATION;
+  }
   fill_desc(h, desc);
   return GQSA_OK;
 }
@@ -315,10 +335,11 @@ extern "C" int gqsa_unpack(const void* blob, size_t blob_bytes, gqsa_bsr_t* out)
 
   const uint8_t* b = static_cast<const uint8_t*>(blob);
   const int32_t* ri = reinterpret_cast<const int32_t*>(b + d.off_row_index);
-  const int32_t* perm = reinterpret_cast<const int32_t*>(b + d.off_nzrow);
+  const int32_t* perm = reinterpret_cast<const int32_t*>(b + d.off_perm);
   const int32_t* em = reinterpret_cast<const int32_t*>(b + d.off_empty);
+  const int32_t* ts = reinterpret_cast<const int32_t*>(b + d.off_tile_slice);
   const int bits = d.bits, GS = d.group_size, cb = group_code_bytes(bits, GS);
-  const int S = ((uint32_t)d.flags >> kFlagLanesPerRowShift) & 0xff;
+  const uint16_t padf = (uint16_t)pad_field(d.cols);
 
   struct G {
     uint16_t col, s, z;
@@ -327,29 +348,23 @@ extern "C" int gqsa_unpack(const void* blob, size_t blob_bytes, gqsa_bsr_t* out)
     uint32_t rot;  // G = 32: code words rotated
   };
   std::vector<std::vector<G>> rows(d.rows);
-  int32_t slice = -1, first = -1;
   for (int32_t t = 0; t < d.num_tiles; ++t) {
     const uint8_t* tile = b + d.off_tiles + (uint64_t)t * d.tile_bytes;
-    uint32_t hdr[4];
-    std::memcpy(hdr, tile, sizeof(hdr));
-    if (hdr[0] & kTileFirst) ++slice;
-    if ((int32_t)(hdr[0] >> 2) != slice || slice < 0) return GQSA_ERR_VALIDATION;
-    if (hdr[0] & kTileFirst) first = t;
-    if ((int32_t)hdr[2] != first || hdr[3] != 0u) return GQSA_ERR_VALIDATION;
+    const int32_t slice = ts[t];
     for (int u = 0; u < kPerLane; ++u) {
       for (int l = 0; l < kLanes; ++l) {
         const int32_t row = perm[(int64_t)slice * kLanes + l];
-        const uint16_t* sz = reinterpret_cast<const uint16_t*>(tile + off_sz(bits, GS) + l * 16 + u * 4);
+        const uint16_t* sz = reinterpret_cast<const uint16_t*>(tile + off_sz_g(bits, GS, l, u));
         const uint16_t col = *reinterpret_cast<const uint16_t*>(tile + off_cols_g(bits, GS, l, u));
         const uint8_t* src = tile + off_codes_g(bits, GS, l, u);
         if (sz[0] == 0) {  // padding (a kept group always has s > 0)
-          if (sz[1] || (col & 15u) || col >= 2u * (uint32_t)d.cols) return GQSA_ERR_VALIDATION;
+          if (sz[1] || col != padf) return GQSA_ERR_VALIDATION;
           for (int i = 0; i < cb; ++i)
             if (src[i]) return GQSA_ERR_VALIDATION;
           continue;
         }
         if (row < 0 || row >= d.rows) return GQSA_ERR_VALIDATION;
-        if (col & 15u) return GQSA_ERR_VALIDATION;
+        if ((col & 15u) || col >= 2u * (uint32_t)d.cols) return GQSA_ERR_VALIDATION;
         if (GS == kGroup) {
           rows[row].push_back(G{(uint16_t)(col >> 5), sz[0], sz[1], src, ((col >> 4) & 1u) != 0, 0});
         } else if (GS == 8) {
@@ -391,9 +406,7 @@ extern "C" int gqsa_unpack(const void* blob, size_t blob_bytes, gqsa_bsr_t* out)
       ++acc;
     }
   }
-  const int32_t slices = (d.n_nzrows + kLanes / S - 1) / (kLanes / S);
-  if (acc != d.nnzg || ri[d.rows] != acc || n_nz != d.n_nzrows || slice + 1 != slices)
-    return GQSA_ERR_VALIDATION;
+  if (acc != d.nnzg || ri[d.rows] != acc || n_nz != d.n_nzrows) return GQSA_ERR_VALIDATION;
   o_ri[d.rows] = (int32_t)acc;
   out->rows = d.rows;
   out->cols = d.cols;

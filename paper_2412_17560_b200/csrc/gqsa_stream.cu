@@ -1,0 +1,407 @@
+// gqsa_stream.cu -- sm_100a Stream-K group-sparse W2/W4/W8 GEMV / small-batch
+// GEMM over LAYOUT v3, for one or several independent GEMVs per launch.
+//
+// Computes, for every item (GEMV) of the launch, every batch column b < B and
+// output row r (PAPER.md:64-69 [Eq. 3], 95-101 [§3.2 BSR], 134 [§3.5]):
+//
+//   y[b][r] = sum_{g in row r} s_g * ( sum_t q_{g,t} x[b][c_g*G+t] - z_g * X_{b,c_g} ),
+//   X_{b,c} = sum_t x[b][c*G+t]       (Eq. 3 applied per group, z folded once)
+//
+// Design:
+//  * Layout: rows sorted by kept-group count, cut into 32-lane
+//    slices (sliced ELL); a lane owns a row and walks its groups slot by slot,
+//    so the hot loop has no cross-lane reduction at all.
+//  * Task-centric partition (PAPER.md:161 Stream-K, App. J): the
+//    launch's concatenated tile stream (all items, 128 groups per tile) is cut
+//    into contiguous, equal (+-1 tile) ranges, one per WARP, regardless of
+//    row, slice or item boundaries.
+//  * Weights stream HBM -> registers (128-bit no-allocate loads, evict-first
+//    L2 policy), kBufs tiles per warp in flight, the first ones requested
+//    BEFORE griddepcontrol.wait (they never depend on the previous kernel).
+//    No shared-memory staging of weights: shared memory serves only the
+//    activation gathers.
+//  * Activations are staged in shared memory once per CTA (the items its
+//    range touches), with the negated column-group sums (-P, -Q) the
+//    offset-folded dequantization needs and a zero block for padding slots.
+//  * Dequantization: LOP3 magic (0x6400 = fp16 1024) turns code fields into
+//    exact fp16 (1024 + 2^k q); FHFMA (fma.rn.f32.f16) multiplies them by fp16
+//    x with exact products into an fp32 chain that STARTS at -P - z Q, so the
+//    offsets and z leave with one FFMA and s is applied with one more.  No
+//    tensor cores: the rows of a warp hold groups at unrelated columns
+//    (DESIGN.md §10), and batch 1 is bandwidth-bound.
+//  * Fix-up (slices split across warps), wait-free "last arriver": every
+//    participant publishes its per-lane partials as 64-bit {value, flag}
+//    records and increments the slice's arrival counter; the participant that
+//    arrives last adds all records in warp order (deterministic), stores the
+//    rows and resets counter and flags.  Nobody waits for a warp that has not
+//    already published, so progress never depends on CTA co-residency.
+#include "gqsa_device.cuh"
+
+namespace gqsa {
+
+namespace {
+
+__device__ __forceinline__ void range_of(const Params& p, int w, int& b, int& e) {
+  b = w * p.part_q + min(w, p.part_r);
+  e = b + p.part_q + (w < p.part_r ? 1 : 0);
+}
+// Warp that owns global tile t under the +-1 partition.
+__device__ __forceinline__ int warp_of_tile(const Params& p, int t) {
+  const int big = p.part_r * (p.part_q + 1);
+  return t < big ? t / (p.part_q + 1) : p.part_r + (t - big) / p.part_q;
+}
+__device__ __forceinline__ int item_of(const Params& p, int t) {
+  int i = 0;
+  while (i + 1 < p.n_items && t >= p.item[i].tile_end) ++i;
+  return i;
+}
+__device__ __forceinline__ bool touched(const Item& it, int t0, int t1) {
+  return it.tile_begin < t1 && it.tile_end > t0 && it.tile_end > it.tile_begin;
+}
+// Shared-memory offset of item i's staged activations in a CTA whose tile
+// range is [t0, t1): the touched items are packed in item order.
+__device__ __forceinline__ uint32_t item_smem_off(const Params& p, int i, int t0, int t1) {
+  uint32_t off = 0;
+  for (int j = 0; j < i; ++j)
+    if (touched(p.item[j], t0, t1)) off += (uint32_t)p.item[j].smem_bytes;
+  return off;
+}
+
+// y element i of item `it`: fp32, or fp16 rounded to nearest even (PAPER.md:134 step 5).
+__device__ __forceinline__ void store_y(const Item& it, int out_f16, int64_t i, float v) {
+  if (it.n_peers) {  // fused all-gather: this shard's rows land in every rank's full y
+#pragma unroll 1
+    for (int k = 0; k < it.n_peers; ++k) {
+      if (out_f16) reinterpret_cast<__half*>(it.peer_y[k])[i + it.row_offset] = __float2half_rn(v);
+      else reinterpret_cast<float*>(it.peer_y[k])[i + it.row_offset] = v;
+    }
+    return;
+  }
+  if (out_f16) reinterpret_cast<__half*>(it.Y)[i] = __float2half_rn(v);
+  else reinterpret_cast<float*>(it.Y)[i] = v;
+}
+
+// Sum over the S lanes of a row (S = lanes per row, a power of two) and store.
+template <int B>
+__device__ __forceinline__ void store_rows(const Params& p, const Item& it, float (&v)[B], int row, int lane) {
+  const int S = it.lanes_per_row;
+  for (int d = 1; d < S; d <<= 1) {
+#pragma unroll
+    for (int b = 0; b < B; ++b) v[b] += __shfl_xor_sync(0xffffffffu, v[b], d);
+  }
+  if (row >= 0 && (lane & (S - 1)) == 0) {
+    const float bias = it.bias ? __ldg(it.bias + row) : 0.f;
+#pragma unroll
+    for (int b = 0; b < B; ++b) store_y(it, p.out_f16, (int64_t)b * it.ldy + row, v[b] + bias);
+  }
+}
+
+// ---------------------------------------------------------------- fix-up
+// Record of warp w for its head (which = 0) or tail (which = 1) slice:
+// [B][32 lanes] 8-byte words {partial, flag}; each is ONE 64-bit store, so a
+// reader that sees the flag sees the value (single-copy atomicity).
+template <int B>
+__device__ __forceinline__ unsigned long long* rec_ptr(const Params& p, int w, int which, int b, int lane) {
+  return p.rec + (((int64_t)w * 2 + which) * B + b) * kLanes + lane;
+}
+__device__ __forceinline__ void st_relaxed64(unsigned long long* a, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* a) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+  return v;
+}
+template <int B>
+__device__ __forceinline__ void publish(const Params& p, int w, int which, const float (&v)[B], int lane) {
+#pragma unroll
+  for (int b = 0; b < B; ++b)
+    st_relaxed64(rec_ptr<B>(p, w, which, b, lane), (1ull << 32) | __float_as_uint(v[b]));
+}
+// Arrive on slice counter cnt[w0] (after this warp's records are issued);
+// returns the previous count in lane 0 (other lanes: 0).
+__device__ __forceinline__ int arrive(const Params& p, int w0, int lane) {
+  __syncwarp();
+  int old = 0;
+  if (lane == 0) old = (int)atomicAdd(p.cnt + w0, 1u);
+  return old;
+}
+// The last arriver of a slice split over warps w0..w1: add every
+// participant's record in warp order (w0's tail record, then the head records
+// of w0+1..w1), reset the flags and the counter, store the rows.  The spin
+// only waits for stores already issued (their writers arrived before us).
+template <int B>
+__device__ __noinline__ void collect(const Params& p, int w0, int w1, int item, int row, int lane) {
+  float v[B];
+#pragma unroll
+  for (int b = 0; b < B; ++b) v[b] = 0.f;
+  constexpr int kBatch = 4;  // records requested per round trip
+  for (int wb = w0; wb <= w1; wb += kBatch) {
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      unsigned long long r[kBatch];
+#pragma unroll
+      for (int k = 0; k < kBatch; ++k)
+        r[k] = (wb + k <= w1) ? ld_relaxed64(rec_ptr<B>(p, wb + k, wb + k == w0 ? 1 : 0, b, lane)) : 0ull;
+#pragma unroll
+      for (int k = 0; k < kBatch; ++k) {
+        if (wb + k > w1) break;
+        unsigned long long* a = rec_ptr<B>(p, wb + k, wb + k == w0 ? 1 : 0, b, lane);
+        unsigned int spins = 0;
+        while ((r[k] >> 32) == 0ull) {
+          if (++spins > (1u << 26)) __trap();  // a lost record: fail loudly, never hang
+          __nanosleep(32);
+          r[k] = ld_relaxed64(a);
+        }
+        v[b] += __uint_as_float((uint32_t)r[k]);
+        st_relaxed64(a, 0ull);
+      }
+    }
+  }
+  if (lane == 0) asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p.cnt + w0), "r"(0u) : "memory");
+  store_rows<B>(p, p.item[item], v, row, lane);
+}
+
+// Optional timeline instrumentation (gqsa_debug_trace): lane 0 of each warp
+// stamps %globaltimer at fixed points; off (one predicated branch) by default.
+__device__ __forceinline__ void trace_point(const Params& p, int gw, int lane, int k) {
+  if (p.trace && lane == 0 && gw < p.active_warps) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[(int64_t)gw * 8 + k] = t;
+  }
+}
+
+}  // namespace
+
+template <int BITS, int B, int G>
+__global__ void __launch_bounds__(32 * warps_for(B), 1) gqsa_stream_kernel(const __grid_constant__ Params p) {
+  constexpr int W = warps_for(B);
+  constexpr int TB = tile_bytes(BITS, G);
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int gw = blockIdx.x * W + warp;
+  trace_point(p, gw, lane, 0);
+
+  // ---- task-centric partition: contiguous tile range per warp (+-1 tile)
+  int t_begin = 0, t_end = 0;
+  if (gw < p.active_warps) range_of(p, gw, t_begin, t_end);
+  // the CTA's range (its warps' ranges are consecutive): which items it stages
+  int cta_t0 = 0, cta_t1 = 0;
+  {
+    const int w0 = blockIdx.x * W, w1 = min(w0 + W, p.active_warps) - 1;
+    if (w0 < p.active_warps) {
+      int e;
+      range_of(p, w0, cta_t0, e);
+      range_of(p, w1, e, cta_t1);
+    }
+  }
+  if (p.slice_k && t_end > t_begin) {
+    // data-centric partition (Slice-K): the warp owns the slices whose FIRST
+    // tile lies in its Stream-K range, each in full
+    const int ib = item_of(p, t_begin);
+    const Item& a = p.item[ib];
+    const int sb = __ldg(a.tile_slice + (t_begin - a.tile_begin));
+    const int st = a.tile_begin + __ldg(a.slice_tile0 + sb);
+    const int b = st == t_begin ? t_begin : a.tile_begin + __ldg(a.slice_tile0 + sb + 1);
+    const int ie = item_of(p, t_end - 1);
+    const Item& c = p.item[ie];
+    const int se = __ldg(c.tile_slice + (t_end - 1 - c.tile_begin));
+    const int e = c.tile_begin + __ldg(c.slice_tile0 + se + 1);
+    t_begin = b;
+    t_end = b < t_end ? e : b;
+  }
+
+  // ---- the first tiles: requested before anything else (weights never
+  //      depend on the previous kernel on the stream)
+  const uint64_t pol = evict_first_policy();
+  TileRegs<BITS, G> buf[kBufs];
+  int li = 0, lend = 0;  // load cursor: item, end of its tiles
+  const uint8_t* lptr = nullptr;
+  if (t_end > t_begin) {
+    li = item_of(p, t_begin);
+    lptr = p.item[li].tiles + (size_t)(t_begin - p.item[li].tile_begin) * TB;
+    lend = p.item[li].tile_end;
+  }
+  auto issue = [&](TileRegs<BITS, G>& r, int t) {  // t: the next tile of the load cursor
+    if (t == lend) {
+      do { ++li; } while (p.item[li].tile_end == p.item[li].tile_begin);
+      lptr = p.item[li].tiles;
+      lend = p.item[li].tile_end;
+    }
+    load_tile<BITS, G>(r, lptr, lane, pol);
+    lptr += TB;
+  };
+#pragma unroll
+  for (int k = 0; k < kBufs; ++k)
+    if (t_begin + k < t_end) issue(buf[k], t_begin + k);
+
+  // ---- slice cursor: current slice (item ci, slice cs, global end tile
+  //      cend, this lane's row crow) and the next one, prefetched
+  int ci = 0, cs = 0, cend = 0, crow = -1;
+  int ni = 0, ns = 0, nend = 0, nrow = -1;
+  bool foreign = false;  // the current slice began in an earlier warp's range
+  int cw0 = gw;          // warp owning the current slice's first tile
+  auto prefetch_next = [&]() {  // successor of (ci, cs), if the range continues past cend
+    if (cend >= t_end) return;
+    ni = ci;
+    ns = cs + 1;
+    if (ns == p.item[ci].num_slices) {
+      do { ++ni; } while (p.item[ni].tile_end == p.item[ni].tile_begin);
+      ns = 0;
+    }
+    const Item& it = p.item[ni];
+    nend = it.tile_begin + __ldg(it.slice_tile0 + ns + 1);
+    nrow = __ldg(it.perm + (int64_t)ns * kLanes + lane);
+  };
+  if (t_end > t_begin) {
+    ci = item_of(p, t_begin);
+    const Item& it = p.item[ci];
+    cs = __ldg(it.tile_slice + (t_begin - it.tile_begin));
+    const int st0 = it.tile_begin + __ldg(it.slice_tile0 + cs);
+    cend = it.tile_begin + __ldg(it.slice_tile0 + cs + 1);
+    crow = __ldg(it.perm + (int64_t)cs * kLanes + lane);
+    foreign = st0 < t_begin;
+    if (foreign) cw0 = warp_of_tile(p, st0);
+    prefetch_next();
+  }
+
+  // let the next launch on the stream start its prologue (its weight loads)
+  pdl_launch_dependents();
+  if (!p.x_ready) pdl_wait();  // x may be the previous kernel's output
+  trace_point(p, gw, lane, 1);
+
+  // ---- stage the activations of every item this CTA's range touches
+  for (int i = 0; i < p.n_items; ++i) {
+    const Item& it = p.item[i];
+    if (!touched(it, cta_t0, cta_t1)) continue;
+    uint8_t* xs = smem + item_smem_off(p, i, cta_t0, cta_t1);
+    stage_item<BITS, B, G>(it, xs, xs + (size_t)B * it.xrow);
+  }
+  if (p.x_ready) pdl_wait();  // y, bias and the workspace may still belong to the previous kernel
+  __syncthreads();
+  trace_point(p, gw, lane, 2);
+
+  // ---- empty rows get bias (or 0): grid-stride over every item's list
+  for (int i = 0; i < p.n_items; ++i) {
+    const Item& it = p.item[i];
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < it.n_empty; k += gridDim.x * blockDim.x) {
+      const int erow = __ldg(it.empty + k);
+      const float bias = it.bias ? __ldg(it.bias + erow) : 0.f;
+#pragma unroll
+      for (int b = 0; b < B; ++b) store_y(it, p.out_f16, (int64_t)b * it.ldy + erow, bias);
+    }
+  }
+  if (t_end <= t_begin) {
+    if (p.item[0].n_peers) __threadfence_system();
+    return;
+  }
+
+  // ---- stream the warp's tile range; lane = one row of the current slice
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  XView xv;
+  auto set_item = [&]() {
+    const Item& it = p.item[ci];
+    xv.xs = sbase + item_smem_off(p, ci, cta_t0, cta_t1);
+    xv.xrow = (uint32_t)it.xrow;
+    xv.pq = xv.xs + (uint32_t)B * xv.xrow;
+    xv.pqrow = (uint32_t)it.pqrow;
+  };
+  set_item();
+  float acc[B];
+#pragma unroll
+  for (int b = 0; b < B; ++b) acc[b] = 0.f;
+  // head slice (began upstream, closed in this range): arrival deferred to the range end
+  bool h_pending = false;
+  int h_old = 0, h_w0 = 0, h_item = 0, h_row = -1;
+  trace_point(p, gw, lane, 3);
+
+  auto consume = [&](const TileRegs<BITS, G>& tr, int t) {
+#pragma unroll
+    for (int u = 0; u < kPerLane; ++u) group_accumulate<BITS, B, G>(tr, u, acc, xv);
+    if (t + 1 == cend) {  // the slice ends with this tile: its rows are complete here
+      if (foreign) {  // ... but began upstream: publish, arrive, check at the range end
+        publish<B>(p, gw, 0, acc, lane);
+        h_old = arrive(p, cw0, lane);
+        h_pending = true;
+        h_w0 = cw0;
+        h_item = ci;
+        h_row = crow;
+      } else {
+        store_rows<B>(p, p.item[ci], acc, crow, lane);
+      }
+#pragma unroll
+      for (int b = 0; b < B; ++b) acc[b] = 0.f;
+      foreign = false;
+      cw0 = gw;
+      if (t + 1 < t_end) {  // advance to the prefetched next slice
+        const bool new_item = ni != ci;
+        ci = ni;
+        cs = ns;
+        cend = nend;
+        crow = nrow;
+        if (new_item) set_item();
+        prefetch_next();
+      }
+    }
+  };
+
+  int t = t_begin;
+  while (t < t_end) {
+#pragma unroll
+    for (int k = 0; k < kBufs; ++k) {
+      if (t < t_end) {
+        consume(buf[k], t);
+        if (t + kBufs < t_end) issue(buf[k], t + kBufs);
+        ++t;
+      }
+    }
+  }
+  trace_point(p, gw, lane, 4);
+
+  // ---- a slice left open at the end of the range continues downstream
+  if (cend > t_end) {
+    const int which = foreign ? 0 : 1;  // middle participant: head record; first warp: tail record
+    publish<B>(p, gw, which, acc, lane);
+    const int old = __shfl_sync(0xffffffffu, arrive(p, cw0, lane), 0);
+    const int w1 = warp_of_tile(p, cend - 1);
+    if (old == w1 - cw0) collect<B>(p, cw0, w1, ci, crow, lane);
+  }
+  if (h_pending) {
+    const int old = __shfl_sync(0xffffffffu, h_old, 0);
+    if (old == gw - h_w0) collect<B>(p, h_w0, gw, h_item, h_row, lane);
+  }
+  trace_point(p, gw, lane, 5);
+  if (p.item[0].n_peers) __threadfence_system();  // peer stores visible before the launch completes
+}
+
+// ---------------------------------------------------------------- selection
+template <int BITS, int B, int G = kGroup>
+const void* kernel_ptr() {
+  return reinterpret_cast<const void*>(&gqsa_stream_kernel<BITS, B, G>);
+}
+
+#define GQSA_KSEL(BITS, G)                    \
+  switch (B) {                                \
+    case 1: return kernel_ptr<BITS, 1, G>();  \
+    case 2: return kernel_ptr<BITS, 2, G>();  \
+    case 3: return kernel_ptr<BITS, 3, G>();  \
+    case 4: return kernel_ptr<BITS, 4, G>();  \
+    case 5: return kernel_ptr<BITS, 5, G>();  \
+    case 6: return kernel_ptr<BITS, 6, G>();  \
+    case 7: return kernel_ptr<BITS, 7, G>();  \
+    case 8: return kernel_ptr<BITS, 8, G>();  \
+    default: return nullptr;                  \
+  }
+
+const void* select_kernel(int bits, int G, int B) {
+  if (G == 8 && bits == 4) { GQSA_KSEL(4, 8) }
+  if (G == 32 && bits == 4) { GQSA_KSEL(4, 32) }
+  if (G != kGroup) return nullptr;
+  if (bits == 4) { GQSA_KSEL(4, 16) }
+  if (bits == 2) { GQSA_KSEL(2, 16) }
+  if (bits == 8) { GQSA_KSEL(8, 16) }
+  return nullptr;
+}
+
+}  // namespace gqsa

@@ -6,7 +6,8 @@ import of any entry point raises: there is no CPU fallback.
 
 Names follow the C ABI: :func:`pack`, :func:`unpack`, :func:`read_desc`,
 :func:`workspace_size`, :func:`gemv`, :func:`gemm_smallbatch`,
-:func:`gemm_hostio`, plus :class:`Layer`, a device-resident packed layer.
+:func:`gemm_hostio`, :func:`gemm_grouped`, plus :class:`Layer`, a
+device-resident packed layer.
 """
 from __future__ import annotations
 
@@ -50,8 +51,10 @@ class Desc(ctypes.Structure):
         ("n_nzrows", ctypes.c_int32), ("n_empty", ctypes.c_int32),
         ("tile_bytes", ctypes.c_int32), ("flags", ctypes.c_int32),
         ("row_begin", ctypes.c_int32), ("row_end", ctypes.c_int32),
-        ("off_row_index", ctypes.c_uint64), ("off_nzrow", ctypes.c_uint64),
-        ("off_empty", ctypes.c_uint64), ("off_tiles", ctypes.c_uint64),
+        ("num_slices", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+        ("off_row_index", ctypes.c_uint64), ("off_perm", ctypes.c_uint64),
+        ("off_empty", ctypes.c_uint64), ("off_slice_tile0", ctypes.c_uint64),
+        ("off_tile_slice", ctypes.c_uint64), ("off_tiles", ctypes.c_uint64),
         ("blob_bytes", ctypes.c_uint64),
     ]
 
@@ -65,20 +68,24 @@ class Plan(ctypes.Structure):
                  "stages", "ctas_per_sm", "ring_bytes", "batch_per_launch", "launches", "coresident")]
 
 
-class ChainItem(ctypes.Structure):
+class GemmItem(ctypes.Structure):
     _fields_ = [
         ("desc", ctypes.POINTER(Desc)), ("d_blob", ctypes.c_void_p),
         ("d_X", ctypes.c_void_p), ("ldx", ctypes.c_int64),
         ("d_Y", ctypes.c_void_p), ("ldy", ctypes.c_int64),
-        ("d_bias", ctypes.c_void_p), ("wait_prev", ctypes.c_int32),
-        ("out_f16", ctypes.c_int32),
+        ("d_bias", ctypes.c_void_p),
     ]
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("partition", ctypes.c_int32), ("out_f16", ctypes.c_int32),
+                ("x_ready", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 EXPORTS = (
     "gqsa_pack_size", "gqsa_pack", "gqsa_read_desc", "gqsa_unpack", "gqsa_workspace_size",
-    "gqsa_gemv", "gqsa_gemm_smallbatch", "gqsa_gemm_ex", "gqsa_hostio_stage_size",
-    "gqsa_gemm_hostio", "gqsa_chain_workspace_size", "gqsa_gemm_chain",
+    "gqsa_gemv", "gqsa_gemm_smallbatch", "gqsa_gemm_ex", "gqsa_gemm_grouped", "gqsa_hostio_stage_size",
+    "gqsa_gemm_hostio",
     "gqsa_compress_nnzg", "gqsa_compress", "gqsa_multi_hostio_stage_size", "gqsa_gemm_multi_hostio",
     "gqsa_gemm_allgather",
     "gqsa_launch_plan", "gqsa_launch_count", "gqsa_status_string", "gqsa_version",
@@ -117,8 +124,7 @@ def lib() -> ctypes.CDLL:
                                       P, P, SZ, P]
     L.gqsa_compress_nnzg.argtypes = [I32, I32, I32, ctypes.c_double, ctypes.POINTER(ctypes.c_int64)]
     L.gqsa_compress.argtypes = [P, I32, I32, I32, I32, P, ctypes.c_double, ctypes.POINTER(BSR), P]
-    L.gqsa_chain_workspace_size.argtypes = [ctypes.POINTER(ChainItem), I32, I32, PSZ]
-    L.gqsa_gemm_chain.argtypes = [ctypes.POINTER(ChainItem), I32, I32, P, SZ, P]
+    L.gqsa_gemm_grouped.argtypes = [ctypes.POINTER(GemmItem), I32, I32, ctypes.POINTER(Options), P, SZ, P]
     L.gqsa_launch_count.restype = ctypes.c_uint64
     L.gqsa_debug_trace.argtypes = [P, SZ]
     L.gqsa_status_string.restype = ctypes.c_char_p
@@ -261,16 +267,12 @@ PARTITION_STREAM_K = 0  # task-centric (default everywhere)
 PARTITION_SLICE_K = 1   # data-centric: whole slices (rows) per warp, no fix-up
 
 
-class Options(ctypes.Structure):
-    _fields_ = [("partition", ctypes.c_int32), ("out_f16", ctypes.c_int32)]
-
-
 def gemm_ex(desc: Desc, d_blob, X, Y, partition: int = PARTITION_STREAM_K, bias=None, ws=None,
-            stream=None) -> None:
+            stream=None, x_ready: bool = False) -> None:
     """gqsa_gemm_ex: explicit Stream-K / Slice-K partition; Y fp32 or fp16 (RNE)."""
     import torch
     B = X.shape[0]
-    opts = Options(int(partition), 1 if Y.dtype == torch.float16 else 0)
+    opts = Options(int(partition), 1 if Y.dtype == torch.float16 else 0, int(bool(x_ready)), 0)
     _check(lib().gqsa_gemm_ex(ctypes.byref(desc), d_blob.data_ptr(), X.data_ptr(), B, X.stride(0),
                               Y.data_ptr(), Y.stride(0), bias.data_ptr() if bias is not None else None,
                               ws.data_ptr(), ws.numel(), ctypes.byref(opts), _stream_ptr(stream)),
@@ -286,38 +288,33 @@ def gemm_hostio(desc: Desc, d_blob, h_X, h_Y, stage, ws, bias=None, stream=None)
                                   _stream_ptr(stream)), "gqsa_gemm_hostio")
 
 
-def _chain_items(items):
-    """items: sequence of (desc, d_blob, X [B][ldx] fp16, Y [B][ldy] fp32 or fp16, bias or None,
-    wait_prev)."""
-    import torch
-    arr = (ChainItem * len(items))()
-    keep = []
-    for j, (desc, d_blob, X, Y, bias, wait_prev) in enumerate(items):
-        keep.append(desc)
-        arr[j] = ChainItem(ctypes.pointer(desc), d_blob.data_ptr(), X.data_ptr(), X.stride(0),
-                           Y.data_ptr(), Y.stride(0), bias.data_ptr() if bias is not None else None,
-                           int(wait_prev), 1 if Y.dtype == torch.float16 else 0)
-    return arr, keep
+class Grouped:
+    """A prepared gqsa_gemm_grouped call (argument arrays built once): the
+    independent GEMMs ``items`` = sequence of (desc, d_blob, X fp16 [B][ldx],
+    Y [B][ldy] fp32 (or all fp16), bias or None) in ONE launch."""
+
+    def __init__(self, items, ws, partition: int = PARTITION_STREAM_K, x_ready: bool = False):
+        import torch
+        n = len(items)
+        arr = (GemmItem * n)()
+        keep = []
+        for j, (desc, d_blob, X, Y, bias) in enumerate(items):
+            keep.append((desc, d_blob, X, Y, bias))
+            arr[j] = GemmItem(ctypes.pointer(desc), d_blob.data_ptr(), X.data_ptr(), X.stride(0),
+                              Y.data_ptr(), Y.stride(0), bias.data_ptr() if bias is not None else None)
+        out16 = 1 if items[0][3].dtype == torch.float16 else 0
+        self._keep = (keep, ws)
+        self._opts = Options(int(partition), out16, int(bool(x_ready)), 0)
+        self._args = (arr, n, int(items[0][2].shape[0]), ctypes.byref(self._opts), ws.data_ptr(), ws.numel())
+        self._fn = lib().gqsa_gemm_grouped
+
+    def __call__(self, stream=None) -> None:
+        _check(self._fn(*self._args, _stream_ptr(stream)), "gqsa_gemm_grouped")
 
 
-def chain_workspace_size(items, batch: int = 1) -> int:
-    arr, _keep = _chain_items(items)
-    n = ctypes.c_size_t(0)
-    _check(lib().gqsa_chain_workspace_size(arr, len(items), int(batch), ctypes.byref(n)),
-           "gqsa_chain_workspace_size")
-    return n.value
-
-
-def gemm_chain(items, ws, stream=None) -> None:
-    """gqsa_gemm_chain: the GEMVs of ``items`` in order, in one persistent launch.
-
-    items: sequence of (desc, d_blob, X fp16 [B][ldx], Y fp32 [B][ldy], bias or None,
-    wait_prev); ws: zero-initialised uint8 tensor of chain_workspace_size bytes.
-    """
-    arr, _keep = _chain_items(items)
-    B = items[0][2].shape[0]
-    _check(lib().gqsa_gemm_chain(arr, len(items), B, ws.data_ptr(), ws.numel(), _stream_ptr(stream)),
-           "gqsa_gemm_chain")
+def gemm_grouped(items, ws, partition: int = PARTITION_STREAM_K, x_ready: bool = False, stream=None) -> None:
+    """gqsa_gemm_grouped (one-shot form of :class:`Grouped`)."""
+    Grouped(items, ws, partition, x_ready)(stream)
 
 
 def _desc_array(descs):
@@ -351,15 +348,19 @@ def gemm_allgather(desc: Desc, d_blob, X, peer_Y, row_offset: int, bias=None, ws
 class MultiHostIO:
     """A prepared gqsa_gemm_multi_hostio call (argument arrays built once):
     n independent layers, host (pinned) fp16 inputs concatenated in h_X, fp32
-    outputs concatenated into h_Y; one copy each way per call."""
+    outputs concatenated into h_Y; one copy each way per call, the layers as
+    grouped launches.  ``ws_list``: one workspace (or a list whose first
+    entry is used)."""
 
     def __init__(self, descs, d_blobs, h_X, h_Y, stage, ws_list, batch: int = 1):
         n = len(descs)
+        if not isinstance(ws_list, (list, tuple)):
+            ws_list = [ws_list]
         self._keep = (descs, d_blobs, h_X, h_Y, stage, ws_list)
         self._args = (_desc_array(descs), (ctypes.c_void_p * n)(*[b.data_ptr() for b in d_blobs]), n, int(batch),
                       h_X.data_ptr(), h_Y.data_ptr(), stage.data_ptr(), stage.numel(),
-                      (ctypes.c_void_p * n)(*[w.data_ptr() for w in ws_list]),
-                      (ctypes.c_size_t * n)(*[w.numel() for w in ws_list]))
+                      (ctypes.c_void_p * len(ws_list))(*[w.data_ptr() for w in ws_list]),
+                      (ctypes.c_size_t * len(ws_list))(*[w.numel() for w in ws_list]))
         self._fn = lib().gqsa_gemm_multi_hostio
 
     def __call__(self, stream=None) -> None:

@@ -1,6 +1,6 @@
 """Small launches of every kernel family for compute-sanitizer (memcheck /
-racecheck / synccheck): gemv, small-batch GEMM (split and co-resident
-plans), Slice-K, fp16 output, chain, fused all-gather.  Exits non-zero on a
+racecheck / synccheck): gemv, small-batch GEMM (batch split), Slice-K,
+fp16 output, grouped launch, fused all-gather.  Exits non-zero on a
 mismatch against the oracle (exact-integer mode)."""
 import os
 import sys
@@ -27,12 +27,11 @@ for rows, cols, bits, B, mask in ((300, 1024, 4, 1, "uniform"), (77, 208, 2, 3, 
         ok &= np.array_equal(y, ref)
     y16 = L.gemm(X, out_dtype=torch.float16, partition=gqsa.PARTITION_SLICE_K).cpu().numpy()
     ok &= np.array_equal(y16, ref.astype(np.float16))
-    if bits != 8 and B <= 2:
-        Y = torch.empty(B, rows, dtype=torch.float32, device="cuda")
-        items = [(L.desc, L.blob, X, Y, None, 1)]
-        ws = torch.zeros(gqsa.chain_workspace_size(items, B), dtype=torch.uint8, device="cuda")
-        gqsa.gemm_chain(items, ws)
-        ok &= np.array_equal(Y.cpu().numpy().astype(np.float64), ref)
+    Y = torch.empty(B, rows, dtype=torch.float32, device="cuda")
+    Y2 = torch.empty(B, rows, dtype=torch.float32, device="cuda")
+    gqsa.gemm_grouped([(L.desc, L.blob, X, Y, None), (L.desc, L.blob, X, Y2, None)], L.ws)
+    ok &= np.array_equal(Y.cpu().numpy().astype(np.float64), ref)
+    ok &= np.array_equal(Y2.cpu().numpy().astype(np.float64), ref)
     Ys = [torch.zeros(B, rows, dtype=torch.float32, device="cuda") for _ in range(2)]
     for r in range(2):
         lo, hi = synth.shard_rows(rows, 2, r)

@@ -26,3 +26,5 @@ def test_bench_two_ranks_one_json_line():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "rowshard2" and d["value"] > 0
     assert d["scaling"] == "strong" and d["gpu_launches"] > 0
+    mg = d["multi_gpu"]  # kernels and exchange reported apart
+    assert mg["per_rank_kernel_us"] > 0 and mg["allgather_us"] > 0 and mg["kernel_only_aggregate_gbs"] > 0

@@ -33,8 +33,7 @@ def run(bsr, xbits, bias=None, layer=None, partition=gqsa.PARTITION_STREAM_K, **
     else:
         y = L.gemm(X, bias=b, partition=partition)
     torch.cuda.synchronize()
-    flags = L.ws.view(torch.int32).view(-1, 16)[:, 15]
-    assert int(flags.count_nonzero()) == 0, "every fix-up flag must be left zero"
+    assert int(L.ws.count_nonzero()) == 0, "the workspace (fix-up counters and records) must be left zero"
     return y.cpu().numpy()
 
 
@@ -78,13 +77,13 @@ EXACT_CASES = [
     (77, 208, 2, 0.5, "uniform", 3),      # x + column sums of 1560 B: ring alignment (sanitizer find)
     (41, 48, 4, 0.5, "uniform", 5),       # K = 48: 3 column groups, odd batch
     (3, 16384, 4, 0.5, "uniform", 2),     # few long rows: rows span many warps
-    (1, 32768, 4, 0.5, "uniform", 1),     # one row over 32 lanes (S = 32), max K
+    (1, 32736, 4, 0.5, "uniform", 1),     # one row over 32 lanes (S = 32), max K
     (4096, 16, 4, 0.5, "uniform", 1),     # K = G: many empty rows, 1-group rows
     (5, 64, 4, 0.5, "uniform", 1),        # nnzg < one tile
     (640, 512, 2, 0.9, "uniform", 5),     # mostly-empty rows
     (2048, 28672, 4, 0.5, "uniform", 4),  # x of 4 columns exceeds an SM: 2 launches of 2
     (1024, 14336, 4, 0.5, "uniform", 8),  # x of 8 columns exceeds an SM: 2 launches of 4
-    (512, 14336, 2, 0.5, "skewed", 3),    # CTA takes the whole SM (no PDL co-residency)
+    (512, 14336, 2, 0.5, "skewed", 3),    # half the rows empty, long rows
     # W8 (exact-int needs 255*2*4*K < 2^23: K <= 4096)
     (1024, 4096, 8, 0.5, "uniform", 1),
     (300, 1024, 8, 0.3, "row_balanced", 4),
@@ -231,8 +230,8 @@ def test_hostio_end_to_end_path():
 
 
 def test_multi_hostio_end_to_end_path():
-    """gqsa_gemm_multi_hostio: one H2D copy of concatenated inputs, one launch
-    per layer, one D2H copy of concatenated outputs (bench.py's e2e path)."""
+    """gqsa_gemm_multi_hostio: one H2D copy of concatenated inputs, ONE grouped
+    launch for the layers, one D2H copy of concatenated outputs (bench.py's e2e path)."""
     shapes = [(300, 1024), (77, 208), (1024, 4096)]
     for B in (1, 2):
         layers, xs, refs, xs2, refs2 = [], [], [], [], []
@@ -250,15 +249,15 @@ def test_multi_hostio_end_to_end_path():
         hX = torch.from_numpy(np.concatenate(xs)).view(torch.float16).pin_memory()
         hY = torch.full((sum(B * n for n, _ in shapes),), float("nan"), dtype=torch.float32).pin_memory()
         stage = torch.empty(gqsa.multi_hostio_stage_size(descs, B), dtype=torch.uint8, device="cuda")
-        # default stream (eager) once, then a side stream three times: the
-        # library captures a CUDA graph on the first call and replays it
-        # (fresh host inputs each time: the graph's copies read them at replay)
+        # default stream once, then a side stream three times (fresh host inputs each time)
         side = torch.cuda.Stream()
         for k, st in enumerate([None, side, side, side]):
             hX.copy_(torch.from_numpy(np.concatenate(xs) if k % 2 == 0 else np.concatenate(xs2)).view(torch.float16))
             hY.fill_(float("nan"))
-            gqsa.gemm_multi_hostio(descs, [L.blob for L in layers], hX, hY, stage, [L.ws for L in layers], batch=B,
+            n0 = gqsa.launch_count()
+            gqsa.gemm_multi_hostio(descs, [L.blob for L in layers], hX, hY, stage, [layers[0].ws], batch=B,
                                    stream=st)
+            assert gqsa.launch_count() == n0 + 1
             torch.cuda.synchronize()
             got = hY.numpy().astype(np.float64)
             off = 0
@@ -283,20 +282,18 @@ def test_argument_errors():
     assert e.value.status == -4
 
 
-def test_launch_plan_batch_split_and_residency():
-    """x (+ column sums) must fit in shared memory: larger batches split into
-    several launches; CTAs that leave no room (shared memory or registers)
-    for the next launch take the SM."""
+def test_launch_plan_batch_split():
+    """x (+ column sums + zero block) must fit in shared memory: larger batches
+    split into several launches; one CTA per SM."""
     sms = torch.cuda.get_device_properties(0).multi_processor_count
-    for rows, cols, B, launches, coresident in ((4096, 4096, 1, 1, 1), (4096, 4096, 8, 1, 1),
-                                                 (4096, 14336, 1, 1, 1), (4096, 14336, 4, 1, 0),
-                                                 (4096, 14336, 8, 2, 0), (64, 28672, 4, 2, 0)):
+    for rows, cols, B, launches in ((4096, 4096, 1, 1), (4096, 4096, 8, 1), (4096, 14336, 1, 1),
+                                    (4096, 14336, 4, 1), (4096, 14336, 8, 2), (64, 28672, 4, 2)):
         bsr = synth.make_layer(rows + cols + B, rows, cols, sparsity=0.5)
         _, d = gqsa.pack(bsr)
         p = gqsa.launch_plan(d, B)
-        assert (p.launches, p.coresident) == (launches, coresident), (rows, cols, B, p.launches, p.coresident)
+        assert p.launches == launches, (rows, cols, B, p.launches)
         assert p.batch_per_launch * p.launches >= B and p.smem_bytes <= 227 * 1024
-        assert p.grid <= sms
+        assert p.grid <= sms and p.ctas_per_sm == 1 and p.coresident == 0
     n0 = gqsa.launch_count()
     L = gqsa.Layer(synth.make_layer(5, 256, 14336, sparsity=0.5))
     L.gemm(torch.zeros(8, 14336, dtype=torch.float16, device="cuda"))
@@ -310,7 +307,7 @@ def test_launch_plan_is_persistent_stream_k():
     p = gqsa.launch_plan(d, 1)
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     assert p.active_warps == min(d.num_tiles, p.grid * p.warps_per_cta)
-    assert p.grid <= 2 * sms and p.x_in_smem == 1
+    assert p.grid <= sms and p.x_in_smem == 1
 
 
 @pytest.mark.parametrize("rows,cols,B,P,f16", [(1000, 2048, 1, 2, False), (4096, 4096, 2, 4, False),

@@ -31,7 +31,7 @@ def test_exports_every_declared_symbol():
     exported = set(re.findall(r"\bT (gqsa_\w+)", out))
     assert set(names) <= exported
     assert set(gqsa.EXPORTS) == set(names)
-    assert gqsa.lib().gqsa_version() == 2
+    assert gqsa.lib().gqsa_version() == 3
     assert gqsa.status_string(-2) == "validation error"
 
 
@@ -79,7 +79,7 @@ def test_roundtrip_and_reference_bytes(rows, cols, bits, sp, mask, seed):
 def test_group_sizes_roundtrip_and_reference_bytes(rows, cols, G, sp, mask, seed):
     bsr = synth.make_layer(seed, rows, cols, G=G, bits=4, sparsity=sp, mask=mask)
     blob, desc = gqsa.pack(bsr)
-    assert desc.group_size == G and desc.tile_bytes == 32 + 128 * G // 2 + 512 + 256
+    assert desc.group_size == G and desc.tile_bytes == 128 * G // 2 + 512 + 256
     assert bytes(blob) == pack_reference(bsr)
     _eq_bsr(gqsa.unpack(blob), bsr)
 
@@ -115,18 +115,21 @@ def test_shard_ranges_rebase_and_reassemble():
 
 
 def test_tile_fields_match_layout():
-    """Spot-check the documented tile fields directly."""
+    """Spot-check the documented tile fields and slice tables directly."""
     bsr = synth.make_layer(10, 64, 256, sparsity=0.5)
     blob, d = gqsa.pack(bsr)
-    assert d.tile_bytes == 1824 and d.version == 2 and (d.flags >> 8) & 0xFF == 1
+    assert d.tile_bytes == 1792 and d.tile_bytes % 128 == 0 and d.version == 3 and (d.flags >> 8) & 0xFF == 1
     counts = np.diff(bsr["row_index"])
-    perm = blob[d.off_nzrow:d.off_nzrow + 4 * 64].view(np.int32)
+    perm = blob[d.off_perm:d.off_perm + 4 * 64].view(np.int32)
     # slices hold rows by descending kept-group count
     assert list(counts[perm]) == sorted(counts, reverse=True)
+    # slice tables: slice 0 (32 rows) spans ceil(longest / 4) tiles
+    st0 = blob[d.off_slice_tile0:d.off_slice_tile0 + 4 * (d.num_slices + 1)].view(np.int32)
+    ts = blob[d.off_tile_slice:d.off_tile_slice + 4 * d.num_tiles].view(np.int32)
+    assert d.num_slices == 2 and st0[0] == 0 and st0[1] == -(-int(counts.max()) // 4) and st0[2] == d.num_tiles
+    assert list(ts) == [0] * int(st0[1]) + [1] * int(st0[2] - st0[1])
     t0 = blob[d.off_tiles:d.off_tiles + d.tile_bytes]
-    hdr = t0[:16].view(np.uint32)
-    assert hdr[0] >> 2 == 0 and hdr[0] & 1 and hdr[1] == -(-int(counts.max()) // 4) - 1
-    cols = t0[32 + 1024 + 512:].view(np.uint16)
+    cols = t0[1024 + 512:].view(np.uint16)
     hit = 0
     for u in range(4):
         for lane in range(32):
@@ -141,6 +144,13 @@ def test_tile_fields_match_layout():
             hit += ((f >> 1) % 4 == want % 4)  # the lane's target bank quad
     # bank-aware dealing: early slots almost always get the lane's target quad
     assert hit >= 0.9 * 128, hit
+    # padding entries: s = z = 0, codes 0, column field = the zero block at byte 2K
+    last = blob[d.off_tiles + (d.num_tiles - 1) * d.tile_bytes:d.off_tiles + d.num_tiles * d.tile_bytes]
+    sz = last[1024:1536].view(np.uint16).reshape(32, 4, 2)
+    pad = sz[:, :, 0] == 0
+    assert pad.any()
+    assert np.all(sz[pad][:, 1] == 0)
+    assert np.all(last[1536:].view(np.uint16).reshape(32, 4)[pad] == 2 * 256)
 
 
 def test_validation_errors():
@@ -183,10 +193,22 @@ def test_read_desc_rejects_corruption():
             gqsa.read_desc(b)
     with pytest.raises(gqsa.GQSAError):
         gqsa.read_desc(blob[:blob.size - 256])
-    # a flipped row-start bit is caught by unpack's consistency checks
+    # a corrupted slice table is caught by read_desc (the kernel trusts it)
     d = gqsa.read_desc(blob)
     b = blob.copy()
-    b[d.off_tiles] ^= 0x01
+    b[d.off_tile_slice + 4 * (d.num_tiles - 1)] ^= 0x01
+    with pytest.raises(gqsa.GQSAError):
+        gqsa.read_desc(b)
+    b = blob.copy()
+    b[d.off_slice_tile0 + 4] ^= 0x02
+    with pytest.raises(gqsa.GQSAError):
+        gqsa.read_desc(b)
+    # a padding entry that does not point at the zero block is caught by unpack
+    last = d.off_tiles + (d.num_tiles - 1) * d.tile_bytes
+    sz = blob[last + 1024:last + 1536].view(np.uint16).reshape(32, 4, 2)
+    lane, u = map(int, np.argwhere(sz[:, :, 0] == 0)[0])
+    b = blob.copy()
+    b[last + 1536 + lane * 8 + u * 2] = 0x20
     with pytest.raises(gqsa.GQSAError):
         gqsa.unpack(b)
 
@@ -195,7 +217,7 @@ def test_lanes_per_row_rule():
     # long rows are dealt over several lanes: the longest slice has at most
     # `target` slots per lane, target = 16 / 32 / 64 for layers under 1.6 /
     # 4 / more tiles per warp of a 148 x 16-warp grid
-    for rows, cols in ((256, 4096), (64, 14336), (8, 4096), (3, 256), (64, 512), (1, 32768),
+    for rows, cols in ((256, 4096), (64, 14336), (8, 4096), (3, 256), (64, 512), (1, 32736),
                        (14336, 4096), (4096, 4096)):
         bsr = synth.make_layer(rows + cols, rows, cols, sparsity=0.5)
         _, d = gqsa.pack(bsr)
@@ -208,8 +230,11 @@ def test_lanes_per_row_rule():
     assert target == 32 and S == 8  # 4096 x 4096: 1.7 tiles per warp
 
 
-def test_workspace_size_is_device_independent():
-    bsr = synth.make_layer(13, 4096, 4096, sparsity=0.5)
-    _, d = gqsa.pack(bsr)
-    recs = min(d.num_tiles, 8192)  # one record per possible active warp
-    assert gqsa.workspace_size(d, 1) == recs * 256 and gqsa.workspace_size(d, 8) == recs * 2048
+def test_workspace_size_is_layer_independent():
+    # per launch: 256 B + one u32 arrival counter and two [B][32] 8-B records
+    # per possible warp (148 SMs x 32 warps bound), whatever the layer
+    _, d = gqsa.pack(synth.make_layer(13, 4096, 4096, sparsity=0.5))
+    _, d2 = gqsa.pack(synth.make_layer(14, 64, 256, sparsity=0.3))
+    for B in (1, 2, 8):
+        want = 256 + 4736 * 4 + 4736 * 2 * B * 32 * 8
+        assert gqsa.workspace_size(d, B) == want == gqsa.workspace_size(d2, B)
