@@ -70,8 +70,10 @@ size_t ws_bytes_for(int B) {
 
 struct Launch {
   int grid = 0, W = 0, active = 0, total_tiles = 0, part_q = 0, part_r = 0;
-  size_t smem = 0;
+  size_t smem = 0, tab_offset = 0;
 };
+// shared bytes of the per-CTA staging table (gqsa_device.cuh StageEntry x kMaxItems + 16)
+constexpr size_t kStageTab = kMaxItems * 40 + 16;
 
 // Stream-K grid over the concatenated tiles of `n` items at batch Bc, and the
 // largest shared-memory footprint of any CTA (the items its range touches).
@@ -112,7 +114,8 @@ int plan_launch(const gqsa_desc_t* const* d, int n, int Bc, Launch* L) {
       if (tb[j] < t1 && te[j] > t0 && te[j] > tb[j]) s += (size_t)item_smem(d[j], Bc);
     worst = std::max(worst, s);
   }
-  L->smem = worst;
+  L->smem = worst + kStageTab;  // + the staging table
+  L->tab_offset = worst;
   return GQSA_OK;
 }
 
@@ -212,6 +215,7 @@ int launch_items(const gqsa_gemm_item_t* items, int n, int Bc, const gqsa_option
   p.slice_k = o.partition == GQSA_PARTITION_SLICE_K ? 1 : 0;
   p.out_f16 = o.out_f16;
   p.x_ready = o.x_ready;
+  p.stage_tab_offset = (int32_t)L.tab_offset;
   uint8_t* ws = static_cast<uint8_t*>(d_ws);
   p.cnt = reinterpret_cast<uint32_t*>(ws + 256);
   p.rec = reinterpret_cast<unsigned long long*>(ws + 256 + (size_t)kMaxWarpsBound * 4);

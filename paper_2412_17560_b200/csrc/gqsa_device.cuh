@@ -55,6 +55,9 @@ __device__ __forceinline__ uint2 ldg_stream64(const void* ptr, uint64_t pol) {
                : "l"(ptr), "l"(pol));
   return v;
 }
+__device__ __forceinline__ void prefetch_l2(const void* ptr, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
@@ -254,34 +257,82 @@ __device__ __forceinline__ void group_accumulate(const TileRegs<BITS, G>& tr, in
   }
 }
 
-// Stage x of one item (B rows of `cols` fp16, row stride ldx) into shared
-// memory: x rows of xrow bytes followed by a zero block, and the negated
-// column-group sums (-P, -Q) (fp32, fixed t order) computed from the same
-// registers, plus zero entries for padding.  Caller synchronises.
+// Stage the activations of every item a CTA's tile range [t0, t1) touches,
+// in one round of loads for the common sizes: the column groups of all
+// touched items form one index space (a small table of the touched items is
+// built in shared memory first, so the lookups stay on chip), each thread
+// loads U of them (all loads in flight together), then writes x rows (of
+// xrow bytes, followed by a zero block) and the negated column-group sums
+// (-P, -Q) (fp32, fixed t order) computed from the same registers, plus zero
+// entries for padding.  Items are packed in item order from shared offset 0
+// (mirrors the host's plan).  `tab` is kStageTabBytes of shared memory after
+// the staging area (kMaxItems entries, then the count and total).  Caller
+// synchronises.
+__device__ __forceinline__ bool item_touched(const Item& it, int t0, int t1) {
+  return it.tile_begin < t1 && it.tile_end > t0 && it.tile_end > it.tile_begin;
+}
+struct StageEntry {
+  const uint16_t* X;
+  int64_t ldx;
+  int32_t first;   // first global column-group index of this item
+  int32_t kg;      // column groups per batch row
+  int32_t cols, xrow, pqrow;
+  uint32_t off;    // shared offset of the item's x rows
+};
+constexpr int kStageTabBytes = kMaxItems * (int)sizeof(StageEntry) + 16;
+static_assert(sizeof(StageEntry) == 40, "gqsa_capi.cu kStageTab");
 template <int BITS, int B, int G>
-__device__ __forceinline__ void stage_item(const Item& it, uint8_t* xs, uint8_t* pq) {
+__device__ __forceinline__ void stage_all(const Params& p, int t0, int t1, uint8_t* sm, StageEntry* tab) {
   constexpr int NC = G / 8;            // 16-B chunks per column group
-  constexpr int U = NC >= 4 ? 1 : 2;  // column groups per thread per round in flight
-  const int KG = it.cols / G;
+#ifndef GQSA_STAGE_U
+#define GQSA_STAGE_U 4
+#endif
+  constexpr int U = NC >= 4 ? 2 : GQSA_STAGE_U;  // column groups per thread in flight per round
+  constexpr int PG = (G == 16 && B <= 2) ? 2 : 1;  // (-P, -Q) entries per column group (one per chunk order)
   const int nthreads = blockDim.x;
-  for (int i0 = threadIdx.x; i0 < B * KG; i0 += U * nthreads) {
+  if (threadIdx.x == 0) {
+    int first = 0, n = 0;
+    uint32_t off = 0;
+    for (int i = 0; i < p.n_items; ++i) {
+      const Item& it = p.item[i];
+      if (!item_touched(it, t0, t1)) continue;
+      tab[n] = StageEntry{it.X, it.ldx, first, it.cols / G, it.cols, it.xrow, it.pqrow, off};
+      first += B * (it.cols / G);
+      off += (uint32_t)it.smem_bytes;
+      ++n;
+    }
+    reinterpret_cast<volatile int*>(tab + kMaxItems)[0] = n;
+    reinterpret_cast<volatile int*>(tab + kMaxItems)[1] = first;
+  }
+  __syncthreads();
+  const int n_t = reinterpret_cast<const int*>(tab + kMaxItems)[0];
+  const int total = reinterpret_cast<const int*>(tab + kMaxItems)[1];
+  auto locate = [&](int gi) {  // entry of global column-group index gi
+    int k = 0;
+    while (k + 1 < n_t && gi >= tab[k + 1].first) ++k;
+    return k;
+  };
+  for (int base = threadIdx.x; base < total; base += U * nthreads) {
     uint4 v[U][NC];
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-      const int i = i0 + k * nthreads;
-      if (i < B * KG) {
-        const int b = i / KG, c = i - b * KG;
-        const uint4* src = reinterpret_cast<const uint4*>(it.X + (int64_t)b * it.ldx) + NC * c;
+      const int gi = base + k * nthreads;
+      if (gi < total) {
+        const StageEntry& e = tab[locate(gi)];
+        const int l = gi - e.first, b = B == 1 ? 0 : l / e.kg, c = l - b * e.kg;
+        const uint4* src = reinterpret_cast<const uint4*>(e.X + (int64_t)b * e.ldx) + NC * c;
 #pragma unroll
         for (int h = 0; h < NC; ++h) v[k][h] = __ldg(src + h);
       }
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-      const int i = i0 + k * nthreads;
-      if (i < B * KG) {
-        const int b = i / KG, c = i - b * KG;
-        uint4* dst = reinterpret_cast<uint4*>(xs + (size_t)b * it.xrow) + NC * c;
+      const int gi = base + k * nthreads;
+      if (gi < total) {
+        const StageEntry& e = tab[locate(gi)];
+        const int l = gi - e.first, b = B == 1 ? 0 : l / e.kg, c = l - b * e.kg;
+        uint8_t* xs = sm + e.off;
+        uint4* dst = reinterpret_cast<uint4*>(xs + (size_t)b * e.xrow) + NC * c;
         uint32_t w[4 * NC];
 #pragma unroll
         for (int h = 0; h < NC; ++h) {
@@ -292,21 +343,25 @@ __device__ __forceinline__ void stage_item(const Item& it, uint8_t* xs, uint8_t*
           w[4 * h + 3] = v[k][h].w;
         }
         const float2 v2 = neg_column_sums<BITS, G>(w);
-        constexpr int PG = (G == 16 && B <= 2) ? 2 : 1;  // entries per column group (one per chunk order)
-        float2* pdst = reinterpret_cast<float2*>(pq + (size_t)b * it.pqrow) + (size_t)c * PG;
+        float2* pdst = reinterpret_cast<float2*>(xs + (size_t)B * e.xrow + (size_t)b * e.pqrow) + (size_t)c * PG;
         pdst[0] = v2;
         if (PG == 2) pdst[1] = v2;
       }
     }
   }
-  // zero block after each x row and the padding entries of the column-sum table
-  for (int i = threadIdx.x; i < B * (kXPadBytes / 16); i += nthreads) {
-    const int b = i / (kXPadBytes / 16), k = i % (kXPadBytes / 16);
-    reinterpret_cast<uint4*>(xs + (size_t)b * it.xrow + 2 * it.cols)[k] = make_uint4(0, 0, 0, 0);
+  // zero block after each x row and the padding entries of the column-sum tables
+  for (int k = 0; k < n_t; ++k) {
+    const StageEntry& e = tab[k];
+    uint8_t* xs = sm + e.off;
+    for (int j = threadIdx.x; j < B * (kXPadBytes / 16); j += nthreads) {
+      const int b = j / (kXPadBytes / 16), q = j % (kXPadBytes / 16);
+      reinterpret_cast<uint4*>(xs + (size_t)b * e.xrow + 2 * e.cols)[q] = make_uint4(0, 0, 0, 0);
+    }
+    const int ne = pq_entries(B, G, e.cols);
+    for (int j = threadIdx.x; j < B * 2; j += nthreads)
+      reinterpret_cast<float2*>(xs + (size_t)B * e.xrow + (size_t)(j >> 1) * e.pqrow)[ne + (j & 1)] =
+          make_float2(0.f, 0.f);
   }
-  const int ne = pq_entries(B, G, it.cols);
-  for (int i = threadIdx.x; i < B * 2; i += nthreads)
-    reinterpret_cast<float2*>(pq + (size_t)(i >> 1) * it.pqrow)[ne + (i & 1)] = make_float2(0.f, 0.f);
 }
 
 }  // namespace gqsa

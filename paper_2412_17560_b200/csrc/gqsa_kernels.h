@@ -18,19 +18,34 @@ constexpr int kMaxItems = 8;            // independent GEMVs per launch (gqsa_ge
 constexpr int kMaxBatch = 8;
 constexpr int kMaxPeers = 8;            // ranks of a fused all-gather (one NVLink domain)
 constexpr int kSmemPerSm = 228 * 1024;  // shared memory per SM
-constexpr int kMaxDynSmem = 227 * 1024; // opt-in dynamic shared memory per CTA
+constexpr int kMaxDynSmem = 225 * 1024; // opt-in dynamic shared memory per CTA (227 KB - the static item table)
 // Tile register buffers per warp: while one tile is consumed the next
 // kBufs - 1 are in flight (HBM -> registers, no shared-memory staging).
 #ifndef GQSA_BUFS
-#define GQSA_BUFS 3
+#define GQSA_BUFS 2
 #endif
 constexpr int kBufs = GQSA_BUFS;
-// Warps per CTA (one CTA per SM): 16 at batch <= 2, 8 above (more
-// accumulators and activation gathers per lane).
-#ifndef GQSA_WARPS_SMALL
-#define GQSA_WARPS_SMALL 16
+// L2 prefetch distance in tiles (<= kBufs: off): lane 0 issues
+// cp.async.bulk.prefetch.L2 for tile t + kL2Pf as it requests tile t into registers.
+#ifndef GQSA_L2PF
+#define GQSA_L2PF 0
 #endif
-__host__ __device__ constexpr int warps_for(int B) { return B <= 2 ? GQSA_WARPS_SMALL : 8; }
+constexpr int kL2Pf = GQSA_L2PF;
+// Warps per CTA (one CTA per SM): more warps keep more weight loads in
+// flight (a read-only stream of the same tiles reaches 4.9 / 5.3 / 5.5 TB/s
+// with 16 / 24 / 32 warps per SM on the 59 MB bench step,
+// profiles/r02_stream_bench.jsonl); the register budget (<= 65536 / 32W per
+// thread, no spills) sets the count: 20 at batch 1, 16 at batch 2, 8 above.
+#ifndef GQSA_WARPS_SMALL
+#define GQSA_WARPS_SMALL 20
+#endif
+__host__ __device__ constexpr int warps_for(int B) { return B == 1 ? GQSA_WARPS_SMALL : B == 2 ? 16 : 8; }
+// Resident CTAs per SM the kernel is compiled for (launch bounds): 2 lets the
+// next launch on the stream be resident during this one's tail (PDL).
+#ifndef GQSA_MINB
+#define GQSA_MINB 1
+#endif
+__host__ __device__ constexpr int min_blocks_for(int B) { return B <= 2 ? GQSA_MINB : 1; }
 constexpr int kMaxWarpsBound = 148 * 32;  // fix-up records the workspace holds per launch (any B200 grid)
 
 // One GEMV of a launch.  Its tiles occupy global tile indices
@@ -61,6 +76,7 @@ struct Params {
   int32_t slice_k;   // 1: data-centric partition (whole slices per warp, no fix-up)
   int32_t out_f16;   // 1: Y is fp16 (RNE of the fp32 result)
   int32_t x_ready;   // 1: X is not written by the previous kernel on the stream: stage it before the PDL wait
+  int32_t stage_tab_offset;  // shared offset of the staging table (after the largest staged footprint)
   uint32_t* cnt;                 // [active_warps] fix-up arrival counters (zero between launches)
   unsigned long long* rec;       // [active_warps][2][B][32] fix-up records {partial, flag}
   uint64_t* trace;               // optional [active_warps][8] %globaltimer stamps (debug)

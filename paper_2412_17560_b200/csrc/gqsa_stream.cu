@@ -55,15 +55,12 @@ __device__ __forceinline__ int item_of(const Params& p, int t) {
   while (i + 1 < p.n_items && t >= p.item[i].tile_end) ++i;
   return i;
 }
-__device__ __forceinline__ bool touched(const Item& it, int t0, int t1) {
-  return it.tile_begin < t1 && it.tile_end > t0 && it.tile_end > it.tile_begin;
-}
 // Shared-memory offset of item i's staged activations in a CTA whose tile
 // range is [t0, t1): the touched items are packed in item order.
-__device__ __forceinline__ uint32_t item_smem_off(const Params& p, int i, int t0, int t1) {
+__device__ __forceinline__ uint32_t item_smem_off(const Item* items, int i, int t0, int t1) {
   uint32_t off = 0;
   for (int j = 0; j < i; ++j)
-    if (touched(p.item[j], t0, t1)) off += (uint32_t)p.item[j].smem_bytes;
+    if (item_touched(items[j], t0, t1)) off += (uint32_t)items[j].smem_bytes;
   return off;
 }
 
@@ -131,7 +128,7 @@ __device__ __forceinline__ int arrive(const Params& p, int w0, int lane) {
 // of w0+1..w1), reset the flags and the counter, store the rows.  The spin
 // only waits for stores already issued (their writers arrived before us).
 template <int B>
-__device__ __noinline__ void collect(const Params& p, int w0, int w1, int item, int row, int lane) {
+__device__ __noinline__ void collect(const Params& p, const Item* items, int w0, int w1, int item, int row, int lane) {
   float v[B];
 #pragma unroll
   for (int b = 0; b < B; ++b) v[b] = 0.f;
@@ -153,13 +150,27 @@ __device__ __noinline__ void collect(const Params& p, int w0, int w1, int item, 
           __nanosleep(32);
           r[k] = ld_relaxed64(a);
         }
-        v[b] += __uint_as_float((uint32_t)r[k]);
+        v[b] = (wb + k == w0) ? __uint_as_float((uint32_t)r[k]) : v[b] + __uint_as_float((uint32_t)r[k]);
         st_relaxed64(a, 0ull);
       }
     }
   }
   if (lane == 0) asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p.cnt + w0), "r"(0u) : "memory");
-  store_rows<B>(p, p.item[item], v, row, lane);
+  store_rows<B>(p, items[item], v, row, lane);
+}
+
+// Empty rows get bias (or 0): grid-stride over every item's empty-row list.
+template <int B>
+__device__ __forceinline__ void store_empty_rows(const Params& p, const Item* items) {
+  for (int i = 0; i < p.n_items; ++i) {
+    const Item& it = items[i];
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < it.n_empty; k += gridDim.x * blockDim.x) {
+      const int erow = __ldg(it.empty + k);
+      const float bias = it.bias ? __ldg(it.bias + erow) : 0.f;
+#pragma unroll
+      for (int b = 0; b < B; ++b) store_y(it, p.out_f16, (int64_t)b * it.ldy + erow, bias);
+    }
+  }
 }
 
 // Optional timeline instrumentation (gqsa_debug_trace): lane 0 of each warp
@@ -175,13 +186,21 @@ __device__ __forceinline__ void trace_point(const Params& p, int gw, int lane, i
 }  // namespace
 
 template <int BITS, int B, int G>
-__global__ void __launch_bounds__(32 * warps_for(B), 1) gqsa_stream_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(32 * warps_for(B), min_blocks_for(B)) gqsa_stream_kernel(const __grid_constant__ Params p) {
   constexpr int W = warps_for(B);
   constexpr int TB = tile_bytes(BITS, G);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int gw = blockIdx.x * W + warp;
   trace_point(p, gw, lane, 0);
+  // per-item parameters, copied to shared memory: the loop indexes them by
+  // a runtime item number (indexed parameter-space loads can miss the
+  // constant cache); visible after the staging barrier
+  __shared__ Item s_item[kMaxItems];
+  static_assert(sizeof(Item) % 8 == 0, "item copy");
+  for (int i = threadIdx.x; i < p.n_items * (int)(sizeof(Item) / 8); i += blockDim.x)
+    reinterpret_cast<uint64_t*>(s_item)[i] = reinterpret_cast<const uint64_t*>(p.item)[i];
+  const Item* its = p.item;  // -> s_item after the barrier
 
   // ---- task-centric partition: contiguous tile range per warp (+-1 tile)
   int t_begin = 0, t_end = 0;
@@ -225,84 +244,85 @@ __global__ void __launch_bounds__(32 * warps_for(B), 1) gqsa_stream_kernel(const
   }
   auto issue = [&](TileRegs<BITS, G>& r, int t) {  // t: the next tile of the load cursor
     if (t == lend) {
-      do { ++li; } while (p.item[li].tile_end == p.item[li].tile_begin);
-      lptr = p.item[li].tiles;
-      lend = p.item[li].tile_end;
+      do { ++li; } while (its[li].tile_end == its[li].tile_begin);
+      lptr = its[li].tiles;
+      lend = its[li].tile_end;
     }
     load_tile<BITS, G>(r, lptr, lane, pol);
+    if (kL2Pf > kBufs && lane == 0 && t + kL2Pf < min(t_end, lend)) prefetch_l2(lptr + (size_t)kL2Pf * TB, TB);
     lptr += TB;
   };
+  if (kL2Pf > kBufs && lane == 0 && t_end > t_begin) {  // tiles the first refills need (later ones: issue())
+    for (int k = kBufs; k < kL2Pf && t_begin + k < min(t_end, lend); ++k) prefetch_l2(lptr + (size_t)k * TB, TB);
+  }
 #pragma unroll
   for (int k = 0; k < kBufs; ++k)
     if (t_begin + k < t_end) issue(buf[k], t_begin + k);
 
-  // ---- slice cursor: current slice (item ci, slice cs, global end tile
-  //      cend, this lane's row crow) and the next one, prefetched
-  int ci = 0, cs = 0, cend = 0, crow = -1;
+  // ---- slice cursor: current slice (item ci, slice cs, global first / end
+  //      tile cst0 / cend, this lane's row crow) and the next one, prefetched.
+  //      Only the first lookup is issued before the PDL trigger; everything
+  //      that depends on it is consumed after the activations are staged.
+  int ci = 0, cs = 0, cst0 = 0, cend = 0, crow = -1;
   int ni = 0, ns = 0, nend = 0, nrow = -1;
-  bool foreign = false;  // the current slice began in an earlier warp's range
-  int cw0 = gw;          // warp owning the current slice's first tile
   auto prefetch_next = [&]() {  // successor of (ci, cs), if the range continues past cend
     if (cend >= t_end) return;
     ni = ci;
     ns = cs + 1;
-    if (ns == p.item[ci].num_slices) {
-      do { ++ni; } while (p.item[ni].tile_end == p.item[ni].tile_begin);
+    if (ns == its[ci].num_slices) {
+      do { ++ni; } while (its[ni].tile_end == its[ni].tile_begin);
       ns = 0;
     }
-    const Item& it = p.item[ni];
+    const Item& it = its[ni];
     nend = it.tile_begin + __ldg(it.slice_tile0 + ns + 1);
     nrow = __ldg(it.perm + (int64_t)ns * kLanes + lane);
   };
   if (t_end > t_begin) {
     ci = item_of(p, t_begin);
-    const Item& it = p.item[ci];
-    cs = __ldg(it.tile_slice + (t_begin - it.tile_begin));
-    const int st0 = it.tile_begin + __ldg(it.slice_tile0 + cs);
-    cend = it.tile_begin + __ldg(it.slice_tile0 + cs + 1);
-    crow = __ldg(it.perm + (int64_t)cs * kLanes + lane);
-    foreign = st0 < t_begin;
-    if (foreign) cw0 = warp_of_tile(p, st0);
-    prefetch_next();
+    cs = __ldg(p.item[ci].tile_slice + (t_begin - p.item[ci].tile_begin));
   }
 
   // let the next launch on the stream start its prologue (its weight loads)
   pdl_launch_dependents();
-  if (!p.x_ready) pdl_wait();  // x may be the previous kernel's output
+  // x may be the previous kernel's output; with x_ready the wait is deferred
+  // to just before this launch's first global write (y, records, counters)
+  bool waited = !p.x_ready;
+  if (waited) pdl_wait();
   trace_point(p, gw, lane, 1);
+  if (t_end > t_begin) {
+    const Item& it = p.item[ci];
+    cst0 = it.tile_begin + __ldg(it.slice_tile0 + cs);
+    cend = it.tile_begin + __ldg(it.slice_tile0 + cs + 1);
+    crow = __ldg(it.perm + (int64_t)cs * kLanes + lane);
+  }
 
   // ---- stage the activations of every item this CTA's range touches
-  for (int i = 0; i < p.n_items; ++i) {
-    const Item& it = p.item[i];
-    if (!touched(it, cta_t0, cta_t1)) continue;
-    uint8_t* xs = smem + item_smem_off(p, i, cta_t0, cta_t1);
-    stage_item<BITS, B, G>(it, xs, xs + (size_t)B * it.xrow);
-  }
-  if (p.x_ready) pdl_wait();  // y, bias and the workspace may still belong to the previous kernel
+  stage_all<BITS, B, G>(p, cta_t0, cta_t1, smem, reinterpret_cast<StageEntry*>(smem + p.stage_tab_offset));
   __syncthreads();
+  its = s_item;
   trace_point(p, gw, lane, 2);
-
-  // ---- empty rows get bias (or 0): grid-stride over every item's list
-  for (int i = 0; i < p.n_items; ++i) {
-    const Item& it = p.item[i];
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < it.n_empty; k += gridDim.x * blockDim.x) {
-      const int erow = __ldg(it.empty + k);
-      const float bias = it.bias ? __ldg(it.bias + erow) : 0.f;
-#pragma unroll
-      for (int b = 0; b < B; ++b) store_y(it, p.out_f16, (int64_t)b * it.ldy + erow, bias);
+  auto ensure_wait = [&]() {
+    if (!waited) {
+      pdl_wait();
+      waited = true;
     }
-  }
+  };
   if (t_end <= t_begin) {
+    ensure_wait();
+    store_empty_rows<B>(p, its);
     if (p.item[0].n_peers) __threadfence_system();
     return;
   }
+  bool foreign = cst0 < t_begin;  // the current slice began in an earlier warp's range
+  int cw0 = foreign ? warp_of_tile(p, cst0) : gw;  // warp owning the current slice's first tile
+  prefetch_next();
 
   // ---- stream the warp's tile range; lane = one row of the current slice
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   XView xv;
   auto set_item = [&]() {
-    const Item& it = p.item[ci];
-    xv.xs = sbase + item_smem_off(p, ci, cta_t0, cta_t1);
+    const Item& it = its[ci];
+    xv.xs = sbase + item_smem_off(its, ci, cta_t0, cta_t1);
     xv.xrow = (uint32_t)it.xrow;
     xv.pq = xv.xs + (uint32_t)B * xv.xrow;
     xv.pqrow = (uint32_t)it.pqrow;
@@ -311,16 +331,35 @@ __global__ void __launch_bounds__(32 * warps_for(B), 1) gqsa_stream_kernel(const
   float acc[B];
 #pragma unroll
   for (int b = 0; b < B; ++b) acc[b] = 0.f;
-  // head slice (began upstream, closed in this range): arrival deferred to the range end
+  // head slice (began upstream, closed in this range): arrival result checked at the range end
   bool h_pending = false;
   int h_old = 0, h_w0 = 0, h_item = 0, h_row = -1;
+  // first-warp fast path: the successors' head records, requested during the last tile
+  constexpr int kPre = B <= 2 ? 3 : 0;
+  unsigned long long pre[kPre > 0 ? kPre : 1][B];
   trace_point(p, gw, lane, 3);
 
   auto consume = [&](const TileRegs<BITS, G>& tr, int t) {
+    if (kPre > 0 && t == t_end - 1 && cend > t_end && !foreign) {
+      // this warp owns the slice left open at its range end: request the
+      // successors' records now, so they are here when the tile is done
+      const int n = warp_of_tile(p, cend - 1) - gw;
+#pragma unroll
+      for (int k = 0; k < kPre; ++k)
+#pragma unroll
+        for (int b = 0; b < B; ++b)
+          pre[k][b] = k < n ? ld_relaxed64(rec_ptr<B>(p, gw + 1 + k, 0, b, lane)) : (1ull << 32);
+    }
 #pragma unroll
     for (int u = 0; u < kPerLane; ++u) group_accumulate<BITS, B, G>(tr, u, acc, xv);
+    if (p.trace && t == t_begin) trace_point(p, gw, lane, 6);  // first tile landed and consumed
     if (t + 1 == cend) {  // the slice ends with this tile: its rows are complete here
+      ensure_wait();
+#ifdef GQSA_EXP_NOFIX
+      if (false) {
+#else
       if (foreign) {  // ... but began upstream: publish, arrive, check at the range end
+#endif
         publish<B>(p, gw, 0, acc, lane);
         h_old = arrive(p, cw0, lane);
         h_pending = true;
@@ -328,7 +367,7 @@ __global__ void __launch_bounds__(32 * warps_for(B), 1) gqsa_stream_kernel(const
         h_item = ci;
         h_row = crow;
       } else {
-        store_rows<B>(p, p.item[ci], acc, crow, lane);
+        store_rows<B>(p, its[ci], acc, crow, lane);
       }
 #pragma unroll
       for (int b = 0; b < B; ++b) acc[b] = 0.f;
@@ -358,19 +397,55 @@ __global__ void __launch_bounds__(32 * warps_for(B), 1) gqsa_stream_kernel(const
     }
   }
   trace_point(p, gw, lane, 4);
+  ensure_wait();
 
+  trace_point(p, gw, lane, 7);
   // ---- a slice left open at the end of the range continues downstream
+#ifdef GQSA_EXP_NOFIX  // timing experiment only: results are wrong
+  if (false) {
+#else
   if (cend > t_end) {
-    const int which = foreign ? 0 : 1;  // middle participant: head record; first warp: tail record
-    publish<B>(p, gw, which, acc, lane);
-    const int old = __shfl_sync(0xffffffffu, arrive(p, cw0, lane), 0);
+#endif
     const int w1 = warp_of_tile(p, cend - 1);
-    if (old == w1 - cw0) collect<B>(p, cw0, w1, ci, crow, lane);
+    bool done = false;
+    if (kPre > 0 && !foreign && w1 - gw <= kPre) {
+      // fast path: every successor already published -> add them in warp
+      // order and finish the rows here, without arriving (the successors'
+      // arrivals are cancelled so the counter returns to zero)
+      bool ready = true;
+#pragma unroll
+      for (int k = 0; k < kPre; ++k)
+#pragma unroll
+        for (int b = 0; b < B; ++b) ready &= (pre[k][b] >> 32) != 0ull;
+      if (__all_sync(0xffffffffu, ready)) {
+        float v[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+          v[b] = acc[b];
+#pragma unroll
+          for (int k = 0; k < kPre; ++k)
+            if (k < w1 - gw) {
+              v[b] += __uint_as_float((uint32_t)pre[k][b]);
+              st_relaxed64(rec_ptr<B>(p, gw + 1 + k, 0, b, lane), 0ull);
+            }
+        }
+        if (lane == 0) atomicAdd(p.cnt + gw, (unsigned)(gw - w1));
+        store_rows<B>(p, its[ci], v, crow, lane);
+        done = true;
+      }
+    }
+    if (!done) {
+      const int which = foreign ? 0 : 1;  // middle participant: head record; first warp: tail record
+      publish<B>(p, gw, which, acc, lane);
+      const int old = __shfl_sync(0xffffffffu, arrive(p, cw0, lane), 0);
+      if (old == w1 - cw0) collect<B>(p, its, cw0, w1, ci, crow, lane);
+    }
   }
   if (h_pending) {
     const int old = __shfl_sync(0xffffffffu, h_old, 0);
-    if (old == gw - h_w0) collect<B>(p, h_w0, gw, h_item, h_row, lane);
+    if (old == gw - h_w0) collect<B>(p, its, h_w0, gw, h_item, h_row, lane);
   }
+  store_empty_rows<B>(p, its);
   trace_point(p, gw, lane, 5);
   if (p.item[0].n_peers) __threadfence_system();  // peer stores visible before the launch completes
 }
@@ -395,6 +470,11 @@ const void* kernel_ptr() {
   }
 
 const void* select_kernel(int bits, int G, int B) {
+#ifdef GQSA_FAST_BUILD  // experiments: W4, G = 16, B <= 2 only
+  if (bits == 4 && G == kGroup && B == 1) return kernel_ptr<4, 1, 16>();
+  if (bits == 4 && G == kGroup && B == 2) return kernel_ptr<4, 2, 16>();
+  return nullptr;
+#endif
   if (G == 8 && bits == 4) { GQSA_KSEL(4, 8) }
   if (G == 32 && bits == 4) { GQSA_KSEL(4, 32) }
   if (G != kGroup) return nullptr;

@@ -20,7 +20,7 @@ import torch  # noqa: E402
 
 from paper_2412_17560_b200 import gqsa, synth  # noqa: E402
 
-NAMES = ["start", "pdl_wait", "x_staged", "tile0", "loop_end", "exit"]
+NAMES = ["start", "pdl_wait", "x_staged", "loop0", "loop_end", "exit", "tile0_done"]
 
 
 def main():
@@ -62,7 +62,7 @@ def main():
             g.replay()
     gqsa.debug_trace(None)
     torch.cuda.synchronize()
-    T = np.stack([b.cpu().numpy().reshape(W, 8)[:, :6] for b in bufs])  # [R][W][6]
+    T = np.stack([b.cpu().numpy().reshape(W, 8)[:, :7] for b in bufs])  # [R][W][7]
     t0 = T[0, :, 0].min()
     T = (T - t0) / 1e3
     print(f"{a.rows}x{a.cols} W{a.bits}: grid={plan.grid} warps={W} stages={plan.stages} "
@@ -70,36 +70,21 @@ def main():
     print("launch  " + "  ".join(f"{n:>17s}" for n in NAMES) + "   (min/median/max µs)")
     for i in range(min(R, a.launches)):
         cols = []
-        for k in range(6):
+        for k in range(7):
             v = T[i, :, k]
             cols.append(f"{v.min():5.2f}/{np.median(v):5.2f}/{v.max():5.2f}")
         print(f"{i:6d}  " + "  ".join(f"{c:>17s}" for c in cols))
     per = [(T[i + 1, :, 5].max() - T[i, :, 5].max()) for i in range(min(R, a.launches) - 1)]
     print("exit-to-exit per launch (µs):", " ".join(f"{p:.2f}" for p in per))
     d = T[1:, :, :]
-    print("median phase durations (µs): wait=%.2f stage=%.2f tile0=%.2f loop=%.2f fixup=%.2f" % (
-        np.median(d[..., 1] - d[..., 0]), np.median(d[..., 2] - d[..., 1]), np.median(d[..., 3] - d[..., 2]),
+    print("median phase durations (µs): wait=%.2f stage=%.2f first_tile=%.2f loop=%.2f fixup=%.2f" % (
+        np.median(d[..., 1] - d[..., 0]), np.median(d[..., 2] - d[..., 1]), np.median(d[..., 6] - d[..., 3]),
         np.median(d[..., 4] - d[..., 3]), np.median(d[..., 5] - d[..., 4])))
-    raw = np.stack([b.cpu().numpy().reshape(W, 8) for b in bufs])
-    role = raw[1:, :, 7]
-    T8 = (raw - t0) / 1e3
-    e = T8[1:]
-    print("staging split (µs): x_loads+xc=%.2f barrier+rest=%.2f" % (
-        np.median(e[..., 6] - e[..., 1]), np.median(e[..., 2] - e[..., 6])))
-    fx = e[..., 5] - e[..., 4]
-    for name, m in (("closed", role == 0), ("publisher", role == 1), ("owner", role >= 100)):
-        if m.any():
-            v = fx[m]
-            print("fixup %-9s %4.0f%% of warps: p50/p90/max %.2f/%.2f/%.2f us" % (
-                name, 100 * m.mean(), np.median(v), np.percentile(v, 90), v.max()))
-    if (role >= 100).any():
-        ch = role[role >= 100] - 100
-        print("owner chain length (successor warps) p50/p90/max: %d/%d/%d" % (
-            np.median(ch), np.percentile(ch, 90), ch.max()))
+    e = d
     q, r = divmod(plan.num_tiles, W)  # Stream-K units are tiles
     ntile = np.array([q + (1 if w < r else 0) for w in range(W)], dtype=float)
-    loop = e[..., 4] - e[..., 3]
-    per = loop / ntile[None, :]
+    loop = e[..., 4] - e[..., 6]  # steady state: after the first tile
+    per = loop / np.maximum(ntile[None, :] - 1, 1)
     print("loop µs per tile (p10/p50/p90/max): %.3f/%.3f/%.3f/%.3f; warps with q+1 tiles: %.0f%%" % (
         np.percentile(per, 10), np.median(per), np.percentile(per, 90), per.max(), 100 * r / W))
     sm = np.arange(W) // plan.warps_per_cta
