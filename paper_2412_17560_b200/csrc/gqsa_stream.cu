@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(32 * warps_for(B), min_blocks_for(B)) gqsa_str
   trace_point(p, gw, lane, 4);
   ensure_wait();
 
-  trace_point(p, gw, lane, 7);
+  int fix_path = 0;  // debug trace: 1 fast, 2 published (not last), 3 published + collected; +10 head collected
   // ---- a slice left open at the end of the range continues downstream
 #ifdef GQSA_EXP_NOFIX  // timing experiment only: results are wrong
   if (false) {
@@ -432,19 +432,28 @@ __global__ void __launch_bounds__(32 * warps_for(B), min_blocks_for(B)) gqsa_str
         if (lane == 0) atomicAdd(p.cnt + gw, (unsigned)(gw - w1));
         store_rows<B>(p, its[ci], v, crow, lane);
         done = true;
+        fix_path = 1;
       }
     }
     if (!done) {
       const int which = foreign ? 0 : 1;  // middle participant: head record; first warp: tail record
       publish<B>(p, gw, which, acc, lane);
       const int old = __shfl_sync(0xffffffffu, arrive(p, cw0, lane), 0);
-      if (old == w1 - cw0) collect<B>(p, its, cw0, w1, ci, crow, lane);
+      fix_path = 2;
+      if (old == w1 - cw0) {
+        collect<B>(p, its, cw0, w1, ci, crow, lane);
+        fix_path = 3;
+      }
     }
   }
   if (h_pending) {
     const int old = __shfl_sync(0xffffffffu, h_old, 0);
-    if (old == gw - h_w0) collect<B>(p, its, h_w0, gw, h_item, h_row, lane);
+    if (old == gw - h_w0) {
+      collect<B>(p, its, h_w0, gw, h_item, h_row, lane);
+      fix_path += 10;
+    }
   }
+  if (p.trace && lane == 0 && gw < p.active_warps) p.trace[(int64_t)gw * 8 + 7] = (uint64_t)fix_path;
   store_empty_rows<B>(p, its);
   trace_point(p, gw, lane, 5);
   if (p.item[0].n_peers) __threadfence_system();  // peer stores visible before the launch completes

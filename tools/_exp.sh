@@ -1,7 +1,4 @@
 make -s >/dev/null 2>&1 || { echo BUILD FAILED; exit 1; }
-timeout 1800 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu.log 2>&1; tail -15 gpurun_out/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
-timeout 300 python bench.py --steps 20 --warmup 5 --cpu-budget 3 > gpurun_out/b20.json 2> gpurun_out/b20.err; python -c "
-import json;d=json.load(open('gpurun_out/b20.json'));print('steps20', d['us_per_step'], d['value'], d['roofline']['frac'], d['cpu_baseline']['gpu_parity'], d['clocks'])"; tail -3 gpurun_out/b20.err
-timeout 300 python bench.py --steps 20000 --warmup 200 --no-cpu-baseline > gpurun_out/b20k.json 2>> gpurun_out/b20.err; python -c "
-import json;d=json.load(open('gpurun_out/b20k.json'));print('steps20000', d['us_per_step'], d['value'], d['roofline']['frac'], [ (l['shape'], l['us']) for l in d['layers']], d['e2e']['value'])"
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_grouped.py tests/test_gpu_frontend.py tests/test_gpu_fuzz.py -x -q -m gpu > gpurun_out/t1.log 2>&1; tail -2 gpurun_out/t1.log
+tools/ab.sh "A D" 2
+for v in D; do echo $v; GQSA_LIB_PATH=paper_2412_17560_b200/lib/var/$v.so timeout 300 python tools/trace_step.py 2>&1 | grep -E "exit-to-exit|phase|per tile|fixup|last exit|warps="; done

@@ -21,7 +21,7 @@ from paper_2412_17560_b200 import gqsa, synth  # noqa: E402
 
 NAMES = ["start", "pdl_wait", "x_staged", "loop0", "loop_end", "exit", "tile0_done"]
 SHAPES = [(4096, 4096), (14336, 4096), (4096, 14336)]
-ORDERS = {"default": [0, 1, 2], "rev": [2, 1, 0]}
+ORDERS = {"default": [0, 1, 2], "rev": [2, 1, 0], "q": [0], "gate": [1], "down": [2]}
 
 
 def main():
@@ -58,7 +58,9 @@ def main():
         g.replay()
     gqsa.debug_trace(None)
     torch.cuda.synchronize()
-    T = np.stack([b.cpu().numpy().reshape(W, 8)[:, :8] for b in bufs]).astype(np.float64)
+    raw = np.stack([b.cpu().numpy().reshape(W, 8) for b in bufs])
+    path = raw[1:, :, 7]
+    T = raw[:, :, :7].astype(np.float64)
     t0 = T[0, :, 0].min()
     T = (T - t0) / 1e3
     print(f"grouped step: warps={W} tiles={total_tiles} x_ready={a.x_ready} R={R}")
@@ -80,9 +82,25 @@ def main():
     fx = d[..., 5] - d[..., 4]
     print("fixup (exit - loop end) p10/p50/p90/max: %.2f/%.2f/%.2f/%.2f" % (
         np.percentile(fx, 10), np.median(fx), np.percentile(fx, 90), fx.max()))
-    f0 = d[..., 7] - d[..., 4]
-    print("  loop end -> fixup start p10/p50/p90/max: %.2f/%.2f/%.2f/%.2f" % (
-        np.percentile(f0, 10), np.median(f0), np.percentile(f0, 90), f0.max()))
+    for code, name in ((0, "no open slice"), (1, "fast path"), (2, "published, not last"),
+                       (3, "published + collected"), (10, "head collected only"), (11, "fast + head"),
+                       (12, "published + head"), (13, "collected + head")):
+        m = path == code
+        if m.any():
+            print("  fixup %-22s %5.1f%% of warps: p50/p90/max %.2f/%.2f/%.2f us" % (
+                name, 100 * m.mean(), np.median(fx[m]), np.percentile(fx[m], 90), fx[m].max()))
+    if os.environ.get("GQSA_TRACE_PRO"):
+        v = d[..., 3] - d[..., 0]
+        print("  prologue: start -> tile loads issued p10/p50/p90 %.2f/%.2f/%.2f" % (
+            np.percentile(v, 10), np.median(v), np.percentile(v, 90)))
+        v = d[..., 1] - d[..., 3]
+        print("  prologue: tile loads issued -> stamp 1 p10/p50/p90 %.2f/%.2f/%.2f" % (
+            np.percentile(v, 10), np.median(v), np.percentile(v, 90)))
+    if os.environ.get("GQSA_TRACE_FIX"):
+        m = path == 1
+        for k, name in ((3, "ready checked"), (6, "all_sync passed"), (2, "rows stored"), (5, "exit")):
+            v = (d[..., k] - d[..., 4])[m]
+            print("  fast path: loop end -> %-16s p50/p90 %.2f/%.2f" % (name, np.median(v), np.percentile(v, 90)))
     prev_exit = T[:-1, :, 5].max(axis=1)
     rel = T[1:, :, 1].min(axis=1) - prev_exit
     print("PDL release after previous step's last exit (µs):", " ".join(f"{v:.2f}" for v in rel[:5]))
