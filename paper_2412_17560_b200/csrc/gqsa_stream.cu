@@ -123,23 +123,43 @@ __device__ __forceinline__ int arrive(const Params& p, int w0, int lane) {
   if (lane == 0) old = (int)atomicAdd(p.cnt + w0, 1u);
   return old;
 }
+// The records of the first kRec participants of a slice split over warps
+// w0..w1 (w0's tail record, then head records), requested ahead of the
+// arrival so that the last arriver has them one round trip earlier.
+constexpr int kRec = 4;
+template <int B>
+struct Recs {
+  unsigned long long r[kRec][B];
+};
+template <int B>
+__device__ __forceinline__ Recs<B> request_records(const Params& p, int w0, int w1, int lane) {
+  Recs<B> q;
+#pragma unroll
+  for (int k = 0; k < kRec; ++k)
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+      q.r[k][b] = (w0 + k <= w1) ? ld_relaxed64(rec_ptr<B>(p, w0 + k, k == 0 ? 1 : 0, b, lane)) : 0ull;
+  return q;
+}
 // The last arriver of a slice split over warps w0..w1: add every
 // participant's record in warp order (w0's tail record, then the head records
 // of w0+1..w1), reset the flags and the counter, store the rows.  The spin
 // only waits for stores already issued (their writers arrived before us).
+// `q` holds the first kRec records as requested before the arrival (flag 0: reload).
 template <int B>
-__device__ __noinline__ void collect(const Params& p, const Item* items, int w0, int w1, int item, int row, int lane) {
+__device__ __noinline__ void collect(const Params& p, const Item* items, int w0, int w1, int item, int row, int lane,
+                                     Recs<B> q) {
   float v[B];
 #pragma unroll
   for (int b = 0; b < B; ++b) v[b] = 0.f;
-  constexpr int kBatch = 4;  // records requested per round trip
+  constexpr int kBatch = kRec;  // records requested per round trip
   for (int wb = w0; wb <= w1; wb += kBatch) {
 #pragma unroll
     for (int b = 0; b < B; ++b) {
       unsigned long long r[kBatch];
 #pragma unroll
       for (int k = 0; k < kBatch; ++k)
-        r[k] = (wb + k <= w1) ? ld_relaxed64(rec_ptr<B>(p, wb + k, wb + k == w0 ? 1 : 0, b, lane)) : 0ull;
+        r[k] = wb == w0 ? q.r[k][b] : (wb + k <= w1) ? ld_relaxed64(rec_ptr<B>(p, wb + k, 0, b, lane)) : 0ull;
 #pragma unroll
       for (int k = 0; k < kBatch; ++k) {
         if (wb + k > w1) break;
@@ -438,10 +458,11 @@ __global__ void __launch_bounds__(32 * warps_for(B), min_blocks_for(B)) gqsa_str
     if (!done) {
       const int which = foreign ? 0 : 1;  // middle participant: head record; first warp: tail record
       publish<B>(p, gw, which, acc, lane);
+      const Recs<B> q = request_records<B>(p, cw0, w1, lane);  // in flight with the arrival
       const int old = __shfl_sync(0xffffffffu, arrive(p, cw0, lane), 0);
       fix_path = 2;
       if (old == w1 - cw0) {
-        collect<B>(p, its, cw0, w1, ci, crow, lane);
+        collect<B>(p, its, cw0, w1, ci, crow, lane, q);
         fix_path = 3;
       }
     }
@@ -449,7 +470,7 @@ __global__ void __launch_bounds__(32 * warps_for(B), min_blocks_for(B)) gqsa_str
   if (h_pending) {
     const int old = __shfl_sync(0xffffffffu, h_old, 0);
     if (old == gw - h_w0) {
-      collect<B>(p, its, h_w0, gw, h_item, h_row, lane);
+      collect<B>(p, its, h_w0, gw, h_item, h_row, lane, request_records<B>(p, h_w0, gw, lane));
       fix_path += 10;
     }
   }

@@ -20,6 +20,11 @@ Value modes:
                     exact -> bit-exact parity).
   * ``onehot_safe`` realistic, but z rounded to a multiple of 1/128 with
                     |z| < 16 (y = W_hat[:, j] exact in fp32).
+  * ``extreme``     reading R6's full range (any finite fp16 z):
+                    uniform codes; s log-uniform over [2^-24, 1] (fp16
+                    subnormals included); z a mixture of uniform [-1000, 1000],
+                    integers in [-2^n, 2^(n+1)] (outside [0, 2^n-1] too) and
+                    tiny values of either sign (fp16 subnormals included).
 
 Masks (exactly floor(S * N*K/G) groups pruned):
   * ``uniform``      chosen uniformly without replacement over the layer;
@@ -139,6 +144,15 @@ def make_layer(seed: int, rows: int, cols: int, G: int = 16, bits: int = 4,
         z = np.rint(rng.uniform(0.3, 0.7, size=nnzg) * qmax) + rng.uniform(-0.5, 0.5, size=nnzg)
         if mode == "onehot_safe":
             z = np.clip(np.rint(z * 128.0) / 128.0, -15.9921875, 15.9921875)
+    elif mode == "extreme":
+        for g0 in range(0, nnzg, chunk):
+            m = min(chunk, nnzg - g0)
+            packed.append(pack_bits(rng.integers(0, qmax + 1, size=(m, G), dtype=np.uint8), bits))
+        s = 2.0 ** rng.uniform(-24.0, 0.0, size=nnzg)
+        kind = rng.integers(0, 3, size=nnzg)
+        z = np.where(kind == 0, rng.uniform(-1000.0, 1000.0, size=nnzg),
+                     np.where(kind == 1, rng.integers(-(qmax + 1), 2 * (qmax + 1) + 1, size=nnzg).astype(np.float64),
+                              rng.choice([-1.0, 1.0], size=nnzg) * 2.0 ** rng.uniform(-24.0, -10.0, size=nnzg)))
     elif mode == "exact_int":
         for g0 in range(0, nnzg, chunk):
             m = min(chunk, nnzg - g0)
@@ -155,7 +169,10 @@ def make_x(seed: int, batch: int, cols: int, mode: str = "realistic") -> np.ndar
     """Activations as fp16 bit patterns, shape [batch][cols] (uint16).
 
     realistic: N(0,1) with 0.5 % of channels scaled x20 (activation outliers);
-    exact_int: integers in [-4, 4];  onehot: row b is e_{j_b}.
+    exact_int: integers in [-4, 4];  onehot: row b is e_{j_b};
+    extreme: N(0,1) with 1 % of entries of magnitude 10^U(3, 4.8) (up to the
+    fp16 maximum 65504), 1 % fp16 subnormals/tiny (2^U(-24, -14)) and 1 %
+    exact zeros, signs random.
     """
     rng = np.random.default_rng(seed)
     if mode == "realistic":
@@ -165,6 +182,13 @@ def make_x(seed: int, batch: int, cols: int, mode: str = "realistic") -> np.ndar
         x[:, ch] *= 20.0
     elif mode == "exact_int":
         x = rng.integers(-4, 5, size=(batch, cols)).astype(np.float64)
+    elif mode == "extreme":
+        x = rng.normal(0.0, 1.0, size=(batch, cols))
+        u = rng.uniform(size=(batch, cols))
+        sign = rng.choice([-1.0, 1.0], size=(batch, cols))
+        x = np.where(u < 0.01, sign * np.minimum(10.0 ** rng.uniform(3.0, 4.8, size=(batch, cols)), 65504.0), x)
+        x = np.where((u >= 0.01) & (u < 0.02), sign * 2.0 ** rng.uniform(-24.0, -14.0, size=(batch, cols)), x)
+        x = np.where((u >= 0.02) & (u < 0.03), 0.0, x)
     elif mode == "onehot":
         x = np.zeros((batch, cols))
         x[np.arange(batch), rng.integers(0, cols, size=batch)] = 1.0

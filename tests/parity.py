@@ -17,14 +17,22 @@ def _fold_offsets(bits: int, G: int) -> np.ndarray:
 
 
 FOLD_REL = 2.0 ** -23 / 1e-5  # fold error: 2 roundings (2^-24) of o_t|x_t| per group, in G2 units
+# G2x: the worst-case recursive-summation bound of the folded
+# chains, for inputs whose |x| spans the fp16 range.  A W4 group's two FHFMA
+# chains each add G/2 = 8 exact products, every addition rounding at most
+# 2^-24 |partial| <= 2^-24 F_group, plus the fold and scale roundings: (8 + 2)
+# roundings of F per group (W2: 4 chains of 4 adds; W8: 2 chains of 8).
+FOLD_REL_WORST = 10 * 2.0 ** -24 / 1e-5
 
 
-def abs_bound(bsr: dict, x_bits: np.ndarray, rows=None) -> np.ndarray:
-    """G2's scale per row (and batch): A_r + FOLD_REL * F_r with
+def abs_bound(bsr: dict, x_bits: np.ndarray, rows=None, fold_rel: float = FOLD_REL) -> np.ndarray:
+    """G2's scale per row (and batch): A_r + fold_rel * F_r with
     A_r = sum_g |s_g| (sum_t |q_t x_t| + |z_g| sum_t |x_t|), the magnitude of
     the terms the fp32 kernel adds, and F_r = sum_g |s_g| sum_t o_t |x_t|, the
     magnitude of the fold offsets o_t it carries and removes once per group
-    (so |dy_r| <= 1e-5 A_r + 2^-23 F_r).  Returns [B][len(rows)]."""
+    (so |dy_r| <= 1e-5 A_r + 2^-23 F_r).  fold_rel =
+    FOLD_REL_WORST gives G2x, the worst-case bound for extreme |x|.
+    Returns [B][len(rows)]."""
     G, n = int(bsr["group_size"]), int(bsr["bits"])
     X = np.asarray(x_bits).view(np.float16).astype(np.float64)
     if X.ndim == 1:
@@ -49,7 +57,7 @@ def abs_bound(bsr: dict, x_bits: np.ndarray, rows=None) -> np.ndarray:
         for b in range(X.shape[0]):
             ax = np.abs(X[b][idx])
             out[b, j] = np.sum(s[g0:g1] * ((q * ax).sum(1) + z[g0:g1] * ax.sum(1)))
-            out[b, j] += FOLD_REL * np.sum(s[g0:g1] * (ax * off).sum(1))
+            out[b, j] += fold_rel * np.sum(s[g0:g1] * (ax * off).sum(1))
     return out
 
 
