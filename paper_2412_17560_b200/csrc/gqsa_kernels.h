@@ -35,11 +35,15 @@ constexpr int kL2Pf = GQSA_L2PF;
 // flight (a read-only stream of the same tiles reaches 4.9 / 5.3 / 5.5 TB/s
 // with 16 / 24 / 32 warps per SM on the 59 MB bench step,
 // profiles/r02_stream_bench.jsonl); the register budget (<= 65536 / 32W per
-// thread, no spills) sets the count: 20 at batch 1, 16 at batch 2, 8 above.
+// thread, no spills) sets the count: 20 at batch 1, 16 above (batch 8 on
+// 14336x4096: 8 warps 46 us, 16 warps 39 us).
 #ifndef GQSA_WARPS_SMALL
 #define GQSA_WARPS_SMALL 20
 #endif
-__host__ __device__ constexpr int warps_for(int B) { return B == 1 ? GQSA_WARPS_SMALL : B == 2 ? 16 : 8; }
+#ifndef GQSA_WARPS_LARGE
+#define GQSA_WARPS_LARGE 16
+#endif
+__host__ __device__ constexpr int warps_for(int B) { return B == 1 ? GQSA_WARPS_SMALL : B == 2 ? 16 : GQSA_WARPS_LARGE; }
 // Resident CTAs per SM the kernel is compiled for (launch bounds): 2 lets the
 // next launch on the stream be resident during this one's tail (PDL).
 #ifndef GQSA_MINB

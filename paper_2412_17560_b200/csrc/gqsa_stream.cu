@@ -500,9 +500,8 @@ const void* kernel_ptr() {
   }
 
 const void* select_kernel(int bits, int G, int B) {
-#ifdef GQSA_FAST_BUILD  // experiments: W4, G = 16, B <= 2 only
-  if (bits == 4 && G == kGroup && B == 1) return kernel_ptr<4, 1, 16>();
-  if (bits == 4 && G == kGroup && B == 2) return kernel_ptr<4, 2, 16>();
+#ifdef GQSA_FAST_BUILD  // experiments: W4, G = 16 only
+  if (bits == 4 && G == kGroup) { GQSA_KSEL(4, 16) }
   return nullptr;
 #endif
   if (G == 8 && bits == 4) { GQSA_KSEL(4, 8) }
