@@ -7,7 +7,7 @@ CUFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3,-Wall -Xptxas -
 
 $(LIB): $(wildcard $(SRC)/*.cu $(SRC)/*.cuh $(SRC)/*.cpp $(SRC)/*.h) include/gqsa.h
 	@mkdir -p $(dir $(LIB))
-	$(NVCC) $(CUFLAGS) -shared -o $@ $(SRC)/gqsa_stream.cu $(SRC)/gqsa_capi.cu $(SRC)/gqsa_pack.cpp $(SRC)/gqsa_compress.cpp 2> $(dir $(LIB))/ptxas.log || (cat $(dir $(LIB))/ptxas.log; false)
+	$(NVCC) $(CUFLAGS) -shared -o $@ $(SRC)/gqsa_stream.cu $(SRC)/gqsa_tc.cu $(SRC)/gqsa_capi.cu $(SRC)/gqsa_pack.cpp $(SRC)/gqsa_pack_tc.cpp $(SRC)/gqsa_compress.cpp 2> $(dir $(LIB))/ptxas.log || (cat $(dir $(LIB))/ptxas.log; false)
 
 clean:
 	rm -f $(LIB)

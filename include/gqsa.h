@@ -142,6 +142,28 @@ int gqsa_pack_size(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_end, si
 int gqsa_pack(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_end,
               void* blob, size_t blob_bytes, gqsa_desc_t* desc);
 
+/*
+ * gqsa_pack_size_ex / gqsa_pack_ex: as gqsa_pack_size / gqsa_pack with a
+ * choice of device layout:
+ *   GQSA_LAYOUT_STREAM (gqsa_pack's): the sliced-ELL tile stream for the
+ *     CUDA-core kernel -- the fastest at batch 1-2, every bit width and G.
+ *   GQSA_LAYOUT_TC: W4, G = 16 only: rows in blocks of 16, each block's kept
+ *     group columns stored as 16 x 16 code matrices (rows that do not keep a
+ *     column: zero codes, s = z = 0) in tensor-core fragment order, for the
+ *     batch 2-8 GEMM on mma.sync ("TensorCores (MMA) or
+ *     CudaCores (FMA)").  It reads ~2x the bytes of the BSR at 50 % group
+ *     sparsity but replaces 16 FMA per weight and batch column by one MMA per
+ *     16 x 16 x 8 block.  gqsa_gemv / gqsa_gemm_* accept either blob.
+ * GQSA_ERR_SHAPE for another layout value, GQSA_ERR_UNSUPPORTED for a TC
+ * layout of bits != 4 or G != 16.
+ */
+#define GQSA_LAYOUT_STREAM 0
+#define GQSA_LAYOUT_TC 1
+int gqsa_pack_size_ex(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_end, int32_t layout,
+                      size_t* blob_bytes);
+int gqsa_pack_ex(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_end, int32_t layout,
+                 void* blob, size_t blob_bytes, gqsa_desc_t* desc);
+
 /* Parse and bounds-check a (host) blob header: magic, version, section
  * offsets, sizes.  GQSA_ERR_VALIDATION on any inconsistency. */
 int gqsa_read_desc(const void* blob, size_t blob_bytes, gqsa_desc_t* desc);

@@ -174,3 +174,100 @@ def pack_reference(bsr: dict, row_begin: int = 0, row_end=None) -> bytes:
                     struct.pack_into("<H", out, off_col, field)
             t += 1
     return bytes(out)
+
+
+# ---------------------------------------------------------------- LAYOUT-TC
+TC_ROWS = 16
+TC_ITEMS = 4
+TC_TILE = 768
+FLAG_TC = 2
+
+
+def pack_reference_tc(bsr: dict, row_begin: int = 0, row_end=None) -> bytes:
+    """LAYOUT-TC, written from its description: rows in
+    blocks of 16; a block's items are the group columns kept by any of its
+    rows, ascending (a block with none gets one padding item at column K/16);
+    tiles of 4 items: codes at lane * 16 + item * 4 (lane L's 32-bit word,
+    nibble j = A[(L >> 2) + 8 (j & 1)][2 (L & 3) + 8 ((j >> 1) & 1) + (j >> 2)]),
+    then (s, z) of rows g and g + 8 at 512 + g * 32 + item * 8; side arrays:
+    item columns u16 [tile][4], first tile of each block, block of each tile."""
+    row_end = int(bsr["rows"]) if row_end is None else int(row_end)
+    G, n, K = int(bsr["group_size"]), int(bsr["bits"]), int(bsr["cols"])
+    assert G == 16 and n == 4
+    ri_all = [int(v) for v in np.asarray(bsr["row_index"])]
+    g0 = ri_all[row_begin]
+    rows = row_end - row_begin
+    nnzg = ri_all[row_end] - g0
+    gcols = np.asarray(bsr["group_cols"], np.int64)
+    codes = np.asarray(bsr["codes"], np.uint8)
+    sc = np.asarray(bsr["scales_f16"], np.uint16)
+    zr = np.asarray(bsr["zeros_f16"], np.uint16)
+    nb = -(-rows // TC_ROWS)
+    pad_col = K // G
+    block_cols, empty = [], []
+    for blk in range(nb):
+        cs = set()
+        for r in range(blk * TC_ROWS, min(rows, (blk + 1) * TC_ROWS)):
+            a, b = ri_all[row_begin + r], ri_all[row_begin + r + 1]
+            if a == b:
+                empty.append(r)
+            cs.update(int(c) for c in gcols[a:b])
+        block_cols.append(sorted(cs) if cs else [pad_col])
+    block_tiles = [-(-len(c) // TC_ITEMS) for c in block_cols]
+    first = [sum(block_tiles[:b]) for b in range(nb + 1)]
+    num_tiles = first[nb]
+    off_ri = HDR
+    off_tc = _align(off_ri + 4 * (rows + 1))
+    off_em = _align(off_tc + 2 * TC_ITEMS * num_tiles)
+    off_bt0 = _align(off_em + 4 * len(empty))
+    off_tb = _align(off_bt0 + 4 * (nb + 1))
+    off_tiles = _align(off_tb + 4 * num_tiles)
+    total = _align(off_tiles + num_tiles * TC_TILE)
+    out = bytearray(total)
+    struct.pack_into("<IIiiiiqiiiiiiiiiiQQQQQQQ", out, 0,
+                     MAGIC, VERSION, rows, K, G, n, nnzg, TC_ITEMS * TC_ROWS, num_tiles, rows - len(empty),
+                     len(empty), TC_TILE, FLAG_TC | (1 << 8), row_begin, row_end, nb, 0,
+                     off_ri, off_tc, off_em, off_bt0, off_tb, off_tiles, total)
+    struct.pack_into(f"<{rows + 1}i", out, off_ri, *[v - g0 for v in ri_all[row_begin:row_end + 1]])
+    if empty:
+        struct.pack_into(f"<{len(empty)}i", out, off_em, *empty)
+    struct.pack_into(f"<{nb + 1}i", out, off_bt0, *first)
+    if num_tiles:
+        struct.pack_into(f"<{num_tiles}i", out, off_tb, *[b for b in range(nb) for _ in range(block_tiles[b])])
+    for blk in range(nb):
+        cols = block_cols[blk]
+        # (block row, column) -> group index
+        where = {}
+        for rr in range(TC_ROWS):
+            r = blk * TC_ROWS + rr
+            if r >= rows:
+                break
+            for g in range(ri_all[row_begin + r], ri_all[row_begin + r + 1]):
+                where[(rr, int(gcols[g]))] = g
+        for k in range(block_tiles[blk]):
+            t = first[blk] + k
+            base = off_tiles + t * TC_TILE
+            for u in range(TC_ITEMS):
+                item = k * TC_ITEMS + u
+                col = cols[item] if item < len(cols) else pad_col
+                struct.pack_into("<H", out, off_tc + 2 * (t * TC_ITEMS + u), col)
+                if item >= len(cols):
+                    continue
+                for lane in range(LANES):
+                    w = 0
+                    for j in range(8):
+                        rr = (lane >> 2) + 8 * (j & 1)
+                        kk = 2 * (lane & 3) + 8 * ((j >> 1) & 1) + (j >> 2)
+                        g = where.get((rr, col))
+                        if g is None:
+                            continue
+                        e = g * G + kk
+                        w |= ((int(codes[e // 2]) >> (4 * (e % 2))) & 0xF) << (4 * j)
+                    struct.pack_into("<I", out, base + lane * 16 + u * 4, w)
+                for gp in range(8):
+                    vals = []
+                    for h in range(2):
+                        g = where.get((gp + 8 * h, col))
+                        vals += [int(sc[g]), int(zr[g])] if g is not None else [0, 0]
+                    struct.pack_into("<4H", out, base + 512 + gp * 32 + u * 8, *vals)
+    return bytes(out)

@@ -46,7 +46,13 @@ int current_sms() {
 
 bool lanes_per_row_ok(uint32_t s) { return s >= 1 && s <= 32 && (s & (s - 1)) == 0; }
 
+bool is_tc(const gqsa_desc_t* d) { return ((uint32_t)d->flags & kFlagTC) != 0; }
+
 bool desc_ok(const gqsa_desc_t* d) {
+  if (d && is_tc(d))
+    return d->magic == kMagic && d->version == (uint32_t)kVersion && d->bits == 4 && d->group_size == kGroup &&
+           d->tile_bytes == kTcTileBytes && d->rows >= 0 && d->cols > 0 && d->cols % kGroup == 0 &&
+           d->cols <= kMaxCols && d->num_tiles >= 0 && d->num_slices == (d->rows + kTcRows - 1) / kTcRows;
   return d && d->magic == kMagic && d->version == (uint32_t)kVersion && group_supported(d->bits, d->group_size) &&
          d->tile_groups == kTileGroups && d->rows >= 0 && d->cols > 0 && d->cols % d->group_size == 0 &&
          d->cols <= kMaxCols && d->num_tiles >= 0 && d->num_slices >= 0 &&
@@ -285,13 +291,87 @@ int run_grouped(const gqsa_gemm_item_t* items, int n, int B, const gqsa_options_
   return GQSA_OK;
 }
 
+// ---- LAYOUT-TC (small-batch tensor-core GEMM, gqsa_tc.cu)
+size_t tc_smem(const gqsa_desc_t* d, int Bc) {
+  const size_t xrow = 2 * (size_t)d->cols + 32;
+  return (size_t)Bc * xrow + ((size_t)d->cols / kGroup + 1) * 32;
+}
+
+int run_tc(const gqsa_desc_t* d, const void* d_blob, const uint16_t* d_X, int B, int64_t ldx, void* d_Y, int64_t ldy,
+           const float* d_bias, const gqsa_options_t& o, void* d_ws, size_t ws_bytes, void* stream) {
+  if (!d_ws || !aligned(d_ws, 256)) return GQSA_ERR_BUFFER;
+  if (ws_bytes < ws_bytes_for(std::max(B, 4))) return GQSA_ERR_BUFFER;
+  const int sms = current_sms();
+  if (sms <= 0) return GQSA_ERR_CUDA;
+  int Bc = B;  // largest balanced batch chunk whose x fits (each chunk re-streams the weights)
+  for (; Bc >= 1; --Bc) {
+    const int launches = (B + Bc - 1) / Bc, Bb = (B + launches - 1) / launches;
+    if (tc_smem(d, Bb) <= (size_t)kMaxDynSmem) {
+      Bc = Bb;
+      break;
+    }
+  }
+  if (Bc < 1) return GQSA_ERR_UNSUPPORTED;
+  const size_t es = o.out_f16 ? 2 : 4;
+  const uint8_t* blob = static_cast<const uint8_t*>(d_blob);
+  for (int b0 = 0; b0 < B; b0 += Bc) {
+    const int nb = std::min(Bc, B - b0);
+    const void* fn = select_tc_kernel(nb);
+    if (!fn) return GQSA_ERR_UNSUPPORTED;
+    int st = set_attrs(fn);
+    if (st) return st;
+    TcParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.tiles = blob + d->off_tiles;
+    p.tile_cols = reinterpret_cast<const uint16_t*>(blob + d->off_perm);
+    p.block_tile0 = reinterpret_cast<const int32_t*>(blob + d->off_slice_tile0);
+    p.tile_block = reinterpret_cast<const int32_t*>(blob + d->off_tile_slice);
+    p.X = d_X + (int64_t)b0 * ldx;
+    p.Y = static_cast<uint8_t*>(d_Y) + (size_t)b0 * ldy * es;
+    p.bias = d_bias;
+    p.ldx = ldx;
+    p.ldy = ldy;
+    p.rows = d->rows;
+    p.cols = d->cols;
+    p.num_tiles = d->num_tiles;
+    p.nb = d->num_slices;
+    const int warps = std::min(sms * kTcWarps, kMaxWarpsBound);
+    p.active_warps = std::min(d->num_tiles, warps);
+    p.part_q = p.active_warps ? d->num_tiles / p.active_warps : 0;
+    p.part_r = p.active_warps ? d->num_tiles % p.active_warps : 0;
+    p.slice_k = o.partition == GQSA_PARTITION_SLICE_K ? 1 : 0;
+    p.out_f16 = o.out_f16;
+    p.x_ready = o.x_ready;
+    p.xrow = 2 * d->cols + 32;
+    uint8_t* ws = static_cast<uint8_t*>(d_ws);
+    p.cnt = reinterpret_cast<uint32_t*>(ws + 256);
+    p.rec = reinterpret_cast<unsigned long long*>(ws + 256 + (size_t)kMaxWarpsBound * 4);
+    p.trace = (g_trace && g_trace_bytes >= (size_t)p.active_warps * 64) ? g_trace : nullptr;
+    if (d->rows == 0 || p.active_warps == 0) continue;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((p.active_warps + kTcWarps - 1) / kTcWarps);
+    cfg.blockDim = dim3(32 * kTcWarps);
+    cfg.dynamicSmemBytes = tc_smem(d, nb);
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    void* args[] = {&p};
+    if (cudaLaunchKernelExC(&cfg, fn, args) != cudaSuccess) return GQSA_ERR_CUDA;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  return GQSA_OK;
+}
+
 }  // namespace
 
 extern "C" int gqsa_workspace_size(const gqsa_desc_t* desc, int32_t batch, size_t* bytes) {
   if (!desc || !bytes) return GQSA_ERR_BUFFER;
   if (!desc_ok(desc)) return GQSA_ERR_VALIDATION;
   if (batch < 1 || batch > kMaxBatch) return GQSA_ERR_SHAPE;
-  *bytes = ws_bytes_for(batch);
+  *bytes = ws_bytes_for(is_tc(desc) ? std::max(batch, 4) : batch);  // LAYOUT-TC: 4 values per lane
   return GQSA_OK;
 }
 
@@ -299,6 +379,27 @@ extern "C" int gqsa_launch_plan(const gqsa_desc_t* desc, int32_t B, gqsa_plan_t*
   if (!desc || !plan) return GQSA_ERR_BUFFER;
   if (!desc_ok(desc)) return GQSA_ERR_VALIDATION;
   if (B < 1 || B > kMaxBatch) return GQSA_ERR_SHAPE;
+  if (is_tc(desc)) {  // LAYOUT-TC: 16 warps per CTA, one CTA per SM, x of the batch chunk in shared memory
+    const int sms = current_sms();
+    if (sms <= 0) return GQSA_ERR_CUDA;
+    int Bc = B;
+    for (; Bc > 1 && tc_smem(desc, (B + ((B + Bc - 1) / Bc) - 1) / ((B + Bc - 1) / Bc)) > (size_t)kMaxDynSmem; --Bc) {
+    }
+    const int launches = (B + Bc - 1) / Bc;
+    Bc = (B + launches - 1) / launches;
+    std::memset(plan, 0, sizeof(*plan));
+    plan->warps_per_cta = kTcWarps;
+    plan->active_warps = std::min(desc->num_tiles, std::min(sms * kTcWarps, kMaxWarpsBound));
+    plan->grid = (plan->active_warps + kTcWarps - 1) / kTcWarps;
+    plan->num_tiles = desc->num_tiles;
+    plan->smem_bytes = (int32_t)tc_smem(desc, Bc);
+    plan->x_in_smem = 1;
+    plan->stages = kBufs;
+    plan->ctas_per_sm = 1;
+    plan->batch_per_launch = Bc;
+    plan->launches = launches;
+    return GQSA_OK;
+  }
   Launch L;
   int Bc = B;
   const int st = batch_chunk(&desc, 1, B, &Bc, &L);
@@ -328,7 +429,8 @@ extern "C" int gqsa_gemm_grouped(const gqsa_gemm_item_t* items, int32_t n, int32
   if (n < 1 || n > kMaxItems) return GQSA_ERR_SHAPE;
   for (int j = 0; j < n; ++j) {
     if ((st = check_item(items[j], B, o.out_f16))) return st;
-    if (items[j].desc->bits != items[0].desc->bits || items[j].desc->group_size != items[0].desc->group_size)
+    if (items[j].desc->bits != items[0].desc->bits || items[j].desc->group_size != items[0].desc->group_size ||
+        is_tc(items[j].desc))  // LAYOUT-TC blobs run through gqsa_gemm_ex / gqsa_gemm_smallbatch
       return GQSA_ERR_UNSUPPORTED;
   }
   return run_grouped(items, n, B, o, d_ws, ws_bytes, stream);
@@ -342,6 +444,7 @@ extern "C" int gqsa_gemm_ex(const gqsa_desc_t* desc, const void* d_blob, const u
   if (st) return st;
   const gqsa_gemm_item_t it{desc, d_blob, d_X, ldx, d_Y, ldy, d_bias};
   if ((st = check_item(it, B, o.out_f16))) return st;
+  if (is_tc(desc)) return run_tc(desc, d_blob, d_X, B, ldx, d_Y, ldy, d_bias, o, d_ws, ws_bytes, stream);
   return run_grouped(&it, 1, B, o, d_ws, ws_bytes, stream);
 }
 
@@ -351,6 +454,7 @@ extern "C" int gqsa_gemm_allgather(const gqsa_desc_t* desc, const void* d_blob, 
                                    size_t ws_bytes, void* stream) {
   if (!desc || !d_blob || !d_X || !d_peer_Y || !d_ws) return GQSA_ERR_BUFFER;
   if (!desc_ok(desc)) return GQSA_ERR_VALIDATION;
+  if (is_tc(desc)) return GQSA_ERR_UNSUPPORTED;  // the fused epilogue is the CUDA-core kernel's
   if (n_peers < 1 || n_peers > kMaxPeers || B < 1 || B > kMaxBatch || (out_f16 != 0 && out_f16 != 1))
     return GQSA_ERR_SHAPE;
   if (row_offset < 0 || ldy < (int64_t)row_offset + desc->rows || ldx < desc->cols || ldx % 8) return GQSA_ERR_SHAPE;

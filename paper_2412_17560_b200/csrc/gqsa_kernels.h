@@ -99,4 +99,26 @@ __host__ __device__ constexpr int pq_row_bytes(int B, int G, int cols) {
 
 const void* select_kernel(int bits, int G, int B);
 
+// LAYOUT-TC kernel (gqsa_tc.cu): one GEMM over 16-row blocks on mma.sync.
+constexpr int kTcWarps = 16;
+struct TcParams {
+  const uint8_t* tiles;         // blob + off_tiles (768-B tiles of 4 items)
+  const uint16_t* tile_cols;    // [num_tiles][4] item columns
+  const int32_t* block_tile0;   // [nb + 1]
+  const int32_t* tile_block;    // [num_tiles]
+  const uint16_t* X;            // [B][ldx] fp16
+  void* Y;                      // [B][ldy] fp32 (fp16 when out_f16)
+  const float* bias;            // [rows] or null
+  int64_t ldx, ldy;
+  int32_t rows, cols, num_tiles, nb;
+  int32_t active_warps, part_q, part_r;
+  int32_t slice_k, out_f16, x_ready;
+  int32_t xrow;                 // shared bytes per staged x row (2K + 32: zero chunk for padding items)
+  int32_t pad_;
+  uint32_t* cnt;                // [active_warps] fix-up arrival counters (zero between launches)
+  unsigned long long* rec;      // [active_warps][2][4][32] fix-up records
+  uint64_t* trace;
+};
+const void* select_tc_kernel(int B);
+
 }  // namespace gqsa

@@ -84,6 +84,24 @@ __host__ __device__ constexpr uint32_t lane_rot(int G, int lane) {
 // Column field of a padding entry: the zero block after the activations.
 __host__ __device__ constexpr uint32_t pad_field(int cols) { return 2u * (uint32_t)cols; }
 
+// LAYOUT-TC (the small-batch tensor-core layout, W4 G16):
+// rows in blocks of 16 (the mma M dimension); a block's ITEMS are the group
+// columns kept by any of its rows, ascending, each the 16 x 16 code matrix of
+// the block at that column (zeros and s = 0 for rows that do not keep it) in
+// mma.m16n8k16 A-fragment order, so a lane loads its fragment with one 32-bit
+// word; tiles of 4 items: codes [lane][item] 4 B (512 B) + (s, z) [row pair
+// g, g+8][item] 8 B (256 B).  Item columns live in a side array (u16 [tile][4]).
+constexpr uint32_t kFlagTC = 2u;   // flags bit 1: the blob is LAYOUT-TC
+constexpr int kTcRows = 16;        // rows per block
+constexpr int kTcItems = 4;        // items per tile
+constexpr int kTcTileBytes = 768;  // 4 x 32 lanes x 4 B codes + 8 row pairs x 4 items x 8 B (s, z)
+// Nibble j (bits 4j..4j+3) of lane L's word for one item holds A[row][k],
+// row = (L >> 2) + 8 * (j & 1), k = 2 (L & 3) + ((j >> 1) & 1) * 8 + (j >> 2):
+// LOP3(w >> 4m, 0x000F000F) for m = 0..3 gives the fragment registers
+// a_m = half2(1024 + A[row_m][k_m], 1024 + A[row_m][k_m + 1]).
+__host__ __device__ constexpr int tc_nib_row(int lane, int j) { return (lane >> 2) + 8 * (j & 1); }
+__host__ __device__ constexpr int tc_nib_k(int lane, int j) { return 2 * (lane & 3) + ((j >> 1) & 1) * 8 + (j >> 2); }
+
 constexpr int kTargetSlots = 64;  // slots per lane of the longest slice (16 tiles)
 
 // Target slots per lane for a layer of nnzg kept groups: short slices when the

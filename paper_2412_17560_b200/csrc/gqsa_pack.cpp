@@ -26,6 +26,7 @@
 
 #include "../../include/gqsa.h"
 #include "gqsa_layout.h"
+#include "gqsa_pack_internal.h"
 
 using namespace gqsa;
 
@@ -137,24 +138,37 @@ void fill_desc(const BlobHeader& h, gqsa_desc_t* d) {
 
 }  // namespace
 
-extern "C" int gqsa_pack_size(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_end,
-                              size_t* blob_bytes) {
+extern "C" int gqsa_pack_size_ex(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_end, int32_t layout,
+                                 size_t* blob_bytes) {
   int st = check_bsr_header(bsr);
   if (st) return st;
   if (!blob_bytes) return GQSA_ERR_BUFFER;
   if (row_begin < 0 || row_end < row_begin || row_end > bsr->rows) return GQSA_ERR_SHAPE;
+  if (layout != GQSA_LAYOUT_STREAM && layout != GQSA_LAYOUT_TC) return GQSA_ERR_SHAPE;
   if ((st = validate(bsr, row_begin, row_end))) return st;
+  if (layout == GQSA_LAYOUT_TC) return pack_tc_size(bsr, row_begin, row_end, blob_bytes);
   *blob_bytes = (size_t)offsets(make_slices(bsr, row_begin, row_end), bsr->bits, bsr->group_size).total;
   return GQSA_OK;
 }
 
+extern "C" int gqsa_pack_size(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_end, size_t* blob_bytes) {
+  return gqsa_pack_size_ex(bsr, row_begin, row_end, GQSA_LAYOUT_STREAM, blob_bytes);
+}
+
 extern "C" int gqsa_pack(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_end, void* blob,
                          size_t blob_bytes, gqsa_desc_t* desc) {
+  return gqsa_pack_ex(bsr, row_begin, row_end, GQSA_LAYOUT_STREAM, blob, blob_bytes, desc);
+}
+
+extern "C" int gqsa_pack_ex(const gqsa_bsr_t* bsr, int32_t row_begin, int32_t row_end, int32_t layout, void* blob,
+                            size_t blob_bytes, gqsa_desc_t* desc) {
   int st = check_bsr_header(bsr);
   if (st) return st;
   if (!blob) return GQSA_ERR_BUFFER;
   if (row_begin < 0 || row_end < row_begin || row_end > bsr->rows) return GQSA_ERR_SHAPE;
+  if (layout != GQSA_LAYOUT_STREAM && layout != GQSA_LAYOUT_TC) return GQSA_ERR_SHAPE;
   if ((st = validate(bsr, row_begin, row_end))) return st;
+  if (layout == GQSA_LAYOUT_TC) return pack_tc(bsr, row_begin, row_end, blob, blob_bytes, desc);
   const Slices s = make_slices(bsr, row_begin, row_end);
   const Offsets o = offsets(s, bsr->bits, bsr->group_size);
   if (blob_bytes < o.total) return GQSA_ERR_BUFFER;
@@ -290,6 +304,15 @@ extern "C" int gqsa_read_desc(const void* blob, size_t blob_bytes, gqsa_desc_t* 
   std::memcpy(&h, blob, sizeof(h));
   if (h.magic != kMagic || h.version != (uint32_t)kVersion) return GQSA_ERR_VALIDATION;
   if (!group_supported(h.bits, h.group_size)) return GQSA_ERR_UNSUPPORTED;
+  if (h.rows < 0 || h.cols <= 0 || h.cols % h.group_size || h.cols > kMaxCols || h.nnzg < 0 || h.num_tiles < 0)
+    return GQSA_ERR_VALIDATION;
+  if ((uint32_t)h.flags & kFlagTC) {  // LAYOUT-TC (the small-batch tensor-core layout)
+    if (h.blob_bytes > blob_bytes) return GQSA_ERR_BUFFER;
+    const int st = read_desc_tc(h, static_cast<const uint8_t*>(blob));
+    if (st) return st;
+    fill_desc(h, desc);
+    return GQSA_OK;
+  }
   if (h.tile_groups != kTileGroups || h.tile_bytes != tile_bytes(h.bits, h.group_size)) return GQSA_ERR_VALIDATION;
   if (h.rows < 0 || h.cols <= 0 || h.cols % h.group_size || h.cols > kMaxCols || h.nnzg < 0)
     return GQSA_ERR_VALIDATION;
@@ -332,6 +355,10 @@ extern "C" int gqsa_unpack(const void* blob, size_t blob_bytes, gqsa_bsr_t* out)
   uint16_t* o_s = const_cast<uint16_t*>(out->scales_f16);
   uint16_t* o_z = const_cast<uint16_t*>(out->zeros_f16);
   if (!o_ri || (d.nnzg > 0 && (!o_gc || !o_codes || !o_s || !o_z))) return GQSA_ERR_BUFFER;
+  if ((uint32_t)d.flags & kFlagTC) {
+    st = unpack_tc(d, static_cast<const uint8_t*>(blob), out);
+    return st ? st : validate(out, 0, d.rows);
+  }
 
   const uint8_t* b = static_cast<const uint8_t*>(blob);
   const int32_t* ri = reinterpret_cast<const int32_t*>(b + d.off_row_index);

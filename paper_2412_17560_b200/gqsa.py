@@ -83,7 +83,7 @@ class Options(ctypes.Structure):
 
 
 EXPORTS = (
-    "gqsa_pack_size", "gqsa_pack", "gqsa_read_desc", "gqsa_unpack", "gqsa_workspace_size",
+    "gqsa_pack_size", "gqsa_pack", "gqsa_pack_size_ex", "gqsa_pack_ex", "gqsa_read_desc", "gqsa_unpack", "gqsa_workspace_size",
     "gqsa_gemv", "gqsa_gemm_smallbatch", "gqsa_gemm_ex", "gqsa_gemm_grouped", "gqsa_hostio_stage_size",
     "gqsa_gemm_hostio",
     "gqsa_compress_nnzg", "gqsa_compress", "gqsa_multi_hostio_stage_size", "gqsa_gemm_multi_hostio",
@@ -107,6 +107,8 @@ def lib() -> ctypes.CDLL:
     PSZ = ctypes.POINTER(ctypes.c_size_t)
     L.gqsa_pack_size.argtypes = [ctypes.POINTER(BSR), I32, I32, PSZ]
     L.gqsa_pack.argtypes = [ctypes.POINTER(BSR), I32, I32, P, SZ, ctypes.POINTER(Desc)]
+    L.gqsa_pack_size_ex.argtypes = [ctypes.POINTER(BSR), I32, I32, I32, PSZ]
+    L.gqsa_pack_ex.argtypes = [ctypes.POINTER(BSR), I32, I32, I32, P, SZ, ctypes.POINTER(Desc)]
     L.gqsa_read_desc.argtypes = [P, SZ, ctypes.POINTER(Desc)]
     L.gqsa_unpack.argtypes = [P, SZ, ctypes.POINTER(BSR)]
     L.gqsa_workspace_size.argtypes = [ctypes.POINTER(Desc), I32, PSZ]
@@ -164,18 +166,23 @@ def _bsr_struct(bsr: dict, keep: list) -> BSR:
                _ptr(arrs["scales_f16"]), _ptr(arrs["zeros_f16"]))
 
 
-def pack(bsr: dict, row_begin: int = 0, row_end: Optional[int] = None):
-    """gqsa_pack: plain BSR (host) -> (blob uint8 ndarray, Desc)."""
+LAYOUT_STREAM = 0  # sliced-ELL tile stream, CUDA cores (batch 1-2, every width)
+LAYOUT_TC = 1      # 16-row blocks in tensor-core fragment order (W4 G16, batch 2-8)
+
+
+def pack(bsr: dict, row_begin: int = 0, row_end: Optional[int] = None, layout: int = LAYOUT_STREAM):
+    """gqsa_pack_ex: plain BSR (host) -> (blob uint8 ndarray, Desc)."""
     L = lib()
     keep: list = []
     b = _bsr_struct(bsr, keep)
     row_end = int(bsr["rows"]) if row_end is None else int(row_end)
     n = ctypes.c_size_t(0)
-    _check(L.gqsa_pack_size(ctypes.byref(b), int(row_begin), row_end, ctypes.byref(n)), "gqsa_pack_size")
+    _check(L.gqsa_pack_size_ex(ctypes.byref(b), int(row_begin), row_end, int(layout), ctypes.byref(n)),
+           "gqsa_pack_size_ex")
     blob = np.empty(n.value, dtype=np.uint8)
     d = Desc()
-    _check(L.gqsa_pack(ctypes.byref(b), int(row_begin), row_end, _ptr(blob), n.value, ctypes.byref(d)),
-           "gqsa_pack")
+    _check(L.gqsa_pack_ex(ctypes.byref(b), int(row_begin), row_end, int(layout), _ptr(blob), n.value,
+                          ctypes.byref(d)), "gqsa_pack_ex")
     return blob, d
 
 
@@ -381,10 +388,10 @@ class Layer:
 
     def __init__(self, bsr: Optional[dict] = None, blob: Optional[np.ndarray] = None,
                  row_begin: int = 0, row_end: Optional[int] = None, device=None,
-                 max_batch: int = 8):
+                 max_batch: int = 8, layout: int = LAYOUT_STREAM):
         import torch
         if blob is None:
-            blob, desc = pack(bsr, row_begin, row_end)
+            blob, desc = pack(bsr, row_begin, row_end, layout)
         else:
             desc = read_desc(blob)
         self.desc = desc

@@ -9,7 +9,8 @@ import subprocess
 import numpy as np
 import pytest
 
-from oracle.layout_reference import pack_reference
+from oracle import gqsa_oracle as O
+from oracle.layout_reference import pack_reference, pack_reference_tc
 from paper_2412_17560_b200 import gqsa, synth
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -238,3 +239,51 @@ def test_workspace_size_is_layer_independent():
     for B in (1, 2, 8):
         want = 256 + 4736 * 4 + 4736 * 2 * B * 32 * 8
         assert gqsa.workspace_size(d, B) == want == gqsa.workspace_size(d2, B)
+
+
+# ---------------------------------------------------------------- LAYOUT-TC
+@pytest.mark.parametrize("rows,cols,sp,mask,seed", [
+    (64, 256, 0.5, "uniform", 31), (37, 512, 0.5, "uniform", 32), (40, 96, 0.0, "uniform", 33),
+    (100, 1024, 0.9, "uniform", 34), (64, 512, 0.5, "skewed", 35), (5, 64, 0.5, "uniform", 36),
+    (48, 2048, 0.3, "row_balanced", 37), (16, 32736, 0.5, "uniform", 38)])
+def test_tc_layout_reference_bytes_and_roundtrip(rows, cols, sp, mask, seed):
+    """LAYOUT-TC: the C++ packer's bytes equal the independent Python
+    implementation of the DESIGN.md §5.2 description, unpack inverts it
+    exactly (empty blocks, ragged last block, S0 / S90, K at its maximum)."""
+    bsr = synth.make_layer(seed, rows, cols, bits=4, sparsity=sp, mask=mask)
+    blob, d = gqsa.pack(bsr, layout=gqsa.LAYOUT_TC)
+    assert d.flags & 2 and d.tile_bytes == 768 and d.num_slices == -(-rows // 16)
+    assert bytes(blob) == pack_reference_tc(bsr)
+    _eq_bsr(gqsa.unpack(blob), bsr)
+    lo, hi = rows // 3, rows - rows // 5  # a row shard, rebased
+    blob2, d2 = gqsa.pack(bsr, lo, hi, layout=gqsa.LAYOUT_TC)
+    assert bytes(blob2) == pack_reference_tc(bsr, lo, hi)
+    _eq_bsr(gqsa.unpack(blob2), synth.slice_rows(bsr, lo, hi))
+
+
+def test_tc_layout_fragment_words_and_errors():
+    """Spot-check the fragment order: lane L's word of an item holds, in
+    nibble j, A[(L >> 2) + 8 (j & 1)][2 (L & 3) + 8 ((j >> 1) & 1) + (j >> 2)]."""
+    bsr = synth.make_layer(41, 16, 64, bits=4, sparsity=0.0, mode="exact_int")
+    blob, d = gqsa.pack(bsr, layout=gqsa.LAYOUT_TC)
+    q = O.unpack_codes(bsr["codes"], bsr["nnzg"] * 16, 4).reshape(16, 4, 16)  # [row][col][k] (S0: all kept)
+    tile = blob[d.off_tiles:d.off_tiles + 768]
+    for lane in range(32):
+        w = int(tile[lane * 16:lane * 16 + 4].view(np.uint32)[0])  # item 0 = column 0
+        for j in range(8):
+            r, k = (lane >> 2) + 8 * (j & 1), 2 * (lane & 3) + 8 * ((j >> 1) & 1) + (j >> 2)
+            assert (w >> (4 * j)) & 0xF == q[r, 0, k]
+    with pytest.raises(gqsa.GQSAError) as e:
+        gqsa.pack(synth.make_layer(42, 16, 64, bits=2, sparsity=0.5), layout=gqsa.LAYOUT_TC)
+    assert e.value.status == -3
+    with pytest.raises(gqsa.GQSAError) as e:
+        gqsa.pack(bsr, layout=7)
+    assert e.value.status == -1
+    b = blob.copy()
+    b[d.off_tile_slice] ^= 1  # tile 0 claims block 1
+    with pytest.raises(gqsa.GQSAError):
+        gqsa.read_desc(b)
+    b = blob.copy()
+    b[d.off_perm:d.off_perm + 2] = np.frombuffer(np.uint16(9).tobytes(), np.uint8)  # column beyond K/16
+    with pytest.raises(gqsa.GQSAError):
+        gqsa.read_desc(b)

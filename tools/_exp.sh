@@ -1,2 +1,1 @@
-tools/ab.sh "L8 L12 L16" 1 --batch 8
-tools/ab.sh "L8 L12 L16" 1 --batch 4
+for B in 1 8; do timeout 300 python tools/trace_tc.py --batch $B 2>&1 | tail -6; done

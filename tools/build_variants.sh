@@ -10,7 +10,7 @@ while [ $# -ge 2 ]; do
   name=$1; flags=$2; shift 2
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 \
     --expt-relaxed-constexpr -DGQSA_FAST_BUILD $flags -Xptxas -v -shared -o $OUT/$name.so \
-    $SRC/gqsa_stream.cu $SRC/gqsa_capi.cu $SRC/gqsa_pack.cpp $SRC/gqsa_compress.cpp 2> $OUT/$name.ptxas &
+    $SRC/gqsa_stream.cu $SRC/gqsa_tc.cu $SRC/gqsa_capi.cu $SRC/gqsa_pack.cpp $SRC/gqsa_pack_tc.cpp $SRC/gqsa_compress.cpp 2> $OUT/$name.ptxas &
 done
 wait
 grep -h "Used" $OUT/*.ptxas | head -40

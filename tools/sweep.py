@@ -35,9 +35,9 @@ from paper_2412_17560_b200 import frontend, gqsa, synth  # noqa: E402
 SHAPES = [(4096, 4096), (14336, 4096), (4096, 14336)]
 
 
-def measure(bsr, B, partition=gqsa.PARTITION_STREAM_K, reps=20):
+def measure(bsr, B, partition=gqsa.PARTITION_STREAM_K, reps=20, layout=gqsa.LAYOUT_STREAM):
     rows, cols = int(bsr["rows"]), int(bsr["cols"])
-    blob, desc = gqsa.pack(bsr)
+    blob, desc = gqsa.pack(bsr, layout=layout)
     R = max(2, math.ceil(300e6 / blob.size))
     blobs = [torch.from_numpy(blob).cuda() for _ in range(R)]
     ws = torch.zeros(gqsa.workspace_size(desc, B), dtype=torch.uint8, device="cuda")
@@ -104,6 +104,24 @@ def main():
                     cells[B] = f"{r['us']:.2f} ({r['gbs']:.0f})"
                 lines.append(f"| W{bits}S{int(sp * 100)} | {rows}x{cols} | " +
                              " | ".join(cells.get(B, "-") for B in (1, 2, 4, 8)) + " |")
+        lines.append("")
+
+    if "T" in a.sections:  # small-batch tensor-core layout vs the CUDA-core stream
+        lines += ["## T. Small batch: LAYOUT-TC (mma.sync) vs the CUDA-core stream, W4S50", "",
+                  "GB/s over the counted (BSR) bytes; the TC blob reads about 2x them (blob MB column).", "",
+                  "| shape | layout | blob MB | B=1 µs | B=2 | B=4 | B=8 |", "|---|---|---|---|---|---|---|"]
+        for rows, cols in SHAPES:
+            bsr = synth.make_layer(synth.seed_for(f"llama3-8b/{rows}x{cols}/4/0.5/16/uniform"),
+                                   rows, cols, bits=4, sparsity=0.5)
+            for lay, name in ((gqsa.LAYOUT_STREAM, "stream"), (gqsa.LAYOUT_TC, "tc")):
+                cells, mb = {}, 0.0
+                for B in (1, 2, 4, 8):
+                    r = measure(bsr, B, layout=lay)
+                    r["layout"] = name
+                    emit("T", r)
+                    cells[B] = f"{r['us']:.2f}"
+                    mb = r["blob_bytes"] / 1e6
+                lines.append(f"| {rows}x{cols} | {name} | {mb:.1f} | " + " | ".join(cells[B] for B in (1, 2, 4, 8)) + " |")
         lines.append("")
 
     if "B" in a.sections:  # partition ablation
