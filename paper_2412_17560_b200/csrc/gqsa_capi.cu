@@ -292,9 +292,28 @@ int run_grouped(const gqsa_gemm_item_t* items, int n, int B, const gqsa_options_
 }
 
 // ---- LAYOUT-TC (small-batch tensor-core GEMM, gqsa_tc.cu)
-size_t tc_smem(const gqsa_desc_t* d, int Bc) {
+// Shared memory of one LAYOUT-TC launch over Bc batch rows: x (+ a zero chunk
+// per row) and, unless the column sums come from the mma (xq_mma), the X_c table.
+size_t tc_smem(const gqsa_desc_t* d, int Bc, bool xq_mma) {
   const size_t xrow = 2 * (size_t)d->cols + 32;
-  return (size_t)Bc * xrow + ((size_t)d->cols / kGroup + 1) * 32;
+  return (size_t)Bc * xrow + (xq_mma ? 0 : ((size_t)d->cols / kGroup + 1) * 32);
+}
+
+// Batch chunking of a LAYOUT-TC GEMM: the largest balanced chunk whose x fits,
+// preferring the X_c table; each extra launch re-streams the weights.
+bool tc_chunking(const gqsa_desc_t* d, int B, int* Bc_out, int* launches_out, bool* xq_mma_out) {
+  for (int Bc = B; Bc >= 1; --Bc) {
+    const int launches = (B + Bc - 1) / Bc, Bb = (B + launches - 1) / launches;
+    for (int xm = 0; xm < 2; ++xm) {
+      if (tc_smem(d, Bb, xm != 0) <= (size_t)kMaxDynSmem) {
+        *Bc_out = Bb;
+        *launches_out = launches;
+        *xq_mma_out = xm != 0;
+        return true;
+      }
+    }
+  }
+  return false;
 }
 
 int run_tc(const gqsa_desc_t* d, const void* d_blob, const uint16_t* d_X, int B, int64_t ldx, void* d_Y, int64_t ldy,
@@ -303,20 +322,14 @@ int run_tc(const gqsa_desc_t* d, const void* d_blob, const uint16_t* d_X, int B,
   if (ws_bytes < ws_bytes_for(std::max(B, 4))) return GQSA_ERR_BUFFER;
   const int sms = current_sms();
   if (sms <= 0) return GQSA_ERR_CUDA;
-  int Bc = B;  // largest balanced batch chunk whose x fits (each chunk re-streams the weights)
-  for (; Bc >= 1; --Bc) {
-    const int launches = (B + Bc - 1) / Bc, Bb = (B + launches - 1) / launches;
-    if (tc_smem(d, Bb) <= (size_t)kMaxDynSmem) {
-      Bc = Bb;
-      break;
-    }
-  }
-  if (Bc < 1) return GQSA_ERR_UNSUPPORTED;
+  int Bc = 0, launches = 0;
+  bool xm = false;
+  if (!tc_chunking(d, B, &Bc, &launches, &xm)) return GQSA_ERR_UNSUPPORTED;
   const size_t es = o.out_f16 ? 2 : 4;
   const uint8_t* blob = static_cast<const uint8_t*>(d_blob);
   for (int b0 = 0; b0 < B; b0 += Bc) {
     const int nb = std::min(Bc, B - b0);
-    const void* fn = select_tc_kernel(nb);
+    const void* fn = select_tc_kernel(nb, xm);
     if (!fn) return GQSA_ERR_UNSUPPORTED;
     int st = set_attrs(fn);
     if (st) return st;
@@ -351,7 +364,7 @@ int run_tc(const gqsa_desc_t* d, const void* d_blob, const uint16_t* d_X, int B,
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((p.active_warps + kTcWarps - 1) / kTcWarps);
     cfg.blockDim = dim3(32 * kTcWarps);
-    cfg.dynamicSmemBytes = tc_smem(d, nb);
+    cfg.dynamicSmemBytes = tc_smem(d, nb, xm);
     cfg.stream = static_cast<cudaStream_t>(stream);
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -382,19 +395,17 @@ extern "C" int gqsa_launch_plan(const gqsa_desc_t* desc, int32_t B, gqsa_plan_t*
   if (is_tc(desc)) {  // LAYOUT-TC: 16 warps per CTA, one CTA per SM, x of the batch chunk in shared memory
     const int sms = current_sms();
     if (sms <= 0) return GQSA_ERR_CUDA;
-    int Bc = B;
-    for (; Bc > 1 && tc_smem(desc, (B + ((B + Bc - 1) / Bc) - 1) / ((B + Bc - 1) / Bc)) > (size_t)kMaxDynSmem; --Bc) {
-    }
-    const int launches = (B + Bc - 1) / Bc;
-    Bc = (B + launches - 1) / launches;
+    int Bc = 0, launches = 0;
+    bool xm = false;
+    if (!tc_chunking(desc, B, &Bc, &launches, &xm)) return GQSA_ERR_UNSUPPORTED;
     std::memset(plan, 0, sizeof(*plan));
     plan->warps_per_cta = kTcWarps;
     plan->active_warps = std::min(desc->num_tiles, std::min(sms * kTcWarps, kMaxWarpsBound));
     plan->grid = (plan->active_warps + kTcWarps - 1) / kTcWarps;
     plan->num_tiles = desc->num_tiles;
-    plan->smem_bytes = (int32_t)tc_smem(desc, Bc);
+    plan->smem_bytes = (int32_t)tc_smem(desc, Bc, xm);
     plan->x_in_smem = 1;
-    plan->stages = kBufs;
+    plan->stages = kTcBufs;
     plan->ctas_per_sm = 1;
     plan->batch_per_launch = Bc;
     plan->launches = launches;

@@ -101,6 +101,12 @@ const void* select_kernel(int bits, int G, int B);
 
 // LAYOUT-TC kernel (gqsa_tc.cu): one GEMM over 16-row blocks on mma.sync.
 constexpr int kTcWarps = 16;
+// LAYOUT-TC tiles are 768 B (vs 1792 B for the stream layout): more of them in
+// flight per warp to keep the same bytes in flight per SM.
+#ifndef GQSA_TC_BUFS
+#define GQSA_TC_BUFS 4
+#endif
+constexpr int kTcBufs = GQSA_TC_BUFS;
 struct TcParams {
   const uint8_t* tiles;         // blob + off_tiles (768-B tiles of 4 items)
   const uint16_t* tile_cols;    // [num_tiles][4] item columns
@@ -119,6 +125,6 @@ struct TcParams {
   unsigned long long* rec;      // [active_warps][2][4][32] fix-up records
   uint64_t* trace;
 };
-const void* select_tc_kernel(int B);
+const void* select_tc_kernel(int B, bool xq_mma);
 
 }  // namespace gqsa

@@ -31,9 +31,12 @@ namespace gqsa {
 namespace {
 
 constexpr int kNV = 4;  // accumulators per lane: rows g, g+8 x batch 2t, 2t+1
+constexpr uint32_t kOnes = 0x3C003C00u;  // fp16 (1, 1)
 
+// Record k of lane `lane` of warp w's head (which = 0) / tail (1) partial sum:
+// a lane's kNV records are contiguous (two 128-bit accesses).
 __device__ __forceinline__ unsigned long long* tc_rec(const TcParams& p, int w, int which, int v, int lane) {
-  return p.rec + (((int64_t)w * 2 + which) * kNV + v) * kLanes + lane;
+  return p.rec + (((int64_t)w * 2 + which) * kLanes + lane) * kNV + v;
 }
 __device__ __forceinline__ void st_rel64(unsigned long long* a, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
@@ -43,9 +46,16 @@ __device__ __forceinline__ unsigned long long ld_rel64(const unsigned long long*
   asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
   return v;
 }
+__device__ __forceinline__ void st_rel64x2(unsigned long long* a, unsigned long long v0, unsigned long long v1) {
+  asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(a), "l"(v0), "l"(v1) : "memory");
+}
+__device__ __forceinline__ void ld_rel64x2(const unsigned long long* a, unsigned long long& v0, unsigned long long& v1) {
+  asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(v0), "=l"(v1) : "l"(a) : "memory");
+}
 __device__ __forceinline__ void tc_publish(const TcParams& p, int w, int which, const float (&v)[kNV], int lane) {
-#pragma unroll
-  for (int k = 0; k < kNV; ++k) st_rel64(tc_rec(p, w, which, k, lane), (1ull << 32) | __float_as_uint(v[k]));
+  unsigned long long* a = tc_rec(p, w, which, 0, lane);
+  st_rel64x2(a, (1ull << 32) | __float_as_uint(v[0]), (1ull << 32) | __float_as_uint(v[1]));
+  st_rel64x2(a + 2, (1ull << 32) | __float_as_uint(v[2]), (1ull << 32) | __float_as_uint(v[3]));
 }
 __device__ __forceinline__ int tc_arrive(const TcParams& p, int w0, int lane) {
   __syncwarp();
@@ -78,28 +88,61 @@ __device__ __forceinline__ void tc_store(const TcParams& p, int blk, const float
 // warp order (w0's tail record, then head records), resets them and the
 // counter, and stores.  Only waits for records already issued.
 template <int B>
-__device__ __noinline__ void tc_collect(const TcParams& p, int w0, int w1, int blk, int lane) {
+__device__ __forceinline__ void tc_collect(const TcParams& p, int w0, int w1, int blk, int lane) {
+  // A block spans up to ~12 warps.  The records of kChunk warps are requested
+  // at once, and the code is kept compact (rolled loops, one re-read loop for
+  // the rare not-yet-visible record): this tail code runs once per block on a
+  // cold instruction cache, and an unrolled version cost several microseconds
+  // of instruction fetch.
+  constexpr int kChunk = 8;
+  unsigned int total_spins = 0;
   float v[kNV];
 #pragma unroll
   for (int k = 0; k < kNV; ++k) v[k] = 0.f;
-  for (int w = w0; w <= w1; ++w) {
-    unsigned long long r[kNV];
+#pragma unroll 1
+  for (int wb = w0; wb <= w1; wb += kChunk) {
+    unsigned long long r[kChunk][kNV];
+#pragma unroll 1
+    for (unsigned int spins = 0;; ++spins) {
+      bool ok = true;
 #pragma unroll
-    for (int k = 0; k < kNV; ++k) r[k] = ld_rel64(tc_rec(p, w, w == w0 ? 1 : 0, k, lane));
+      for (int j = 0; j < kChunk; ++j) {
+        if (wb + j <= w1) {
+          const unsigned long long* a = tc_rec(p, wb + j, wb + j == w0 ? 1 : 0, 0, lane);
+          ld_rel64x2(a, r[j][0], r[j][1]);
+          ld_rel64x2(a + 2, r[j][2], r[j][3]);
+        } else {
 #pragma unroll
-    for (int k = 0; k < kNV; ++k) {
-      unsigned long long* a = tc_rec(p, w, w == w0 ? 1 : 0, k, lane);
-      unsigned int spins = 0;
-      while ((r[k] >> 32) == 0ull) {
-        if (++spins > (1u << 26)) __trap();
-        r[k] = ld_rel64(a);
+          for (int k = 0; k < kNV; ++k) r[j][k] = 1ull << 32;
+        }
       }
-      v[k] = (w == w0) ? __uint_as_float((uint32_t)r[k]) : v[k] + __uint_as_float((uint32_t)r[k]);
-      st_rel64(a, 0ull);
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j)
+#pragma unroll
+        for (int k = 0; k < kNV; ++k) ok = ok && (r[j][k] >> 32) != 0ull;
+      if (ok) break;
+      total_spins++;
+      if (spins > (1u << 26)) __trap();
     }
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j)
+      if (wb + j <= w1)
+#pragma unroll
+        for (int k = 0; k < kNV; ++k)
+          v[k] = (wb + j == w0) ? __uint_as_float((uint32_t)r[j][k]) : v[k] + __uint_as_float((uint32_t)r[j][k]);
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j)
+      if (wb + j <= w1) {
+        unsigned long long* a = tc_rec(p, wb + j, wb + j == w0 ? 1 : 0, 0, lane);
+        st_rel64x2(a, 0ull, 0ull);
+        st_rel64x2(a + 2, 0ull, 0ull);
+      }
   }
   if (lane == 0) asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p.cnt + w0), "r"(0u) : "memory");
   tc_store<B>(p, blk, v, lane);
+#ifdef GQSA_TC_SPINTRACE
+  if (p.trace && lane == 0) p.trace[(int64_t)(blockIdx.x * kTcWarps + (threadIdx.x >> 5)) * 8 + 7] = 1000000ull * (w1 - w0 + 1) + total_spins;
+#endif
 }
 
 struct TcTile {
@@ -136,7 +179,10 @@ __device__ __forceinline__ void trace_tc(const TcParams& p, int gw, int lane, in
 
 }  // namespace
 
-template <int B>
+// XM: the column sums X_c come from a second mma against an all-ones A
+// (every row of D' is X_c) instead of a staged table -- the shared memory then
+// holds x alone, which is what lets B = 8 at K = 14336 run as one launch.
+template <int B, bool XM>
 __global__ void __launch_bounds__(32 * kTcWarps, 1) gqsa_tc_kernel(const __grid_constant__ TcParams p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gw = blockIdx.x * kTcWarps + warp;
@@ -155,11 +201,11 @@ __global__ void __launch_bounds__(32 * kTcWarps, 1) gqsa_tc_kernel(const __grid_
     t_end = b < t_end ? e : b;
   }
   const uint64_t pol = evict_first_policy();
-  TcTile buf[kBufs];
+  TcTile buf[kTcBufs];
 #pragma unroll
-  for (int k = 0; k < kBufs; ++k)
+  for (int k = 0; k < kTcBufs; ++k)
     if (t_begin + k < t_end) tc_load(buf[k], p, t_begin + k, lane, pol);
-  int blk = 0, bend = 0, bst = 0;
+  int blk = 0, bend = 0, bst = 0, bnext = 0;
   if (t_end > t_begin) blk = __ldg(p.tile_block + t_begin);
   pdl_launch_dependents();
   bool waited = !p.x_ready;
@@ -167,6 +213,7 @@ __global__ void __launch_bounds__(32 * kTcWarps, 1) gqsa_tc_kernel(const __grid_
   if (t_end > t_begin) {
     bst = __ldg(p.block_tile0 + blk);
     bend = __ldg(p.block_tile0 + blk + 1);
+    if (blk + 1 < p.nb) bnext = __ldg(p.block_tile0 + blk + 2);
   }
 
   // ---- stage x [B][K] (+ a zero chunk per row for padding items) and the
@@ -174,27 +221,46 @@ __global__ void __launch_bounds__(32 * kTcWarps, 1) gqsa_tc_kernel(const __grid_
   const int KG = p.cols / kGroup;
   uint8_t* xs = smem;
   float* xq = reinterpret_cast<float*>(smem + (size_t)B * p.xrow);
-  for (int i = threadIdx.x; i < B * KG; i += blockDim.x) {
-    const int b = i / KG, c = i - b * KG;
-    const uint4* src = reinterpret_cast<const uint4*>(p.X + (int64_t)b * p.ldx) + 2 * c;
-    const uint4 v0 = __ldg(src), v1 = __ldg(src + 1);
-    uint4* dst = reinterpret_cast<uint4*>(xs + (size_t)b * p.xrow) + 2 * c;
-    dst[0] = v0;
-    dst[1] = v1;
-    const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-    const uint32_t one = 0x3C003C00u;
-    float ae = 0.f, ao = 0.f;
+  constexpr int kSt = 4;  // column groups per thread in flight
+  for (int i0 = threadIdx.x; i0 < B * KG; i0 += kSt * blockDim.x) {
+    uint4 v[kSt][2];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      ae = fhfma<0, 0>(w[e], one, ae);
-      ao = fhfma<1, 0>(w[e], one, ao);
+    for (int j = 0; j < kSt; ++j) {
+      const int i = i0 + j * blockDim.x;
+      if (i < B * KG) {
+        const int b = i / KG, c = i - b * KG;
+        const uint4* src = reinterpret_cast<const uint4*>(p.X + (int64_t)b * p.ldx) + 2 * c;
+        v[j][0] = __ldg(src);
+        v[j][1] = __ldg(src + 1);
+      }
     }
-    xq[c * 8 + b] = ae + ao;
+#pragma unroll
+    for (int j = 0; j < kSt; ++j) {
+      const int i = i0 + j * blockDim.x;
+      if (i < B * KG) {
+        const int b = i / KG, c = i - b * KG;
+        uint4* dst = reinterpret_cast<uint4*>(xs + (size_t)b * p.xrow) + 2 * c;
+        dst[0] = v[j][0];
+        dst[1] = v[j][1];
+        if (XM) continue;
+        const uint32_t w[8] = {v[j][0].x, v[j][0].y, v[j][0].z, v[j][0].w,
+                               v[j][1].x, v[j][1].y, v[j][1].z, v[j][1].w};
+        const uint32_t one = 0x3C003C00u;
+        float ae = 0.f, ao = 0.f;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          ae = fhfma<0, 0>(w[e], one, ae);
+          ao = fhfma<1, 0>(w[e], one, ao);
+        }
+        xq[c * 8 + b] = ae + ao;
+      }
+    }
   }
-  for (int i = threadIdx.x; i < (KG + 1) * 8; i += blockDim.x) {
-    const int c = i >> 3, b = i & 7;
-    if (c == KG || b >= B) xq[i] = 0.f;
-  }
+  if (!XM)
+    for (int i = threadIdx.x; i < (KG + 1) * 8; i += blockDim.x) {
+      const int c = i >> 3, b = i & 7;
+      if (c == KG || b >= B) xq[i] = 0.f;
+    }
   for (int i = threadIdx.x; i < B * 2; i += blockDim.x)
     reinterpret_cast<uint4*>(xs + (size_t)(i >> 1) * p.xrow + 2 * p.cols)[i & 1] = make_uint4(0, 0, 0, 0);
   __syncthreads();
@@ -236,7 +302,14 @@ __global__ void __launch_bounds__(32 * kTcWarps, 1) gqsa_tc_kernel(const __grid_
       }
       float d[4];
       mma16816(d, a0, a1, a2, a3, b0, b1);
-      const float2 X = lds64f(xq_s + c * 32u + 8u * tq);  // column sums of batch 2t, 2t+1
+      float2 X;  // column sums of batch 2t, 2t+1
+      if (XM) {
+        float dx[4];
+        mma16816(dx, kOnes, kOnes, kOnes, kOnes, b0, b1);
+        X = make_float2(dx[0], dx[1]);
+      } else {
+        X = lds64f(xq_s + c * 32u + 8u * tq);
+      }
       const uint4& szv = u < 2 ? tr.sz0 : tr.sz1;
       const uint32_t slo = (u & 1) ? szv.z : szv.x, shi = (u & 1) ? szv.w : szv.y;
       const __half2 hlo = *reinterpret_cast<const __half2*>(&slo), hhi = *reinterpret_cast<const __half2*>(&shi);
@@ -265,7 +338,8 @@ __global__ void __launch_bounds__(32 * kTcWarps, 1) gqsa_tc_kernel(const __grid_
       cw0 = gw;
       if (t + 1 < t_end) {
         ++blk;
-        bend = __ldg(p.block_tile0 + blk + 1);
+        bend = bnext;  // loaded one block ahead: no load latency on the next compare
+        if (blk + 1 < p.nb) bnext = __ldg(p.block_tile0 + blk + 2);
       }
     }
   };
@@ -273,44 +347,59 @@ __global__ void __launch_bounds__(32 * kTcWarps, 1) gqsa_tc_kernel(const __grid_
   int t = t_begin;
   while (t < t_end) {
 #pragma unroll
-    for (int k = 0; k < kBufs; ++k) {
+    for (int k = 0; k < kTcBufs; ++k) {
       if (t < t_end) {
         consume(buf[k], t);
-        if (t + kBufs < t_end) tc_load(buf[k], p, t + kBufs, lane, pol);
+        if (t + kTcBufs < t_end) tc_load(buf[k], p, t + kTcBufs, lane, pol);
         ++t;
       }
     }
   }
   trace_tc(p, gw, lane, 4);
   ensure_wait();
+  // Up to two collections (the block continuing downstream, the head block
+  // that ended in this range), run through one call site of the collect code.
+  int a_w0 = 0, a_w1 = 0, a_blk = 0, b_w0 = 0, b_w1 = 0, b_blk = 0, nc = 0;
   if (bend > t_end) {  // the block continues downstream
     const int w1 = tc_warp_of_tile(p, bend - 1);
     tc_publish(p, gw, foreign ? 0 : 1, acc, lane);
     const int old = tc_arrive(p, cw0, lane);
-    if (old == w1 - cw0) tc_collect<B>(p, cw0, w1, blk, lane);
+    trace_tc(p, gw, lane, 1);
+    if (old == w1 - cw0) {
+      a_w0 = cw0, a_w1 = w1, a_blk = blk;
+      nc = 1;
+    }
   }
   if (h_pending) {
     const int old = __shfl_sync(0xffffffffu, h_old, 0);
-    if (old == gw - h_w0) tc_collect<B>(p, h_w0, gw, h_blk, lane);
+    if (old == gw - h_w0) {
+      if (nc == 0) a_w0 = h_w0, a_w1 = gw, a_blk = h_blk;
+      else b_w0 = h_w0, b_w1 = gw, b_blk = h_blk;
+      ++nc;
+    }
   }
+#pragma unroll 1
+  for (int i = 0; i < nc; ++i) tc_collect<B>(p, i ? b_w0 : a_w0, i ? b_w1 : a_w1, i ? b_blk : a_blk, lane);
+  trace_tc(p, gw, lane, 6);
   trace_tc(p, gw, lane, 5);
 }
 
 template <int B>
-const void* tc_ptr() {
-  return reinterpret_cast<const void*>(&gqsa_tc_kernel<B>);
+const void* tc_ptr(bool xm) {
+  return xm ? reinterpret_cast<const void*>(&gqsa_tc_kernel<B, true>)
+            : reinterpret_cast<const void*>(&gqsa_tc_kernel<B, false>);
 }
 
-const void* select_tc_kernel(int B) {
+const void* select_tc_kernel(int B, bool xq_mma) {
   switch (B) {
-    case 1: return tc_ptr<1>();
-    case 2: return tc_ptr<2>();
-    case 3: return tc_ptr<3>();
-    case 4: return tc_ptr<4>();
-    case 5: return tc_ptr<5>();
-    case 6: return tc_ptr<6>();
-    case 7: return tc_ptr<7>();
-    case 8: return tc_ptr<8>();
+    case 1: return tc_ptr<1>(xq_mma);
+    case 2: return tc_ptr<2>(xq_mma);
+    case 3: return tc_ptr<3>(xq_mma);
+    case 4: return tc_ptr<4>(xq_mma);
+    case 5: return tc_ptr<5>(xq_mma);
+    case 6: return tc_ptr<6>(xq_mma);
+    case 7: return tc_ptr<7>(xq_mma);
+    case 8: return tc_ptr<8>(xq_mma);
     default: return nullptr;
   }
 }

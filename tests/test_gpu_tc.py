@@ -3,7 +3,8 @@ mma.sync.m16n8k16 over 16-row blocks) against the fp64
 oracle: bit-exact in exact-integer mode for every batch 1..8 (all partial
 sums are exact in fp32, whatever order the tensor core adds the products
 in), Stream-K and Slice-K, ragged shapes (last block partial, blocks with no
-kept group, K at its maximum, batch split when x does not fit); the gates
+kept group, K at its maximum, column sums from the mma when the X_c table does
+not fit beside x, batch split when x itself does not fit); the gates
 G1-G3 on realistic values; fp16 output with bias; bit-identical reruns."""
 import numpy as np
 import pytest
@@ -42,9 +43,21 @@ TC_EXACT = [
     (4096, 16, 0.5, "uniform", 1),       # K = G
     (5, 64, 0.5, "uniform", 7),
     (640, 512, 0.9, "uniform", 6),
-    (64, 32736, 0.5, "uniform", 8),      # K at its maximum: batch split
-    (2048, 14336, 0.5, "uniform", 8),    # LLaMA down_proj width: batch split into 2 x 4
+    (64, 32736, 0.5, "uniform", 8),      # K at its maximum: batch split (3 x 3 rows, X_c by mma)
+    (2048, 14336, 0.5, "uniform", 8),    # LLaMA down_proj width: one launch, X_c by mma
 ]
+
+
+def test_tc_launch_plan_x_only_at_down_proj_width():
+    """B = 8 at K = 14336: x (8 x (2K + 32) B) fits the 225-KB budget only
+    without the X_c table -- one launch, weights streamed once."""
+    bsr = synth.make_layer(5, 64, 14336, bits=4, sparsity=0.5)
+    blob, desc = gqsa.pack(bsr, layout=gqsa.LAYOUT_TC)
+    plan = gqsa.launch_plan(desc, 8)
+    assert plan.launches == 1 and plan.batch_per_launch == 8
+    assert plan.smem_bytes == 8 * (2 * 14336 + 32)
+    plan = gqsa.launch_plan(desc, 4)  # the table fits: the cheaper staging
+    assert plan.smem_bytes == 4 * (2 * 14336 + 32) + (14336 // 16 + 1) * 32
 
 
 @pytest.mark.parametrize("rows,cols,sp,mask,B", TC_EXACT)

@@ -47,6 +47,7 @@ def main():
     torch.cuda.synchronize()
     T = np.stack([b.cpu().numpy().reshape(W, 8) for b in bufs]).astype(np.float64)
     t0 = T[0, :, 0].min()
+    Traw = T.copy()
     T = (T - t0) / 1e3
     d = T[1:]
     print(f"TC {a.rows}x{a.cols} B={a.batch}: warps={W} tiles={desc.num_tiles} blocks={desc.num_slices} "
@@ -61,6 +62,20 @@ def main():
     print("loop µs per tile p10/p50/p90: %.3f/%.3f/%.3f (tiles per warp %d)" % (
         np.percentile(per, 10), np.median(per), np.percentile(per, 90), q))
     print("last exit - median exit (µs): %.2f" % np.median(d[..., 5].max(axis=1) - np.median(d[..., 5], axis=1)))
+    # per launch, relative to its median "staged" stamp
+    rel = d - np.median(d[..., 2], axis=1)[:, None, None]
+    for k, name in ((0, "start"), (2, "staged"), (4, "loop end"), (5, "exit")):
+        v = rel[..., k]
+        print("  %-8s p1 %.2f  p50 %.2f  p99 %.2f  max %.2f" % (
+            name, np.median(np.percentile(v, 1, axis=1)), np.median(np.percentile(v, 50, axis=1)),
+            np.median(np.percentile(v, 99, axis=1)), np.median(v.max(axis=1))))
+    late = np.argsort(rel[1, :, 5])[-8:]
+    print("  latest exits of one launch: warp, start, staged, loop, fixup, exit; fix-up stamps (arrived, tail collect, head collect; -: not reached)")
+    for w in late:
+        r = rel[1, w]
+        raw = Traw[2, w]
+        fx = " ".join("%6.2f" % ((raw[k] - raw[4]) / 1e3) if raw[k] > 0 else "     -" for k in (1, 6, 7))
+        print("   %5d %6.2f %6.2f %6.2f %6.2f %6.2f | %s | raw7 %d" % (w, r[0], r[2], r[4] - r[3], r[5] - r[4], r[5], fx, raw[7]))
 
 
 if __name__ == "__main__":
