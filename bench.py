@@ -57,6 +57,14 @@ def counted_bytes(rows, cols, nnzg, bits, batch=1, G=16):
     return nnzg * (G * bits // 8 + 6) + 4 * (rows + 1) + 2 * batch * cols + 4 * batch * rows
 
 
+def workload_config(batch, world):
+    """The workload both arms run (identical dicts: the driver compares them)."""
+    return {"workload": f"llama3-8b-layer-shapes-w4s50-b{batch} (4096x4096, 14336x4096, 4096x14336)",
+            "global_batch": batch, "seq_len": 1, "group_size": 16, "bits": 4, "sparsity": 0.5,
+            "parallelism": f"rowshard{world}" if world > 1 else "single",
+            "l2": "inputs larger than L2 (weights rotate over device copies > 2x L2)"}
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -252,8 +260,8 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded; DESIGN.md §4 recipe)",
-        "config": {"workload": "llama3-8b-layer-shapes-w4s50-b1", "global_batch": args.batch,
-                   "seq_len": 1, "parallelism": "host-cpu"},
+        "config": workload_config(args.batch, args.gpus),
+        "method": {"host": "CPU fp64 oracle (oracle/gqsa_oracle.py), 1 core, rank 0"},
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -464,7 +472,7 @@ def run_gpu(args):
 
     # ---- per-layer device time (one launch per layer), outside the timed region
     layer_rows = []
-    if world == 1:
+    if world == 1 and not args.no_layers:
         for i, L in enumerate(layers):
             d = descs[i]
 
@@ -545,10 +553,8 @@ def run_gpu(args):
         "dtype": "u4xf16->f32",
         "data": "synthetic (seeded random W4 codes, fp16 s/z, uniform 50% group mask, N(0,1) fp16 x "
                 "with 0.5% outlier channels; DESIGN.md §4)",
-        "config": {"workload": "llama3-8b-layer-shapes-w4s50-b1 (4096x4096, 14336x4096, 4096x14336)",
-                   "global_batch": B, "seq_len": 1, "group_size": 16, "bits": bits, "sparsity": sp,
-                   "parallelism": f"rowshard{world}" if world > 1 else "single",
-                   "allgather": (args.allgather if (world > 1 or fused) else None),
+        "config": workload_config(B, world),
+        "method": {"allgather": (args.allgather if (world > 1 or fused) else None),
                    "l2": f"inputs larger than L2: weights rotate over {R} device copies of the layer set "
                          f"({R * set_bytes / 2**20:.0f} MiB > 2x L2)",
                    "path": {"grouped": "one gqsa_gemm_grouped launch per step (the 3 independent GEMVs "
@@ -587,6 +593,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rotate", action="store_true")
+    ap.add_argument("--no-layers", action="store_true", help="skip the per-layer timing loop (ncu launch lists)")
     ap.add_argument("--allgather", default="nccl", choices=["nccl", "fused"],
                     help="row-shard output exchange: NCCL all_gather, or the fused GEMV epilogue storing "
                          "into every rank's y over symmetric memory (gqsa_gemm_allgather)")
