@@ -7,7 +7,13 @@ i.e. every row of SURVEY §8(a) over one batch of synthetic input.  value =
 counted (compressed, algorithmic) bytes of all steps / device time, in GB/s.
 
 The step runs as ONE gqsa_gemm_grouped launch (the three GEMVs are
-independent; `--path launches` runs one gqsa_gemv per layer instead).
+independent; `--path launches` runs one gqsa_gemv per layer instead).  The
+step's activations are inputs that nothing in the timed region writes, so the
+launch declares them ready (x_ready, `--x-ready 0` turns it off): the library
+then runs it PIPELINED -- half of every SM, all global writes deferred until
+the previous step's launch has completed -- so consecutive steps overlap
+their start-up and drain.  `layers[]` are standalone
+launches of each layer with x_ready = 0 (the dependent-chain case).
 
 Timing: the weights rotate over R device copies of the layer set (> 2x the
 126 MB L2), so every launch streams from HBM.  K steps are replayed from CUDA
@@ -600,8 +606,10 @@ def main():
     ap.add_argument("--path", default="grouped", choices=["grouped", "launches"],
                     help="grouped: the step's GEMVs in one gqsa_gemm_grouped launch; launches: one gqsa_gemv "
                          "per layer")
-    ap.add_argument("--x-ready", type=int, default=0, choices=[0, 1],
-                    help="declare x not produced by the previous kernel (staged before the PDL wait)")
+    ap.add_argument("--x-ready", type=int, default=1, choices=[0, 1],
+                    help="declare the step's x not produced by the previous kernel (true here: nothing in the "
+                         "timed region writes x), so consecutive steps pipeline (DESIGN.md §6.2); 0 = every "
+                         "launch waits for the previous one to complete before it reads x")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

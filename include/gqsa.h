@@ -225,8 +225,14 @@ int gqsa_gemm_smallbatch(const gqsa_desc_t* desc, const void* d_blob, const uint
  *     the stream, so it is read after that kernel completes; 1 = the caller
  *     guarantees X is NOT written by the previous kernel (e.g. several
  *     GEMVs of one input, or inputs copied before an earlier launch), so the
- *     kernel stages X while the previous kernel drains.  Y, bias and the
- *     workspace are always touched only after the previous kernel completes.
+ *     kernel stages X while the previous kernel drains.  At B <= 2 such a
+ *     launch is PIPELINED: it takes half of every SM, so it
+ *     streams its weights and computes beside the previous launch, and
+ *     defers all its global writes until that launch has completed.  Y, bias
+ *     and the workspace are always touched only after the previous kernel
+ *     completes, so consecutive launches may share one workspace.  The
+ *     pipelined launch uses another grid, hence another fp32 summation order
+ *     than x_ready = 0 (both within the parity gates, each deterministic).
  * Other option values return GQSA_ERR_SHAPE.
  */
 #define GQSA_PARTITION_STREAM_K 0
@@ -331,15 +337,20 @@ int gqsa_gemm_multi_hostio(const gqsa_desc_t* const* descs, const void* const* d
 
 /* Launch plan the next gemv/gemm call will use on the current device (for
  * a split batch: the plan of its first launch):
- * CTAs, warps per CTA, active warps (Stream-K units), tiles.  For tooling. */
+ * CTAs, warps per CTA, active warps (Stream-K units), tiles.  For tooling.
+ * gqsa_launch_plan_ex takes the call's options (NULL = defaults): with
+ * x_ready at B <= 2 the launch is the pipelined one. */
 typedef struct {
   int32_t grid, warps_per_cta, active_warps, num_tiles, smem_bytes, x_in_smem;
-  int32_t stages, ctas_per_sm, ring_bytes;  /* tiles in flight per warp (register buffers), 1, 0 */
+  int32_t stages, ctas_per_sm, ring_bytes;  /* tiles in flight per warp (register buffers); CTAs
+                                               per SM the kernel is compiled for; 0 */
   int32_t batch_per_launch, launches;  /* x of batch_per_launch columns fits in shared memory;
                                           larger batches run as `launches` launches */
-  int32_t coresident;                  /* always 0: one CTA per SM owns the SM */
+  int32_t coresident;                  /* 1: pipelined -- the launch takes part of every SM and the
+                                          next launch on the stream may run beside it */
 } gqsa_plan_t;
 int gqsa_launch_plan(const gqsa_desc_t* desc, int32_t B, gqsa_plan_t* plan);
+int gqsa_launch_plan_ex(const gqsa_desc_t* desc, int32_t B, const gqsa_options_t* opts, gqsa_plan_t* plan);
 
 /* Number of GQSA kernels launched by this process so far (all entry points). */
 uint64_t gqsa_launch_count(void);

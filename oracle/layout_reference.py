@@ -31,13 +31,13 @@ def tile_bytes(bits: int, G: int = 16) -> int:
 
 def target_slots(nnzg: int) -> int:
     """Slots per lane of the longest slice: 16 when the layer
-    has under 1.6 tiles (of 128 groups) per warp of a 148 x 16-warp grid, 32
-    under 4, else 64."""
+    has under 1.6 tiles (of 128 groups) per warp of a 148 x 16-warp grid, 128
+    under 4, else 256."""
     tpw = nnzg / 128.0 / (148.0 * 16.0)
-    return 16 if tpw < 1.6 else 32 if tpw < 4.0 else 64
+    return 16 if tpw < 1.6 else 128 if tpw < 4.0 else 256
 
 
-def lanes_per_row(n_nz: int, max_len: int, target: int = 64) -> int:
+def lanes_per_row(n_nz: int, max_len: int, target: int = 256) -> int:
     """S = the larger of (a) the smallest power of two with
     ceil(max_len / S) <= target slots per lane and (b) 32 / (next power of
     two >= n_nz) when fewer than 32 rows are non-empty; capped at 32."""

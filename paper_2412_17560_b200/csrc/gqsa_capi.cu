@@ -44,6 +44,16 @@ int current_sms() {
   return device_sms(dev);
 }
 
+// Pipelined launches: GQSA_PIPELINE=0 off, 1 (default) for
+// x_ready calls, 2 for every call at B <= 2 (A/B experiments).
+int pipeline_mode() {
+  static const int mode = [] {
+    const char* e = std::getenv("GQSA_PIPELINE");
+    return e && (e[0] == '0' || e[0] == '2') ? e[0] - '0' : 1;
+  }();
+  return mode;
+}
+
 bool lanes_per_row_ok(uint32_t s) { return s >= 1 && s <= 32 && (s & (s - 1)) == 0; }
 
 bool is_tc(const gqsa_desc_t* d) { return ((uint32_t)d->flags & kFlagTC) != 0; }
@@ -76,17 +86,19 @@ size_t ws_bytes_for(int B) {
 
 struct Launch {
   int grid = 0, W = 0, active = 0, total_tiles = 0, part_q = 0, part_r = 0;
-  size_t smem = 0, tab_offset = 0;
+  int half = 0;  // pipelined mode: half of every SM, deferred writes
+  size_t smem = 0, tab_offset = 0, defer_offset = 0;
 };
 // shared bytes of the per-CTA staging table (gqsa_device.cuh StageEntry x kMaxItems + 16)
 constexpr size_t kStageTab = kMaxItems * 40 + 16;
 
 // Stream-K grid over the concatenated tiles of `n` items at batch Bc, and the
 // largest shared-memory footprint of any CTA (the items its range touches).
-int plan_launch(const gqsa_desc_t* const* d, int n, int Bc, Launch* L) {
+int plan_launch(const gqsa_desc_t* const* d, int n, int Bc, Launch* L, int half = 0) {
   const int sms = current_sms();
   if (sms <= 0) return GQSA_ERR_CUDA;
-  L->W = warps_for(Bc);
+  L->half = half;
+  L->W = warps_of(Bc, half);
   int64_t total = 0, n_empty = 0;
   for (int j = 0; j < n; ++j) {
     total += d[j]->num_tiles;
@@ -122,7 +134,26 @@ int plan_launch(const gqsa_desc_t* const* d, int n, int Bc, Launch* L) {
   }
   L->smem = worst + kStageTab;  // + the staging table
   L->tab_offset = worst;
+  L->defer_offset = 0;
+  if (half) {  // + the per-warp deferred-store buffers (16-B aligned)
+    L->defer_offset = (L->smem + 15) / 16 * 16;
+    L->smem = L->defer_offset + (size_t)L->W * defer_bytes_per_warp(Bc);
+  }
   return GQSA_OK;
+}
+
+// The launch of n items at batch Bc under options o: the pipelined mode
+// (half of every SM, deferred writes) when X is declared ready -- the launch
+// may then overlap the previous one on the stream -- and its footprint fits
+// kPipeCtas times per SM; else the whole-SM launch.
+int choose_launch(const gqsa_desc_t* const* d, int n, int Bc, const gqsa_options_t& o, Launch* L) {
+  int st = GQSA_OK;
+  const int mode = pipeline_mode();
+  if (Bc <= 2 && (mode == 2 || (mode == 1 && o.x_ready))) {
+    if ((st = plan_launch(d, n, Bc, L, 1))) return st;
+    if (L->smem <= (size_t)kHalfSmemLimit) return GQSA_OK;
+  }
+  return plan_launch(d, n, Bc, L);
 }
 
 // Largest batch chunk whose footprint fits; the batch runs as ceil(B / Bc)
@@ -168,11 +199,11 @@ int launch_items(const gqsa_gemm_item_t* items, int n, int Bc, const gqsa_option
   std::vector<const gqsa_desc_t*> d(n);
   for (int j = 0; j < n; ++j) d[j] = items[j].desc;
   Launch L;
-  int st = plan_launch(d.data(), n, Bc, &L);
+  int st = choose_launch(d.data(), n, Bc, o, &L);
   if (st) return st;
   if (L.smem > (size_t)kMaxDynSmem) return GQSA_ERR_UNSUPPORTED;
   const int bits = d[0]->bits, G = d[0]->group_size;
-  const void* fn = select_kernel(bits, G, Bc);
+  const void* fn = select_kernel(bits, G, Bc, L.half);
   if (!fn) return GQSA_ERR_UNSUPPORTED;
   if ((st = set_attrs(fn))) return st;
 
@@ -222,6 +253,7 @@ int launch_items(const gqsa_gemm_item_t* items, int n, int Bc, const gqsa_option
   p.out_f16 = o.out_f16;
   p.x_ready = o.x_ready;
   p.stage_tab_offset = (int32_t)L.tab_offset;
+  p.defer_offset = (int32_t)L.defer_offset;
   uint8_t* ws = static_cast<uint8_t*>(d_ws);
   p.cnt = reinterpret_cast<uint32_t*>(ws + 256);
   p.rec = reinterpret_cast<unsigned long long*>(ws + 256 + (size_t)kMaxWarpsBound * 4);
@@ -389,7 +421,14 @@ extern "C" int gqsa_workspace_size(const gqsa_desc_t* desc, int32_t batch, size_
 }
 
 extern "C" int gqsa_launch_plan(const gqsa_desc_t* desc, int32_t B, gqsa_plan_t* plan) {
+  return gqsa_launch_plan_ex(desc, B, nullptr, plan);
+}
+
+extern "C" int gqsa_launch_plan_ex(const gqsa_desc_t* desc, int32_t B, const gqsa_options_t* opts,
+                                   gqsa_plan_t* plan) {
   if (!desc || !plan) return GQSA_ERR_BUFFER;
+  const gqsa_options_t o = opts ? *opts : gqsa_options_t{GQSA_PARTITION_STREAM_K, 0, 0, 0};
+  if (check_options(o)) return GQSA_ERR_SHAPE;
   if (!desc_ok(desc)) return GQSA_ERR_VALIDATION;
   if (B < 1 || B > kMaxBatch) return GQSA_ERR_SHAPE;
   if (is_tc(desc)) {  // LAYOUT-TC: 16 warps per CTA, one CTA per SM, x of the batch chunk in shared memory
@@ -413,8 +452,9 @@ extern "C" int gqsa_launch_plan(const gqsa_desc_t* desc, int32_t B, gqsa_plan_t*
   }
   Launch L;
   int Bc = B;
-  const int st = batch_chunk(&desc, 1, B, &Bc, &L);
+  int st = batch_chunk(&desc, 1, B, &Bc, &L);
   if (st) return st;
+  if ((st = choose_launch(&desc, 1, Bc, o, &L))) return st;
   std::memset(plan, 0, sizeof(*plan));
   plan->grid = L.grid;
   plan->warps_per_cta = L.W;
@@ -423,11 +463,11 @@ extern "C" int gqsa_launch_plan(const gqsa_desc_t* desc, int32_t B, gqsa_plan_t*
   plan->smem_bytes = (int32_t)L.smem;
   plan->x_in_smem = 1;
   plan->stages = kBufs;
-  plan->ctas_per_sm = 1;
+  plan->ctas_per_sm = L.half ? kPipeCtas : 1;
   plan->ring_bytes = 0;
   plan->batch_per_launch = Bc;
   plan->launches = (B + Bc - 1) / Bc;
-  plan->coresident = 0;
+  plan->coresident = L.half;
   return GQSA_OK;
 }
 

@@ -26,11 +26,18 @@ constexpr int kMaxDynSmem = 225 * 1024; // opt-in dynamic shared memory per CTA 
 #endif
 constexpr int kBufs = GQSA_BUFS;
 // L2 prefetch distance in tiles (<= kBufs: off): lane 0 issues
-// cp.async.bulk.prefetch.L2 for tile t + kL2Pf as it requests tile t into registers.
+// cp.async.bulk.prefetch.L2 for tile t + kL2Pf as it requests tile t into
+// registers, so each warp keeps kL2Pf tiles moving from HBM while only kBufs
+// occupy registers (bench step, pipelined: 15.1 -> 13.6 us at 3; 4: 13.8, 6: 14.2).
 #ifndef GQSA_L2PF
-#define GQSA_L2PF 0
+#define GQSA_L2PF 3
 #endif
 constexpr int kL2Pf = GQSA_L2PF;
+// Tiles prefetched to L2 at the start of a warp's range (before the PDL wait), >= kL2Pf.
+#ifndef GQSA_L2PF0
+#define GQSA_L2PF0 GQSA_L2PF
+#endif
+constexpr int kL2Pf0 = GQSA_L2PF0 > GQSA_L2PF ? GQSA_L2PF0 : GQSA_L2PF;
 // Warps per CTA (one CTA per SM): more warps keep more weight loads in
 // flight (a read-only stream of the same tiles reaches 4.9 / 5.3 / 5.5 TB/s
 // with 16 / 24 / 32 warps per SM on the 59 MB bench step,
@@ -50,6 +57,25 @@ __host__ __device__ constexpr int warps_for(int B) { return B == 1 ? GQSA_WARPS_
 #define GQSA_MINB 1
 #endif
 __host__ __device__ constexpr int min_blocks_for(int B) { return B <= 2 ? GQSA_MINB : 1; }
+// Pipelined mode (x_ready, B <= 2): the launch takes HALF of
+// every SM (one CTA of half the warps, compiled for 2 resident CTAs), so the
+// next independent launch on the stream runs its prologue, activation staging
+// and tile loop on the other half while this one drains; every global write
+// of the loop is deferred until after griddepcontrol.wait.
+#ifndef GQSA_WARPS_HALF
+#define GQSA_WARPS_HALF 10
+#endif
+#ifndef GQSA_PIPE_CTAS
+#define GQSA_PIPE_CTAS 2
+#endif
+constexpr int kPipeCtas = GQSA_PIPE_CTAS;  // resident CTAs per SM the pipelined kernel is compiled for
+__host__ __device__ constexpr int warps_half(int B) { return B == 1 ? GQSA_WARPS_HALF : 8; }
+__host__ __device__ constexpr int warps_of(int B, int half) { return half ? warps_half(B) : warps_for(B); }
+// Deferred row stores buffered per warp in shared memory before the wait
+// (more closed slices than this in one range: the warp waits and stores).
+constexpr int kDeferSlots = 8;
+__host__ __device__ constexpr int defer_bytes_per_warp(int B) { return kDeferSlots * 32 * 4 * (B + 1); }
+constexpr int kHalfSmemLimit = (kSmemPerSm - kPipeCtas * 2048) / kPipeCtas;  // per CTA, kPipeCtas CTAs per SM
 constexpr int kMaxWarpsBound = 148 * 32;  // fix-up records the workspace holds per launch (any B200 grid)
 
 // One GEMV of a launch.  Its tiles occupy global tile indices
@@ -81,6 +107,8 @@ struct Params {
   int32_t out_f16;   // 1: Y is fp16 (RNE of the fp32 result)
   int32_t x_ready;   // 1: X is not written by the previous kernel on the stream: stage it before the PDL wait
   int32_t stage_tab_offset;  // shared offset of the staging table (after the largest staged footprint)
+  int32_t defer_offset;      // pipelined mode: shared offset of the per-warp deferred-store buffers
+  int32_t pad0_;
   uint32_t* cnt;                 // [active_warps] fix-up arrival counters (zero between launches)
   unsigned long long* rec;       // [active_warps][2][B][32] fix-up records {partial, flag}
   uint64_t* trace;               // optional [active_warps][8] %globaltimer stamps (debug)
@@ -97,7 +125,7 @@ __host__ __device__ constexpr int pq_row_bytes(int B, int G, int cols) {
   return ((pq_entries(B, G, cols) + 2) * 8 + 15) / 16 * 16;  // + zero entries for padding
 }
 
-const void* select_kernel(int bits, int G, int B);
+const void* select_kernel(int bits, int G, int B, int half = 0);
 
 // LAYOUT-TC kernel (gqsa_tc.cu): one GEMM over 16-row blocks on mma.sync.
 constexpr int kTcWarps = 16;

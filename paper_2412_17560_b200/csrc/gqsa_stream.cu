@@ -93,6 +93,35 @@ __device__ __forceinline__ void store_rows(const Params& p, const Item& it, floa
   }
 }
 
+// Pipelined mode: reduce over the row's S lanes as store_rows does, but keep
+// the result in the warp's shared-memory buffer slot k (the lane that would
+// store it records row | item << 28, the others -1).
+template <int B>
+__device__ __forceinline__ void defer_rows(const Item& it, float (&v)[B], int row, int item, int lane, uint32_t* buf,
+                                           int k) {
+  const int S = it.lanes_per_row;
+  for (int d = 1; d < S; d <<= 1) {
+#pragma unroll
+    for (int b = 0; b < B; ++b) v[b] += __shfl_xor_sync(0xffffffffu, v[b], d);
+  }
+  uint32_t* e = buf + k * 32 * (B + 1);
+  e[lane] = (row >= 0 && (lane & (S - 1)) == 0) ? ((uint32_t)row | ((uint32_t)item << 28)) : 0xffffffffu;
+#pragma unroll
+  for (int b = 0; b < B; ++b) e[(b + 1) * 32 + lane] = __float_as_uint(v[b]);
+}
+template <int B>
+__device__ __forceinline__ void flush_deferred(const Params& p, const Item* items, const uint32_t* buf, int k,
+                                               int lane) {
+  const uint32_t* e = buf + k * 32 * (B + 1);
+  const uint32_t ri = e[lane];
+  if (ri == 0xffffffffu) return;
+  const int row = (int)(ri & 0x0fffffffu);
+  const Item& it = items[ri >> 28];
+  const float bias = it.bias ? __ldg(it.bias + row) : 0.f;
+#pragma unroll
+  for (int b = 0; b < B; ++b) store_y(it, p.out_f16, (int64_t)b * it.ldy + row, __uint_as_float(e[(b + 1) * 32 + lane]) + bias);
+}
+
 // ---------------------------------------------------------------- fix-up
 // Record of warp w for its head (which = 0) or tail (which = 1) slice:
 // [B][32 lanes] 8-byte words {partial, flag}; each is ONE 64-bit store, so a
@@ -152,25 +181,32 @@ __device__ __noinline__ void collect(const Params& p, const Item* items, int w0,
   float v[B];
 #pragma unroll
   for (int b = 0; b < B; ++b) v[b] = 0.f;
-  constexpr int kBatch = kRec;  // records requested per round trip
-  for (int wb = w0; wb <= w1; wb += kBatch) {
+  // records requested per round trip: all of them are loaded before the
+  // first is waited on, so a slice split over many warps costs few round trips
+  constexpr int KB = B <= 2 ? 16 / B : kRec;
+  static_assert(KB >= kRec, "the pre-requested records fit the first batch");
+  for (int wb = w0; wb <= w1; wb += KB) {
+    unsigned long long r[KB][B];
 #pragma unroll
-    for (int b = 0; b < B; ++b) {
-      unsigned long long r[kBatch];
+    for (int k = 0; k < KB; ++k)
 #pragma unroll
-      for (int k = 0; k < kBatch; ++k)
-        r[k] = wb == w0 ? q.r[k][b] : (wb + k <= w1) ? ld_relaxed64(rec_ptr<B>(p, wb + k, 0, b, lane)) : 0ull;
+      for (int b = 0; b < B; ++b)
+        r[k][b] = (wb == w0 && k < kRec) ? q.r[k][b]
+                  : (wb + k <= w1)       ? ld_relaxed64(rec_ptr<B>(p, wb + k, wb + k == w0 ? 1 : 0, b, lane))
+                                         : 0ull;
 #pragma unroll
-      for (int k = 0; k < kBatch; ++k) {
-        if (wb + k > w1) break;
+    for (int k = 0; k < KB; ++k) {
+      if (wb + k > w1) break;
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
         unsigned long long* a = rec_ptr<B>(p, wb + k, wb + k == w0 ? 1 : 0, b, lane);
         unsigned int spins = 0;
-        while ((r[k] >> 32) == 0ull) {
+        while ((r[k][b] >> 32) == 0ull) {
           if (++spins > (1u << 26)) __trap();  // a lost record: fail loudly, never hang
           __nanosleep(32);
-          r[k] = ld_relaxed64(a);
+          r[k][b] = ld_relaxed64(a);
         }
-        v[b] = (wb + k == w0) ? __uint_as_float((uint32_t)r[k]) : v[b] + __uint_as_float((uint32_t)r[k]);
+        v[b] = (wb + k == w0) ? __uint_as_float((uint32_t)r[k][b]) : v[b] + __uint_as_float((uint32_t)r[k][b]);
         st_relaxed64(a, 0ull);
       }
     }
@@ -205,9 +241,10 @@ __device__ __forceinline__ void trace_point(const Params& p, int gw, int lane, i
 
 }  // namespace
 
-template <int BITS, int B, int G>
-__global__ void __launch_bounds__(32 * warps_for(B), min_blocks_for(B)) gqsa_stream_kernel(const __grid_constant__ Params p) {
-  constexpr int W = warps_for(B);
+template <int BITS, int B, int G, int HALF>
+__global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? kPipeCtas : min_blocks_for(B))
+    gqsa_stream_kernel(const __grid_constant__ Params p) {
+  constexpr int W = warps_of(B, HALF);
   constexpr int TB = tile_bytes(BITS, G);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -269,11 +306,16 @@ __global__ void __launch_bounds__(32 * warps_for(B), min_blocks_for(B)) gqsa_str
       lend = its[li].tile_end;
     }
     load_tile<BITS, G>(r, lptr, lane, pol);
-    if (kL2Pf > kBufs && lane == 0 && t + kL2Pf < min(t_end, lend)) prefetch_l2(lptr + (size_t)kL2Pf * TB, TB);
+    if (kL2Pf > kBufs && lane == 0 && t + kL2Pf >= t_begin + kL2Pf0 && t + kL2Pf < min(t_end, lend))
+      prefetch_l2(lptr + (size_t)kL2Pf * TB, TB);
     lptr += TB;
   };
-  if (kL2Pf > kBufs && lane == 0 && t_end > t_begin) {  // tiles the first refills need (later ones: issue())
-    for (int k = kBufs; k < kL2Pf && t_begin + k < min(t_end, lend); ++k) prefetch_l2(lptr + (size_t)k * TB, TB);
+  if (kL2Pf > kBufs && lane == 0 && t_end > t_begin) {
+    // the tiles after the register buffers, up to kL2Pf0 ahead, as ONE bulk
+    // prefetch (they are contiguous within the item): HBM keeps streaming this
+    // launch's weights while it waits for the previous kernel (later tiles: issue())
+    const int n = min(t_begin + kL2Pf0, min(t_end, lend)) - (t_begin + kBufs);
+    if (n > 0) prefetch_l2(lptr + (size_t)kBufs * TB, (uint32_t)(n * TB));
   }
 #pragma unroll
   for (int k = 0; k < kBufs; ++k)
@@ -357,10 +399,19 @@ __global__ void __launch_bounds__(32 * warps_for(B), min_blocks_for(B)) gqsa_str
   // first-warp fast path: the successors' head records, requested during the last tile
   constexpr int kPre = B <= 2 ? 3 : 0;
   unsigned long long pre[kPre > 0 ? kPre : 1][B];
+  bool pre_loaded = false;
+  // pipelined mode: rows of slices closed before the PDL wait, buffered per
+  // lane in shared memory ([slot][lane] row | item << 28, then [slot][b][lane]
+  // values), and the head slice's partial (published after the wait)
+  uint32_t* dbuf = HALF ? reinterpret_cast<uint32_t*>(smem + p.defer_offset + warp * defer_bytes_per_warp(B)) : nullptr;
+  int n_def = 0;
+  bool h_defer = false;
+  float hacc[B];
   trace_point(p, gw, lane, 3);
 
   auto consume = [&](const TileRegs<BITS, G>& tr, int t) {
-    if (kPre > 0 && t == t_end - 1 && cend > t_end && !foreign) {
+    if (kPre > 0 && t == t_end - 1 && cend > t_end && !foreign && waited) {
+      pre_loaded = true;
       // this warp owns the slice left open at its range end: request the
       // successors' records now, so they are here when the tile is done
       const int n = warp_of_tile(p, cend - 1) - gw;
@@ -374,19 +425,24 @@ __global__ void __launch_bounds__(32 * warps_for(B), min_blocks_for(B)) gqsa_str
     for (int u = 0; u < kPerLane; ++u) group_accumulate<BITS, B, G>(tr, u, acc, xv);
     if (p.trace && t == t_begin) trace_point(p, gw, lane, 6);  // first tile landed and consumed
     if (t + 1 == cend) {  // the slice ends with this tile: its rows are complete here
-      ensure_wait();
-#ifdef GQSA_EXP_NOFIX
-      if (false) {
-#else
+      if (!HALF) ensure_wait();
       if (foreign) {  // ... but began upstream: publish, arrive, check at the range end
-#endif
-        publish<B>(p, gw, 0, acc, lane);
-        h_old = arrive(p, cw0, lane);
-        h_pending = true;
         h_w0 = cw0;
         h_item = ci;
         h_row = crow;
+        if (HALF && !waited) {  // publish after the wait
+          h_defer = true;
+#pragma unroll
+          for (int b = 0; b < B; ++b) hacc[b] = acc[b];
+        } else {
+          publish<B>(p, gw, 0, acc, lane);
+          h_old = arrive(p, cw0, lane);
+          h_pending = true;
+        }
+      } else if (HALF && !waited && n_def < kDeferSlots) {
+        defer_rows<B>(its[ci], acc, crow, ci, lane, dbuf, n_def++);
       } else {
+        ensure_wait();
         store_rows<B>(p, its[ci], acc, crow, lane);
       }
 #pragma unroll
@@ -418,14 +474,26 @@ __global__ void __launch_bounds__(32 * warps_for(B), min_blocks_for(B)) gqsa_str
   }
   trace_point(p, gw, lane, 4);
   ensure_wait();
+  if (HALF) {  // the writes deferred during the loop
+    for (int k = 0; k < n_def; ++k) flush_deferred<B>(p, its, dbuf, k, lane);
+    if (h_defer) {
+      publish<B>(p, gw, 0, hacc, lane);
+      h_old = arrive(p, h_w0, lane);
+      h_pending = true;
+    }
+  }
+  if (kPre > 0 && cend > t_end && !foreign && !pre_loaded) {  // not requested during the last tile (x_ready)
+    const int n = warp_of_tile(p, cend - 1) - gw;
+#pragma unroll
+    for (int k = 0; k < kPre; ++k)
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+        pre[k][b] = k < n ? ld_relaxed64(rec_ptr<B>(p, gw + 1 + k, 0, b, lane)) : (1ull << 32);
+  }
 
   int fix_path = 0;  // debug trace: 1 fast, 2 published (not last), 3 published + collected; +10 head collected
   // ---- a slice left open at the end of the range continues downstream
-#ifdef GQSA_EXP_NOFIX  // timing experiment only: results are wrong
-  if (false) {
-#else
   if (cend > t_end) {
-#endif
     const int w1 = warp_of_tile(p, cend - 1);
     bool done = false;
     if (kPre > 0 && !foreign && w1 - gw <= kPre) {
@@ -481,15 +549,15 @@ __global__ void __launch_bounds__(32 * warps_for(B), min_blocks_for(B)) gqsa_str
 }
 
 // ---------------------------------------------------------------- selection
-template <int BITS, int B, int G = kGroup>
+template <int BITS, int B, int G = kGroup, int HALF = 0>
 const void* kernel_ptr() {
-  return reinterpret_cast<const void*>(&gqsa_stream_kernel<BITS, B, G>);
+  return reinterpret_cast<const void*>(&gqsa_stream_kernel<BITS, B, G, HALF>);
 }
 
 #define GQSA_KSEL(BITS, G)                    \
   switch (B) {                                \
-    case 1: return kernel_ptr<BITS, 1, G>();  \
-    case 2: return kernel_ptr<BITS, 2, G>();  \
+    case 1: return half ? kernel_ptr<BITS, 1, G, 1>() : kernel_ptr<BITS, 1, G>();  \
+    case 2: return half ? kernel_ptr<BITS, 2, G, 1>() : kernel_ptr<BITS, 2, G>();  \
     case 3: return kernel_ptr<BITS, 3, G>();  \
     case 4: return kernel_ptr<BITS, 4, G>();  \
     case 5: return kernel_ptr<BITS, 5, G>();  \
@@ -499,7 +567,8 @@ const void* kernel_ptr() {
     default: return nullptr;                  \
   }
 
-const void* select_kernel(int bits, int G, int B) {
+const void* select_kernel(int bits, int G, int B, int half) {
+  if (half && B > 2) return nullptr;
 #ifdef GQSA_FAST_BUILD  // experiments: W4, G = 16 only
   if (bits == 4 && G == kGroup) { GQSA_KSEL(4, 16) }
   return nullptr;

@@ -88,7 +88,7 @@ EXPORTS = (
     "gqsa_gemm_hostio",
     "gqsa_compress_nnzg", "gqsa_compress", "gqsa_multi_hostio_stage_size", "gqsa_gemm_multi_hostio",
     "gqsa_gemm_allgather",
-    "gqsa_launch_plan", "gqsa_launch_count", "gqsa_status_string", "gqsa_version",
+    "gqsa_launch_plan", "gqsa_launch_plan_ex", "gqsa_launch_count", "gqsa_status_string", "gqsa_version",
     "gqsa_debug_trace",
 )
 
@@ -225,9 +225,12 @@ def hostio_stage_size(desc: Desc, batch: int = 1) -> int:
     return n.value
 
 
-def launch_plan(desc: Desc, batch: int = 1) -> Plan:
+def launch_plan(desc: Desc, batch: int = 1, x_ready: bool = False) -> Plan:
+    """gqsa_launch_plan_ex with default options except x_ready."""
     p = Plan()
-    _check(lib().gqsa_launch_plan(ctypes.byref(desc), int(batch), ctypes.byref(p)), "gqsa_launch_plan")
+    opts = Options(PARTITION_STREAM_K, 0, int(bool(x_ready)), 0)
+    _check(lib().gqsa_launch_plan_ex(ctypes.byref(desc), int(batch), ctypes.byref(opts), ctypes.byref(p)),
+           "gqsa_launch_plan_ex")
     return p
 
 

@@ -71,12 +71,13 @@ def test_grouped_exact_integer_bit_exact(shapes, bits, B):
         items.append((desc, d_blob, _x(x), Y, None))
         refs.append(O.gemv(bsr, x))
     for part in (gqsa.PARTITION_STREAM_K, gqsa.PARTITION_SLICE_K):
-        for it in items:
-            it[3].fill_(float("nan"))
-        _, launches = run_grouped(items, partition=part)
-        assert launches == 1
-        for it, ref in zip(items, refs):
-            assert np.array_equal(it[3].cpu().numpy().astype(np.float64), ref), part
+        for x_ready in (False, True):  # x_ready at B <= 2: the pipelined half-SM launch
+            for it in items:
+                it[3].fill_(float("nan"))
+            _, launches = run_grouped(items, partition=part, x_ready=x_ready)
+            assert launches == 1
+            for it, ref in zip(items, refs):
+                assert np.array_equal(it[3].cpu().numpy().astype(np.float64), ref), (part, x_ready)
 
 
 @pytest.mark.parametrize("shapes,bits,sp,B", [
@@ -108,7 +109,9 @@ def test_grouped_realistic_gates_llama_shapes(shapes, bits, sp, B):
 
 def test_grouped_matches_single_launches_within_gates_and_x_ready():
     """Each item of a grouped launch agrees with its own single launch (the
-    fp32 order may differ); x_ready = 1 gives bit-identical results to 0."""
+    fp32 order may differ); x_ready = 1 (at B <= 2 the pipelined launch over
+    half of every SM: another grid, so another fp32 order) agrees within the
+    gates and is bit-identical across reruns."""
     shapes = [(1024, 4096), (2048, 2048), (512, 14336)]
     items, singles, data = [], [], []
     for i, (rows, cols) in enumerate(shapes):
@@ -119,11 +122,80 @@ def test_grouped_matches_single_launches_within_gates_and_x_ready():
         singles.append(L.gemm(_x(x)))
         data.append((bsr, x))
     run_grouped(items)
-    base = [it[3].clone() for it in items]
-    run_grouped(items, x_ready=True)
-    for it, b, s, (bsr, x) in zip(items, base, singles, data):
-        assert torch.equal(it[3], b)
+    for it, s, (bsr, x) in zip(items, singles, data):
         check_gates(it[3].cpu().numpy(), s.cpu().numpy().astype(np.float64), abs_bound(bsr, x), "grouped vs single")
+    run_grouped(items, x_ready=True)
+    base = [it[3].clone() for it in items]
+    for it, s, (bsr, x) in zip(items, singles, data):
+        check_gates(it[3].cpu().numpy(), s.cpu().numpy().astype(np.float64), abs_bound(bsr, x), "x_ready vs single")
+    for _ in range(3):
+        run_grouped(items, x_ready=True)
+        for it, b in zip(items, base):
+            assert torch.equal(it[3], b), "x_ready reruns must be bit-identical"
+
+
+@pytest.mark.parametrize("use_graph", [False, True])
+def test_pipelined_back_to_back_launches(use_graph):
+    """Consecutive x_ready launches on one stream overlap (each takes half of
+    every SM; the next one streams and stages while this one drains) and share
+    ONE workspace: every launch's results stay exact, also interleaved with a
+    dependent x_ready = 0 launch that reads the previous launch's fp16 output,
+    and when the whole sequence is replayed from a CUDA graph."""
+    B = 1
+    sets = []
+    for k in range(4):
+        shapes = [(1024, 4096), (3000, 1024), (512, 2048)][: 1 + k % 3]
+        items, refs = [], []
+        for i, (rows, cols) in enumerate(shapes):
+            seed = synth.seed_for(f"pipe/{k}/{i}")
+            bsr = synth.make_layer(seed, rows, cols, sparsity=0.5, mode="exact_int")
+            x = synth.make_x(seed + 1, B, cols, mode="exact_int")
+            desc, d_blob = _dev_blob(bsr)
+            items.append((desc, d_blob, _x(x), torch.empty(B, rows, dtype=torch.float32, device="cuda"), None))
+            refs.append(O.gemv(bsr, x))
+        sets.append((items, refs))
+    # a dependent pair: A writes fp16 y (exact: small integers), B reads it as its x
+    bA = synth.make_layer(7001, 2048, 1024, sparsity=0.5, mode="exact_int")
+    xA = synth.make_x(7002, B, 1024, mode="exact_int")
+    yA_ref = O.gemv(bA, xA)
+    bB = synth.make_layer(7003, 512, 2048, sparsity=0.5, mode="exact_int")
+    assert np.all(np.abs(yA_ref) < 2048)
+    yB_ref = O.gemv(bB, yA_ref.astype(np.float16).view(np.uint16))
+    dA, blobA = _dev_blob(bA)
+    dB, blobB = _dev_blob(bB)
+    YA = torch.empty(B, 2048, dtype=torch.float16, device="cuda")
+    YB = torch.empty(B, 512, dtype=torch.float32, device="cuda")
+    ws = _ws(B)
+    s = torch.cuda.Stream()
+
+    def seq():
+        for rep in range(3):
+            for items, _ in sets:
+                gqsa.gemm_grouped(items, ws, x_ready=True, stream=s)
+            gqsa.gemm_grouped([(dA, blobA, _xA, YA, None)], ws, x_ready=True, stream=s)
+            gqsa.gemm_grouped([(dB, blobB, YA, YB, None)], ws, x_ready=False, stream=s)
+
+    _xA = _x(xA)
+    for items, _ in sets:
+        for it in items:
+            it[3].fill_(float("nan"))
+    YB.fill_(float("nan"))
+    torch.cuda.synchronize()
+    if use_graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            seq()
+        g.replay()
+        g.replay()
+    else:
+        seq()
+    torch.cuda.synchronize()
+    assert int(ws.count_nonzero()) == 0, "workspace must be left zero"
+    for items, refs in sets:
+        for it, ref in zip(items, refs):
+            assert np.array_equal(it[3].cpu().numpy().astype(np.float64), ref)
+    assert np.array_equal(YA.cpu().numpy().astype(np.float64), yA_ref.astype(np.float16).astype(np.float64))
+    assert np.array_equal(YB.cpu().numpy().astype(np.float64), yB_ref)
 
 
 def test_grouped_bias_and_fp16_output():

@@ -216,7 +216,7 @@ def test_read_desc_rejects_corruption():
 
 def test_lanes_per_row_rule():
     # long rows are dealt over several lanes: the longest slice has at most
-    # `target` slots per lane, target = 16 / 32 / 64 for layers under 1.6 /
+    # `target` slots per lane, target = 16 / 128 / 256 for layers under 1.6 /
     # 4 / more tiles per warp of a 148 x 16-warp grid
     for rows, cols in ((256, 4096), (64, 14336), (8, 4096), (3, 256), (64, 512), (1, 32736),
                        (14336, 4096), (4096, 4096)):
@@ -224,11 +224,11 @@ def test_lanes_per_row_rule():
         _, d = gqsa.pack(bsr)
         S = (d.flags >> 8) & 0xFF
         tpw = d.nnzg / 128 / (148 * 16)
-        target = 16 if tpw < 1.6 else 32 if tpw < 4 else 64
+        target = 16 if tpw < 1.6 else 128 if tpw < 4 else 256
         longest = int(np.diff(bsr["row_index"]).max())
         assert -(-longest // S) <= target or S == 32
         assert S == 1 or -(-longest // (S // 2)) > target or S // 2 < 32 // (1 << (rows - 1).bit_length())
-    assert target == 32 and S == 8  # 4096 x 4096: 1.7 tiles per warp
+    assert target == 128 and S == 2  # 4096 x 4096: 1.7 tiles per warp
 
 
 def test_workspace_size_is_layer_independent():

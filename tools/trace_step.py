@@ -45,7 +45,8 @@ def main():
                           x_ready=bool(a.x_ready)) for r in range(R)]
     total_tiles = sum(d.num_tiles for _, d in packed)
     sms = torch.cuda.get_device_properties(0).multi_processor_count
-    wpc = gqsa.launch_plan(packed[0][1], 1).warps_per_cta
+    plan = gqsa.launch_plan(packed[0][1], 1, x_ready=bool(a.x_ready))
+    wpc = plan.warps_per_cta
     W = min(total_tiles, sms * wpc)
     bufs = [torch.zeros(W * 8, dtype=torch.int64, device="cuda") for _ in range(R)]
     s = torch.cuda.Stream()
@@ -63,7 +64,8 @@ def main():
     T = raw[:, :, :7].astype(np.float64)
     t0 = T[0, :, 0].min()
     T = (T - t0) / 1e3
-    print(f"grouped step: warps={W} tiles={total_tiles} x_ready={a.x_ready} R={R}")
+    print(f"grouped step: warps={W} ({wpc} per CTA, pipelined={plan.coresident}) tiles={total_tiles} "
+          f"x_ready={a.x_ready} R={R}")
     print("step    " + "  ".join(f"{n:>17s}" for n in NAMES) + "   (min/median/max µs)")
     for i in range(a.steps):
         cols = [f"{T[i, :, k].min():5.2f}/{np.median(T[i, :, k]):5.2f}/{T[i, :, k].max():5.2f}" for k in range(7)]
