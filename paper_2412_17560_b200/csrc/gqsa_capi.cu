@@ -145,13 +145,13 @@ int plan_launch(const gqsa_desc_t* const* d, int n, int Bc, Launch* L, int half 
 // The launch of n items at batch Bc under options o: the pipelined mode
 // (half of every SM, deferred writes) when X is declared ready -- the launch
 // may then overlap the previous one on the stream -- and its footprint fits
-// kPipeCtas times per SM; else the whole-SM launch.
+// pipe_ctas_for(Bc) times per SM; else the whole-SM launch.
 int choose_launch(const gqsa_desc_t* const* d, int n, int Bc, const gqsa_options_t& o, Launch* L) {
   int st = GQSA_OK;
   const int mode = pipeline_mode();
   if (Bc <= 2 && (mode == 2 || (mode == 1 && o.x_ready))) {
     if ((st = plan_launch(d, n, Bc, L, 1))) return st;
-    if (L->smem <= (size_t)kHalfSmemLimit) return GQSA_OK;
+    if (L->smem <= (size_t)half_smem_limit(Bc)) return GQSA_OK;
   }
   return plan_launch(d, n, Bc, L);
 }
@@ -462,8 +462,8 @@ extern "C" int gqsa_launch_plan_ex(const gqsa_desc_t* desc, int32_t B, const gqs
   plan->num_tiles = L.total_tiles;
   plan->smem_bytes = (int32_t)L.smem;
   plan->x_in_smem = 1;
-  plan->stages = kBufs;
-  plan->ctas_per_sm = L.half ? kPipeCtas : 1;
+  plan->stages = bufs_for(Bc);
+  plan->ctas_per_sm = L.half ? pipe_ctas_for(Bc) : 1;
   plan->ring_bytes = 0;
   plan->batch_per_launch = Bc;
   plan->launches = (B + Bc - 1) / Bc;

@@ -19,25 +19,29 @@ constexpr int kMaxBatch = 8;
 constexpr int kMaxPeers = 8;            // ranks of a fused all-gather (one NVLink domain)
 constexpr int kSmemPerSm = 228 * 1024;  // shared memory per SM
 constexpr int kMaxDynSmem = 225 * 1024; // opt-in dynamic shared memory per CTA (227 KB - the static item table)
-// Tile register buffers per warp: while one tile is consumed the next
-// kBufs - 1 are in flight (HBM -> registers, no shared-memory staging).
-#ifndef GQSA_BUFS
-#define GQSA_BUFS 2
+// Tile register buffers per warp (HBM -> registers, no shared-memory
+// staging): one at B <= 2, where more warps (fewer registers each) plus L2
+// prefetching keep more bytes in flight than a second register buffer does
+// (bench step 11.8 vs 12.6 us); two above.
+#ifndef GQSA_BUFS_SMALL
+#define GQSA_BUFS_SMALL 1
 #endif
-constexpr int kBufs = GQSA_BUFS;
-// L2 prefetch distance in tiles (<= kBufs: off): lane 0 issues
-// cp.async.bulk.prefetch.L2 for tile t + kL2Pf as it requests tile t into
-// registers, so each warp keeps kL2Pf tiles moving from HBM while only kBufs
-// occupy registers (bench step, pipelined: 15.1 -> 13.6 us at 3; 4: 13.8, 6: 14.2).
-#ifndef GQSA_L2PF
-#define GQSA_L2PF 3
+#ifndef GQSA_BUFS_LARGE
+#define GQSA_BUFS_LARGE 2
 #endif
-constexpr int kL2Pf = GQSA_L2PF;
-// Tiles prefetched to L2 at the start of a warp's range (before the PDL wait), >= kL2Pf.
-#ifndef GQSA_L2PF0
-#define GQSA_L2PF0 GQSA_L2PF
+__host__ __device__ constexpr int bufs_for(int B) { return B <= 2 ? GQSA_BUFS_SMALL : GQSA_BUFS_LARGE; }
+// L2 prefetch distance in tiles (<= the register buffers: off): lane 0 issues
+// cp.async.bulk.prefetch.L2 for tile t + d as it requests tile t into
+// registers, so each warp keeps d tiles moving from HBM while only the
+// register buffers hold data (bench step, measured: d = 2..4 within 1 %;
+// no prefetch with two register buffers: 15.1 us).
+#ifndef GQSA_L2PF_SMALL
+#define GQSA_L2PF_SMALL 2
 #endif
-constexpr int kL2Pf0 = GQSA_L2PF0 > GQSA_L2PF ? GQSA_L2PF0 : GQSA_L2PF;
+#ifndef GQSA_L2PF_LARGE
+#define GQSA_L2PF_LARGE 3
+#endif
+__host__ __device__ constexpr int l2pf_for(int B) { return B <= 2 ? GQSA_L2PF_SMALL : GQSA_L2PF_LARGE; }
 // Warps per CTA (one CTA per SM): more warps keep more weight loads in
 // flight (a read-only stream of the same tiles reaches 4.9 / 5.3 / 5.5 TB/s
 // with 16 / 24 / 32 warps per SM on the 59 MB bench step,
@@ -63,19 +67,25 @@ __host__ __device__ constexpr int min_blocks_for(int B) { return B <= 2 ? GQSA_M
 // and tile loop on the other half while this one drains; every global write
 // of the loop is deferred until after griddepcontrol.wait.
 #ifndef GQSA_WARPS_HALF
-#define GQSA_WARPS_HALF 10
+#define GQSA_WARPS_HALF 8
 #endif
 #ifndef GQSA_PIPE_CTAS
-#define GQSA_PIPE_CTAS 2
+#define GQSA_PIPE_CTAS 3
 #endif
-constexpr int kPipeCtas = GQSA_PIPE_CTAS;  // resident CTAs per SM the pipelined kernel is compiled for
+// Resident CTAs per SM the pipelined kernel is compiled for: three launches
+// in flight at B = 1 (8 warps each, <= 80 registers: bench step 11.8 -> 11.2 us
+// against two of 12 warps); two at B = 2 (its accumulators need the registers).
+__host__ __device__ constexpr int pipe_ctas_for(int B) { return B == 1 ? GQSA_PIPE_CTAS : 2; }
 __host__ __device__ constexpr int warps_half(int B) { return B == 1 ? GQSA_WARPS_HALF : 8; }
 __host__ __device__ constexpr int warps_of(int B, int half) { return half ? warps_half(B) : warps_for(B); }
 // Deferred row stores buffered per warp in shared memory before the wait
 // (more closed slices than this in one range: the warp waits and stores).
 constexpr int kDeferSlots = 8;
 __host__ __device__ constexpr int defer_bytes_per_warp(int B) { return kDeferSlots * 32 * 4 * (B + 1); }
-constexpr int kHalfSmemLimit = (kSmemPerSm - kPipeCtas * 2048) / kPipeCtas;  // per CTA, kPipeCtas CTAs per SM
+// dynamic shared memory per CTA of a pipelined launch (pipe_ctas_for(B) CTAs per SM)
+__host__ __device__ constexpr int half_smem_limit(int B) {
+  return (kSmemPerSm - pipe_ctas_for(B) * 2048) / pipe_ctas_for(B);
+}
 constexpr int kMaxWarpsBound = 148 * 32;  // fix-up records the workspace holds per launch (any B200 grid)
 
 // One GEMV of a launch.  Its tiles occupy global tile indices

@@ -16,7 +16,7 @@
 //    into contiguous, equal (+-1 tile) ranges, one per WARP, regardless of
 //    row, slice or item boundaries.
 //  * Weights stream HBM -> registers (128-bit no-allocate loads, evict-first
-//    L2 policy), kBufs tiles per warp in flight, the first ones requested
+//    L2 policy) plus L2 bulk prefetches a few tiles ahead, the first ones requested
 //    BEFORE griddepcontrol.wait (they never depend on the previous kernel).
 //    No shared-memory staging of weights: shared memory serves only the
 //    activation gathers.
@@ -242,7 +242,7 @@ __device__ __forceinline__ void trace_point(const Params& p, int gw, int lane, i
 }  // namespace
 
 template <int BITS, int B, int G, int HALF>
-__global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? kPipeCtas : min_blocks_for(B))
+__global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B) : min_blocks_for(B))
     gqsa_stream_kernel(const __grid_constant__ Params p) {
   constexpr int W = warps_of(B, HALF);
   constexpr int TB = tile_bytes(BITS, G);
@@ -291,6 +291,7 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? kPipeCtas : min
   // ---- the first tiles: requested before anything else (weights never
   //      depend on the previous kernel on the stream)
   const uint64_t pol = evict_first_policy();
+  constexpr int kBufs = bufs_for(B), kL2Pf = l2pf_for(B);
   TileRegs<BITS, G> buf[kBufs];
   int li = 0, lend = 0;  // load cursor: item, end of its tiles
   const uint8_t* lptr = nullptr;
@@ -306,15 +307,14 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? kPipeCtas : min
       lend = its[li].tile_end;
     }
     load_tile<BITS, G>(r, lptr, lane, pol);
-    if (kL2Pf > kBufs && lane == 0 && t + kL2Pf >= t_begin + kL2Pf0 && t + kL2Pf < min(t_end, lend))
-      prefetch_l2(lptr + (size_t)kL2Pf * TB, TB);
+    if (kL2Pf > kBufs && lane == 0 && t + kL2Pf < min(t_end, lend)) prefetch_l2(lptr + (size_t)kL2Pf * TB, TB);
     lptr += TB;
   };
   if (kL2Pf > kBufs && lane == 0 && t_end > t_begin) {
-    // the tiles after the register buffers, up to kL2Pf0 ahead, as ONE bulk
-    // prefetch (they are contiguous within the item): HBM keeps streaming this
-    // launch's weights while it waits for the previous kernel (later tiles: issue())
-    const int n = min(t_begin + kL2Pf0, min(t_end, lend)) - (t_begin + kBufs);
+    // the tiles between the register buffers and the prefetch distance, as
+    // ONE bulk prefetch (contiguous within the item; later tiles: issue());
+    // prefetching further ahead here measured slower
+    const int n = min(t_begin + kL2Pf, min(t_end, lend)) - (t_begin + kBufs);
     if (n > 0) prefetch_l2(lptr + (size_t)kBufs * TB, (uint32_t)(n * TB));
   }
 #pragma unroll
@@ -344,7 +344,8 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? kPipeCtas : min
     cs = __ldg(p.item[ci].tile_slice + (t_begin - p.item[ci].tile_begin));
   }
 
-  // let the next launch on the stream start its prologue (its weight loads)
+  // let the next launch on the stream start its prologue (its weight loads);
+  // triggering later (e.g. half-way through the range) measured slower
   pdl_launch_dependents();
   // x may be the previous kernel's output; with x_ready the wait is deferred
   // to just before this launch's first global write (y, records, counters)
