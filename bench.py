@@ -345,7 +345,8 @@ def run_gpu(args):
         local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    fused = args.allgather == "fused"
+    fused = args.allgather in ("fused", "nvls")
+    nvls = args.allgather == "nvls"
     if os.environ.get("NCCL_DEBUG") and not os.environ.get("NCCL_DEBUG_FILE"):
         os.environ["NCCL_DEBUG_FILE"] = "/dev/stderr"  # NCCL's log to stderr: stdout carries the JSON line
     if world > 1 or fused:
@@ -390,6 +391,9 @@ def run_gpu(args):
         hdl = [symm_mem.rendezvous(t, gname) for t in yf]
         peers = [[h.get_buffer(p, (B, L["rows"]), torch.float32) for p in range(world)]
                  for h, L in zip(hdl, layers)]
+        if nvls and not all(getattr(h, "multicast_ptr", 0) for h in hdl):
+            raise SystemExit("--allgather nvls: symmetric memory has no multicast object on this system "
+                             "(NVLS needs a multicast-capable NVSwitch domain of >= 2 GPUs)")
 
     path = "launches" if fused else args.path
     grouped = [gqsa.Grouped([(descs[i], copies[r][i], xs[i], ys[i], None) for i in range(len(layers))], ws,
@@ -399,7 +403,11 @@ def run_gpu(args):
         """The step's sparse GEMVs (this rank's shards)."""
         if fused:
             for i in range(len(layers)):
-                gqsa.gemm_allgather(descs[i], copies[r][i], xs[i], peers[i], row_offset=layers[i]["lo"], ws=ws)
+                if nvls:  # one multimem.st per element; the NVSwitch replicates it to every rank
+                    gqsa.gemm_allgather_multicast(descs[i], copies[r][i], xs[i], hdl[i].multicast_ptr,
+                                                  ldy=layers[i]["rows"], row_offset=layers[i]["lo"], ws=ws)
+                else:
+                    gqsa.gemm_allgather(descs[i], copies[r][i], xs[i], peers[i], row_offset=layers[i]["lo"], ws=ws)
                 hdl[i].barrier(channel=0)
         elif path == "grouped":
             grouped[r]()
@@ -600,8 +608,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rotate", action="store_true")
     ap.add_argument("--no-layers", action="store_true", help="skip the per-layer timing loop (ncu launch lists)")
-    ap.add_argument("--allgather", default="nccl", choices=["nccl", "fused"],
-                    help="row-shard output exchange: NCCL all_gather, or the fused GEMV epilogue storing "
+    ap.add_argument("--allgather", default="nccl", choices=["nccl", "fused", "nvls"],
+                    help="row-shard output exchange: NCCL all_gather, the fused GEMV epilogue storing (nvls: "
+                         "multicasting through NVLink SHARP) "
                          "into every rank's y over symmetric memory (gqsa_gemm_allgather)")
     ap.add_argument("--path", default="grouped", choices=["grouped", "launches"],
                     help="grouped: the step's GEMVs in one gqsa_gemm_grouped launch; launches: one gqsa_gemv "

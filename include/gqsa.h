@@ -268,6 +268,23 @@ int gqsa_gemm_allgather(const gqsa_desc_t* desc, const void* d_blob, const uint1
                         const float* d_bias, void* d_ws, size_t ws_bytes, void* stream);
 
 /*
+ * gqsa_gemm_allgather_multicast: gqsa_gemm_allgather over NVLink SHARP
+ * (NVLS): d_mc_Y is the MULTICAST address of the
+ * ranks' full-length outputs [B][ldy] (a CUDA multicast object every rank's y
+ * is bound to, e.g. torch symmetric memory's multicast_ptr); every output
+ * element of this shard is written ONCE with multimem.st and the NVSwitch
+ * replicates it into every rank's y.  Same ordering contract as
+ * gqsa_gemm_allgather (system-scope fence at the end; the caller orders the
+ * consumers after all ranks' launches).  Needs a multicast-capable device and
+ * a multicast object of >= 2 devices: not exercised on a one-GPU box
+ * (DESIGN.md §9).  fp32 output only (out_f16 = 1: GQSA_ERR_UNSUPPORTED,
+ * multimem.st has no 16-bit scalar form).  Other errors as gqsa_gemm_allgather.
+ */
+int gqsa_gemm_allgather_multicast(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_X, int32_t B,
+                                  int64_t ldx, void* d_mc_Y, int64_t ldy, int32_t row_offset, int32_t out_f16,
+                                  const float* d_bias, void* d_ws, size_t ws_bytes, void* stream);
+
+/*
  * gqsa_gemm_grouped: n INDEPENDENT GEMMs (e.g. the q/k/v or gate/up
  * projections of a decoder step, or the step's layers when their inputs are
  * ready) in ONE launch: Y_j[b] = W_hat_j X_j[b] (+ bias_j), j < n.  The tile

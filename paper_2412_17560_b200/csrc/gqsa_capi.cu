@@ -54,6 +54,15 @@ int pipeline_mode() {
   return mode;
 }
 
+// Minimum tiles per warp when sizing a launch's warps per CTA (0 = off); A/B knob GQSA_MIN_TPW.
+int min_tiles_per_warp() {
+  static const int v = [] {
+    const char* e = std::getenv("GQSA_MIN_TPW");
+    return e ? std::atoi(e) : kMinTilesPerWarp;
+  }();
+  return v;
+}
+
 bool lanes_per_row_ok(uint32_t s) { return s >= 1 && s <= 32 && (s & (s - 1)) == 0; }
 
 bool is_tc(const gqsa_desc_t* d) { return ((uint32_t)d->flags & kFlagTC) != 0; }
@@ -106,7 +115,13 @@ int plan_launch(const gqsa_desc_t* const* d, int n, int Bc, Launch* L, int half 
   }
   if (total > INT32_MAX / 2) return GQSA_ERR_SHAPE;
   L->total_tiles = (int)total;
-  const int warps = std::min(sms * L->W, kMaxWarpsBound);
+  // small launches: fewer warps per CTA (on every SM), so each warp streams
+  // at least min_tiles_per_warp() tiles -- shorter fix-up chains, less
+  // per-warp start-up, and CTAs small enough for the next launch to be
+  // resident beside them
+  const int mt = min_tiles_per_warp();
+  if (mt > 0) L->W = (int)std::max<int64_t>(1, std::min<int64_t>(L->W, (total + (int64_t)sms * mt - 1) / ((int64_t)sms * mt)));
+  const int warps = std::min(sms * L->W * (half ? 1 : full_ctas_for(Bc)), kMaxWarpsBound);
   L->active = (int)std::min<int64_t>(total, warps);
   L->part_q = L->active ? L->total_tiles / L->active : 0;
   L->part_r = L->active ? L->total_tiles % L->active : 0;
@@ -188,6 +203,7 @@ int set_attrs(const void* fn) {
 // Fused all-gather destinations of one item (n == 0: plain Y).
 struct Peers {
   int n = 0;
+  int mc = 0;  // y[0] is a multicast address
   int32_t row_offset = 0;
   void* y[kMaxPeers] = {};
 };
@@ -238,6 +254,7 @@ int launch_items(const gqsa_gemm_item_t* items, int n, int Bc, const gqsa_option
     rows += desc->rows;
     if (peers && peers->n) {
       it.n_peers = peers->n;
+      it.peer_mc = peers->mc;
       it.row_offset = peers->row_offset;
       for (int k = 0; k < peers->n; ++k)  // batch chunk offset is folded into d_Y relative to peer 0
         it.peer_y[k] = reinterpret_cast<uint64_t>(peers->y[k]) +
@@ -518,6 +535,29 @@ extern "C" int gqsa_gemm_allgather(const gqsa_desc_t* desc, const void* d_blob, 
   peers.row_offset = row_offset;
   for (int k = 0; k < n_peers; ++k) peers.y[k] = d_peer_Y[k];
   const gqsa_gemm_item_t it{desc, d_blob, d_X, ldx, d_peer_Y[0], ldy, d_bias};
+  return run_grouped(&it, 1, B, o, d_ws, ws_bytes, stream, &peers);
+}
+
+extern "C" int gqsa_gemm_allgather_multicast(const gqsa_desc_t* desc, const void* d_blob, const uint16_t* d_X,
+                                             int32_t B, int64_t ldx, void* d_mc_Y, int64_t ldy, int32_t row_offset,
+                                             int32_t out_f16, const float* d_bias, void* d_ws, size_t ws_bytes,
+                                             void* stream) {
+  if (!desc || !d_blob || !d_X || !d_mc_Y || !d_ws) return GQSA_ERR_BUFFER;
+  if (!desc_ok(desc)) return GQSA_ERR_VALIDATION;
+  if (is_tc(desc)) return GQSA_ERR_UNSUPPORTED;
+  if (B < 1 || B > kMaxBatch || (out_f16 != 0 && out_f16 != 1)) return GQSA_ERR_SHAPE;
+  if (out_f16) return GQSA_ERR_UNSUPPORTED;  // multimem.st has no 16-bit scalar form
+  if (row_offset < 0 || ldy < (int64_t)row_offset + desc->rows || ldx < desc->cols || ldx % 8) return GQSA_ERR_SHAPE;
+  if (!aligned(d_mc_Y, 4) || !aligned(d_blob, 256) || !aligned(d_X, 16) ||
+      (d_bias && !aligned(d_bias, 4)))
+    return GQSA_ERR_BUFFER;
+  const gqsa_options_t o{GQSA_PARTITION_STREAM_K, out_f16, 0, 0};
+  Peers peers;
+  peers.n = 1;
+  peers.mc = 1;
+  peers.row_offset = row_offset;
+  peers.y[0] = d_mc_Y;
+  const gqsa_gemm_item_t it{desc, d_blob, d_X, ldx, d_mc_Y, ldy, d_bias};
   return run_grouped(&it, 1, B, o, d_ws, ws_bytes, stream, &peers);
 }
 

@@ -281,15 +281,9 @@ struct StageEntry {
 };
 constexpr int kStageTabBytes = kMaxItems * (int)sizeof(StageEntry) + 16;
 static_assert(sizeof(StageEntry) == 40, "gqsa_capi.cu kStageTab");
-template <int BITS, int B, int G>
-__device__ __forceinline__ void stage_all(const Params& p, int t0, int t1, uint8_t* sm, StageEntry* tab) {
-  constexpr int NC = G / 8;            // 16-B chunks per column group
-#ifndef GQSA_STAGE_U
-#define GQSA_STAGE_U 4
-#endif
-  constexpr int U = NC >= 4 ? 2 : GQSA_STAGE_U;  // column groups per thread in flight per round
-  constexpr int PG = (G == 16 && B <= 2) ? 2 : 1;  // (-P, -Q) entries per column group (one per chunk order)
-  const int nthreads = blockDim.x;
+// The staging table (thread 0; parameters only, so it may run before the PDL wait).
+template <int B, int G>
+__device__ __forceinline__ void stage_table(const Params& p, int t0, int t1, StageEntry* tab) {
   if (threadIdx.x == 0) {
     int first = 0, n = 0;
     uint32_t off = 0;
@@ -304,7 +298,18 @@ __device__ __forceinline__ void stage_all(const Params& p, int t0, int t1, uint8
     reinterpret_cast<volatile int*>(tab + kMaxItems)[0] = n;
     reinterpret_cast<volatile int*>(tab + kMaxItems)[1] = first;
   }
-  __syncthreads();
+}
+// Loads and sums (all threads; after stage_table and, unless x_ready, the PDL wait).
+template <int BITS, int B, int G>
+__device__ __forceinline__ void stage_all(const Params& p, uint8_t* sm, StageEntry* tab) {
+  constexpr int NC = G / 8;            // 16-B chunks per column group
+#ifndef GQSA_STAGE_U
+#define GQSA_STAGE_U 4
+#endif
+  constexpr int U = NC >= 4 ? 2 : GQSA_STAGE_U;  // column groups per thread in flight per round
+  constexpr int PG = (G == 16 && B <= 2) ? 2 : 1;  // (-P, -Q) entries per column group (one per chunk order)
+  const int nthreads = blockDim.x;
+  __syncthreads();  // the table
   const int n_t = reinterpret_cast<const int*>(tab + kMaxItems)[0];
   const int total = reinterpret_cast<const int*>(tab + kMaxItems)[1];
   auto locate = [&](int gi) {  // entry of global column-group index gi

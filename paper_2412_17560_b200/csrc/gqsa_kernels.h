@@ -29,7 +29,10 @@ constexpr int kMaxDynSmem = 225 * 1024; // opt-in dynamic shared memory per CTA 
 #ifndef GQSA_BUFS_LARGE
 #define GQSA_BUFS_LARGE 2
 #endif
-__host__ __device__ constexpr int bufs_for(int B) { return B <= 2 ? GQSA_BUFS_SMALL : GQSA_BUFS_LARGE; }
+#ifndef GQSA_BUFS_B2
+#define GQSA_BUFS_B2 GQSA_BUFS_SMALL
+#endif
+__host__ __device__ constexpr int bufs_for(int B) { return B == 1 ? GQSA_BUFS_SMALL : B == 2 ? GQSA_BUFS_B2 : GQSA_BUFS_LARGE; }
 // L2 prefetch distance in tiles (<= the register buffers: off): lane 0 issues
 // cp.async.bulk.prefetch.L2 for tile t + d as it requests tile t into
 // registers, so each warp keeps d tiles moving from HBM while only the
@@ -61,6 +64,11 @@ __host__ __device__ constexpr int warps_for(int B) { return B == 1 ? GQSA_WARPS_
 #define GQSA_MINB 1
 #endif
 __host__ __device__ constexpr int min_blocks_for(int B) { return B <= 2 ? GQSA_MINB : 1; }
+// CTAs per SM of a whole-SM launch at B = 1 (the grid is this many x #SMs).
+#ifndef GQSA_FULL_CTAS
+#define GQSA_FULL_CTAS 1
+#endif
+__host__ __device__ constexpr int full_ctas_for(int B) { return B == 1 ? GQSA_FULL_CTAS : 1; }
 // Pipelined mode (x_ready, B <= 2): the launch takes HALF of
 // every SM (one CTA of half the warps, compiled for 2 resident CTAs), so the
 // next independent launch on the stream runs its prologue, activation staging
@@ -86,6 +94,10 @@ __host__ __device__ constexpr int defer_bytes_per_warp(int B) { return kDeferSlo
 __host__ __device__ constexpr int half_smem_limit(int B) {
   return (kSmemPerSm - pipe_ctas_for(B) * 2048) / pipe_ctas_for(B);
 }
+#ifndef GQSA_MIN_TPW
+#define GQSA_MIN_TPW 0
+#endif
+constexpr int kMinTilesPerWarp = GQSA_MIN_TPW;  // see min_tiles_per_warp() in gqsa_capi.cu
 constexpr int kMaxWarpsBound = 148 * 32;  // fix-up records the workspace holds per launch (any B200 grid)
 
 // One GEMV of a launch.  Its tiles occupy global tile indices
@@ -107,6 +119,9 @@ struct Item {
   int32_t smem_bytes; // B * (xrow + pqrow), rounded to 128
   int32_t n_peers;    // fused all-gather: store every element into each peer_y (global row row_offset + r)
   int32_t row_offset;
+  int32_t peer_mc;    // 1: peer_y[0] is an NVLS multicast address, stored with multimem.st (one store
+                      //    reaches every rank bound to the multicast object)
+  int32_t pad_;
   uint64_t peer_y[kMaxPeers];
 };
 

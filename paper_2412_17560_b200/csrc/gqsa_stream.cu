@@ -66,6 +66,13 @@ __device__ __forceinline__ uint32_t item_smem_off(const Item* items, int i, int 
 
 // y element i of item `it`: fp32, or fp16 rounded to nearest even (PAPER.md:134 step 5).
 __device__ __forceinline__ void store_y(const Item& it, int out_f16, int64_t i, float v) {
+  if (it.peer_mc) {  // fused all-gather over NVLink SHARP: one multicast store reaches every rank (fp32 only)
+    asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(reinterpret_cast<float*>(it.peer_y[0]) + i +
+                                                                      it.row_offset),
+                 "f"(v)
+                 : "memory");
+    return;
+  }
   if (it.n_peers) {  // fused all-gather: this shard's rows land in every rank's full y
 #pragma unroll 1
     for (int k = 0; k < it.n_peers; ++k) {
@@ -244,7 +251,7 @@ __device__ __forceinline__ void trace_point(const Params& p, int gw, int lane, i
 template <int BITS, int B, int G, int HALF>
 __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B) : min_blocks_for(B))
     gqsa_stream_kernel(const __grid_constant__ Params p) {
-  constexpr int W = warps_of(B, HALF);
+  const int W = blockDim.x >> 5;  // warps per CTA (<= warps_of(B, HALF); fewer for small launches)
   constexpr int TB = tile_bytes(BITS, G);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -347,20 +354,24 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B
   // let the next launch on the stream start its prologue (its weight loads);
   // triggering later (e.g. half-way through the range) measured slower
   pdl_launch_dependents();
-  // x may be the previous kernel's output; with x_ready the wait is deferred
-  // to just before this launch's first global write (y, records, counters)
-  bool waited = !p.x_ready;
-  if (waited) pdl_wait();
-  trace_point(p, gw, lane, 1);
+  // the first slice's bounds and rows and the staging table: immutable blob
+  // and parameters only, so they are fetched before the PDL wait
   if (t_end > t_begin) {
     const Item& it = p.item[ci];
     cst0 = it.tile_begin + __ldg(it.slice_tile0 + cs);
     cend = it.tile_begin + __ldg(it.slice_tile0 + cs + 1);
     crow = __ldg(it.perm + (int64_t)cs * kLanes + lane);
   }
+  StageEntry* const stab = reinterpret_cast<StageEntry*>(smem + p.stage_tab_offset);
+  stage_table<B, G>(p, cta_t0, cta_t1, stab);
+  // x may be the previous kernel's output; with x_ready the wait is deferred
+  // to just before this launch's first global write (y, records, counters)
+  bool waited = !p.x_ready;
+  if (waited) pdl_wait();
+  trace_point(p, gw, lane, 1);
 
   // ---- stage the activations of every item this CTA's range touches
-  stage_all<BITS, B, G>(p, cta_t0, cta_t1, smem, reinterpret_cast<StageEntry*>(smem + p.stage_tab_offset));
+  stage_all<BITS, B, G>(p, smem, stab);
   __syncthreads();
   its = s_item;
   trace_point(p, gw, lane, 2);
@@ -483,14 +494,6 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B
       h_pending = true;
     }
   }
-  if (kPre > 0 && cend > t_end && !foreign && !pre_loaded) {  // not requested during the last tile (x_ready)
-    const int n = warp_of_tile(p, cend - 1) - gw;
-#pragma unroll
-    for (int k = 0; k < kPre; ++k)
-#pragma unroll
-      for (int b = 0; b < B; ++b)
-        pre[k][b] = k < n ? ld_relaxed64(rec_ptr<B>(p, gw + 1 + k, 0, b, lane)) : (1ull << 32);
-  }
 
   int fix_path = 0;  // debug trace: 1 fast, 2 published (not last), 3 published + collected; +10 head collected
   // ---- a slice left open at the end of the range continues downstream
@@ -500,7 +503,16 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B
     if (kPre > 0 && !foreign && w1 - gw <= kPre) {
       // fast path: every successor already published -> add them in warp
       // order and finish the rows here, without arriving (the successors'
-      // arrivals are cancelled so the counter returns to zero)
+      // arrivals are cancelled so the counter returns to zero).  Bounded
+      // waiting for the successors here measured no faster than the
+      // last-arriver path below, so the owner never waits.
+      if (!pre_loaded) {  // not requested during the last tile (x_ready)
+#pragma unroll
+        for (int k = 0; k < kPre; ++k)
+#pragma unroll
+          for (int b = 0; b < B; ++b)
+            pre[k][b] = k < w1 - gw ? ld_relaxed64(rec_ptr<B>(p, gw + 1 + k, 0, b, lane)) : (1ull << 32);
+      }
       bool ready = true;
 #pragma unroll
       for (int k = 0; k < kPre; ++k)

@@ -87,7 +87,7 @@ EXPORTS = (
     "gqsa_gemv", "gqsa_gemm_smallbatch", "gqsa_gemm_ex", "gqsa_gemm_grouped", "gqsa_hostio_stage_size",
     "gqsa_gemm_hostio",
     "gqsa_compress_nnzg", "gqsa_compress", "gqsa_multi_hostio_stage_size", "gqsa_gemm_multi_hostio",
-    "gqsa_gemm_allgather",
+    "gqsa_gemm_allgather", "gqsa_gemm_allgather_multicast",
     "gqsa_launch_plan", "gqsa_launch_plan_ex", "gqsa_launch_count", "gqsa_status_string", "gqsa_version",
     "gqsa_debug_trace",
 )
@@ -118,6 +118,8 @@ def lib() -> ctypes.CDLL:
     L.gqsa_hostio_stage_size.argtypes = [ctypes.POINTER(Desc), I32, PSZ]
     L.gqsa_gemm_hostio.argtypes = [ctypes.POINTER(Desc), P, P, I32, P, P, P, SZ, P, SZ, P]
     L.gqsa_launch_plan.argtypes = [ctypes.POINTER(Desc), I32, ctypes.POINTER(Plan)]
+    L.gqsa_launch_plan_ex.argtypes = [ctypes.POINTER(Desc), I32, ctypes.POINTER(Options), ctypes.POINTER(Plan)]
+    L.gqsa_gemm_allgather_multicast.argtypes = [ctypes.POINTER(Desc), P, P, I32, I64, P, I64, I32, I32, P, P, SZ, P]
     PDESC = ctypes.POINTER(ctypes.POINTER(Desc))
     L.gqsa_multi_hostio_stage_size.argtypes = [PDESC, I32, I32, PSZ]
     L.gqsa_gemm_multi_hostio.argtypes = [PDESC, ctypes.POINTER(P), I32, I32, P, P, P, SZ, ctypes.POINTER(P),
@@ -353,6 +355,18 @@ def gemm_allgather(desc: Desc, d_blob, X, peer_Y, row_offset: int, bias=None, ws
                                      ptrs, n, peer_Y[0].stride(0), int(row_offset), out16,
                                      bias.data_ptr() if bias is not None else None, ws.data_ptr(), ws.numel(),
                                      _stream_ptr(stream)), "gqsa_gemm_allgather")
+
+
+def gemm_allgather_multicast(desc: Desc, d_blob, X, mc_ptr: int, ldy: int, row_offset: int, out_f16: bool = False,
+                             bias=None, ws=None, stream=None) -> None:
+    """gqsa_gemm_allgather_multicast: this rank's shard GEMM storing each output
+    element once with multimem.st into the NVLS multicast address ``mc_ptr``
+    of the ranks' full [B][ldy] outputs (fp32, or fp16 when out_f16)."""
+    _check(lib().gqsa_gemm_allgather_multicast(ctypes.byref(desc), d_blob.data_ptr(), X.data_ptr(), X.shape[0],
+                                               X.stride(0), ctypes.c_void_p(int(mc_ptr)), int(ldy), int(row_offset),
+                                               int(bool(out_f16)), bias.data_ptr() if bias is not None else None,
+                                               ws.data_ptr(), ws.numel(), _stream_ptr(stream)),
+           "gqsa_gemm_allgather_multicast")
 
 
 class MultiHostIO:

@@ -338,6 +338,32 @@ def test_fused_allgather_epilogue_simulated_ranks(rows, cols, B, P, f16):
             assert np.array_equal(got.astype(np.float64), ref)
 
 
+def test_multicast_allgather_argument_contract():
+    """gqsa_gemm_allgather_multicast (NVLS multimem.st epilogue) validates its
+    arguments like gqsa_gemm_allgather and refuses fp16 output (multimem.st
+    has no 16-bit scalar form).  Its stores need a real multicast object of
+    >= 2 GPUs, which a one-GPU box cannot create, so only the
+    contract is exercised here."""
+    bsr = synth.make_layer(91, 256, 512, sparsity=0.5)
+    blob, desc = gqsa.pack(bsr)
+    d_blob = torch.from_numpy(blob).cuda()
+    X = torch.zeros(1, 512, dtype=torch.float16, device="cuda")
+    ws = torch.zeros(gqsa.workspace_size(desc, 1), dtype=torch.uint8, device="cuda")
+    fake_mc = torch.zeros(1, 256, dtype=torch.float32, device="cuda").data_ptr()
+    with pytest.raises(gqsa.GQSAError) as e:
+        gqsa.gemm_allgather_multicast(desc, d_blob, X, fake_mc, ldy=256, row_offset=0, out_f16=True, ws=ws)
+    assert e.value.status == -3
+    with pytest.raises(gqsa.GQSAError) as e:  # shard rows beyond ldy
+        gqsa.gemm_allgather_multicast(desc, d_blob, X, fake_mc, ldy=255, row_offset=0, ws=ws)
+    assert e.value.status == -1
+    with pytest.raises(gqsa.GQSAError) as e:
+        gqsa.gemm_allgather_multicast(desc, d_blob, X, 0, ldy=256, row_offset=0, ws=ws)
+    assert e.value.status == -4
+    with pytest.raises(gqsa.GQSAError) as e:  # misaligned multicast address
+        gqsa.gemm_allgather_multicast(desc, d_blob, X, fake_mc + 2, ldy=256, row_offset=0, ws=ws)
+    assert e.value.status == -4
+
+
 def test_pdl_dependent_launch_chain_reads_producer_output():
     """Back-to-back launches where launch k reads, as its x, the fp16 output
     launch k-1 just wrote (Programmatic Dependent Launch: weights are

@@ -39,7 +39,10 @@ def full(rep):
     res = []
     keys = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
             "dram__bytes_read.sum.pct_of_peak_sustained_elapsed", "dram__bytes_write.sum.pct_of_peak_sustained_elapsed",
-            "dram__bytes.sum.per_second", "dram__cycles_active.avg.pct_of_peak_sustained_elapsed",
+            "dram__bytes.sum.per_second", "dram__bytes.sum.peak_sustained", "dram__cycles_elapsed.avg.per_second",
+            "dram__cycles_active.avg.pct_of_peak_sustained_elapsed",
+            "gpu__compute_memory_access_throughput.avg.pct_of_peak_sustained_elapsed",
+            "launch__occupancy_limit_registers", "sm__warps_active.avg.pct_of_peak_sustained_active",
             "sm__cycles_active.avg", "sm__cycles_elapsed.avg", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
             "sm__throughput.avg.pct_of_peak_sustained_elapsed",
             "smsp__issue_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
@@ -79,7 +82,7 @@ def main():
         res = full(a.full)
         step_bytes, step_us = 0.0, 0.0
         with open(a.out + "_full.md", "w") as f:
-            f.write("# ncu --set full (one launch per layer shape, in bench order)\n\n")
+            f.write("# ncu --set full (captured launches of the bench step; serialised, cold caches)\n\n")
             for i, r in enumerate(res):
                 f.write(f"## launch {i}: `{r['Kernel Name'][0][:100]}`\n\n")
                 for k, (v, u) in r.items():
@@ -90,8 +93,11 @@ def main():
                 f.write(f"- dram read+write bytes: {rb:.0f}\n\n")
                 t = float(str(r["gpu__time_duration.sum"][0]).replace(",", ""))
                 step_us += t / 1e3 if r["gpu__time_duration.sum"][1] == "nsecond" else t
-        json.dump({"step_dram_bytes": step_bytes, "launches": len(res), "source": os.path.basename(a.full),
-                   "sum_gpu_time_us_cold": step_us},
+        json.dump({"dram_bytes_per_launch": step_bytes / max(len(res), 1), "launches": len(res),
+                   "source": os.path.basename(a.full), "gpu_time_us_per_launch_cold": step_us / max(len(res), 1),
+                   "kernels": [r["Kernel Name"][0] for r in res],
+                   "note": "dram__bytes_read.sum + dram__bytes_write.sum of the captured launch(es) of "
+                           "`ncu --set full` (serialised, cold caches)"},
                   open(os.path.join(os.path.dirname(a.out), "ncu_traffic.json"), "w"), indent=1)
         print(open(a.out + "_full.md").read()[:3000])
 

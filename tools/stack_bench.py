@@ -7,10 +7,11 @@ E. LLaMA-3-8B decoder LINEAR STACK per token (32 layers x q, k, v, o, gate,
    up, down = 224 GEMVs) at W4S30 / W4S50 / W2S50, B = 1, 2, 4, 8: one CUDA
    graph of the whole stack (PDL between launches), µs per token, counted GB/s.
    Also the merged form production servers use (vLLM-style fused qkv
-   6144x4096 and gate_up 28672x4096: 128 GEMVs per token), and both forms as
-   one gqsa_gemm_chain launch per decoder layer (k, v and up read the input
-   of the item before them, so they do not wait; the other items wait for
-   every earlier item; B <= 2).
+   6144x4096 and gate_up 28672x4096: 128 GEMVs per token), and the separate
+   matrices as gqsa_gemm_grouped launches of the GEMVs that share an input
+   ({q, k, v}, {o}, {gate, up}, {down}: 128 launches per token).  Every launch
+   reads the previous launch's output in a real decoder, so none declares
+   x_ready (whole-SM launches, PDL between them).
 F. Qwen2.5-14B (5120 / 13824, 48 layers) W4S50 and LLaMA-3.1-70B (8192 /
    28672) W4S50 row shards: the per-rank GEMV of a P-way row split
    (N/P x K) measured on this GPU, P = 1, 2, 4, 8 (Qwen) and P = 8 (70B).
@@ -41,14 +42,13 @@ LLAMA3_8B = [("q", 4096, 4096), ("k", 1024, 4096), ("v", 1024, 4096), ("o", 4096
 LLAMA3_8B_MERGED = [("qkv", 6144, 4096), ("o", 4096, 4096), ("gate_up", 28672, 4096), ("down", 4096, 14336)]
 
 
-# wait_prev per item of one decoder layer's chain: k, v read q's input and up
-# reads gate's input (independent of the previous item); the others wait.
-CHAIN_WAIT = {"q": 1, "k": 0, "v": 0, "o": 1, "gate": 1, "up": 0, "down": 1, "qkv": 1, "gate_up": 1}
+# groups of GEMVs that share one input (one gqsa_gemm_grouped launch each)
+GROUPS = {"q": 0, "k": 0, "v": 0, "o": 1, "gate": 2, "up": 2, "down": 3}
 
 
-def time_stack(mats, n_layers, bits, sp, B, reps=20, chain=False):
+def time_stack(mats, n_layers, bits, sp, B, reps=20, grouped=False):
     """mats: [(name, rows, cols)] of one decoder layer; returns µs per token and bytes.
-    chain: one gqsa_gemm_chain launch per decoder layer instead of one launch per GEMV."""
+    grouped: the GEMVs sharing an input as one gqsa_gemm_grouped launch."""
     dev = torch.device("cuda")
     packed = []
     for name, rows, cols in mats:
@@ -69,16 +69,20 @@ def time_stack(mats, n_layers, bits, sp, B, reps=20, chain=False):
     xs = [xin[src[name]] for name, _, _ in mats]
     ys = [torch.empty(B, r, dtype=torch.float32, device=dev) for _, r, _ in mats]
     s = torch.cuda.Stream()
-    if chain:
-        items = [[(d, copies[L][i], xs[i], ys[i], None, CHAIN_WAIT[mats[i][0]]) for i, (_, d) in enumerate(packed)]
-                 for L in range(n_layers)]
-        cws = torch.zeros(gqsa.chain_workspace_size(items[0], B), dtype=torch.uint8, device=dev)
+    if grouped:
+        calls = []
+        for L in range(n_layers):
+            gs = {}
+            for i, (name, _, _) in enumerate(mats):
+                gs.setdefault(GROUPS[name], []).append((packed[i][1], copies[L][i], xs[i], ys[i], None))
+            calls += [gqsa.Grouped(gs[k], ws[0]) for k in sorted(gs)]
 
     def token():
+        if grouped:
+            for c in calls:
+                c(s)
+            return
         for L in range(n_layers):
-            if chain:
-                gqsa.gemm_chain(items[L], cws, stream=s)
-                continue
             for i, (_, d) in enumerate(packed):
                 gqsa.gemm_smallbatch(d, copies[L][i], xs[i], ys[i], None, ws[i], stream=s)
 
@@ -99,7 +103,7 @@ def time_stack(mats, n_layers, bits, sp, B, reps=20, chain=False):
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / reps
     nb = n_layers * sum(counted_bytes(d.rows, d.cols, d.nnzg, bits, B) for _, d in packed)
-    launches = n_layers * (1 if chain else len(packed))
+    launches = len(calls) if grouped else n_layers * len(packed)
     del copies
     torch.cuda.empty_cache()
     return us, nb, launches
@@ -139,6 +143,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     ap.add_argument("--batches", default="1,2,4,8")
+    ap.add_argument("--settings", default="W4S30,W4S50,W2S50", help="subset of section E's settings")
+    ap.add_argument("--forms", default="separate,merged,grouped", help="subset of section E's forms")
+    ap.add_argument("--sections", default="EFG")
     a = ap.parse_args()
     peak, src = peaks()
     batches = [int(b) for b in a.batches.split(",")]
@@ -148,15 +155,17 @@ def main():
              "PDL between launches, weights in 32 (48) distinct device copies (HBM-resident, >> L2).", "",
              "## E. LLaMA-3-8B decoder linear stack per token (SURVEY §8(d) C3)", "",
              "| setting | form | launches | B | µs / token | GB per token | GB/s | frac |", "|---|---|---|---|---|---|---|---|"]
+    forms = (("separate", "separate q/k/v, gate/up", LLAMA3_8B, False),
+             ("merged", "merged qkv, gate_up", LLAMA3_8B_MERGED, False),
+             ("grouped", "separate, grouped {qkv}{o}{gate,up}{down}", LLAMA3_8B, True))
     for bits, sp in ((4, 0.3), (4, 0.5), (2, 0.5)):
-        for form, mats, chain in (("separate q/k/v, gate/up", LLAMA3_8B, False),
-                                  ("merged qkv, gate_up", LLAMA3_8B_MERGED, False),
-                                  ("separate, 1 chain launch per layer", LLAMA3_8B, True),
-                                  ("merged, 1 chain launch per layer", LLAMA3_8B_MERGED, True)):
+        if "E" not in a.sections or f"W{bits}S{int(sp * 100)}" not in a.settings.split(","):
+            continue
+        for key, form, mats, grouped in forms:
+            if key not in a.forms.split(","):
+                continue
             for B in batches:
-                if chain and B > 2:
-                    continue
-                us, nb, nl = time_stack(mats, 32, bits, sp, B, chain=chain)
+                us, nb, nl = time_stack(mats, 32, bits, sp, B, grouped=grouped)
                 r = dict(section="E", setting=f"W{bits}S{int(sp * 100)}", form=form, B=B, us=round(us, 1),
                          bytes=nb, launches=nl, gbs=round(nb / us / 1e3, 1), frac=round(nb / us / 1e3 / peak, 4))
                 recs.append(r)
@@ -167,7 +176,7 @@ def main():
               "| model | matrix | full N x K | P | rank shard | µs | GB/s per rank |", "|---|---|---|---|---|---|---|"]
     qwen = [("q/o", 5120, 5120), ("k/v", 1024, 5120), ("gate/up", 13824, 5120), ("down", 5120, 13824)]
     l70 = [("q/o", 8192, 8192), ("k/v", 1024, 8192), ("gate/up", 28672, 8192), ("down", 8192, 28672)]
-    for model, mats, Ps in (("Qwen2.5-14B", qwen, (1, 2, 4, 8)), ("LLaMA-3.1-70B", l70, (8,))):
+    for model, mats, Ps in (("Qwen2.5-14B", qwen, (1, 2, 4, 8)), ("LLaMA-3.1-70B", l70, (8,))) if "F" in a.sections else ():
         for name, n, k in mats:
             for P in Ps:
                 us, nb = time_layer(n // P, k, 4, 0.5, 1)
@@ -178,7 +187,7 @@ def main():
                 lines.append(f"| {model} | {name} | {n}x{k} | {P} | {n // P}x{k} | {us:.2f} | {r['gbs']:.0f} |")
     lines += ["", "## G. Qwen2.5-14B full matrices, W4S50, B = 1 / 2 / 4 / 8 on one GPU (SURVEY §8(d) C4, P = 1)", "",
               "| matrix | N x K | B | µs | GB/s |", "|---|---|---|---|---|"]
-    for name, n, k in qwen:
+    for name, n, k in qwen if "G" in a.sections else ():
         for B in batches:
             us, nb = time_layer(n, k, 4, 0.5, B)
             r = dict(section="G", model="Qwen2.5-14B", matrix=name, N=n, K=k, B=B, us=round(us, 3), bytes=nb,

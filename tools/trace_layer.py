@@ -100,6 +100,17 @@ def main():
               np.median(np.percentile(cta_max, 10, axis=1) - np.median(ex, axis=1)),
               np.median(np.median(cta_max, axis=1) - np.median(ex, axis=1)),
               np.median(cta_max.max(axis=1) - np.median(ex, axis=1))))
+    # the slowest warps: which phase made them late, and their fix-up path
+    path = np.stack([b.cpu().numpy().reshape(W, 8)[:, 7] for b in bufs])[1:]
+    late = ex - np.median(ex, axis=1, keepdims=True)
+    cut = np.percentile(late, 95)
+    m = late >= cut
+    le = d[..., 4] - np.median(d[..., 4], axis=1, keepdims=True)
+    st = d[..., 2] - np.median(d[..., 2], axis=1, keepdims=True)
+    print("slowest 5%% of warps (exit >= median + %.2f us): loop end vs median %.2f, staged vs median %.2f, "
+          "fix-up (exit - loop end) %.2f us (medians); fix paths %s" % (
+              cut, np.median(le[m]), np.median(st[m]), np.median((d[..., 5] - d[..., 4])[m]),
+              {int(k): int(v) for k, v in zip(*np.unique(path[m], return_counts=True))}))
     prev_exit = T[:-1, :, 5].max(axis=1)
     rel = T[1:, :, 1].min(axis=1) - prev_exit
     print("PDL release after previous launch's last exit (µs):", " ".join(f"{r:.2f}" for r in rel[:5]))
