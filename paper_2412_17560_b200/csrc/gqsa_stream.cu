@@ -162,7 +162,10 @@ __device__ __forceinline__ int arrive(const Params& p, int w0, int lane) {
 // The records of the first kRec participants of a slice split over warps
 // w0..w1 (w0's tail record, then head records), requested ahead of the
 // arrival so that the last arriver has them one round trip earlier.
-constexpr int kRec = 4;
+#ifndef GQSA_KREC
+#define GQSA_KREC 8
+#endif
+constexpr int kRec = GQSA_KREC;
 template <int B>
 struct Recs {
   unsigned long long r[kRec][B];
@@ -177,9 +180,22 @@ __device__ __forceinline__ Recs<B> request_records(const Params& p, int w0, int 
       q.r[k][b] = (w0 + k <= w1) ? ld_relaxed64(rec_ptr<B>(p, w0 + k, k == 0 ? 1 : 0, b, lane)) : 0ull;
   return q;
 }
+// A record whose flag was not yet visible: poll it (rare; kept out of line so
+// that the collect loop stays small -- the fix-up runs once per launch and
+// its code is cold in the instruction cache).
+__device__ __noinline__ unsigned long long wait_record(const unsigned long long* a) {
+  unsigned long long v = ld_relaxed64(a);
+  unsigned int spins = 0;
+  while ((v >> 32) == 0ull) {
+    if (++spins > (1u << 26)) __trap();  // a lost record: fail loudly, never hang
+    __nanosleep(32);
+    v = ld_relaxed64(a);
+  }
+  return v;
+}
 // The last arriver of a slice split over warps w0..w1: add every
 // participant's record in warp order (w0's tail record, then the head records
-// of w0+1..w1), reset the flags and the counter, store the rows.  The spin
+// of w0+1..w1), reset the flags and the counter, store the rows.  The poll
 // only waits for stores already issued (their writers arrived before us).
 // `q` holds the first kRec records as requested before the arrival (flag 0: reload).
 template <int B>
@@ -188,31 +204,25 @@ __device__ __noinline__ void collect(const Params& p, const Item* items, int w0,
   float v[B];
 #pragma unroll
   for (int b = 0; b < B; ++b) v[b] = 0.f;
-  // records requested per round trip: all of them are loaded before the
-  // first is waited on, so a slice split over many warps costs few round trips
-  constexpr int KB = B <= 2 ? 16 / B : kRec;
-  static_assert(KB >= kRec, "the pre-requested records fit the first batch");
-  for (int wb = w0; wb <= w1; wb += KB) {
-    unsigned long long r[KB][B];
+  // kRec records per round trip, all requested before the first is used; the
+  // batch loop is not unrolled (small code: the tail runs cold)
+#pragma unroll 1
+  for (int wb = w0; wb <= w1; wb += kRec) {
+    unsigned long long r[kRec][B];
 #pragma unroll
-    for (int k = 0; k < KB; ++k)
+    for (int k = 0; k < kRec; ++k)
 #pragma unroll
       for (int b = 0; b < B; ++b)
-        r[k][b] = (wb == w0 && k < kRec) ? q.r[k][b]
-                  : (wb + k <= w1)       ? ld_relaxed64(rec_ptr<B>(p, wb + k, wb + k == w0 ? 1 : 0, b, lane))
-                                         : 0ull;
+        r[k][b] = wb == w0         ? q.r[k][b]
+                  : (wb + k <= w1) ? ld_relaxed64(rec_ptr<B>(p, wb + k, 0, b, lane))
+                                   : (1ull << 32);
 #pragma unroll
-    for (int k = 0; k < KB; ++k) {
-      if (wb + k > w1) break;
+    for (int k = 0; k < kRec; ++k) {
 #pragma unroll
       for (int b = 0; b < B; ++b) {
+        if (wb + k > w1) continue;
         unsigned long long* a = rec_ptr<B>(p, wb + k, wb + k == w0 ? 1 : 0, b, lane);
-        unsigned int spins = 0;
-        while ((r[k][b] >> 32) == 0ull) {
-          if (++spins > (1u << 26)) __trap();  // a lost record: fail loudly, never hang
-          __nanosleep(32);
-          r[k][b] = ld_relaxed64(a);
-        }
+        if ((r[k][b] >> 32) == 0ull) r[k][b] = wait_record(a);
         v[b] = (wb + k == w0) ? __uint_as_float((uint32_t)r[k][b]) : v[b] + __uint_as_float((uint32_t)r[k][b]);
         st_relaxed64(a, 0ull);
       }
@@ -542,6 +552,9 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B
       const Recs<B> q = request_records<B>(p, cw0, w1, lane);  // in flight with the arrival
       const int old = __shfl_sync(0xffffffffu, arrive(p, cw0, lane), 0);
       fix_path = 2;
+#ifdef GQSA_TRACE_FIX  // debug builds: time the arrival returned, in trace slot 6
+      trace_point(p, gw, lane, 6);
+#endif
       if (old == w1 - cw0) {
         collect<B>(p, its, cw0, w1, ci, crow, lane, q);
         fix_path = 3;

@@ -111,6 +111,14 @@ def main():
           "fix-up (exit - loop end) %.2f us (medians); fix paths %s" % (
               cut, np.median(le[m]), np.median(st[m]), np.median((d[..., 5] - d[..., 4])[m]),
               {int(k): int(v) for k, v in zip(*np.unique(path[m], return_counts=True))}))
+    if os.environ.get("GQSA_TRACE_FIX"):  # library built with -DGQSA_TRACE_FIX: slot 6 = arrival returned,
+        raw = np.stack([b.cpu().numpy().reshape(W, 8) for b in bufs])[1:]  # slot 2 = re-polls in collect
+        arr = (raw[..., 6].astype(np.float64) - t0) / 1e3 - d[..., 4]
+        m3 = m & (path == 3)
+        if m3.any():
+            print("  slow collectors: arrival returned %.2f us after loop end, exit %.2f us after the arrival, "
+                  "re-polls p50/max %d/%d" % (np.median(arr[m3]), np.median((d[..., 5] - d[..., 4] - arr)[m3]),
+                                             np.median(raw[..., 2][m3]), raw[..., 2][m3].max()))
     prev_exit = T[:-1, :, 5].max(axis=1)
     rel = T[1:, :, 1].min(axis=1) - prev_exit
     print("PDL release after previous launch's last exit (µs):", " ".join(f"{r:.2f}" for r in rel[:5]))
