@@ -79,6 +79,26 @@ def peaks():
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+def read_peak(achieved):
+    """The third denominator: the best read-only stream this build's
+    calibration kernel (tools/stream_bench.cu) measured on a B200, from
+    profiles/r02_stream_bench.jsonl: the same 59 MB per launch, and 300 MB."""
+    p = os.path.join(ROOT, "profiles", "r02_stream_bench.jsonl")
+    if not os.path.exists(p):
+        return {}
+    best = {}
+    for line in open(p):
+        d = json.loads(line)
+        k = "read_peak_59mb_gbs" if d["bytes"] < 100e6 and d["bytes"] > 50e6 else \
+            "read_peak_300mb_gbs" if d["bytes"] > 200e6 else None
+        if k:
+            best[k] = max(best.get(k, 0.0), float(d["gbs"]))
+    if "read_peak_59mb_gbs" in best:
+        best["frac_of_read_peak_59mb"] = round(achieved / best["read_peak_59mb_gbs"], 4)
+    best["read_peak_source"] = "profiles/r02_stream_bench.jsonl (tools/stream_bench.cu, B200)"
+    return best
+
+
 def make_layers(bits, sparsity, batch, world=1, rank=0, mask="uniform"):
     from paper_2412_17560_b200 import synth
     out = []
@@ -580,6 +600,7 @@ def run_gpu(args):
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
                      "peak_source": peak_src, "frac_of_nominal_8tbs": round(achieved / NOMINAL_HBM_GBS, 4),
+                     **read_peak(achieved),
                      "kernel": f"gqsa::gqsa_stream_kernel<{bits},{B},16>",
                      "algorithmic_bytes_per_step": int(step_bytes),
                      "note": "achieved = algorithmic bytes of the step / device time of the step; the step is "

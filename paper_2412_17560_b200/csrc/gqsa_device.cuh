@@ -199,7 +199,7 @@ __device__ __forceinline__ void group_accumulate(const TileRegs<BITS, G>& tr, in
   const uint32_t f0 = (u & 1) ? (colw >> 16) : (colw & 0xffffu);  // byte offset of the first x chunk
   // (-P, -Q) entry: G = 16, B <= 2: per chunk index f (f * 8 = f0 / 2); else
   // per column group c (c * 8 = f0 / 4 at G = 16, f0 / 2 at G = 8, f0 / 8 at G = 32)
-  constexpr bool kPerChunk = (G == 16 && B <= 2);  // see pq_entries()
+  constexpr bool kPerChunk = pq_per_chunk(B, G);  // see pq_entries()
   const uint32_t pqoff = G == 8 ? f0 >> 1 : G == 32 ? (f0 >> 3) & ~7u : kPerChunk ? f0 >> 1 : (f0 >> 2) & ~7u;
   const uint32_t szw = u == 0 ? tr.sz.x : u == 1 ? tr.sz.y : u == 2 ? tr.sz.z : tr.sz.w;
   const __half2 sz = *reinterpret_cast<const __half2*>(&szw);
@@ -307,7 +307,7 @@ __device__ __forceinline__ void stage_all(const Params& p, uint8_t* sm, StageEnt
 #define GQSA_STAGE_U 4
 #endif
   constexpr int U = NC >= 4 ? 2 : GQSA_STAGE_U;  // column groups per thread in flight per round
-  constexpr int PG = (G == 16 && B <= 2) ? 2 : 1;  // (-P, -Q) entries per column group (one per chunk order)
+  constexpr int PG = pq_per_chunk(B, G) ? 2 : 1;  // (-P, -Q) entries per column group (one per chunk order)
   const int nthreads = blockDim.x;
   __syncthreads();  // the table
   const int n_t = reinterpret_cast<const int*>(tab + kMaxItems)[0];

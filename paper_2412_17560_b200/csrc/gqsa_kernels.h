@@ -75,20 +75,25 @@ __host__ __device__ constexpr int full_ctas_for(int B) { return B == 1 ? GQSA_FU
 // and tile loop on the other half while this one drains; every global write
 // of the loop is deferred until after griddepcontrol.wait.
 #ifndef GQSA_WARPS_HALF
-#define GQSA_WARPS_HALF 8
+#define GQSA_WARPS_HALF 6
 #endif
 #ifndef GQSA_PIPE_CTAS
-#define GQSA_PIPE_CTAS 3
+#define GQSA_PIPE_CTAS 4
 #endif
-// Resident CTAs per SM the pipelined kernel is compiled for: three launches
-// in flight at B = 1 (8 warps each, <= 80 registers: bench step 11.8 -> 11.2 us
-// against two of 12 warps); two at B = 2 (its accumulators need the registers).
+// Resident CTAs per SM the pipelined kernel is compiled for: four launches
+// in flight at B = 1 (6 warps each, <= 80 registers; bench step: 2 x 12 warps
+// 11.8 us, 3 x 8 11.1, 4 x 6 10.9 -- the fourth needs the one-entry-per-group
+// column-sum table and 4 deferred-store slots to fit 55 KB of shared memory);
+// two at B = 2 (its accumulators need the registers).
 __host__ __device__ constexpr int pipe_ctas_for(int B) { return B == 1 ? GQSA_PIPE_CTAS : 2; }
 __host__ __device__ constexpr int warps_half(int B) { return B == 1 ? GQSA_WARPS_HALF : 8; }
 __host__ __device__ constexpr int warps_of(int B, int half) { return half ? warps_half(B) : warps_for(B); }
 // Deferred row stores buffered per warp in shared memory before the wait
 // (more closed slices than this in one range: the warp waits and stores).
-constexpr int kDeferSlots = 8;
+#ifndef GQSA_DEFER_SLOTS
+#define GQSA_DEFER_SLOTS 4
+#endif
+constexpr int kDeferSlots = GQSA_DEFER_SLOTS;
 __host__ __device__ constexpr int defer_bytes_per_warp(int B) { return kDeferSlots * 32 * 4 * (B + 1); }
 // dynamic shared memory per CTA of a pipelined launch (pipe_ctas_for(B) CTAs per SM)
 __host__ __device__ constexpr int half_smem_limit(int B) {
@@ -143,8 +148,16 @@ static_assert(sizeof(Params) <= 4096, "kernel parameter space");
 // Shared-memory layout of one staged item (per batch row b):
 //   x  : [B][xrow]  fp16 activations, then kXPadBytes of zeros (padding entries read them)
 //   pq : [B][pqrow] float2 (-P, -Q) per chunk index f (G = 16, B <= 2) or per column group
+// One (-P, -Q) entry per column group (default), or, with GQSA_PQ_PER_GROUP=0
+// at G = 16, B <= 2, one per 16-B x chunk (the pair duplicated: the lookup
+// offset is the column field >> 1, one instruction fewer per group, but twice
+// the table: 2.5 % faster at 3 CTAs per SM, too big for 4).
+#ifndef GQSA_PQ_PER_GROUP
+#define GQSA_PQ_PER_GROUP 1
+#endif
+__host__ __device__ constexpr bool pq_per_chunk(int B, int G) { return G == 16 && B <= 2 && !GQSA_PQ_PER_GROUP; }
 __host__ __device__ constexpr int pq_entries(int B, int G, int cols) {
-  return (G == 16 && B <= 2) ? 2 * (cols / G) : cols / G;
+  return pq_per_chunk(B, G) ? 2 * (cols / G) : cols / G;
 }
 __host__ __device__ constexpr int pq_row_bytes(int B, int G, int cols) {
   return ((pq_entries(B, G, cols) + 2) * 8 + 15) / 16 * 16;  // + zero entries for padding
