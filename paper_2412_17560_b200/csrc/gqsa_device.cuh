@@ -58,6 +58,9 @@ __device__ __forceinline__ uint2 ldg_stream64(const void* ptr, uint64_t pol) {
 __device__ __forceinline__ void prefetch_l2(const void* ptr, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void prefetch_line_l2(const void* ptr) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+}
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
@@ -228,7 +231,7 @@ __device__ __forceinline__ void group_accumulate(const TileRegs<BITS, G>& tr, in
       acc[b] = fmaf(s, fmaf(dd, 0.0625f, de), acc[b]);
     } else {
       const uint4 xa = lds128(xrow + f0);
-      const uint4 xb = lds128(xrow + (f0 ^ 16u));
+      const uint4 xb = lds128((xrow + f0) ^ 16u);  // x rows are 32-B aligned at G = 16
       if (BITS == 8) {  // every element carries +1024: sum (q - z) x = sum (1024 + q) x - 1024 Q - z Q
         const uint4 c = tr.codes[u];
         float d0 = u0, d1 = 0.f;

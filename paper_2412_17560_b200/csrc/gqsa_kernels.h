@@ -45,6 +45,11 @@ __host__ __device__ constexpr int bufs_for(int B) { return B == 1 ? GQSA_BUFS_SM
 #define GQSA_L2PF_LARGE 3
 #endif
 __host__ __device__ constexpr int l2pf_for(int B) { return B <= 2 ? GQSA_L2PF_SMALL : GQSA_L2PF_LARGE; }
+// 1: the in-loop prefetch is one prefetch.global.L2 per lane (a 128-B line
+// each); 0: one cp.async.bulk.prefetch.L2 of the whole tile from lane 0.
+#ifndef GQSA_LANE_PF
+#define GQSA_LANE_PF 1
+#endif
 // Warps per CTA (one CTA per SM): more warps keep more weight loads in
 // flight (a read-only stream of the same tiles reaches 4.9 / 5.3 / 5.5 TB/s
 // with 16 / 24 / 32 warps per SM on the 59 MB bench step,

@@ -324,7 +324,14 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B
       lend = its[li].tile_end;
     }
     load_tile<BITS, G>(r, lptr, lane, pol);
+#if GQSA_LANE_PF
+    // per-lane L2 prefetch of the tile kL2Pf ahead: lane l fetches its 128-B line
+    // (cheaper to issue than one bulk prefetch from lane 0 with uniform operands)
+    if (kL2Pf > kBufs && lane < TB / 128 && t + kL2Pf < min(t_end, lend))
+      prefetch_line_l2(lptr + (size_t)kL2Pf * TB + lane * 128);
+#else
     if (kL2Pf > kBufs && lane == 0 && t + kL2Pf < min(t_end, lend)) prefetch_l2(lptr + (size_t)kL2Pf * TB, TB);
+#endif
     lptr += TB;
   };
   if (kL2Pf > kBufs && lane == 0 && t_end > t_begin) {
@@ -432,7 +439,7 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B
   trace_point(p, gw, lane, 3);
 
   auto consume = [&](const TileRegs<BITS, G>& tr, int t) {
-    if (kPre > 0 && t == t_end - 1 && cend > t_end && !foreign && waited) {
+    if (!HALF && kPre > 0 && t == t_end - 1 && cend > t_end && !foreign && waited) {  // (pipelined: after the loop)
       pre_loaded = true;
       // this warp owns the slice left open at its range end: request the
       // successors' records now, so they are here when the tile is done
@@ -445,7 +452,9 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B
     }
 #pragma unroll
     for (int u = 0; u < kPerLane; ++u) group_accumulate<BITS, B, G>(tr, u, acc, xv);
+#ifdef GQSA_TRACE_TILE0  // debug builds: a per-tile check is too costly in the hot loop
     if (p.trace && t == t_begin) trace_point(p, gw, lane, 6);  // first tile landed and consumed
+#endif
     if (t + 1 == cend) {  // the slice ends with this tile: its rows are complete here
       if (!HALF) ensure_wait();
       if (foreign) {  // ... but began upstream: publish, arrive, check at the range end
