@@ -433,10 +433,7 @@ def run_gpu(args):
             grouped[r]()
         else:
             for i in range(len(layers)):
-                if B == 1:
-                    gqsa.gemv(descs[i], copies[r][i], xs[i][0], ys[i][0], None, ws)
-                else:
-                    gqsa.gemm_smallbatch(descs[i], copies[r][i], xs[i], ys[i], None, ws)
+                gqsa.gemm_ex(descs[i], copies[r][i], xs[i], ys[i], ws=ws, x_ready=bool(args.x_ready))
 
     def gathers():
         """The step's exchange: all-gather of every layer's y shard over NCCL (N > 1)."""
@@ -593,7 +590,7 @@ def run_gpu(args):
                          f"({R * set_bytes / 2**20:.0f} MiB > 2x L2)",
                    "path": {"grouped": "one gqsa_gemm_grouped launch per step (the 3 independent GEMVs "
                                        "share one Stream-K partition)",
-                            "launches": "one gqsa_gemv launch per layer (PDL)"}[path],
+                            "launches": "one gqsa_gemm_ex launch per layer (PDL)"}[path],
                    "x_ready": bool(args.x_ready),
                    "timing": "CUDA graphs of the step (all graphs replayed in warm-up), CUDA events on the "
                              "launch stream, device sleep before the start event"},
