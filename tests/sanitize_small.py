@@ -1,6 +1,7 @@
 """Small launches of every kernel family for compute-sanitizer (memcheck /
 racecheck / synccheck): gemv, small-batch GEMM (batch split), Slice-K,
-fp16 output, grouped launch, fused all-gather.  Exits non-zero on a
+fp16 output, grouped launch (whole-SM and pipelined), LAYOUT-TC, fused
+all-gather.  Exits non-zero on a
 mismatch against the oracle (exact-integer mode)."""
 import os
 import sys
@@ -29,9 +30,16 @@ for rows, cols, bits, B, mask in ((300, 1024, 4, 1, "uniform"), (77, 208, 2, 3, 
     ok &= np.array_equal(y16, ref.astype(np.float16))
     Y = torch.empty(B, rows, dtype=torch.float32, device="cuda")
     Y2 = torch.empty(B, rows, dtype=torch.float32, device="cuda")
-    gqsa.gemm_grouped([(L.desc, L.blob, X, Y, None), (L.desc, L.blob, X, Y2, None)], L.ws)
-    ok &= np.array_equal(Y.cpu().numpy().astype(np.float64), ref)
-    ok &= np.array_equal(Y2.cpu().numpy().astype(np.float64), ref)
+    for x_ready in (False, True):  # x_ready, B <= 2: the pipelined launch (deferred writes)
+        Y.fill_(float("nan"))
+        Y2.fill_(float("nan"))
+        for _ in range(3):  # back to back on one stream, sharing the workspace
+            gqsa.gemm_grouped([(L.desc, L.blob, X, Y, None), (L.desc, L.blob, X, Y2, None)], L.ws, x_ready=x_ready)
+        ok &= np.array_equal(Y.cpu().numpy().astype(np.float64), ref)
+        ok &= np.array_equal(Y2.cpu().numpy().astype(np.float64), ref)
+    if bits == 4 and B >= 2:  # LAYOUT-TC (tensor-core small batch)
+        Lt = gqsa.Layer(bsr, layout=gqsa.LAYOUT_TC)
+        ok &= np.array_equal(Lt.gemm(X).cpu().numpy().astype(np.float64), ref)
     Ys = [torch.zeros(B, rows, dtype=torch.float32, device="cuda") for _ in range(2)]
     for r in range(2):
         lo, hi = synth.shard_rows(rows, 2, r)

@@ -23,7 +23,11 @@ def _cuda():
     torch.cuda.init()
 
 
-def test_three_streams_and_a_side_kernel_bit_exact():
+@pytest.mark.parametrize("x_ready", [False, True])
+def test_three_streams_and_a_side_kernel_bit_exact(x_ready):
+    """x_ready: every launch is a pipelined one (part of every SM, deferred
+    writes, consecutive launches of a stream overlapping and sharing its
+    workspace) -- the same guarantees must hold."""
     shapes = [(4096, 4096), (1024, 4096), (2048, 14336)]
     layers, xs, refs = [], [], []
     for i, (n, k) in enumerate(shapes):
@@ -46,11 +50,12 @@ def test_three_streams_and_a_side_kernel_bit_exact():
             A = A / A.abs().amax()
     for it in range(12):
         for k in range(3):
-            gqsa.gemm_smallbatch(layers[k].desc, layers[k].blob, xs[k], outs[k][it], None, wss[k], stream=streams[k])
+            gqsa.gemm_ex(layers[k].desc, layers[k].blob, xs[k], outs[k][it], ws=wss[k], stream=streams[k],
+                         x_ready=x_ready)
         if it % 3 == 0:
             with torch.cuda.stream(streams[it % 3]):
                 gqsa.gemm_grouped([(L.desc, L.blob, xs[k], grouped_out[it // 3][k], None)
-                                   for k, L in enumerate(layers)], gws, stream=streams[it % 3])
+                                   for k, L in enumerate(layers)], gws, stream=streams[it % 3], x_ready=x_ready)
     torch.cuda.synchronize()
     for k in range(3):
         for Y in outs[k]:
