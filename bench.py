@@ -63,10 +63,11 @@ def counted_bytes(rows, cols, nnzg, bits, batch=1, G=16):
     return nnzg * (G * bits // 8 + 6) + 4 * (rows + 1) + 2 * batch * cols + 4 * batch * rows
 
 
-def workload_config(batch, world):
+def workload_config(batch, world, bits=4, sparsity=0.5):
     """The workload both arms run (identical dicts: the driver compares them)."""
-    return {"workload": f"llama3-8b-layer-shapes-w4s50-b{batch} (4096x4096, 14336x4096, 4096x14336)",
-            "global_batch": batch, "seq_len": 1, "group_size": 16, "bits": 4, "sparsity": 0.5,
+    return {"workload": f"llama3-8b-layer-shapes-w{bits}s{int(round(sparsity * 100))}-b{batch} "
+                        "(4096x4096, 14336x4096, 4096x14336)",
+            "global_batch": batch, "seq_len": 1, "group_size": 16, "bits": bits, "sparsity": sparsity,
             "parallelism": f"rowshard{world}" if world > 1 else "single",
             "l2": "inputs larger than L2 (weights rotate over device copies > 2x L2)"}
 
@@ -252,7 +253,7 @@ def run_reference(args):
     if rank != 0:
         return
     from oracle import gqsa_oracle as O
-    layers = make_layers(4, 0.5, args.batch)
+    layers = make_layers(args.bits, args.sparsity, args.batch)
     total_steps = args.steps + args.warmup
     budget = float(os.environ.get("GQSA_REF_BUDGET_S", "90"))
     per_step = budget / max(total_steps, 1)
@@ -267,7 +268,7 @@ def run_reference(args):
         ri = L["bsr"]["row_index"]
         rs = np.sort(rng.choice(L["rows"], size=min(rows_per_layer, L["rows"]), replace=False))
         nnz = int(np.sum(ri[rs + 1] - ri[rs]))
-        b = nnz * (16 * 4 // 8 + 6) + 4 * (len(rs) + 1) + 2 * L["cols"] + 4 * len(rs)
+        b = nnz * (16 * args.bits // 8 + 6) + 4 * (len(rs) + 1) + 2 * args.batch * L["cols"] + 4 * args.batch * len(rs)
         samples.append((L, rs, b))
     for _ in range(args.warmup):
         for L, rs, _b in samples:
@@ -286,7 +287,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded; DESIGN.md §4 recipe)",
-        "config": workload_config(args.batch, args.gpus),
+        "config": workload_config(args.batch, args.gpus, args.bits, args.sparsity),
         "method": {"host": "CPU fp64 oracle (oracle/gqsa_oracle.py), 1 core, rank 0"},
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -379,7 +380,7 @@ def run_gpu(args):
             dist.init_process_group(backend, rank=rank, world_size=world)
     nccl = dist.is_initialized() and dist.get_backend() == "nccl"
 
-    bits, sp, B = 4, 0.5, args.batch
+    bits, sp, B = args.bits, args.sparsity, args.batch
     layers = make_layers(bits, sp, B, world, rank)
     hbm_peak, peak_src = peaks()
 
@@ -584,7 +585,7 @@ def run_gpu(args):
         "dtype": "u4xf16->f32",
         "data": "synthetic (seeded random W4 codes, fp16 s/z, uniform 50% group mask, N(0,1) fp16 x "
                 "with 0.5% outlier channels; DESIGN.md §4)",
-        "config": workload_config(B, world),
+        "config": workload_config(B, world, bits, sp),
         "method": {"allgather": (args.allgather if (world > 1 or fused) else None),
                    "l2": f"inputs larger than L2: weights rotate over {R} device copies of the layer set "
                          f"({R * set_bytes / 2**20:.0f} MiB > 2x L2)",
@@ -598,7 +599,7 @@ def run_gpu(args):
                      "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
                      "peak_source": peak_src, "frac_of_nominal_8tbs": round(achieved / NOMINAL_HBM_GBS, 4),
                      **read_peak(achieved),
-                     "kernel": f"gqsa::gqsa_stream_kernel<{bits},{B},16>",
+                     "kernel": f"gqsa::gqsa_stream_kernel<{bits},{B},16,{int(bool(args.x_ready) and B <= 2)}>",
                      "algorithmic_bytes_per_step": int(step_bytes),
                      "note": "achieved = algorithmic bytes of the step / device time of the step; the step is "
                              + ("ONE launch of the dominant kernel" if path == "grouped" else "3 launches")},
@@ -621,6 +622,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=200)
     ap.add_argument("--impl", default="gqsa", choices=["gqsa", "reference"])
     ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--bits", type=int, default=4, choices=[2, 4, 8],
+                    help="secondary settings (W2S50, W4S30, ...); the metric's workload is W4S50")
+    ap.add_argument("--sparsity", type=float, default=0.5)
     ap.add_argument("--e2e-steps", type=int, default=2000)
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

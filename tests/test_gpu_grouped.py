@@ -80,13 +80,14 @@ def test_grouped_exact_integer_bit_exact(shapes, bits, B):
                 assert np.array_equal(it[3].cpu().numpy().astype(np.float64), ref), (part, x_ready)
 
 
+@pytest.mark.parametrize("x_ready", [False, True])  # True: the bench's pipelined launch
 @pytest.mark.parametrize("shapes,bits,sp,B", [
     ([(4096, 4096), (14336, 4096), (4096, 14336)], 4, 0.5, 1),   # the bench step
     ([(4096, 4096), (14336, 4096), (4096, 14336)], 2, 0.5, 2),
     ([(4096, 4096), (1024, 4096), (1024, 4096)], 4, 0.3, 1),     # LLaMA-3-8B q/k/v
     ([(13824, 5120), (13824, 5120)], 4, 0.5, 1),                 # Qwen2.5-14B gate/up
 ])
-def test_grouped_realistic_gates_llama_shapes(shapes, bits, sp, B):
+def test_grouped_realistic_gates_llama_shapes(shapes, bits, sp, B, x_ready):
     items, data = [], []
     for i, (rows, cols) in enumerate(shapes):
         seed = synth.seed_for(f"groupedreal/{i}/{rows}/{cols}/{bits}/{sp}")
@@ -95,14 +96,14 @@ def test_grouped_realistic_gates_llama_shapes(shapes, bits, sp, B):
         desc, d_blob = _dev_blob(bsr)
         items.append((desc, d_blob, _x(x), torch.empty(B, rows, dtype=torch.float32, device="cuda"), None))
         data.append((bsr, x))
-    ws, _ = run_grouped(items)
+    ws, _ = run_grouped(items, x_ready=x_ready)
     first = [it[3].clone() for it in items]
     for it, (bsr, x) in zip(items, data):
         rs = np.random.default_rng(0).choice(bsr["rows"], size=min(bsr["rows"], 512), replace=False)
         ref = O.gemv_rows(bsr, x, rs)
         check_gates(it[3].cpu().numpy()[:, rs], ref, abs_bound(bsr, x, rs), f"grouped {bsr['rows']}x{bsr['cols']}")
     for _ in range(3):
-        run_grouped(items, ws)
+        run_grouped(items, ws, x_ready=x_ready)
         for it, f in zip(items, first):
             assert torch.equal(it[3], f), "grouped reruns must be bit-identical"
 
