@@ -47,6 +47,11 @@ __host__ __device__ constexpr int bufs_for(int B) { return B == 1 ? GQSA_BUFS_SM
 __host__ __device__ constexpr int l2pf_for(int B) { return B <= 2 ? GQSA_L2PF_SMALL : GQSA_L2PF_LARGE; }
 // 1: the in-loop prefetch is one prefetch.global.L2 per lane (a 128-B line
 // each); 0: one cp.async.bulk.prefetch.L2 of the whole tile from lane 0.
+// 1: whole-SM launches request the fix-up's successor records during their
+// last tile (one round trip earlier, one per-tile check more); 0: after the loop.
+#ifndef GQSA_PRE_IN_LOOP
+#define GQSA_PRE_IN_LOOP 1
+#endif
 #ifndef GQSA_LANE_PF
 #define GQSA_LANE_PF 1
 #endif

@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B
   trace_point(p, gw, lane, 3);
 
   auto consume = [&](const TileRegs<BITS, G>& tr, int t) {
-    if (!HALF && kPre > 0 && t == t_end - 1 && cend > t_end && !foreign && waited) {  // (pipelined: after the loop)
+    if (!HALF && GQSA_PRE_IN_LOOP && kPre > 0 && t == t_end - 1 && cend > t_end && !foreign && waited) {  // (else after the loop)
       pre_loaded = true;
       // this warp owns the slice left open at its range end: request the
       // successors' records now, so they are here when the tile is done
