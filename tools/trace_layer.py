@@ -116,9 +116,13 @@ def main():
         arr = (raw[..., 6].astype(np.float64) - t0) / 1e3 - d[..., 4]
         m3 = m & (path == 3)
         if m3.any():
-            print("  slow collectors: arrival returned %.2f us after loop end, exit %.2f us after the arrival, "
-                  "re-polls p50/max %d/%d" % (np.median(arr[m3]), np.median((d[..., 5] - d[..., 4] - arr)[m3]),
-                                             np.median(raw[..., 2][m3]), raw[..., 2][m3].max()))
+            ent = (raw[..., 2].astype(np.float64) - t0) / 1e3
+            b1 = (raw[..., 1].astype(np.float64) - t0) / 1e3
+            arr_abs = arr + d[..., 4]
+            print("  slow collectors (medians, us): loop end -> arrival returned %.2f -> collect entry %.2f -> "
+                  "first batch summed %.2f -> exit %.2f" % (
+                      np.median(arr[m3]), np.median((ent - arr_abs)[m3]), np.median((b1 - ent)[m3]),
+                      np.median((d[..., 5] - b1)[m3])))
     prev_exit = T[:-1, :, 5].max(axis=1)
     rel = T[1:, :, 1].min(axis=1) - prev_exit
     print("PDL release after previous launch's last exit (µs):", " ".join(f"{r:.2f}" for r in rel[:5]))
