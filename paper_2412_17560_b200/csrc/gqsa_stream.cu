@@ -201,6 +201,15 @@ __device__ __noinline__ unsigned long long wait_record(const unsigned long long*
 template <int B>
 __device__ __noinline__ void collect(const Params& p, const Item* items, int w0, int w1, int item, int row, int lane,
                                      Recs<B> q) {
+#ifdef GQSA_TRACE_FIX  // debug builds: collect entry (slot 2) and first batch summed (slot 1)
+  const int gwd = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  auto stamp = [&](int k) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (p.trace && lane == 0) p.trace[(int64_t)gwd * 8 + k] = t;
+  };
+  stamp(2);
+#endif
   float v[B];
 #pragma unroll
   for (int b = 0; b < B; ++b) v[b] = 0.f;
@@ -227,6 +236,9 @@ __device__ __noinline__ void collect(const Params& p, const Item* items, int w0,
         st_relaxed64(a, 0ull);
       }
     }
+#ifdef GQSA_TRACE_FIX
+    if (wb == w0) stamp(1);
+#endif
   }
   if (lane == 0) asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p.cnt + w0), "r"(0u) : "memory");
   store_rows<B>(p, items[item], v, row, lane);
