@@ -16,10 +16,16 @@
 //    into contiguous, equal (+-1 tile) ranges, one per WARP, regardless of
 //    row, slice or item boundaries.
 //  * Weights stream HBM -> registers (128-bit no-allocate loads, evict-first
-//    L2 policy) plus L2 bulk prefetches a few tiles ahead, the first ones requested
-//    BEFORE griddepcontrol.wait (they never depend on the previous kernel).
-//    No shared-memory staging of weights: shared memory serves only the
-//    activation gathers.
+//    L2 policy) plus an L2 prefetch of the tile two ahead, the first ones
+//    requested BEFORE griddepcontrol.wait (they never depend on the previous
+//    kernel).  No shared-memory staging of weights: shared memory serves only
+//    the activation gathers.
+//  * Pipelined launches (HALF = 1; x_ready, B <= 2): the grid
+//    takes part of every SM so the next launches run beside it, and every
+//    global write (rows, fix-up records, counters) is deferred until after
+//    griddepcontrol.wait -- closed slices' rows wait in shared memory.
+//  * The loop is issue-bound at 6 TB/s: keep per-tile instructions out of it
+//    (DESIGN.md §11).
 //  * Activations are staged in shared memory once per CTA (the items its
 //    range touches), with the negated column-group sums (-P, -Q) the
 //    offset-folded dequantization needs and a zero block for padding slots.
