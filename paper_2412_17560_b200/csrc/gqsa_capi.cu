@@ -54,6 +54,16 @@ int pipeline_mode() {
   return mode;
 }
 
+// CTA-level fix-up of whole-SM Stream-K launches:
+// GQSA_CTA_FIX=0 turns it off (the warp-level protocol; A/B experiments).
+int cta_fix_mode() {
+  static const int mode = [] {
+    const char* e = std::getenv("GQSA_CTA_FIX");
+    return e && e[0] == '0' ? 0 : 1;
+  }();
+  return mode;
+}
+
 // Minimum tiles per warp when sizing a launch's warps per CTA (0 = off); A/B knob GQSA_MIN_TPW.
 int min_tiles_per_warp() {
   static const int v = [] {
@@ -150,6 +160,8 @@ int plan_launch(const gqsa_desc_t* const* d, int n, int Bc, Launch* L, int half 
   L->smem = worst + kStageTab;  // + the staging table
   L->tab_offset = worst;
   L->defer_offset = 0;
+  if (!half && cta_fix_mode())  // the CTA-level fix-up reuses the staging area: [W][2][Bc][32] f32 + [W] i32
+    L->smem = std::max(L->smem, (size_t)L->W * 2 * Bc * kLanes * 4 + (size_t)L->W * 4);
   if (half) {  // + the per-warp deferred-store buffers (16-B aligned)
     L->defer_offset = (L->smem + 15) / 16 * 16;
     L->smem = L->defer_offset + (size_t)L->W * defer_bytes_per_warp(Bc);
@@ -271,6 +283,7 @@ int launch_items(const gqsa_gemm_item_t* items, int n, int Bc, const gqsa_option
   p.x_ready = o.x_ready;
   p.stage_tab_offset = (int32_t)L.tab_offset;
   p.defer_offset = (int32_t)L.defer_offset;
+  p.cta_fix = (!L.half && !p.slice_k && cta_fix_mode()) ? 1 : 0;
   uint8_t* ws = static_cast<uint8_t*>(d_ws);
   p.cnt = reinterpret_cast<uint32_t*>(ws + 256);
   p.rec = reinterpret_cast<unsigned long long*>(ws + 256 + (size_t)kMaxWarpsBound * 4);

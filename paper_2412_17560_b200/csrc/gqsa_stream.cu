@@ -250,6 +250,20 @@ __device__ __noinline__ void collect(const Params& p, const Item* items, int w0,
   store_rows<B>(p, items[item], v, row, lane);
 }
 
+// CTA-level fix-up (whole-SM launches, Params::cta_fix): CTA c's partial of a
+// slice split over CTAs c0..c1 is published as c's record (c0: tail record,
+// the others: head records) and arrives on cnt[c0]; the last arriving CTA
+// adds the records in CTA order.  Same wait-free protocol as the warp level,
+// with a CTA's (already reduced) partial as one participant.
+template <int B>
+__device__ __forceinline__ void cta_arrive(const Params& p, const Item* items, const float (&v)[B], int c0, int c,
+                                           int c1, int item, int row, int lane) {
+  publish<B>(p, c, c == c0 ? 1 : 0, v, lane);
+  const Recs<B> q = request_records<B>(p, c0, c1, lane);  // in flight with the arrival
+  const int old = __shfl_sync(0xffffffffu, arrive(p, c0, lane), 0);
+  if (old == c1 - c0) collect<B>(p, items, c0, c1, item, row, lane, q);
+}
+
 // Empty rows get bias (or 0): grid-stride over every item's empty-row list.
 template <int B>
 __device__ __forceinline__ void store_empty_rows(const Params& p, const Item* items) {
@@ -452,12 +466,15 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B
   // values), and the head slice's partial (published after the wait)
   uint32_t* dbuf = HALF ? reinterpret_cast<uint32_t*>(smem + p.defer_offset + warp * defer_bytes_per_warp(B)) : nullptr;
   int n_def = 0;
+  // CTA-level fix-up (whole-SM launches): split slices are reduced in shared
+  // memory after the loop; the head slice's partial waits in hacc
+  const bool cfix = !HALF && p.cta_fix && !p.slice_k;
   bool h_defer = false;
   float hacc[B];
   trace_point(p, gw, lane, 3);
 
   auto consume = [&](const TileRegs<BITS, G>& tr, int t) {
-    if (!HALF && GQSA_PRE_IN_LOOP && kPre > 0 && t == t_end - 1 && cend > t_end && !foreign && waited) {  // (else after the loop)
+    if (!HALF && GQSA_PRE_IN_LOOP && kPre > 0 && t == t_end - 1 && cend > t_end && !foreign && waited && !cfix) {  // (else after the loop)
       pre_loaded = true;
       // this warp owns the slice left open at its range end: request the
       // successors' records now, so they are here when the tile is done
@@ -479,7 +496,7 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B
         h_w0 = cw0;
         h_item = ci;
         h_row = crow;
-        if (HALF && !waited) {  // publish after the wait
+        if ((HALF && !waited) || cfix) {  // publish after the wait / reduce in the CTA after the loop
           h_defer = true;
 #pragma unroll
           for (int b = 0; b < B; ++b) hacc[b] = acc[b];
@@ -533,8 +550,55 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B
   }
 
   int fix_path = 0;  // debug trace: 1 fast, 2 published (not last), 3 published + collected; +10 head collected
+  if (cfix) {
+    // ---- CTA-level fix-up.  The CTA's warps hold consecutive ranges, so the
+    //      pieces of a slice inside the CTA belong to consecutive warps: the
+    //      slice's first warp here (its owner, or warp 0 for a slice that
+    //      began in an earlier CTA) adds them in warp order from shared
+    //      memory (the activation staging is dead once every loop is done).
+    //      Only slices crossing a CTA boundary reach the global protocol,
+    //      with one record per CTA instead of one per warp.
+    const int nw = min(W, p.active_warps - blockIdx.x * W);  // warps with tiles (the trailing ones are idle)
+    asm volatile("bar.sync 1, %0;" ::"r"(nw * 32) : "memory");
+    float* P = reinterpret_cast<float*>(smem);  // [W][2: head, tail][B][32]
+    int* meta = reinterpret_cast<int*>(smem + (size_t)W * 2 * B * kLanes * 4);
+    const bool has_t = cend > t_end;
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      if (h_defer) P[((warp * 2 + 0) * B + b) * kLanes + lane] = hacc[b];
+      if (has_t) P[((warp * 2 + 1) * B + b) * kLanes + lane] = acc[b];
+    }
+    if (lane == 0) meta[warp] = (h_defer ? 1 : 0) | (has_t && foreign ? 2 : 0);
+    asm volatile("bar.sync 1, %0;" ::"r"(nw * 32) : "memory");
+    const int c = blockIdx.x;
+    if (warp == 0 && h_defer) {  // a slice from an earlier CTA closed in warp 0: its only piece here
+      cta_arrive<B>(p, its, hacc, h_w0 / W, c, c, h_item, h_row, lane);
+      fix_path += 10;
+    }
+    if (has_t && (!foreign || warp == 0)) {  // this warp starts the CTA's piece of its open slice
+      float v[B];
+#pragma unroll
+      for (int b = 0; b < B; ++b) v[b] = acc[b];
+      bool closed = false;
+#pragma unroll 1
+      for (int k = warp + 1; k < nw && !closed; ++k) {
+        const int m = meta[k];
+        closed = !(m & 2);  // warp k is not a middle participant: the slice closes in its range
+#pragma unroll
+        for (int b = 0; b < B; ++b) v[b] += P[((k * 2 + (closed ? 0 : 1)) * B + b) * kLanes + lane];
+      }
+      if (closed && !foreign) {
+        store_rows<B>(p, its[ci], v, crow, lane);
+        fix_path += 4;
+      } else {
+        cta_arrive<B>(p, its, v, foreign ? cw0 / W : c, c, closed ? c : warp_of_tile(p, cend - 1) / W, ci, crow,
+                      lane);
+        fix_path += 5;
+      }
+    }
+  }
   // ---- a slice left open at the end of the range continues downstream
-  if (cend > t_end) {
+  if (!cfix && cend > t_end) {
     const int w1 = warp_of_tile(p, cend - 1);
     bool done = false;
     if (kPre > 0 && !foreign && w1 - gw <= kPre) {
