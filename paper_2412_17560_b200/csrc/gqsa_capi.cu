@@ -64,6 +64,22 @@ int cta_fix_mode() {
   return mode;
 }
 
+// Experiments (dependent launches, x_ready = 0): GQSA_DEP_PDL=0 launches them
+// without programmatic dependent launch; GQSA_DEP_WAIT_FIRST=1 makes them wait
+// for the previous kernel before their first weight loads.
+int env_flag(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e && e[0] ? (e[0] != '0') : dflt;
+}
+int dep_pdl() {
+  static const int v = env_flag("GQSA_DEP_PDL", 1);
+  return v;
+}
+int dep_wait_first() {
+  static const int v = env_flag("GQSA_DEP_WAIT_FIRST", 0);
+  return v;
+}
+
 // Minimum tiles per warp when sizing a launch's warps per CTA (0 = off); A/B knob GQSA_MIN_TPW.
 int min_tiles_per_warp() {
   static const int v = [] {
@@ -284,6 +300,7 @@ int launch_items(const gqsa_gemm_item_t* items, int n, int Bc, const gqsa_option
   p.stage_tab_offset = (int32_t)L.tab_offset;
   p.defer_offset = (int32_t)L.defer_offset;
   p.cta_fix = (!L.half && !p.slice_k && cta_fix_mode()) ? 1 : 0;
+  p.wait_first = (!o.x_ready && dep_wait_first()) ? 1 : 0;
   uint8_t* ws = static_cast<uint8_t*>(d_ws);
   p.cnt = reinterpret_cast<uint32_t*>(ws + 256);
   p.rec = reinterpret_cast<unsigned long long*>(ws + 256 + (size_t)kMaxWarpsBound * 4);
@@ -299,7 +316,7 @@ int launch_items(const gqsa_gemm_item_t* items, int n, int Bc, const gqsa_option
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = (o.x_ready || dep_pdl()) ? 1 : 0;
   void* args[] = {&p};
   if (cudaLaunchKernelExC(&cfg, fn, args) != cudaSuccess) return GQSA_ERR_CUDA;
   g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -337,6 +337,7 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B
     t_end = b < t_end ? e : b;
   }
 
+  if (p.wait_first) pdl_wait();  // experiments: no weight loads before the previous kernel completes
   // ---- the first tiles: requested before anything else (weights never
   //      depend on the previous kernel on the stream)
   const uint64_t pol = evict_first_policy();

@@ -1,16 +1,14 @@
 #!/bin/bash
-# scratch: CTA-level fix-up A/B (GQSA_CTA_FIX=1 default vs 0)
+# scratch: dependent launches -- is the cross-CTA fix-up tail slowed by the next launch's prologue loads?
 cd /root/repo
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu_cfix.log 2>&1; tail -3 gpurun_out/pytest_gpu_cfix.log
-for r in 1 2; do
-for v in 1 0; do
-  GQSA_CTA_FIX=$v timeout 300 python bench.py --steps 2000 --warmup 20 --no-cpu-baseline --e2e-steps 10 --x-ready 0 > gpurun_out/ab_cfix$v.json 2>gpurun_out/ab_cfix$v.err
-  python -c "
-import json;d=json.load(open('gpurun_out/ab_cfix$v.json'));print('cfix=$v xr0', d['us_per_step'], [ (l['shape'], l['us']) for l in d['layers']])" || tail -3 gpurun_out/ab_cfix$v.err
+for cfg in "base|" "nopdl|GQSA_DEP_PDL=0" "waitfirst|GQSA_DEP_WAIT_FIRST=1"; do
+  name=${cfg%%|*}; envs=${cfg#*|}
+  echo "== $name"
+  env $envs timeout 300 python tools/trace_layer.py --rows 4096 --cols 4096 --launches 6 > gpurun_out/trace_4096_$name.log 2>&1; tail -7 gpurun_out/trace_4096_$name.log
 done
-done
-for v in 1 0; do
-  GQSA_CTA_FIX=$v timeout 600 python tools/stack_bench.py --sections E --settings W4S50 --forms merged,grouped --batches 1,8 > gpurun_out/stack_cfix$v.log 2>&1; echo cfix=$v; tail -12 gpurun_out/stack_cfix$v.log
+timeout 1200 python tools/ab.py --rounds 1 "base||--x-ready 0" "nopdl|GQSA_DEP_PDL=0|--x-ready 0" "waitfirst|GQSA_DEP_WAIT_FIRST=1|--x-ready 0" 2>&1 | tee gpurun_out/ab_dep.log
+for cfg in "base|" "nopdl|GQSA_DEP_PDL=0" "waitfirst|GQSA_DEP_WAIT_FIRST=1"; do
+  name=${cfg%%|*}; envs=${cfg#*|}
+  env $envs timeout 600 python tools/stack_bench.py --sections E --settings W4S50 --forms merged --batches 1 > gpurun_out/stack_$name.log 2>&1; echo "$name $(grep '"B": 1' gpurun_out/stack_$name.log)"
 done
