@@ -75,6 +75,17 @@ int dep_pdl() {
   static const int v = env_flag("GQSA_DEP_PDL", 1);
   return v;
 }
+// Slice-aligned CTA ranges for single-item whole-SM launches (no cross-CTA
+// fix-up): by default at batch >= 2 (B = 1 measured neutral:
+// the range lookups delay the first weight loads); GQSA_CTA_SLICEK=1 at every
+// batch, 0 off.
+bool cta_slicek_for(int Bc) {
+  static const int v = [] {
+    const char* e = std::getenv("GQSA_CTA_SLICEK");
+    return e && e[0] ? (e[0] != '0' ? 1 : 0) : 2;
+  }();
+  return v == 1 || (v == 2 && Bc >= 2);
+}
 int dep_wait_first() {
   static const int v = env_flag("GQSA_DEP_WAIT_FIRST", 0);
   return v;
@@ -301,6 +312,7 @@ int launch_items(const gqsa_gemm_item_t* items, int n, int Bc, const gqsa_option
   p.defer_offset = (int32_t)L.defer_offset;
   p.cta_fix = (!L.half && !p.slice_k && cta_fix_mode()) ? 1 : 0;
   p.wait_first = (!o.x_ready && dep_wait_first()) ? 1 : 0;
+  p.cta_slicek = (p.cta_fix && n == 1 && cta_slicek_for(Bc)) ? 1 : 0;
   uint8_t* ws = static_cast<uint8_t*>(d_ws);
   p.cnt = reinterpret_cast<uint32_t*>(ws + 256);
   p.rec = reinterpret_cast<unsigned long long*>(ws + 256 + (size_t)kMaxWarpsBound * 4);

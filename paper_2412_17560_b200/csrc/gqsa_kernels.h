@@ -151,7 +151,7 @@ struct Params {
   int32_t cta_fix;           // whole-SM Stream-K: reduce split slices inside the CTA through shared
                              // memory; only CTA-level partials take the global fix-up
   int32_t wait_first;        // experiments: griddepcontrol.wait before the first weight loads (x_ready = 0)
-  int32_t pad1_;
+  int32_t cta_slicek;        // slice-aligned CTA ranges, Stream-K among the CTA's warps (one item, cta_fix)
   uint32_t* cnt;                 // [active_warps] fix-up arrival counters (zero between launches)
   unsigned long long* rec;       // [active_warps][2][B][32] fix-up records {partial, flag}
   uint64_t* trace;               // optional [active_warps][8] %globaltimer stamps (debug)

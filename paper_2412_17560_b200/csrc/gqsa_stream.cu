@@ -61,6 +61,20 @@ __device__ __forceinline__ int item_of(const Params& p, int t) {
   while (i + 1 < p.n_items && t >= p.item[i].tile_end) ++i;
   return i;
 }
+// First tile of CTA c under slice-aligned CTA ranges (Params::cta_slicek, one
+// item): the slice boundary nearest to the even split c * total / grid.
+// Monotone in c; two CTAs may share a boundary (an empty CTA).
+__device__ __forceinline__ int cta_boundary(const Params& p, int c) {
+  if (c <= 0) return 0;
+  if (c >= (int)gridDim.x) return p.total_tiles;
+  const int ideal = (int)((int64_t)c * p.total_tiles / gridDim.x);
+  const Item& it = p.item[0];
+  const int s = __ldg(it.tile_slice + ideal);
+  const int b0 = __ldg(it.slice_tile0 + s);
+  if (b0 == ideal) return ideal;
+  const int b1 = __ldg(it.slice_tile0 + s + 1);
+  return ideal - b0 <= b1 - ideal ? b0 : b1;
+}
 // Shared-memory offset of item i's staged activations in a CTA whose tile
 // range is [t0, t1): the touched items are packed in item order.
 __device__ __forceinline__ uint32_t item_smem_off(const Item* items, int i, int t0, int t1) {
@@ -310,16 +324,28 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B
 
   // ---- task-centric partition: contiguous tile range per warp (+-1 tile)
   int t_begin = 0, t_end = 0;
-  if (gw < p.active_warps) range_of(p, gw, t_begin, t_end);
   // the CTA's range (its warps' ranges are consecutive): which items it stages
   int cta_t0 = 0, cta_t1 = 0;
-  {
+  int nbusy = 0;  // warps of this CTA with tiles (the trailing ones may be idle)
+  if (p.cta_slicek) {
+    // slice-aligned CTA ranges (single-item whole-SM launches): every CTA
+    // starts and ends on a slice boundary, its warps split its range +-1 tile,
+    // so every split slice is finished inside the CTA (CTA-level fix-up)
+    cta_t0 = cta_boundary(p, blockIdx.x);
+    cta_t1 = cta_boundary(p, blockIdx.x + 1);
+    const int n = cta_t1 - cta_t0, q = n / W, r = n % W;
+    t_begin = cta_t0 + warp * q + min(warp, r);
+    t_end = t_begin + q + (warp < r ? 1 : 0);
+    nbusy = min(W, n);
+  } else {
+    if (gw < p.active_warps) range_of(p, gw, t_begin, t_end);
     const int w0 = blockIdx.x * W, w1 = min(w0 + W, p.active_warps) - 1;
     if (w0 < p.active_warps) {
       int e;
       range_of(p, w0, cta_t0, e);
       range_of(p, w1, e, cta_t1);
     }
+    nbusy = min(W, p.active_warps - blockIdx.x * W);
   }
   if (p.slice_k && t_end > t_begin) {
     // data-centric partition (Slice-K): the warp owns the slices whose FIRST
@@ -559,7 +585,7 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B
     //      memory (the activation staging is dead once every loop is done).
     //      Only slices crossing a CTA boundary reach the global protocol,
     //      with one record per CTA instead of one per warp.
-    const int nw = min(W, p.active_warps - blockIdx.x * W);  // warps with tiles (the trailing ones are idle)
+    const int nw = nbusy;
     asm volatile("bar.sync 1, %0;" ::"r"(nw * 32) : "memory");
     float* P = reinterpret_cast<float*>(smem);  // [W][2: head, tail][B][32]
     int* meta = reinterpret_cast<int*>(smem + (size_t)W * 2 * B * kLanes * 4);
