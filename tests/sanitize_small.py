@@ -1,7 +1,7 @@
 """Small launches of every kernel family for compute-sanitizer (memcheck /
 racecheck / synccheck): gemv, small-batch GEMM (batch split), Slice-K,
 fp16 output, grouped launch (whole-SM and pipelined), LAYOUT-TC, fused
-all-gather.  Exits non-zero on a
+all-gather, whole-GPU launches (CTA-level fix-up, slice-aligned CTA ranges).  Exits non-zero on a
 mismatch against the oracle (exact-integer mode)."""
 import os
 import sys
@@ -17,7 +17,10 @@ from paper_2412_17560_b200 import gqsa, synth  # noqa: E402
 ok = True
 for rows, cols, bits, B, mask in ((300, 1024, 4, 1, "uniform"), (77, 208, 2, 3, "uniform"),
                                   (512, 2048, 4, 2, "skewed"), (64, 4096, 8, 1, "uniform"),
-                                  (128, 14336, 4, 8, "uniform"), (5, 64, 4, 1, "uniform")):
+                                  (128, 14336, 4, 8, "uniform"), (5, 64, 4, 1, "uniform"),
+                                  # every CTA busy: slices cross CTA boundaries (CTA-level fix-up at
+                                  # B = 1, slice-aligned CTA ranges at B >= 2)
+                                  (4096, 4096, 4, 1, "uniform"), (2048, 4096, 4, 3, "skewed")):
     bsr = synth.make_layer(rows + cols, rows, cols, bits=bits, sparsity=0.5, mask=mask, mode="exact_int")
     x = synth.make_x(rows, B, cols, mode="exact_int")
     L = gqsa.Layer(bsr)
