@@ -13,7 +13,8 @@ launch declares them ready (x_ready, `--x-ready 0` turns it off): the library
 then runs it PIPELINED -- half of every SM, all global writes deferred until
 the previous step's launch has completed -- so consecutive steps overlap
 their start-up and drain.  `layers[]` are standalone
-launches of each layer with x_ready = 0 (the dependent-chain case).
+launches of each layer: `us` with x_ready = 0 (the dependent-chain case),
+`us_x_ready` as consecutive independent (pipelined) launches.
 
 Timing: the weights rotate over R device copies of the layer set (> 2x the
 126 MB L2), so every launch streams from HBM.  K steps are replayed from CUDA
@@ -507,21 +508,31 @@ def run_gpu(args):
     if world == 1 and not args.no_layers:
         for i, L in enumerate(layers):
             d = descs[i]
+            # this layer alone rotates over > 2.2x L2 of its own copies
+            Rl = max(R, math.ceil(2.2 * L2_BYTES / int(d.blob_bytes)) + 1) if not args.no_rotate else 1
+            lcop = [copies[r % R][i] if r < R else copies[0][i].clone() for r in range(Rl)]
 
-            def one(k, i=i):
+            def one(k, i=i):  # dependent form: each launch may read the previous one's output
                 if B == 1:
-                    gqsa.gemv(d, copies[k % R][i], xs[i][0], ys[i][0], None, ws)
+                    gqsa.gemv(d, lcop[k % Rl], xs[i][0], ys[i][0], None, ws)
                 else:
-                    gqsa.gemm_smallbatch(d, copies[k % R][i], xs[i], ys[i], None, ws)
-            reps = max(R, (2000 // R) * R)
-            lt = StepTimer(torch, stream, one, R, reps, 3 * R, True)
-            us = lt.run() * 1e3 / reps
+                    gqsa.gemm_smallbatch(d, lcop[k % Rl], xs[i], ys[i], None, ws)
+
+            def one_ready(k, i=i):  # independent form: x declared ready (pipelined launches at B <= 2)
+                gqsa.gemm_ex(d, lcop[k % Rl], xs[i], ys[i], ws=ws, x_ready=True)
+            reps = max(Rl, (2000 // Rl) * Rl)
+            us = StepTimer(torch, stream, one, Rl, reps, 3 * Rl, True).run() * 1e3 / reps
+            us_r = StepTimer(torch, stream, one_ready, Rl, reps, 3 * Rl, True).run() * 1e3 / reps
+            del lcop
             cb = counted_bytes(d.rows, d.cols, d.nnzg, bits, B)
             layer_rows.append({"shape": f"{d.rows}x{d.cols}", "role": L["name"], "nnzg": d.nnzg,
                                "counted_bytes": cb, "blob_bytes": int(d.blob_bytes), "us": round(us, 3),
                                "gbs": round(cb / us / 1e3, 1),
                                "frac_of_8tbs": round(cb / us / 1e3 / NOMINAL_HBM_GBS, 4),
-                               "frac_of_measured": round(cb / us / 1e3 / hbm_peak, 4)})
+                               "frac_of_measured": round(cb / us / 1e3 / hbm_peak, 4),
+                               "us_x_ready": round(us_r, 3), "gbs_x_ready": round(cb / us_r / 1e3, 1),
+                               "frac_of_measured_x_ready": round(cb / us_r / 1e3 / hbm_peak, 4),
+                               "rotation_copies": Rl})
 
     # ---- end to end through the public C ABI with host buffers (pinned):
     #      gqsa_gemm_multi_hostio = one H2D copy of the step's inputs, the
