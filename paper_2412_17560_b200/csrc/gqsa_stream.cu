@@ -264,18 +264,49 @@ __device__ __noinline__ void collect(const Params& p, const Item* items, int w0,
   store_rows<B>(p, items[item], v, row, lane);
 }
 
-// CTA-level fix-up (whole-SM launches, Params::cta_fix): CTA c's partial of a
-// slice split over CTAs c0..c1 is published as c's record (c0: tail record,
-// the others: head records) and arrives on cnt[c0]; the last arriving CTA
-// adds the records in CTA order.  Same wait-free protocol as the warp level,
-// with a CTA's (already reduced) partial as one participant.
+// CTA-level fix-up (whole-SM launches, Params::cta_fix).  A slice split over
+// CTAs c0..c1 is finished by c1, the CTA holding its last tile: CTAs c0..c1-1
+// publish their (already reduced) partial as a record (c0: tail record, the
+// others: head records) and move on; c1 adds the records in CTA order, then
+// its own partial, and stores the rows.  c1 waits only for LOWER-indexed
+// CTAs, which never wait for a higher one -- the forward-progress assumption
+// of decoupled look-back (CTAs are dispatched in index order) -- so there is
+// no arrival counter and no atomic round trip on the critical path.
 template <int B>
-__device__ __forceinline__ void cta_arrive(const Params& p, const Item* items, const float (&v)[B], int c0, int c,
+__device__ __noinline__ void collect_lower(const Params& p, const Item* items, int c0, int c1, const float (&own)[B],
+                                           int item, int row, int lane) {
+  float v[B];
+#pragma unroll
+  for (int b = 0; b < B; ++b) v[b] = 0.f;
+#pragma unroll 1
+  for (int cb = c0; cb < c1; cb += kRec) {
+    unsigned long long r[kRec][B];
+#pragma unroll
+    for (int k = 0; k < kRec; ++k)
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+        r[k][b] = cb + k < c1 ? ld_relaxed64(rec_ptr<B>(p, cb + k, cb + k == c0 ? 1 : 0, b, lane)) : (1ull << 32);
+#pragma unroll
+    for (int k = 0; k < kRec; ++k) {
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        if (cb + k >= c1) continue;
+        unsigned long long* a = rec_ptr<B>(p, cb + k, cb + k == c0 ? 1 : 0, b, lane);
+        if ((r[k][b] >> 32) == 0ull) r[k][b] = wait_record(a);
+        v[b] = (cb + k == c0) ? __uint_as_float((uint32_t)r[k][b]) : v[b] + __uint_as_float((uint32_t)r[k][b]);
+        st_relaxed64(a, 0ull);
+      }
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < B; ++b) v[b] += own[b];
+  store_rows<B>(p, items[item], v, row, lane);
+}
+template <int B>
+__device__ __forceinline__ void cta_finish(const Params& p, const Item* items, const float (&v)[B], int c0, int c,
                                            int c1, int item, int row, int lane) {
-  publish<B>(p, c, c == c0 ? 1 : 0, v, lane);
-  const Recs<B> q = request_records<B>(p, c0, c1, lane);  // in flight with the arrival
-  const int old = __shfl_sync(0xffffffffu, arrive(p, c0, lane), 0);
-  if (old == c1 - c0) collect<B>(p, items, c0, c1, item, row, lane, q);
+  if (c < c1) publish<B>(p, c, c == c0 ? 1 : 0, v, lane);
+  else collect_lower<B>(p, items, c0, c1, v, item, row, lane);
 }
 
 // Empty rows get bias (or 0): grid-stride over every item's empty-row list.
@@ -597,9 +628,12 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B
     }
     if (lane == 0) meta[warp] = (h_defer ? 1 : 0) | (has_t && foreign ? 2 : 0);
     asm volatile("bar.sync 1, %0;" ::"r"(nw * 32) : "memory");
+#ifdef GQSA_TRACE_FIX  // debug builds: the CTA's pieces are in shared memory (trace slot 6)
+    trace_point(p, gw, lane, 6);
+#endif
     const int c = blockIdx.x;
     if (warp == 0 && h_defer) {  // a slice from an earlier CTA closed in warp 0: its only piece here
-      cta_arrive<B>(p, its, hacc, h_w0 / W, c, c, h_item, h_row, lane);
+      cta_finish<B>(p, its, hacc, h_w0 / W, c, c, h_item, h_row, lane);
       fix_path += 10;
     }
     if (has_t && (!foreign || warp == 0)) {  // this warp starts the CTA's piece of its open slice
@@ -618,7 +652,7 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B
         store_rows<B>(p, its[ci], v, crow, lane);
         fix_path += 4;
       } else {
-        cta_arrive<B>(p, its, v, foreign ? cw0 / W : c, c, closed ? c : warp_of_tile(p, cend - 1) / W, ci, crow,
+        cta_finish<B>(p, its, v, foreign ? cw0 / W : c, c, closed ? c : warp_of_tile(p, cend - 1) / W, ci, crow,
                       lane);
         fix_path += 5;
       }

@@ -13,11 +13,12 @@ bookkeeping of the CTA-level fix-up of whole-SM launches:
   * the first warp of a slice's part inside a CTA (the slice's owner, or warp 0
     for a slice begun in an earlier CTA) walks the following warps' pieces in
     warp order until the slice closes or the CTA ends;
-  * a slice that crosses CTA boundaries gets exactly one record from every CTA
-    c0..c1 it touches, and the last of those c1 - c0 + 1 arrivals collects.
+  * a slice that crosses CTA boundaries gets exactly one piece from every CTA
+    c0..c1 it touches; c0..c1-1 publish theirs as records and c1, the CTA
+    holding the slice's last tile, adds them (it waits only for lower CTAs).
 
-It asserts that every tile of every slice is counted exactly once and that the
-arrival count each collector waits for is the number of records published.
+It asserts that every tile of every slice is counted exactly once, that a
+crossing slice has one piece per touched CTA, and that its collector is c1.
 """
 import random
 
@@ -90,6 +91,8 @@ def _model(total, slice_ends, W, nwarps):
             assert s not in stores
             c0, c1 = warp_of_tile(st) // W, warp_of_tile(en - 1) // W
             assert sorted(c for c, _ in records[s]) == list(range(c0, c1 + 1))
+            # the collector is c1, the CTA holding the slice's last tile; it waits only for c0..c1-1
+            assert [c for c, v in records[s] if en - 1 in v] == [c1]
             seen = set()
             for _, v in records[s]:
                 assert not seen & v

@@ -123,6 +123,22 @@ def main():
                   "first batch summed %.2f -> exit %.2f" % (
                       np.median(arr[m3]), np.median((ent - arr_abs)[m3]), np.median((b1 - ent)[m3]),
                       np.median((d[..., 5] - b1)[m3])))
+    if os.environ.get("GQSA_TRACE_FIX"):  # CTA-level fix-up: 6 = pieces in smem, 3 = arrival returned
+        raw = np.stack([b.cpu().numpy().reshape(W, 8) for b in bufs])[1:].astype(np.float64)
+        rel = (raw - t0) / 1e3
+        for paths, name in (((5, 15), "cross-CTA reducers"), ((4, 14), "in-CTA reducers")):
+            m5 = m & np.isin(path, paths)
+            if not m5.any():
+                continue
+            print("  slow %s (n=%d, medians, us): loop end -> pieces in smem %.2f -> arrival returned %.2f "
+                  "-> exit %.2f" % (name, m5.sum(), np.median((rel[..., 6] - d[..., 4])[m5]),
+                                    np.median((rel[..., 3] - rel[..., 6])[m5]),
+                                    np.median((d[..., 5] - rel[..., 3])[m5])))
+        allr = np.isin(path, (5, 15))
+        print("  all cross-CTA reducers: pieces->arrival %.2f, arrival->exit %.2f (medians); "
+              "exit minus launch-median exit p50/p95 %.2f/%.2f" % (
+                  np.median((rel[..., 3] - rel[..., 6])[allr]), np.median((d[..., 5] - rel[..., 3])[allr]),
+                  np.median(late[allr]), np.percentile(late[allr], 95)))
     prev_exit = T[:-1, :, 5].max(axis=1)
     rel = T[1:, :, 1].min(axis=1) - prev_exit
     print("PDL release after previous launch's last exit (µs):", " ".join(f"{r:.2f}" for r in rel[:5]))
