@@ -47,11 +47,6 @@ __host__ __device__ constexpr int bufs_for(int B) { return B == 1 ? GQSA_BUFS_SM
 __host__ __device__ constexpr int l2pf_for(int B) { return B <= 2 ? GQSA_L2PF_SMALL : GQSA_L2PF_LARGE; }
 // 1: the in-loop prefetch is one prefetch.global.L2 per lane (a 128-B line
 // each); 0: one cp.async.bulk.prefetch.L2 of the whole tile from lane 0.
-// 1: whole-SM launches request the fix-up's successor records during their
-// last tile (one round trip earlier, one per-tile check more); 0: after the loop.
-#ifndef GQSA_PRE_IN_LOOP
-#define GQSA_PRE_IN_LOOP 1
-#endif
 #ifndef GQSA_LANE_PF
 #define GQSA_LANE_PF 1
 #endif
@@ -152,7 +147,7 @@ struct Params {
                              // memory; only CTA-level partials take the global fix-up
   int32_t wait_first;        // experiments: griddepcontrol.wait before the first weight loads (x_ready = 0)
   int32_t cta_slicek;        // slice-aligned CTA ranges, Stream-K among the CTA's warps (one item, cta_fix)
-  uint32_t* cnt;                 // [active_warps] fix-up arrival counters (zero between launches)
+  uint32_t* cnt;                 // unused by the stream kernel since the look-back fix-up (kept zero)
   unsigned long long* rec;       // [active_warps][2][B][32] fix-up records {partial, flag}
   uint64_t* trace;               // optional [active_warps][8] %globaltimer stamps (debug)
 };

@@ -35,12 +35,13 @@
 //    offsets and z leave with one FFMA and s is applied with one more.  No
 //    tensor cores: the rows of a warp hold groups at unrelated columns
 //    (DESIGN.md §10), and batch 1 is bandwidth-bound.
-//  * Fix-up (slices split across warps), wait-free "last arriver": every
-//    participant publishes its per-lane partials as 64-bit {value, flag}
-//    records and increments the slice's arrival counter; the participant that
-//    arrives last adds all records in warp order (deterministic), stores the
-//    rows and resets counter and flags.  Nobody waits for a warp that has not
-//    already published, so progress never depends on CTA co-residency.
+//  * Fix-up (slices split across warps), look-back: every participant but the
+//    last publishes its per-lane partials as 64-bit {value, flag} records; the
+//    participant holding the slice's last tile adds them in order
+//    (deterministic), then its own, stores the rows and resets the flags.  It
+//    waits only for lower-indexed participants, which never wait for a higher
+//    one.  Whole-SM launches first reduce the pieces inside each CTA through
+//    shared memory, so only CTA-level partials cross CTAs.
 #include "gqsa_device.cuh"
 
 namespace gqsa {
@@ -171,35 +172,11 @@ __device__ __forceinline__ void publish(const Params& p, int w, int which, const
   for (int b = 0; b < B; ++b)
     st_relaxed64(rec_ptr<B>(p, w, which, b, lane), (1ull << 32) | __float_as_uint(v[b]));
 }
-// Arrive on slice counter cnt[w0] (after this warp's records are issued);
-// returns the previous count in lane 0 (other lanes: 0).
-__device__ __forceinline__ int arrive(const Params& p, int w0, int lane) {
-  __syncwarp();
-  int old = 0;
-  if (lane == 0) old = (int)atomicAdd(p.cnt + w0, 1u);
-  return old;
-}
-// The records of the first kRec participants of a slice split over warps
-// w0..w1 (w0's tail record, then head records), requested ahead of the
-// arrival so that the last arriver has them one round trip earlier.
+// Records loaded per round trip by a collector.
 #ifndef GQSA_KREC
 #define GQSA_KREC 8
 #endif
 constexpr int kRec = GQSA_KREC;
-template <int B>
-struct Recs {
-  unsigned long long r[kRec][B];
-};
-template <int B>
-__device__ __forceinline__ Recs<B> request_records(const Params& p, int w0, int w1, int lane) {
-  Recs<B> q;
-#pragma unroll
-  for (int k = 0; k < kRec; ++k)
-#pragma unroll
-    for (int b = 0; b < B; ++b)
-      q.r[k][b] = (w0 + k <= w1) ? ld_relaxed64(rec_ptr<B>(p, w0 + k, k == 0 ? 1 : 0, b, lane)) : 0ull;
-  return q;
-}
 // A record whose flag was not yet visible: poll it (rare; kept out of line so
 // that the collect loop stays small -- the fix-up runs once per launch and
 // its code is cold in the instruction cache).
@@ -213,65 +190,15 @@ __device__ __noinline__ unsigned long long wait_record(const unsigned long long*
   }
   return v;
 }
-// The last arriver of a slice split over warps w0..w1: add every
-// participant's record in warp order (w0's tail record, then the head records
-// of w0+1..w1), reset the flags and the counter, store the rows.  The poll
-// only waits for stores already issued (their writers arrived before us).
-// `q` holds the first kRec records as requested before the arrival (flag 0: reload).
-template <int B>
-__device__ __noinline__ void collect(const Params& p, const Item* items, int w0, int w1, int item, int row, int lane,
-                                     Recs<B> q) {
-#ifdef GQSA_TRACE_FIX  // debug builds: collect entry (slot 2) and first batch summed (slot 1)
-  const int gwd = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  auto stamp = [&](int k) {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (p.trace && lane == 0) p.trace[(int64_t)gwd * 8 + k] = t;
-  };
-  stamp(2);
-#endif
-  float v[B];
-#pragma unroll
-  for (int b = 0; b < B; ++b) v[b] = 0.f;
-  // kRec records per round trip, all requested before the first is used; the
-  // batch loop is not unrolled (small code: the tail runs cold)
-#pragma unroll 1
-  for (int wb = w0; wb <= w1; wb += kRec) {
-    unsigned long long r[kRec][B];
-#pragma unroll
-    for (int k = 0; k < kRec; ++k)
-#pragma unroll
-      for (int b = 0; b < B; ++b)
-        r[k][b] = wb == w0         ? q.r[k][b]
-                  : (wb + k <= w1) ? ld_relaxed64(rec_ptr<B>(p, wb + k, 0, b, lane))
-                                   : (1ull << 32);
-#pragma unroll
-    for (int k = 0; k < kRec; ++k) {
-#pragma unroll
-      for (int b = 0; b < B; ++b) {
-        if (wb + k > w1) continue;
-        unsigned long long* a = rec_ptr<B>(p, wb + k, wb + k == w0 ? 1 : 0, b, lane);
-        if ((r[k][b] >> 32) == 0ull) r[k][b] = wait_record(a);
-        v[b] = (wb + k == w0) ? __uint_as_float((uint32_t)r[k][b]) : v[b] + __uint_as_float((uint32_t)r[k][b]);
-        st_relaxed64(a, 0ull);
-      }
-    }
-#ifdef GQSA_TRACE_FIX
-    if (wb == w0) stamp(1);
-#endif
-  }
-  if (lane == 0) asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p.cnt + w0), "r"(0u) : "memory");
-  store_rows<B>(p, items[item], v, row, lane);
-}
-
-// CTA-level fix-up (whole-SM launches, Params::cta_fix).  A slice split over
-// CTAs c0..c1 is finished by c1, the CTA holding its last tile: CTAs c0..c1-1
-// publish their (already reduced) partial as a record (c0: tail record, the
-// others: head records) and move on; c1 adds the records in CTA order, then
-// its own partial, and stores the rows.  c1 waits only for LOWER-indexed
-// CTAs, which never wait for a higher one -- the forward-progress assumption
-// of decoupled look-back (CTAs are dispatched in index order) -- so there is
-// no arrival counter and no atomic round trip on the critical path.
+// Look-back fix-up.  A slice split over participants c0..c1 (CTAs in the
+// CTA-level fix-up of whole-SM launches, Params::cta_fix; warps otherwise) is
+// finished by c1, the participant holding its last tile: c0..c1-1 publish
+// their partial as a record (c0: tail record, the others: head records) and
+// move on; c1 adds the records in participant order, then its own partial,
+// and stores the rows.  c1 waits only for LOWER-indexed participants, which
+// never wait for a higher one -- the forward-progress assumption of decoupled
+// look-back (CTAs are dispatched in index order; the warps of a CTA are
+// co-resident) -- so there is no arrival counter and no atomic round trip.
 template <int B>
 __device__ __noinline__ void collect_lower(const Params& p, const Item* items, int c0, int c1, const float (&own)[B],
                                            int item, int row, int lane) {
@@ -512,13 +439,9 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B
   float acc[B];
 #pragma unroll
   for (int b = 0; b < B; ++b) acc[b] = 0.f;
-  // head slice (began upstream, closed in this range): arrival result checked at the range end
-  bool h_pending = false;
-  int h_old = 0, h_w0 = 0, h_item = 0, h_row = -1;
-  // first-warp fast path: the successors' head records, requested during the last tile
-  constexpr int kPre = B <= 2 ? 3 : 0;
-  unsigned long long pre[kPre > 0 ? kPre : 1][B];
-  bool pre_loaded = false;
+  // head slice (began upstream, closed in this range): this warp holds its last
+  // tile, so it collects it after the loop (look-back)
+  int h_w0 = 0, h_item = 0, h_row = -1;
   // pipelined mode: rows of slices closed before the PDL wait, buffered per
   // lane in shared memory ([slot][lane] row | item << 28, then [slot][b][lane]
   // values), and the head slice's partial (published after the wait)
@@ -532,17 +455,6 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B
   trace_point(p, gw, lane, 3);
 
   auto consume = [&](const TileRegs<BITS, G>& tr, int t) {
-    if (!HALF && GQSA_PRE_IN_LOOP && kPre > 0 && t == t_end - 1 && cend > t_end && !foreign && waited && !cfix) {  // (else after the loop)
-      pre_loaded = true;
-      // this warp owns the slice left open at its range end: request the
-      // successors' records now, so they are here when the tile is done
-      const int n = warp_of_tile(p, cend - 1) - gw;
-#pragma unroll
-      for (int k = 0; k < kPre; ++k)
-#pragma unroll
-        for (int b = 0; b < B; ++b)
-          pre[k][b] = k < n ? ld_relaxed64(rec_ptr<B>(p, gw + 1 + k, 0, b, lane)) : (1ull << 32);
-    }
 #pragma unroll
     for (int u = 0; u < kPerLane; ++u) group_accumulate<BITS, B, G>(tr, u, acc, xv);
 #ifdef GQSA_TRACE_TILE0  // debug builds: a per-tile check is too costly in the hot loop
@@ -550,19 +462,13 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B
 #endif
     if (t + 1 == cend) {  // the slice ends with this tile: its rows are complete here
       if (!HALF) ensure_wait();
-      if (foreign) {  // ... but began upstream: publish, arrive, check at the range end
+      if (foreign) {  // ... but began upstream: finished after the loop (look-back / CTA reduction)
         h_w0 = cw0;
         h_item = ci;
         h_row = crow;
-        if ((HALF && !waited) || cfix) {  // publish after the wait / reduce in the CTA after the loop
-          h_defer = true;
+        h_defer = true;
 #pragma unroll
-          for (int b = 0; b < B; ++b) hacc[b] = acc[b];
-        } else {
-          publish<B>(p, gw, 0, acc, lane);
-          h_old = arrive(p, cw0, lane);
-          h_pending = true;
-        }
+        for (int b = 0; b < B; ++b) hacc[b] = acc[b];
       } else if (HALF && !waited && n_def < kDeferSlots) {
         defer_rows<B>(its[ci], acc, crow, ci, lane, dbuf, n_def++);
       } else {
@@ -598,23 +504,18 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B
   }
   trace_point(p, gw, lane, 4);
   ensure_wait();
-  if (HALF) {  // the writes deferred during the loop
+  if (HALF)  // the row stores deferred during the loop
     for (int k = 0; k < n_def; ++k) flush_deferred<B>(p, its, dbuf, k, lane);
-    if (h_defer) {
-      publish<B>(p, gw, 0, hacc, lane);
-      h_old = arrive(p, h_w0, lane);
-      h_pending = true;
-    }
-  }
 
-  int fix_path = 0;  // debug trace: 1 fast, 2 published (not last), 3 published + collected; +10 head collected
+  int fix_path = 0;  // debug trace: 2 published, +10 head collected; CTA level: 4 stored in the CTA, 5 CTA piece
+                     // published or collected
   if (cfix) {
     // ---- CTA-level fix-up.  The CTA's warps hold consecutive ranges, so the
     //      pieces of a slice inside the CTA belong to consecutive warps: the
     //      slice's first warp here (its owner, or warp 0 for a slice that
     //      began in an earlier CTA) adds them in warp order from shared
     //      memory (the activation staging is dead once every loop is done).
-    //      Only slices crossing a CTA boundary reach the global protocol,
+    //      Only slices crossing a CTA boundary reach the global look-back,
     //      with one record per CTA instead of one per warp.
     const int nw = nbusy;
     asm volatile("bar.sync 1, %0;" ::"r"(nw * 32) : "memory");
@@ -658,65 +559,16 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B
       }
     }
   }
-  // ---- a slice left open at the end of the range continues downstream
-  if (!cfix && cend > t_end) {
-    const int w1 = warp_of_tile(p, cend - 1);
-    bool done = false;
-    if (kPre > 0 && !foreign && w1 - gw <= kPre) {
-      // fast path: every successor already published -> add them in warp
-      // order and finish the rows here, without arriving (the successors'
-      // arrivals are cancelled so the counter returns to zero).  Bounded
-      // waiting for the successors here measured no faster than the
-      // last-arriver path below, so the owner never waits.
-      if (!pre_loaded) {  // not requested during the last tile (x_ready)
-#pragma unroll
-        for (int k = 0; k < kPre; ++k)
-#pragma unroll
-          for (int b = 0; b < B; ++b)
-            pre[k][b] = k < w1 - gw ? ld_relaxed64(rec_ptr<B>(p, gw + 1 + k, 0, b, lane)) : (1ull << 32);
-      }
-      bool ready = true;
-#pragma unroll
-      for (int k = 0; k < kPre; ++k)
-#pragma unroll
-        for (int b = 0; b < B; ++b) ready &= (pre[k][b] >> 32) != 0ull;
-      if (__all_sync(0xffffffffu, ready)) {
-        float v[B];
-#pragma unroll
-        for (int b = 0; b < B; ++b) {
-          v[b] = acc[b];
-#pragma unroll
-          for (int k = 0; k < kPre; ++k)
-            if (k < w1 - gw) {
-              v[b] += __uint_as_float((uint32_t)pre[k][b]);
-              st_relaxed64(rec_ptr<B>(p, gw + 1 + k, 0, b, lane), 0ull);
-            }
-        }
-        if (lane == 0) atomicAdd(p.cnt + gw, (unsigned)(gw - w1));
-        store_rows<B>(p, its[ci], v, crow, lane);
-        done = true;
-        fix_path = 1;
-      }
-    }
-    if (!done) {
-      const int which = foreign ? 0 : 1;  // middle participant: head record; first warp: tail record
-      publish<B>(p, gw, which, acc, lane);
-      const Recs<B> q = request_records<B>(p, cw0, w1, lane);  // in flight with the arrival
-      const int old = __shfl_sync(0xffffffffu, arrive(p, cw0, lane), 0);
+  if (!cfix) {
+    // ---- warp-level look-back: publish this warp's piece of the slice left
+    //      open at the range end (head record if the slice began upstream),
+    //      then finish the slice that began upstream and closed here
+    if (cend > t_end) {
+      publish<B>(p, gw, foreign ? 0 : 1, acc, lane);
       fix_path = 2;
-#ifdef GQSA_TRACE_FIX  // debug builds: time the arrival returned, in trace slot 6
-      trace_point(p, gw, lane, 6);
-#endif
-      if (old == w1 - cw0) {
-        collect<B>(p, its, cw0, w1, ci, crow, lane, q);
-        fix_path = 3;
-      }
     }
-  }
-  if (h_pending) {
-    const int old = __shfl_sync(0xffffffffu, h_old, 0);
-    if (old == gw - h_w0) {
-      collect<B>(p, its, h_w0, gw, h_item, h_row, lane, request_records<B>(p, h_w0, gw, lane));
+    if (h_defer) {
+      collect_lower<B>(p, its, h_w0, gw, hacc, h_item, h_row, lane);
       fix_path += 10;
     }
   }
