@@ -533,10 +533,6 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B
     trace_point(p, gw, lane, 6);
 #endif
     const int c = blockIdx.x;
-    if (warp == 0 && h_defer) {  // a slice from an earlier CTA closed in warp 0: its only piece here
-      cta_finish<B>(p, its, hacc, h_w0 / W, c, c, h_item, h_row, lane);
-      fix_path += 10;
-    }
     if (has_t && (!foreign || warp == 0)) {  // this warp starts the CTA's piece of its open slice
       float v[B];
 #pragma unroll
@@ -557,6 +553,11 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B
                       lane);
         fix_path += 5;
       }
+    }
+    // after this warp's own piece is out (publish before waiting: no chains of waits across CTAs)
+    if (warp == 0 && h_defer) {  // a slice from an earlier CTA closed in warp 0: its only piece here
+      cta_finish<B>(p, its, hacc, h_w0 / W, c, c, h_item, h_row, lane);
+      fix_path += 10;
     }
   }
   if (!cfix) {
