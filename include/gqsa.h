@@ -22,8 +22,11 @@
  * different streams, each with its OWN workspace.  A workspace
  * must be zero-filled once when allocated; every call leaves it zero again
  * (fix-up counters and record flags; the partial-sum words are scratch).
- * Forward progress never depends on CTA co-residency: no thread waits for a
- * thread that has not already written what it waits for.
+ * Forward progress never depends on CTA co-residency: the stream kernel's
+ * fix-up (look-back) only waits for LOWER-indexed warps / CTAs of the same
+ * launch, which never wait for a higher one, and CTAs are dispatched in index
+ * order; the LAYOUT-TC kernel's fix-up only waits for records whose writers
+ * have already arrived.
  *
  * Errors: every int-returning function returns GQSA_OK (0) or a negative
  * gqsa_status_t.  Errors raised during asynchronous device execution surface
@@ -176,8 +179,8 @@ int gqsa_read_desc(const void* blob, size_t blob_bytes, gqsa_desc_t* desc);
 int gqsa_unpack(const void* blob, size_t blob_bytes, gqsa_bsr_t* out);
 
 /* Workspace bytes a gemv/gemm (or grouped) call needs for `batch` columns on
- * the current device: per-warp fix-up arrival counters and partial-sum records
- * (DESIGN.md §6).  It depends on the batch and the device's SM count, not on
+ * the current device: per-warp fix-up partial-sum records and (LAYOUT-TC)
+ * arrival counters.  It depends on the batch and the device's SM count, not on
  * the layer.  Zero-fill once; every call leaves it zero. */
 int gqsa_workspace_size(const gqsa_desc_t* desc, int32_t batch, size_t* bytes);
 
