@@ -156,7 +156,7 @@ int plan_launch(const gqsa_desc_t* const* d, int n, int Bc, Launch* L, int half 
   // at least min_tiles_per_warp() tiles -- shorter fix-up chains, less
   // per-warp start-up, and CTAs small enough for the next launch to be
   // resident beside them
-  const int mt = min_tiles_per_warp();
+  const int mt = Bc == 1 ? min_tiles_per_warp() : 0;  // measured neutral-to-worse at batch 8
   if (mt > 0) L->W = (int)std::max<int64_t>(1, std::min<int64_t>(L->W, (total + (int64_t)sms * mt - 1) / ((int64_t)sms * mt)));
   const int warps = std::min(sms * L->W * (half ? 1 : full_ctas_for(Bc)), kMaxWarpsBound);
   L->active = (int)std::min<int64_t>(total, warps);

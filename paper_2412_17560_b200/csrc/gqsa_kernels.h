@@ -104,8 +104,13 @@ __host__ __device__ constexpr int defer_bytes_per_warp(int B) { return kDeferSlo
 __host__ __device__ constexpr int half_smem_limit(int B) {
   return (kSmemPerSm - pipe_ctas_for(B) * 2048) / pipe_ctas_for(B);
 }
+// Small launches use fewer warps per CTA so that each warp streams at least
+// this many tiles (4096^2 dependent launch: 20 warps / 1.4 tiles each 6.10 us,
+// 10 warps / 2.8 tiles 5.59 us; LLaMA-3-8B stack 1188 -> 1155 us per token;
+// larger layers and the bench step have more tiles per warp and are unchanged;
+// batch 1 only: at batch 8 4096^2 measured 16.3 -> 16.8 us).
 #ifndef GQSA_MIN_TPW
-#define GQSA_MIN_TPW 0
+#define GQSA_MIN_TPW 3
 #endif
 constexpr int kMinTilesPerWarp = GQSA_MIN_TPW;  // see min_tiles_per_warp() in gqsa_capi.cu
 constexpr int kMaxWarpsBound = 148 * 32;  // fix-up records the workspace holds per launch (any B200 grid)

@@ -3,6 +3,10 @@ independent GEMVs in ONE launch -- their tile streams concatenated and cut
 into equal per-warp ranges that cross item boundaries -- must give, item by
 item, what the fp64 oracle gives: bit-exact in exact-integer mode, within the
 gates G1/G2/G3 otherwise, bit-identical across reruns, workspace left zero."""
+import os
+import subprocess
+import sys
+
 import numpy as np
 import pytest
 
@@ -238,7 +242,16 @@ def test_grouped_argument_errors():
 def test_grouped_item_split_when_activations_exceed_smem():
     """Eight one-tile items of K = 32736 land in one CTA, whose shared memory
     cannot hold all eight activation vectors: the library splits the item
-    list into several launches, results exact."""
+    list into several launches, results exact.  (Runs with GQSA_MIN_TPW=0:
+    by default a launch this small gets one-warp CTAs, each touching one item,
+    and needs no split.)"""
+    if os.environ.get("GQSA_MIN_TPW") != "0":
+        r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu",
+                            f"{os.path.abspath(__file__)}::test_grouped_item_split_when_activations_exceed_smem"],
+                           env={**os.environ, "GQSA_MIN_TPW": "0"}, capture_output=True, text=True, timeout=600,
+                           cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+        return
     items, refs = [], []
     for i in range(8):
         bsr = synth.make_layer(synth.seed_for(f"gsplit/{i}"), 1, 32736, sparsity=0.99, mode="exact_int")
