@@ -22,7 +22,7 @@
 //    the activation gathers.
 //  * Pipelined launches (HALF = 1; x_ready, B <= 2): the grid
 //    takes part of every SM so the next launches run beside it, and every
-//    global write (rows, fix-up records, counters) is deferred until after
+//    global write (rows, fix-up records) is deferred until after
 //    griddepcontrol.wait -- closed slices' rows wait in shared memory.
 //  * The loop is issue-bound at 6 TB/s: keep per-tile instructions out of it
 //    (DESIGN.md §11).
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(32 * warps_of(B, HALF), HALF ? pipe_ctas_for(B
   StageEntry* const stab = reinterpret_cast<StageEntry*>(smem + p.stage_tab_offset);
   stage_table<B, G>(p, cta_t0, cta_t1, stab);
   // x may be the previous kernel's output; with x_ready the wait is deferred
-  // to just before this launch's first global write (y, records, counters)
+  // to just before this launch's first global write (y, fix-up records)
   bool waited = !p.x_ready;
   if (waited) pdl_wait();
   trace_point(p, gw, lane, 1);
