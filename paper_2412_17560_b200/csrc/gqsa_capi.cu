@@ -387,7 +387,9 @@ int run_grouped(const gqsa_gemm_item_t* items, int n, int B, const gqsa_options_
 // per row) and, unless the column sums come from the mma (xq_mma), the X_c table.
 size_t tc_smem(const gqsa_desc_t* d, int Bc, bool xq_mma) {
   const size_t xrow = 2 * (size_t)d->cols + 32;
-  return (size_t)Bc * xrow + (xq_mma ? 0 : ((size_t)d->cols / kGroup + 1) * 32);
+  const size_t s = (size_t)Bc * xrow + (xq_mma ? 0 : ((size_t)d->cols / kGroup + 1) * 32);
+  // the CTA-level fix-up reuses the staging area: [warps][2][4][32] f32 + [warps] i32
+  return cta_fix_mode() ? std::max(s, (size_t)kTcWarps * 2 * 4 * kLanes * 4 + (size_t)kTcWarps * 4) : s;
 }
 
 // Batch chunking of a LAYOUT-TC GEMM: the largest balanced chunk whose x fits,
@@ -447,6 +449,7 @@ int run_tc(const gqsa_desc_t* d, const void* d_blob, const uint16_t* d_X, int B,
     p.out_f16 = o.out_f16;
     p.x_ready = o.x_ready;
     p.xrow = 2 * d->cols + 32;
+    p.cta_fix = (!p.slice_k && cta_fix_mode()) ? 1 : 0;
     uint8_t* ws = static_cast<uint8_t*>(d_ws);
     p.cnt = reinterpret_cast<uint32_t*>(ws + 256);
     p.rec = reinterpret_cast<unsigned long long*>(ws + 256 + (size_t)kMaxWarpsBound * 4);

@@ -199,7 +199,7 @@ struct TcParams {
   int32_t active_warps, part_q, part_r;
   int32_t slice_k, out_f16, x_ready;
   int32_t xrow;                 // shared bytes per staged x row (2K + 32: zero chunk for padding items)
-  int32_t pad_;
+  int32_t cta_fix;              // reduce split blocks inside the CTA first
   uint32_t* cnt;                // [active_warps] fix-up arrival counters (zero between launches)
   unsigned long long* rec;      // [active_warps][2][4][32] fix-up records
   uint64_t* trace;

@@ -145,6 +145,15 @@ __device__ __forceinline__ void tc_collect(const TcParams& p, int w0, int w1, in
 #endif
 }
 
+// CTA-level fix-up: CTA c's (already reduced) piece of a block split over
+// CTAs c0..c1 takes the last-arriver protocol with CTAs as participants.
+template <int B>
+__device__ __forceinline__ void tc_cta_finish(const TcParams& p, const float (&v)[kNV], int c0, int c, int c1,
+                                              int blk, int lane) {
+  tc_publish(p, c, c == c0 ? 1 : 0, v, lane);
+  if (tc_arrive(p, c0, lane) == c1 - c0) tc_collect<B>(p, c0, c1, blk, lane);
+}
+
 struct TcTile {
   uint4 codes;  // items 0..3: this lane's A-fragment word
   uint4 sz0;    // items 0, 1: (s, z) of rows g, g+8
@@ -279,6 +288,10 @@ __global__ void __launch_bounds__(32 * kTcWarps, 1) gqsa_tc_kernel(const __grid_
   int cw0 = foreign ? tc_warp_of_tile(p, bst) : gw;
   bool h_pending = false;
   int h_old = 0, h_w0 = 0, h_blk = 0;
+  // CTA-level fix-up: the head block's partial waits in hacc for the reduction after the loop
+  const bool cfix = p.cta_fix && !p.slice_k;
+  bool h_defer = false;
+  float hacc[kNV];
   float acc[kNV] = {0.f, 0.f, 0.f, 0.f};
   const uint32_t xs_s = (uint32_t)__cvta_generic_to_shared(xs);
   const uint32_t xq_s = (uint32_t)__cvta_generic_to_shared(xq);
@@ -322,7 +335,13 @@ __global__ void __launch_bounds__(32 * kTcWarps, 1) gqsa_tc_kernel(const __grid_
     }
     if (t + 1 == bend) {  // the block ends with this tile
       ensure_wait();
-      if (foreign) {
+      if (foreign && cfix) {
+        h_defer = true;
+        h_w0 = cw0;
+        h_blk = blk;
+#pragma unroll
+        for (int k = 0; k < kNV; ++k) hacc[k] = acc[k];
+      } else if (foreign) {
         tc_publish(p, gw, 0, acc, lane);
         __syncwarp();
         if (lane == 0) h_old = (int)atomicAdd(p.cnt + cw0, 1u);
@@ -357,6 +376,46 @@ __global__ void __launch_bounds__(32 * kTcWarps, 1) gqsa_tc_kernel(const __grid_
   }
   trace_tc(p, gw, lane, 4);
   ensure_wait();
+  if (cfix) {
+    // ---- CTA-level fix-up (as in the stream kernel): the
+    //      pieces of a block inside the CTA belong to consecutive warps; the
+    //      block's first warp here adds them from shared memory (the staging
+    //      is dead once every loop is done); only blocks crossing a CTA
+    //      boundary take the global protocol, one record per CTA.
+    const int nw = min(kTcWarps, p.active_warps - (int)blockIdx.x * kTcWarps);
+    asm volatile("bar.sync 1, %0;" ::"r"(nw * 32) : "memory");
+    float* P = reinterpret_cast<float*>(smem);  // [warps][2: head, tail][kNV][32]
+    int* meta = reinterpret_cast<int*>(smem + (size_t)kTcWarps * 2 * kNV * kLanes * 4);
+    const bool has_t = bend > t_end;
+#pragma unroll
+    for (int k = 0; k < kNV; ++k) {
+      if (h_defer) P[((warp * 2 + 0) * kNV + k) * kLanes + lane] = hacc[k];
+      if (has_t) P[((warp * 2 + 1) * kNV + k) * kLanes + lane] = acc[k];
+    }
+    if (lane == 0) meta[warp] = (h_defer ? 1 : 0) | (has_t && foreign ? 2 : 0);
+    asm volatile("bar.sync 1, %0;" ::"r"(nw * 32) : "memory");
+    const int c = blockIdx.x;
+    if (has_t && (!foreign || warp == 0)) {  // this warp starts the CTA's piece of its open block
+      float v[kNV];
+#pragma unroll
+      for (int k = 0; k < kNV; ++k) v[k] = acc[k];
+      bool closed = false;
+#pragma unroll 1
+      for (int w = warp + 1; w < nw && !closed; ++w) {
+        closed = !(meta[w] & 2);  // warp w is not a middle participant: the block closes in its range
+#pragma unroll
+        for (int k = 0; k < kNV; ++k) v[k] += P[((w * 2 + (closed ? 0 : 1)) * kNV + k) * kLanes + lane];
+      }
+      if (closed && !foreign) tc_store<B>(p, blk, v, lane);
+      else
+        tc_cta_finish<B>(p, v, foreign ? cw0 / kTcWarps : c, c,
+                         closed ? c : tc_warp_of_tile(p, bend - 1) / kTcWarps, blk, lane);
+    }
+    if (warp == 0 && h_defer) tc_cta_finish<B>(p, hacc, h_w0 / kTcWarps, c, c, h_blk, lane);
+    trace_tc(p, gw, lane, 6);
+    trace_tc(p, gw, lane, 5);
+    return;
+  }
   // Up to two collections (the block continuing downstream, the head block
   // that ended in this range), run through one call site of the collect code.
   int a_w0 = 0, a_w1 = 0, a_blk = 0, b_w0 = 0, b_w1 = 0, b_blk = 0, nc = 0;

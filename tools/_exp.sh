@@ -1,6 +1,7 @@
 #!/bin/bash
+# scratch: LAYOUT-TC with the CTA-level fix-up: tests + sweep T (vs GQSA_CTA_FIX=0)
 cd /root/repo
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log; grep FAILED gpurun_out/pytest_gpu.log | head
-timeout 600 python bench.py --steps 2000 --warmup 20 --no-cpu-baseline --e2e-steps 10 --batch 8 --x-ready 0 > gpurun_out/bench_tpw8.json 2> gpurun_out/bench_tpw8.err; python -c "
-import json;d=json.load(open('gpurun_out/bench_tpw8.json'));print('B8', d['us_per_step']);[print(l['shape'], l['us'], l['us_x_ready']) for l in d['layers']]" || tail -5 gpurun_out/bench_tpw8.err
+timeout 900 python -m pytest tests/test_gpu_tc.py tests/test_gpu_robust.py tests/test_gpu_fixup_modes.py -m gpu -q -x > gpurun_out/pytest_tc.log 2>&1; tail -2 gpurun_out/pytest_tc.log
+timeout 900 python tools/sweep.py --out gpurun_out/sweepT1 --sections T > gpurun_out/sweepT1.log 2>&1; grep "| tc" gpurun_out/sweepT1.md
+GQSA_CTA_FIX=0 timeout 900 python tools/sweep.py --out gpurun_out/sweepT0 --sections T > gpurun_out/sweepT0.log 2>&1; grep "| tc" gpurun_out/sweepT0.md
