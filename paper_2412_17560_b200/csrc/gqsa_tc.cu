@@ -19,9 +19,10 @@
 //    column sums.  Accumulators (2 rows x 2 batch columns per lane) live in
 //    registers for the whole block.
 //  * Weights stream HBM -> registers (768-B tiles of 4 items, 128-bit
-//    no-allocate loads, two tiles in flight per warp), Stream-K over tiles
-//    with the wait-free last-arriver fix-up for blocks split across warps
-//    (4 values per lane), deterministic.
+//    no-allocate loads, four tiles in flight per warp), Stream-K over tiles;
+//    blocks split across warps are reduced inside the CTA through shared
+//    memory, and across CTAs by the wait-free last-arriver fix-up (4 values
+//    per lane, one record per CTA), deterministic.
 #include <cuda_fp16.h>
 
 #include "gqsa_device.cuh"
